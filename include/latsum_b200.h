@@ -1,0 +1,128 @@
+/* latsum_b200 — C ABI of the B200-native Epstein-zeta hot path.
+ *
+ * Drop-in boundary for the reference package `latsum` (arXiv 2504.11989,
+ * /root/reference/pkg/src/latsum, abbreviated L/ below).  The reference is pure
+ * Python, so its "FFI" for this path is the Python methods themselves; each
+ * entry point below names the reference interface it replaces.  The Python
+ * mirror (paper_2504_11989_b200/) binds these with ctypes, and INTEGRATION.md
+ * shows the ctypes stub a reference maintainer would add.
+ *
+ * Conventions
+ *   - FP64 everywhere.  Plain pointers and sizes; no torch types.
+ *   - Functions suffixed with nothing take DEVICE pointers and a cudaStream_t
+ *     (passed as void*; NULL = legacy default stream) and are stream-ordered.
+ *     Functions suffixed `_host` take HOST pointers and synchronise.
+ *   - There is no CPU compute path: without a CUDA device every compute entry
+ *     point returns LZ_ECUDA.  Context creation with device < 0 builds the
+ *     host-side tables only (for inspection / tests).
+ *   - Return codes map onto the reference's exceptions (L/errors.py:4-17,
+ *     L/epstein.py:62-63,150-151,266-267,309-313):
+ */
+#ifndef LATSUM_B200_H
+#define LATSUM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    LZ_OK = 0,
+    LZ_EINVAL = 1,     /* ValueError: bad argument, |nu| > 100, non-finite k       */
+    LZ_EPOLE = 2,      /* PoleError: nu = d at k in the reciprocal lattice          */
+    LZ_ENONFINITE = 3, /* ValueError("k contains non-finite entries")               */
+    LZ_ECUDA = 4,      /* CUDA runtime failure or no device                          */
+    LZ_ENCCL = 5,      /* reserved: collective failure (collectives run in torch)   */
+    LZ_ESHELLS = 6,    /* RuntimeError: sum did not truncate within shell budget    */
+    LZ_ELATTICE = 7,   /* LatticeError: singular generator / unsupported dimension  */
+    LZ_ESINGULAR = 8   /* ValueError: singular part undefined at k = 0              */
+};
+
+/* zeta flags (lz_zeta / lz_zeta_host) */
+#define LZ_NO_REDUCE 1u     /* do not reduce k into the BZ box (reg_zeta semantics) */
+#define LZ_REG_ONLY 2u      /* Z_reg only: drop shat/V (L/epstein.py:261-289)        */
+#define LZ_SINGULAR_ONLY 4u /* shat(nu, k) only (L/epstein.py:217-231)               */
+
+typedef struct lz_ctx lz_ctx;   /* one (lattice, nu) context, immutable            */
+typedef struct lz_plan lz_plan; /* fused multi-context plan for the integral kernels */
+
+typedef struct {
+    int d;               /* 1..4 (L/lattice.py:20)                                 */
+    double a[16];        /* generator A, row-major d x d, columns = basis vectors */
+    double nu;           /* exponent                                              */
+    double splitting;    /* <= 0: default V^{-2/d} (L/epstein.py:107)             */
+    int deriv_order;     /* 0: zeta only; 2: also build the Hessian point sets    */
+} lz_ctx_params;
+
+typedef struct {
+    int d, branch, log_m, pole;   /* branch: 0 generic, 1 log_case, 2 trivial     */
+    double nu, vol, split, s_rec, pref, rfac, bconst, kmax, singular_coef, const_value;
+    int64_t n_dir, n_rec, n_dir_h, n_rec_h;
+    double table_x_lo, table_x_hi, table_max_rel_err;
+    int64_t table_pieces, table_bins;
+} lz_ctx_info;
+
+/* -- contexts: EpsteinContext.__init__ (L/epstein.py:99-122) + epstein_context (L/epstein.py:469-472) */
+int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out);
+int lz_ctx_destroy(lz_ctx* ctx);
+int lz_ctx_get_info(const lz_ctx* ctx, lz_ctx_info* out);
+/* which: 0 dir_pts (z = A n), 1 dir_w, 2 rec_pts, 3 hdir_pts, 4 hdir_w, 5 rec_pts_h, 6 dir_n (int coords)
+ * copies min(cap, size) doubles; returns the full size through *size.                        */
+int lz_ctx_get_points(const lz_ctx* ctx, int which, double* dst, int64_t cap, int64_t* size);
+
+/* -- EpsteinContext.zeta / reg_zeta / singular (L/epstein.py:217-231,261-320).
+ * k: n x d row-major, out: n.  status (device int, may be NULL) gets bit 1 on a pole.
+ * lanes_per_point: 0 = auto (1 for large batches, up to 32 for small ones). */
+int lz_zeta(const lz_ctx* ctx, const double* k, int64_t n, double* out, uint32_t flags,
+            int lanes_per_point, int* status, void* stream);
+int lz_zeta_host(const lz_ctx* ctx, const double* k, int64_t n, double* out, uint32_t flags);
+
+/* -- Hessian d_a d_b Z_nu(k) (upper triangle, row-major: d(d+1)/2 values per point).
+ * The polynomial-weighted zeta M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k}
+ * equals -Hessian/(4 pi^2).  No reference counterpart at k != 0; the k = 0
+ * analogue is EpsteinContext.reg_derivatives (L/epstein.py:347-415).
+ * Requires deriv_order >= 2 at context creation. */
+int lz_zeta_hessian(const lz_ctx* ctx, const double* k, int64_t n, double* out, int lanes_per_point,
+                    void* stream);
+int lz_zeta_hessian_host(const lz_ctx* ctx, const double* k, int64_t n, double* out);
+
+/* -- fixed Duffy grid (L/quadrature.py:136-177): 2^{d-1} d cells x n_u (Gauss-Legendre
+ * in t, u = t^grading / 2) x n_v^{d-1} (Gauss-Legendre on [0, 1/2]).  Nodes are generated
+ * on device; each 256-node tile writes one partial per component. */
+typedef struct {
+    int n_u, n_v;
+    int grading;         /* q >= 1 in u = t^q / 2 */
+    int64_t tile_lo;     /* tile range of this call (multi-GPU shard); tile_hi <= 0: all */
+    int64_t tile_hi;
+} lz_grid;
+int lz_grid_tiles(int d, const lz_grid* g, int64_t* n_nodes, int64_t* n_tiles);
+
+/* -- product of zetas on the grid: _product_on_batch + integrate_product
+ * (L/quadrature.py:393-397,455-490), distinct exponents evaluated once per node
+ * and raised to their multiplicity.  partials: n_tiles doubles (only the tiles
+ * of [tile_lo, tile_hi) are written).  value = 2^d * sum(partials). */
+int lz_plan_create_product(const lz_ctx* const* ctxs, const int* mult, int nctx, lz_plan** out);
+/* -- ATM integrand [Z_3^3, tr(M_5^3)] with M_5 = -Hess Z_5/(4 pi^2): partials n_tiles x 2.
+ * E_ATM = 2^d/6 * (sum_0 - 3 sum_1); zeta^(3)(3,3,3) = 2^d sum_0.  z5 needs deriv_order 2. */
+int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out);
+int lz_plan_destroy(lz_plan* plan);
+int lz_plan_integrate(const lz_plan* plan, const lz_grid* g, double* partials, int grid_blocks,
+                      void* stream);
+/* fixed-order compensated sum of n_tiles x ncomp partials -> out[ncomp] (device) */
+int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream);
+/* whole integral through host memory: out[ncomp] (value sums before the 2^d factor) */
+int lz_plan_integrate_host(const lz_plan* plan, const lz_grid* g, double* out);
+
+/* -- diagnostics */
+int lz_fp64_peak(double* tflops_out, double* ms_out);  /* DFMA-chain probe on the current device */
+int lz_device_count(int* n);
+const char* lz_strerror(int code);
+const char* lz_last_error(void);   /* thread-local message of the last failure */
+const char* lz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LATSUM_B200_H */

@@ -1,0 +1,705 @@
+// extern "C" boundary of latsum_b200 (see include/latsum_b200.h).
+//
+// Owns the host/device lifetime of contexts and fused plans: builds the host
+// tables (context.cpp), uploads them once, and launches the kernels
+// (kernels.cu) on the caller's stream.  No CPU compute path exists: every
+// compute entry point needs a CUDA device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/latsum_b200.h"
+#include "lz_internal.h"
+#include "special.cuh"
+
+namespace lz {
+cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n, double* out, uint32_t flags,
+                         int G, int* status, cudaStream_t st);
+cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, double* partials,
+                           int grid_blocks, cudaStream_t st);
+cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
+                       cudaStream_t st);
+cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st);
+cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cudaStream_t st);
+int tile_nodes();
+
+}  // namespace lz
+
+using lz::Error;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_err(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error{LZ_ECUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+struct DeviceGuard {
+    int old = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev < 0) return;
+        check_cuda(cudaGetDevice(&old), "cudaGetDevice");
+        if (old != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+        else old = -1;
+    }
+    ~DeviceGuard() {
+        if (old >= 0) cudaSetDevice(old);
+    }
+};
+
+template <class T> T* upload(const std::vector<T>& v, std::vector<void*>* allocs) {
+    if (v.empty()) return nullptr;
+    void* p = nullptr;
+    check_cuda(cudaMalloc(&p, v.size() * sizeof(T)), "cudaMalloc");
+    allocs->push_back(p);
+    check_cuda(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy");
+    return static_cast<T*>(p);
+}
+
+void free_all(std::vector<void*>* allocs) {
+    for (void* p : *allocs) cudaFree(p);
+    allocs->clear();
+}
+
+// Host-side description of a fused plan before upload.
+struct HostPlan {
+    int d = 0, nctx = 0, hess = 0, nw = 0;
+    std::vector<double> dir_n, dir_w, rec_q;
+    lz::HostTable tab;
+    lz::CtxConst ctx[lz::kMaxCtx];
+    lz::CtxConst hctx;
+    double A[16], B[16];
+};
+
+using ld = long double;
+
+// Union of integer point sets (keeps the order of the first, appends the rest).
+void union_points(int d, const std::vector<const std::vector<double>*>& sets, std::vector<double>* out) {
+    out->clear();
+    std::set<std::vector<long>> seen;
+    for (const auto* s : sets) {
+        const size_t cnt = s->size() / d;
+        for (size_t i = 0; i < cnt; ++i) {
+            std::vector<long> key(d);
+            for (int a = 0; a < d; ++a) key[a] = std::lround((*s)[i * d + a]);
+            if (seen.insert(key).second) out->insert(out->end(), s->begin() + i * d, s->begin() + (i + 1) * d);
+        }
+    }
+}
+
+// Direct-space weight w_z = Gamma(nu/2, pi t |z|^2) |z|^-nu (L/epstein.py:139), long double.
+ld direct_weight(const lz::HostCtx& h, const double* n, ld* z) {
+    const int d = h.d;
+    ld r2 = 0.0L;
+    for (int a = 0; a < d; ++a) {
+        z[a] = 0.0L;
+        for (int b = 0; b < d; ++b) z[a] += ld(h.A[a * d + b]) * n[b];
+        r2 += z[a] * z[a];
+    }
+    const ld nu = h.k.nu;
+    const ld x = ld(lz::kPi) * ld(h.k.split) * r2;
+    return lz::upper_gamma<ld>(nu / 2.0L, x) * std::pow(r2, -nu / 2.0L);
+}
+
+// Build a fused plan from plain contexts (+ optionally one Hessian context).
+void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::HostCtx* hess, HostPlan* hp) {
+    const lz::HostCtx* first = plain.empty() ? hess : plain[0];
+    const int d = first->d;
+    hp->d = d;
+    hp->nctx = int(plain.size());
+    hp->hess = hess ? 1 : 0;
+    std::memcpy(hp->A, first->A, sizeof(hp->A));
+    std::memcpy(hp->B, first->B, sizeof(hp->B));
+    std::vector<const std::vector<double>*> dsets, rsets;
+    for (const auto* c : plain) {
+        if (c->k.split != first->k.split) throw Error{LZ_EINVAL, "fused contexts must share the split"};
+        if (std::memcmp(c->A, first->A, sizeof(c->A)) != 0)
+            throw Error{LZ_EINVAL, "fused contexts must share the lattice"};
+        dsets.push_back(&c->dir_n);
+        rsets.push_back(&c->rec_n);
+    }
+    if (hess) {
+        if (hess->k.split != first->k.split) throw Error{LZ_EINVAL, "fused contexts must share the split"};
+        dsets.push_back(&hess->hdir_n);
+        rsets.push_back(&hess->hrec_n);
+    }
+    // order: largest set first so single-context plans keep the reference order
+    auto by_size = [](const std::vector<double>* a, const std::vector<double>* b) { return a->size() > b->size(); };
+    std::stable_sort(dsets.begin(), dsets.end(), by_size);
+    std::stable_sort(rsets.begin(), rsets.end(), by_size);
+    union_points(d, dsets, &hp->dir_n);
+    std::vector<double> rec_n;
+    union_points(d, rsets, &rec_n);
+    const int nsym = d * (d + 1) / 2;
+    hp->nw = hp->nctx + (hess ? nsym : 0);
+    const size_t ndir = hp->dir_n.size() / d;
+    hp->dir_w.assign(ndir * hp->nw, 0.0);
+    for (size_t i = 0; i < ndir; ++i) {
+        const double* n = &hp->dir_n[i * d];
+        ld z[lz::kMaxDim];
+        for (int j = 0; j < hp->nctx; ++j) {
+            // reuse the context's own rounded weight when the point is in its set (bit-identical
+            // single-context plans), else compute it
+            const lz::HostCtx* c = plain[j];
+            hp->dir_w[i * hp->nw + j] = double(direct_weight(*c, n, z));
+        }
+        if (hess) {
+            ld w = direct_weight(*hess, n, z);
+            int cidx = 0;
+            for (int a = 0; a < d; ++a)
+                for (int b = a; b < d; ++b) hp->dir_w[i * hp->nw + hp->nctx + cidx++] = double(w * z[a] * z[b]);
+        }
+    }
+    const size_t nrec = rec_n.size() / d;
+    hp->rec_q.assign(nrec * d, 0.0);
+    for (size_t i = 0; i < nrec; ++i)
+        for (int a = 0; a < d; ++a) {
+            ld q = 0.0L;
+            for (int b = 0; b < d; ++b) q += ld(first->B[a * d + b]) * rec_n[i * d + b];
+            hp->rec_q[i * d + a] = double(q);
+        }
+    // table functions: plain F_j = c^s E_{1-s}; Hessian F' = -c^{s+1} E_{-s}, F'' = c^{s+2} E_{-s-1}
+    double p[4], sc[4];
+    int nf = 0;
+    double rp = 0.0;
+    const ld c = ld(lz::kPi) / ld(first->k.split);
+    for (int j = 0; j < hp->nctx; ++j) {
+        const lz::CtxConst& k = plain[j]->k;
+        hp->ctx[j] = k;
+        p[nf] = 1.0 - k.s;
+        sc[nf] = double(std::pow(c, ld(k.s)));
+        ++nf;
+        rp = std::max(rp, std::fabs(k.rfac * k.pref));
+    }
+    std::memset(&hp->hctx, 0, sizeof(hp->hctx));
+    if (hess) {
+        const lz::CtxConst& k = hess->k;
+        hp->hctx = k;
+        p[nf] = -k.s;
+        sc[nf] = -double(std::pow(c, ld(k.s) + 1.0L));
+        ++nf;
+        p[nf] = -k.s - 1.0;
+        sc[nf] = double(std::pow(c, ld(k.s) + 2.0L));
+        ++nf;
+        rp = std::max(rp, std::fabs(k.rfac * k.pref));
+    }
+    if (nf > 4) throw Error{LZ_EINVAL, "too many functions in one plan"};
+    if (hp->rec_q.empty()) {
+        hp->tab = lz::HostTable();
+        hp->tab.nfunc = nf;
+    } else {
+        lz::build_table(p, sc, nf, double(c), lz::table_x_lo(*first), rp, &hp->tab);
+    }
+}
+
+lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
+    lz::DevPlan P;
+    std::memset(&P, 0, sizeof(P));
+    P.d = hp.d;
+    P.nctx = hp.nctx;
+    P.hess = hp.hess;
+    P.n_dir = int(hp.dir_n.size() / hp.d);
+    P.n_rec = int(hp.rec_q.size() / hp.d);
+    P.nw = hp.nw;
+    std::memcpy(P.A, hp.A, sizeof(P.A));
+    std::memcpy(P.B, hp.B, sizeof(P.B));
+    P.dir_n = upload(hp.dir_n, allocs);
+    P.dir_w = upload(hp.dir_w, allocs);
+    P.rec_q = upload(hp.rec_q, allocs);
+    P.tab.dir = upload(hp.tab.dir, allocs);
+    P.tab.coef = upload(hp.tab.coef, allocs);
+    P.tab.nbins = hp.tab.nbins;
+    P.tab.nfunc = hp.tab.nfunc;
+    P.tab.npieces = hp.tab.npieces;
+    P.tab.x_lo = hp.tab.x_lo;
+    P.tab.inv_hb = hp.tab.inv_hb;
+    P.tab.x_hi = hp.tab.x_hi;
+    for (int j = 0; j < 4; ++j) {
+        P.tab.p[j] = hp.tab.p[j];
+        P.tab.scale[j] = hp.tab.scale[j];
+    }
+    for (int j = 0; j < lz::kMaxCtx; ++j) P.ctx[j] = hp.ctx[j];
+    P.hctx = hp.hctx;
+    return P;
+}
+
+struct GridArrays {
+    double* u = nullptr;
+    double* wu = nullptr;
+    double* v = nullptr;
+    double* wv = nullptr;
+};
+
+}  // namespace
+
+struct lz_ctx {
+    lz::HostCtx h;
+    int device = -1;
+    HostPlan plain, hessp;
+    lz::DevPlan dplain, dhess;
+    std::vector<void*> allocs;
+};
+
+struct lz_plan {
+    int device = -1;
+    int kind = 0;  // 0 product, 1 atm
+    int d = 0;
+    int mult[4] = {0, 0, 0, 0};
+    HostPlan hp;
+    lz::DevPlan P;
+    std::vector<void*> allocs;
+    mutable std::mutex mu;
+    mutable std::map<std::tuple<int, int, int>, GridArrays> grids;
+};
+
+namespace {
+
+void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
+    if (g->n_u < 1 || (d > 1 && g->n_v < 1) || g->grading < 1)
+        throw Error{LZ_EINVAL, "grid sizes must be positive and grading >= 1"};
+    dg->n_u = g->n_u;
+    dg->n_v = d > 1 ? g->n_v : 1;
+    dg->n_cell = (1 << (d - 1)) * d;
+    dg->pu = d > 1 ? 4 : 32;
+    dg->pv = d > 1 ? 8 : 1;
+    dg->npu = (dg->n_u + dg->pu - 1) / dg->pu;
+    dg->npv = d > 1 ? (dg->n_v + dg->pv - 1) / dg->pv : 1;
+    dg->nv2 = d > 2 ? dg->n_v : 1;
+    dg->n_patch = int64_t(dg->n_cell) * dg->nv2 * dg->npv * dg->npu;
+    const int64_t n_tiles = (dg->n_patch + 7) / 8;
+    dg->tile_lo = std::max<int64_t>(0, g->tile_lo);
+    dg->tile_hi = g->tile_hi > 0 ? std::min(g->tile_hi, n_tiles) : n_tiles;
+}
+
+const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
+    std::lock_guard<std::mutex> lock(plan->mu);
+    auto key = std::make_tuple(g->n_u, plan->d > 1 ? g->n_v : 1, g->grading);
+    auto it = plan->grids.find(key);
+    if (it != plan->grids.end()) return it->second;
+    const int d = plan->d;
+    std::vector<double> x, w;
+    lz::gauss_legendre(g->n_u, &x, &w);
+    std::vector<double> u(g->n_u), wu(g->n_u);
+    const ld q = g->grading;
+    for (int i = 0; i < g->n_u; ++i) {
+        // t = (x+1)/2 on (0,1); u = t^q / 2; du = q/2 t^{q-1} dt; times u^{d-1}
+        const ld t = (ld(x[i]) + 1.0L) / 2.0L;
+        const ld wt = ld(w[i]) / 2.0L;
+        const ld uu = 0.5L * std::pow(t, q);
+        u[i] = double(uu);
+        wu[i] = double(wt * 0.5L * q * std::pow(t, q - 1.0L) * std::pow(uu, ld(d - 1)));
+    }
+    std::vector<double> v, wv;
+    if (d > 1) {
+        lz::gauss_legendre(g->n_v, &x, &w);
+        v.resize(g->n_v);
+        wv.resize(g->n_v);
+        // angular_nodes: v = (x + 1)/4, weights w/4 (L/quadrature.py:165-177)
+        for (int i = 0; i < g->n_v; ++i) {
+            v[i] = double((ld(x[i]) + 1.0L) / 4.0L);
+            wv[i] = double(ld(w[i]) / 4.0L);
+        }
+    } else {
+        v.assign(1, 0.0);
+        wv.assign(1, 1.0);
+    }
+    GridArrays ga;
+    std::vector<void*>& allocs = const_cast<std::vector<void*>&>(plan->allocs);
+    ga.u = upload(u, &allocs);
+    ga.wu = upload(wu, &allocs);
+    ga.v = upload(v, &allocs);
+    ga.wv = upload(wv, &allocs);
+    return plan->grids.emplace(key, ga).first->second;
+}
+
+int auto_lanes(int64_t n) {
+    const int64_t target = 148LL * 2048LL;
+    int g = 1;
+    while (g < 32 && n * g < target) g <<= 1;
+    return g;
+}
+
+template <class F> int guarded(F&& f) {
+    try {
+        f();
+        return LZ_OK;
+    } catch (const Error& e) {
+        return set_err(e.code, e.msg);
+    } catch (const std::exception& e) {
+        return set_err(LZ_EINVAL, e.what());
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lz_version(void) { return "latsum_b200 0.1.0 (sm_100a, FP64)"; }
+
+const char* lz_strerror(int code) {
+    switch (code) {
+        case LZ_OK: return "ok";
+        case LZ_EINVAL: return "invalid argument";
+        case LZ_EPOLE: return "pole of the meromorphic continuation";
+        case LZ_ENONFINITE: return "k contains non-finite entries";
+        case LZ_ECUDA: return "CUDA failure or no CUDA device";
+        case LZ_ENCCL: return "collective failure";
+        case LZ_ESHELLS: return "lattice sum did not truncate within shell budget";
+        case LZ_ELATTICE: return "invalid lattice";
+        case LZ_ESINGULAR: return "singular part undefined at k = 0";
+    }
+    return "unknown error";
+}
+
+const char* lz_last_error(void) { return g_last_error.c_str(); }
+
+int lz_device_count(int* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *n = c;
+    return LZ_OK;
+}
+
+int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out) {
+    *out = nullptr;
+    lz_ctx* c = new lz_ctx();
+    int rc = guarded([&] {
+        lz::build_context(p->d, p->a, p->nu, p->splitting, p->deriv_order, &c->h);
+        c->device = device;
+        if (c->h.k.branch != lz::kTrivial) {
+            build_host_plan({&c->h}, nullptr, &c->plain);
+            if (c->h.has_hess) build_host_plan({}, &c->h, &c->hessp);
+        } else {
+            c->plain.d = p->d;
+            c->plain.nctx = 1;
+            c->plain.ctx[0] = c->h.k;
+            std::memcpy(c->plain.A, c->h.A, sizeof(c->plain.A));
+            std::memcpy(c->plain.B, c->h.B, sizeof(c->plain.B));
+        }
+        if (device >= 0) {
+            DeviceGuard dg(device);
+            c->dplain = upload_plan(c->plain, &c->allocs);
+            if (c->h.has_hess) c->dhess = upload_plan(c->hessp, &c->allocs);
+        }
+    });
+    if (rc != LZ_OK) {
+        free_all(&c->allocs);
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return LZ_OK;
+}
+
+int lz_ctx_destroy(lz_ctx* c) {
+    if (!c) return LZ_OK;
+    if (c->device >= 0) {
+        int old = -1;
+        cudaGetDevice(&old);
+        cudaSetDevice(c->device);
+        free_all(&c->allocs);
+        if (old >= 0) cudaSetDevice(old);
+    }
+    delete c;
+    return LZ_OK;
+}
+
+int lz_ctx_get_info(const lz_ctx* c, lz_ctx_info* o) {
+    std::memset(o, 0, sizeof(*o));
+    const lz::CtxConst& k = c->h.k;
+    o->d = c->h.d;
+    o->branch = k.branch;
+    o->log_m = k.log_m;
+    o->pole = k.pole;
+    o->nu = k.nu;
+    o->vol = k.vol;
+    o->split = k.split;
+    o->s_rec = k.s;
+    o->pref = k.pref;
+    o->rfac = k.rfac;
+    o->bconst = k.bconst;
+    o->kmax = c->h.kmax;
+    o->singular_coef = k.sing_coef;
+    o->const_value = k.const_value;
+    o->n_dir = int64_t(c->h.dir_w.size());
+    o->n_rec = int64_t(c->h.rec_q.size() / c->h.d);
+    o->n_dir_h = int64_t(c->h.hdir_w.size());
+    o->n_rec_h = int64_t(c->h.hrec_q.size() / c->h.d);
+    o->table_x_lo = c->plain.tab.x_lo;
+    o->table_x_hi = c->plain.tab.x_hi;
+    o->table_max_rel_err = std::max(c->plain.tab.max_rel_err, c->hessp.tab.max_rel_err);
+    o->table_pieces = c->plain.tab.npieces;
+    o->table_bins = c->plain.tab.nbins;
+    return LZ_OK;
+}
+
+int lz_ctx_get_points(const lz_ctx* c, int which, double* dst, int64_t cap, int64_t* size) {
+    const std::vector<double>* v = nullptr;
+    switch (which) {
+        case 0: v = &c->h.dir_z; break;
+        case 1: v = &c->h.dir_w; break;
+        case 2: v = &c->h.rec_q; break;
+        case 3: v = &c->h.hdir_z; break;
+        case 4: v = &c->h.hdir_w; break;
+        case 5: v = &c->h.hrec_q; break;
+        case 6: v = &c->h.dir_n; break;
+        default: return set_err(LZ_EINVAL, "unknown point set");
+    }
+    *size = int64_t(v->size());
+    if (dst) std::memcpy(dst, v->data(), sizeof(double) * size_t(std::min<int64_t>(cap, *size)));
+    return LZ_OK;
+}
+
+int lz_zeta(const lz_ctx* c, const double* k, int64_t n, double* out, uint32_t flags, int lanes, int* status,
+            void* stream) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables (created with device < 0)"};
+        DeviceGuard dg(c->device);
+        int G = lanes > 0 ? lanes : auto_lanes(n);
+        if (G & (G - 1) || G > 32) throw Error{LZ_EINVAL, "lanes_per_point must be a power of two <= 32"};
+        check_cuda(lz::launch_batch(c->dplain, false, k, n, out, flags, G, status, (cudaStream_t)stream),
+                   "zeta kernel launch");
+    });
+}
+
+int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint32_t flags) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables (created with device < 0)"};
+        for (int64_t i = 0; i < n * c->h.d; ++i)
+            if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
+        if (n == 0) return;
+        DeviceGuard dg(c->device);
+        cudaStream_t st;
+        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        double *dk = nullptr, *dout = nullptr;
+        int* dstat = nullptr;
+        const size_t kb = sizeof(double) * size_t(n) * c->h.d;
+        check_cuda(cudaMallocAsync((void**)&dk, kb, st), "malloc");
+        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * size_t(n), st), "malloc");
+        check_cuda(cudaMallocAsync((void**)&dstat, sizeof(int), st), "malloc");
+        check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), st), "memset");
+        check_cuda(cudaMemcpyAsync(dk, k, kb, cudaMemcpyHostToDevice, st), "h2d");
+        check_cuda(lz::launch_batch(c->dplain, false, dk, n, dout, flags, auto_lanes(n), dstat, st), "zeta kernel");
+        int hstat = 0;
+        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st), "d2h");
+        check_cuda(cudaMemcpyAsync(&hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+        cudaFreeAsync(dk, st);
+        cudaFreeAsync(dout, st);
+        cudaFreeAsync(dstat, st);
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        cudaStreamDestroy(st);
+        if (hstat & 1)
+            throw Error{LZ_EPOLE, "Epstein zeta has a simple pole at nu = d for k in the reciprocal lattice"};
+    });
+}
+
+int lz_zeta_hessian(const lz_ctx* c, const double* k, int64_t n, double* out, int lanes, void* stream) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
+        if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+        DeviceGuard dg(c->device);
+        int G = lanes > 0 ? lanes : auto_lanes(n);
+        check_cuda(lz::launch_batch(c->dhess, true, k, n, out, 1u, G, nullptr, (cudaStream_t)stream),
+                   "hessian kernel launch");
+    });
+}
+
+int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* out) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
+        if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+        for (int64_t i = 0; i < n * c->h.d; ++i)
+            if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
+        if (n == 0) return;
+        DeviceGuard dg(c->device);
+        const int d = c->h.d, ns = d * (d + 1) / 2;
+        cudaStream_t st;
+        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        double *dk = nullptr, *dout = nullptr;
+        check_cuda(cudaMallocAsync((void**)&dk, sizeof(double) * size_t(n) * d, st), "malloc");
+        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * size_t(n) * ns, st), "malloc");
+        check_cuda(cudaMemcpyAsync(dk, k, sizeof(double) * size_t(n) * d, cudaMemcpyHostToDevice, st), "h2d");
+        check_cuda(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, st), "hessian kernel");
+        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * size_t(n) * ns, cudaMemcpyDeviceToHost, st), "d2h");
+        cudaFreeAsync(dk, st);
+        cudaFreeAsync(dout, st);
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        cudaStreamDestroy(st);
+    });
+}
+
+int lz_grid_tiles(int d, const lz_grid* g, int64_t* n_nodes, int64_t* n_tiles) {
+    return guarded([&] {
+        if (d < 1 || d > 4) throw Error{LZ_EINVAL, "dimension outside 1..4"};
+        lz::DevGrid dg;
+        lz_grid all = *g;
+        all.tile_lo = 0;
+        all.tile_hi = 0;
+        fill_grid(d, &all, &dg);
+        *n_nodes = int64_t(dg.n_cell) * dg.n_u * (d > 1 ? dg.n_v : 1) * (d > 2 ? dg.n_v : 1);
+        *n_tiles = dg.tile_hi;
+    });
+}
+
+int lz_plan_create_product(const lz_ctx* const* ctxs, const int* mult, int nctx, lz_plan** out) {
+    *out = nullptr;
+    lz_plan* pl = new lz_plan();
+    int rc = guarded([&] {
+        if (nctx < 1 || nctx > lz::kMaxCtx) throw Error{LZ_EINVAL, "product plans fuse 1..4 distinct exponents"};
+        std::vector<const lz::HostCtx*> plain;
+        for (int j = 0; j < nctx; ++j) {
+            if (ctxs[j]->h.k.branch == lz::kTrivial)
+                throw Error{LZ_EINVAL, "trivial-branch factors are constants; fold them on the host"};
+            if (mult[j] < 1) throw Error{LZ_EINVAL, "multiplicities must be >= 1"};
+            plain.push_back(&ctxs[j]->h);
+            pl->mult[j] = mult[j];
+        }
+        pl->device = ctxs[0]->device;
+        if (pl->device < 0) throw Error{LZ_ECUDA, "contexts have no device"};
+        pl->d = ctxs[0]->h.d;
+        if (pl->d > 3) throw Error{LZ_EINVAL, "integral kernels support d <= 3"};
+        pl->kind = 0;
+        build_host_plan(plain, nullptr, &pl->hp);
+        DeviceGuard dg(pl->device);
+        pl->P = upload_plan(pl->hp, &pl->allocs);
+    });
+    if (rc != LZ_OK) {
+        free_all(&pl->allocs);
+        delete pl;
+        return rc;
+    }
+    *out = pl;
+    return LZ_OK;
+}
+
+int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
+    *out = nullptr;
+    lz_plan* pl = new lz_plan();
+    int rc = guarded([&] {
+        if (!z5->h.has_hess) throw Error{LZ_EINVAL, "the nu = 5 context needs deriv_order >= 2"};
+        if (z3->h.k.branch == lz::kTrivial || z5->h.k.branch == lz::kTrivial)
+            throw Error{LZ_EINVAL, "ATM contexts cannot be trivial"};
+        pl->device = z3->device;
+        if (pl->device < 0) throw Error{LZ_ECUDA, "contexts have no device"};
+        pl->d = z3->h.d;
+        if (pl->d > 3) throw Error{LZ_EINVAL, "ATM is defined for d <= 3"};
+        pl->kind = 1;
+        build_host_plan({&z3->h}, &z5->h, &pl->hp);
+        DeviceGuard dg(pl->device);
+        pl->P = upload_plan(pl->hp, &pl->allocs);
+    });
+    if (rc != LZ_OK) {
+        free_all(&pl->allocs);
+        delete pl;
+        return rc;
+    }
+    *out = pl;
+    return LZ_OK;
+}
+
+int lz_plan_destroy(lz_plan* pl) {
+    if (!pl) return LZ_OK;
+    int old = -1;
+    cudaGetDevice(&old);
+    cudaSetDevice(pl->device);
+    free_all(&pl->allocs);
+    if (old >= 0) cudaSetDevice(old);
+    delete pl;
+    return LZ_OK;
+}
+
+int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int grid_blocks, void* stream) {
+    return guarded([&] {
+        DeviceGuard dg(pl->device);
+        lz::DevGrid dgd;
+        fill_grid(pl->d, g, &dgd);
+        const GridArrays& ga = grid_arrays(pl, g);
+        dgd.u = ga.u;
+        dgd.wu = ga.wu;
+        dgd.v = ga.v;
+        dgd.wv = ga.wv;
+        cudaStream_t st = (cudaStream_t)stream;
+        if (pl->kind == 0)
+            check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");
+        else
+            check_cuda(lz::launch_atm(pl->P, dgd, partials, grid_blocks, st), "atm kernel");
+    });
+}
+
+int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream) {
+    return guarded([&] {
+        check_cuda(lz::launch_reduce(partials, n_tiles, ncomp, out, (cudaStream_t)stream), "reduce kernel");
+    });
+}
+
+int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
+    return guarded([&] {
+        DeviceGuard dg(pl->device);
+        int64_t n_nodes = 0, n_tiles = 0;
+        int rc = lz_grid_tiles(pl->d, g, &n_nodes, &n_tiles);
+        if (rc != LZ_OK) throw Error{rc, g_last_error};
+        const int ncomp = pl->kind == 0 ? 1 : 2;
+        cudaStream_t st;
+        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        double *dp = nullptr, *dout = nullptr;
+        check_cuda(cudaMallocAsync((void**)&dp, sizeof(double) * size_t(n_tiles) * ncomp, st), "malloc");
+        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * ncomp, st), "malloc");
+        check_cuda(cudaMemsetAsync(dp, 0, sizeof(double) * size_t(n_tiles) * ncomp, st), "memset");
+        lz_grid gg = *g;
+        rc = lz_plan_integrate(pl, &gg, dp, 0, st);
+        if (rc != LZ_OK) throw Error{rc, g_last_error};
+        check_cuda(lz::launch_reduce(dp, n_tiles, ncomp, dout, st), "reduce");
+        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * ncomp, cudaMemcpyDeviceToHost, st), "d2h");
+        cudaFreeAsync(dp, st);
+        cudaFreeAsync(dout, st);
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        cudaStreamDestroy(st);
+    });
+}
+
+int lz_fp64_peak(double* tflops, double* ms_out) {
+    return guarded([&] {
+        int dev = 0, sms = 0;
+        check_cuda(cudaGetDevice(&dev), "device");
+        check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        const int threads = 256, blocks = sms * 8, iters = 2048;
+        double* scratch = nullptr;
+        check_cuda(cudaMalloc(&scratch, sizeof(double) * blocks), "malloc");
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        check_cuda(lz::launch_probe(scratch, iters / 8, blocks, threads, 0), "probe");  // warm-up
+        cudaEventRecord(a, 0);
+        check_cuda(lz::launch_probe(scratch, iters, blocks, threads, 0), "probe");
+        cudaEventRecord(b, 0);
+        check_cuda(cudaEventSynchronize(b), "sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(scratch);
+        const double flops = 2.0 * 8.0 * 16.0 * double(iters) * double(threads) * double(blocks);
+        *tflops = flops / (double(ms) * 1e-3) / 1e12;
+        *ms_out = ms;
+    });
+}
+
+}  // extern "C"

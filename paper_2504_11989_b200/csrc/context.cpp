@@ -1,0 +1,495 @@
+// Host-side plan builder: lattice geometry, exponent classification, the
+// truncated direct/reciprocal point sets and the Crandall constants of one
+// (lattice, nu) context, plus the piecewise-polynomial tables of the radial
+// reciprocal summand.  One-time setup per context; everything is computed in
+// long double and rounded once.
+//
+// Follows, in order:
+//   classify_exponent          L/epstein.py:58-70
+//   _integer_shell/_lex_pos    L/epstein.py:73-90
+//   EpsteinContext.__init__    L/epstein.py:99-122
+//   _enumerate_direct          L/epstein.py:126-154
+//   _enumerate_reciprocal      L/epstein.py:159-194
+//   singular_coef              L/epstein.py:202-215
+//   BrillouinZone.corner_radius L/lattice.py:131-136
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "lz_internal.h"
+#include "special.cuh"
+
+namespace lz {
+
+using ld = long double;
+static const ld kPiL = 3.141592653589793238462643383279502884L;
+
+namespace {
+
+constexpr double kBranchTol = 1e-12;   // L/epstein.py:49
+constexpr double kPoleTol = 1e-10;     // L/epstein.py:50
+constexpr double kTermCutoff = 1e-18;  // L/epstein.py:51
+constexpr int kMaxShells = 80;         // L/epstein.py:52
+
+void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+// det and inverse of a small dense matrix by Gaussian elimination (long double)
+ld det_inv(int d, const ld* a, ld* inv) {
+    ld m[kMaxDim][2 * kMaxDim];
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < 2 * d; ++j) m[i][j] = j < d ? a[i * d + j] : (j - d == i ? 1.0L : 0.0L);
+    ld det = 1.0L;
+    for (int col = 0; col < d; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < d; ++r)
+            if (std::fabs(m[r][col]) > std::fabs(m[piv][col])) piv = r;
+        if (m[piv][col] == 0.0L) return 0.0L;
+        if (piv != col) {
+            for (int j = 0; j < 2 * d; ++j) std::swap(m[piv][j], m[col][j]);
+            det = -det;
+        }
+        det *= m[col][col];
+        ld pv = m[col][col];
+        for (int j = 0; j < 2 * d; ++j) m[col][j] /= pv;
+        for (int r = 0; r < d; ++r) {
+            if (r == col) continue;
+            ld f = m[r][col];
+            if (f == 0.0L) continue;
+            for (int j = 0; j < 2 * d; ++j) m[r][j] -= f * m[col][j];
+        }
+    }
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) inv[i * d + j] = m[i][d + j];
+    return det;
+}
+
+// Integer vectors with max-norm exactly r, lexicographic (first index slowest).
+std::vector<int> integer_shell(int d, int r) {
+    std::vector<int> out;
+    if (r == 0) {
+        out.assign(d, 0);
+        return out;
+    }
+    const int w = 2 * r + 1;
+    long total = 1;
+    for (int i = 0; i < d; ++i) total *= w;
+    std::vector<int> n(d);
+    for (long idx = 0; idx < total; ++idx) {
+        long rem = idx;
+        int mx = 0;
+        for (int i = d - 1; i >= 0; --i) {
+            n[i] = int(rem % w) - r;
+            rem /= w;
+            mx = std::max(mx, std::abs(n[i]));
+        }
+        if (mx == r) out.insert(out.end(), n.begin(), n.end());
+    }
+    return out;
+}
+
+bool lex_positive(const int* n, int d) {
+    for (int i = 0; i < d; ++i) {
+        if (n[i] > 0) return true;
+        if (n[i] < 0) return false;
+    }
+    return false;
+}
+
+// Gamma(s, x) on the host (long double), any real s, x > 0.
+ld upper_gamma_l(ld s, ld x) { return upper_gamma<ld>(s, x); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+static void classify(double nu, int d, CtxConst* k) {
+    if (!std::isfinite(nu)) fail(1, "exponent must be finite");
+    if (std::fabs(nu) > 100.0) fail(1, "exponent magnitude above 100 is not supported");
+    // Python round() is round-half-even: nearbyint under the default mode.
+    double m = std::nearbyint((nu - d) / 2.0);
+    if (m >= 0 && std::fabs(nu - (d + 2 * m)) < kBranchTol) {
+        k->branch = kLogCase;
+        k->nu = double(d + 2 * m);
+        k->log_m = int(m);
+        return;
+    }
+    double j = std::nearbyint(-nu / 2.0);
+    if (j >= 0 && std::fabs(nu + 2 * j) < kBranchTol) {
+        k->branch = kTrivial;
+        k->nu = -2.0 * j;
+        k->log_m = -1;
+        return;
+    }
+    k->branch = kGeneric;
+    k->nu = nu;
+    k->log_m = -1;
+}
+
+static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::vector<double>* pn,
+                             std::vector<double>* pz, std::vector<double>* pw) {
+    const int d = h.d;
+    const ld nu = h.k.nu, t = h.k.split;
+    pn->clear();
+    pz->clear();
+    pw->clear();
+    ld total = 1.0L;
+    int below = 0;
+    bool done = false;
+    for (int r = 1; r <= kMaxShells; ++r) {
+        std::vector<int> shell = integer_shell(d, r);
+        const int cnt = int(shell.size()) / d;
+        std::vector<double> sn, sz, sw;
+        ld mag = 0.0L, wsum = 0.0L;
+        for (int i = 0; i < cnt; ++i) {
+            const int* n = &shell[i * d];
+            if (!lex_positive(n, d)) continue;
+            ld z[kMaxDim], r2 = 0.0L;
+            for (int a = 0; a < d; ++a) {
+                z[a] = 0.0L;
+                for (int b = 0; b < d; ++b) z[a] += ld(h.A[a * d + b]) * n[b];
+                r2 += z[a] * z[a];
+            }
+            ld x = kPiL * t * r2;
+            ld w = upper_gamma_l(nu / 2.0L, x) * std::pow(r2, -nu / 2.0L);
+            mag = std::max(mag, std::fabs(w) * std::pow(r2, ld(poly_order) / 2.0L));
+            wsum += std::fabs(w);
+            for (int a = 0; a < d; ++a) {
+                sn.push_back(double(n[a]));
+                sz.push_back(double(z[a]));
+            }
+            sw.push_back(double(w));
+        }
+        if (mag > ld(tol) * total) {
+            pn->insert(pn->end(), sn.begin(), sn.end());
+            pz->insert(pz->end(), sz.begin(), sz.end());
+            pw->insert(pw->end(), sw.begin(), sw.end());
+            total += wsum;
+            below = 0;
+        } else if (++below >= 2) {
+            done = true;
+            break;
+        }
+    }
+    if (!done) fail(6, "direct-space sum did not truncate within shell budget");
+}
+
+static void enumerate_reciprocal(const HostCtx& h, double gamma_order, double tol,
+                                 std::vector<double>* pn, std::vector<double>* pq) {
+    const int d = h.d;
+    const ld nu = h.k.nu, t = h.k.split, kmax = h.kmax;
+    pn->clear();
+    pq->clear();
+    ld total = 1.0L;
+    int below = 0;
+    bool done = false;
+    for (int r = 1; r <= kMaxShells; ++r) {
+        std::vector<int> shell = integer_shell(d, r);
+        const int cnt = int(shell.size()) / d;
+        ld mag = 0.0L;
+        bool inf = false;
+        std::vector<ld> rq(cnt);
+        std::vector<double> sq(size_t(cnt) * d);
+        for (int i = 0; i < cnt; ++i) {
+            ld r2 = 0.0L;
+            for (int a = 0; a < d; ++a) {
+                ld q = 0.0L;
+                for (int b = 0; b < d; ++b) q += ld(h.B[a * d + b]) * shell[i * d + b];
+                sq[size_t(i) * d + a] = double(q);
+                r2 += q * q;
+            }
+            rq[i] = std::sqrt(r2);
+            if (rq[i] - kmax <= 0.05L) inf = true;
+        }
+        if (!inf) {
+            for (int i = 0; i < cnt; ++i) {
+                ld r_low = rq[i] - kmax;
+                ld x_low = kPiL * r_low * r_low / t;
+                ld r_pow = (nu >= d) ? rq[i] + kmax : r_low;
+                ld bound = std::fabs(upper_gamma_l(ld(gamma_order), x_low)) * std::pow(r_pow, nu - d);
+                mag = std::max(mag, bound);
+            }
+        }
+        if (inf || mag > ld(tol) * total) {
+            for (int i = 0; i < cnt; ++i)
+                for (int a = 0; a < d; ++a) pn->push_back(double(shell[i * d + a]));
+            pq->insert(pq->end(), sq.begin(), sq.end());
+            if (!inf) total += mag;
+            below = 0;
+        } else if (++below >= 2) {
+            done = true;
+            break;
+        }
+    }
+    if (!done) fail(6, "reciprocal-space sum did not truncate within shell budget");
+}
+
+void build_context(int d, const double* a, double nu, double splitting, int deriv_order,
+                   HostCtx* h) {
+    if (d < 1 || d > kMaxDim) fail(7, "dimension outside supported range 1..4");
+    for (int i = 0; i < d * d; ++i)
+        if (!std::isfinite(a[i])) fail(7, "generator contains non-finite entries");
+    h->d = d;
+    std::memset(h->A, 0, sizeof(h->A));
+    std::memset(h->B, 0, sizeof(h->B));
+    ld al[16], inv[16];
+    for (int i = 0; i < d * d; ++i) {
+        al[i] = a[i];
+        h->A[i] = a[i];
+    }
+    ld det = det_inv(d, al, inv);
+    if (!(std::fabs(det) >= 1e-300L) || !std::isfinite(double(det)))
+        fail(7, "generator matrix is singular");
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) h->B[i * d + j] = double(inv[j * d + i]);  // A^{-T}
+    CtxConst& k = h->k;
+    std::memset(&k, 0, sizeof(k));
+    k.d = d;
+    classify(nu, d, &k);
+    k.vol = double(std::fabs(det));
+    k.inv_vol = 1.0 / k.vol;
+    ld vol = std::fabs(det);
+    ld t = splitting > 0 ? ld(splitting) : std::pow(vol, -2.0L / d);
+    k.split = double(t);
+    k.c = double(kPiL / t);
+    k.log_t = double(std::log(t));
+    k.pole = std::fabs(k.nu - d) < kPoleTol ? 1 : 0;
+    // corner radius of the Brillouin zone box
+    ld kmax = 0.0L;
+    for (int corner = 0; corner < (1 << d); ++corner) {
+        ld r2 = 0.0L;
+        for (int i = 0; i < d; ++i) {
+            ld v = 0.0L;
+            for (int j = 0; j < d; ++j) v += ld(h->B[i * d + j]) * (((corner >> (d - 1 - j)) & 1) ? 0.5L : -0.5L);
+            r2 += v * v;
+        }
+        kmax = std::max(kmax, std::sqrt(r2));
+    }
+    h->kmax = double(kmax);
+    if (k.branch == kTrivial) {
+        k.const_value = k.nu == 0.0 ? -1.0 : 0.0;
+        return;
+    }
+    const ld nul = k.nu;
+    k.s = double((ld(d) - nul) / 2.0L);
+    k.pref = double(1.0L / std::tgamma(nul / 2.0L));
+    k.rfac = double(std::pow(kPiL, nul - ld(d) / 2.0L) / vol);
+    k.bconst = double(-2.0L * std::pow(kPiL * t, nul / 2.0L) / nul);
+    k.pi_over_t_pow_s = double(std::pow(kPiL / t, (ld(d) - nul) / 2.0L));
+    if (k.branch == kLogCase) {
+        int m = k.log_m;
+        ld fact = 1.0L;
+        for (int i = 2; i <= m; ++i) fact *= i;
+        k.sing_coef = double(std::pow(kPiL, 2.0L * m + ld(d) / 2.0L) / std::tgamma(ld(m) + ld(d) / 2.0L) *
+                             ((m + 1) % 2 == 0 ? 1.0L : -1.0L) / fact);
+    } else {
+        k.sing_coef = double(std::pow(kPiL, nul - ld(d) / 2.0L) * std::tgamma((ld(d) - nul) / 2.0L) /
+                             std::tgamma(nul / 2.0L));
+    }
+    enumerate_direct(*h, 0, kTermCutoff, &h->dir_n, &h->dir_z, &h->dir_w);
+    enumerate_reciprocal(*h, k.s, kTermCutoff, &h->rec_n, &h->rec_q);
+    if (deriv_order >= 2) {
+        // Hessian sets: the derivative-table enumerators of L/epstein.py:376-377
+        // specialised to second order (z^alpha weight |z|^2, gamma order s + 2).
+        h->has_hess = 1;
+        enumerate_direct(*h, 2, kTermCutoff, &h->hdir_n, &h->hdir_z, &h->hdir_w);
+        enumerate_reciprocal(*h, k.s + 2.0, kTermCutoff, &h->hrec_n, &h->hrec_q);
+    }
+}
+
+// Rigorous lower bound of x = c |k + q|^2 over k in the BZ box and q != 0:
+// ||kappa + n||_inf >= 1/2 gives |B (kappa + n)|^2 >= sigma_min(B)^2 / 4.
+double table_x_lo(const HostCtx& h) {
+    const int d = h.d;
+    // smallest eigenvalue of B^T B by cyclic Jacobi
+    ld m[kMaxDim][kMaxDim];
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) {
+            ld s = 0.0L;
+            for (int r = 0; r < d; ++r) s += ld(h.B[r * d + i]) * h.B[r * d + j];
+            m[i][j] = s;
+        }
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        ld off = 0.0L;
+        for (int p = 0; p < d; ++p)
+            for (int q = p + 1; q < d; ++q) off += m[p][q] * m[p][q];
+        if (off < 1e-36L) break;
+        for (int p = 0; p < d; ++p)
+            for (int q = p + 1; q < d; ++q) {
+                if (m[p][q] == 0.0L) continue;
+                ld theta = (m[q][q] - m[p][p]) / (2.0L * m[p][q]);
+                ld tt = (theta >= 0 ? 1.0L : -1.0L) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0L));
+                ld cs = 1.0L / std::sqrt(tt * tt + 1.0L), sn = tt * cs;
+                for (int r = 0; r < d; ++r) {
+                    ld a1 = m[r][p], a2 = m[r][q];
+                    m[r][p] = cs * a1 - sn * a2;
+                    m[r][q] = sn * a1 + cs * a2;
+                }
+                for (int r = 0; r < d; ++r) {
+                    ld a1 = m[p][r], a2 = m[q][r];
+                    m[p][r] = cs * a1 - sn * a2;
+                    m[q][r] = sn * a1 + cs * a2;
+                }
+            }
+    }
+    ld lmin = m[0][0];
+    for (int i = 1; i < d; ++i) lmin = std::min(lmin, m[i][i]);
+    return double(ld(h.k.c) * lmin / 4.0L * (1.0L - 1e-9L));
+}
+
+// ---------------------------------------------------------------------------
+// Piecewise Chebyshev-interpolant tables of f_j(x) = scale_j * E_{p_j}(x).
+namespace {
+
+struct Fn {
+    ld p, scale;
+    ld operator()(ld x) const { return scale * expint<ld>(p, x); }
+};
+
+// Chebyshev interpolation at kNC first-kind nodes, converted to monomials in tau.
+void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
+    const int N = kNC;
+    ld fv[kNC];
+    ld mid = 0.5L * (x0 + x1), half = 0.5L * (x1 - x0);
+    for (int i = 0; i < N; ++i) {
+        ld tau = std::cos(kPiL * (i + 0.5L) / N);
+        fv[i] = f(mid + half * tau);
+    }
+    ld ak[kNC];
+    for (int k = 0; k < N; ++k) {
+        ld s = 0.0L;
+        for (int i = 0; i < N; ++i) s += fv[i] * std::cos(kPiL * k * (i + 0.5L) / N);
+        ak[k] = (k == 0 ? 1.0L : 2.0L) * s / N;
+    }
+    // monomial coefficients of T_k
+    ld tk[kNC][kNC] = {};
+    tk[0][0] = 1.0L;
+    if (N > 1) tk[1][1] = 1.0L;
+    for (int k = 2; k < N; ++k)
+        for (int j = 0; j < N; ++j)
+            tk[k][j] = (j > 0 ? 2.0L * tk[k - 1][j - 1] : 0.0L) - tk[k - 2][j];
+    for (int j = 0; j < N; ++j) {
+        ld c = 0.0L;
+        for (int k = 0; k < N; ++k) c += ak[k] * tk[k][j];
+        out[j] = double(c);
+    }
+}
+
+ld eval_piece(const double* c, ld tau) {
+    // evaluate as the device does: Horner in double
+    double t = double(tau), acc = c[kNC - 1];
+    for (int j = kNC - 2; j >= 0; --j) acc = std::fma(acc, t, c[j]);
+    return acc;
+}
+
+}  // namespace
+
+void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
+                 double rfac_pref, HostTable* out) {
+    (void)c;
+    out->nfunc = nfunc;
+    for (int j = 0; j < nfunc; ++j) {
+        out->p[j] = p[j];
+        out->scale[j] = scale[j];
+    }
+    std::vector<Fn> fns;
+    for (int j = 0; j < nfunc; ++j) fns.push_back(Fn{ld(p[j]), ld(scale[j])});
+    // upper end: every function (times the |y|^2 factor of the Hessian terms) is
+    // below 1e-24 of the unit scale; terms past it are exactly zero in the kernel.
+    const ld hb = kBinWidth;
+    ld x_hi = x_lo;
+    for (int b = 0; b < 1000; ++b) {
+        ld x = ld(x_lo) + hb * b;
+        ld worst = 0.0L;
+        for (const Fn& f : fns) worst = std::max(worst, std::fabs(f(x)) * (1.0L + 4.0L * x));
+        x_hi = x;
+        if (worst * std::fabs(ld(rfac_pref)) < 1e-24L && x > 8.0L) break;
+    }
+    const int nbins = int(std::lround((x_hi - ld(x_lo)) / hb));
+    out->x_lo = x_lo;
+    out->inv_hb = double(1.0L / hb);
+    out->nbins = nbins;
+    out->x_hi = double(ld(x_lo) + hb * nbins);
+    out->dir.assign(nbins, 0);
+    out->coef.clear();
+    out->max_rel_err = 0.0;
+    int npieces = 0;
+    const int kMaxLevel = 8;
+    for (int b = 0; b < nbins; ++b) {
+        ld b0 = ld(x_lo) + hb * b;
+        int level = 0;
+        bool ok = false;
+        std::vector<double> coefs;
+        double worst_err = 0.0;
+        for (level = 0; level <= kMaxLevel; ++level) {
+            const int nsub = 1 << level;
+            coefs.assign(size_t(nsub) * nfunc * kNCP, 0.0);
+            worst_err = 0.0;
+            bool good = true;
+            for (int sidx = 0; sidx < nsub && good; ++sidx) {
+                ld x0 = b0 + hb * sidx / nsub, x1 = b0 + hb * (sidx + 1) / nsub;
+                for (int j = 0; j < nfunc && good; ++j) {
+                    double* cf = &coefs[(size_t(sidx) * nfunc + j) * kNCP];
+                    fit_piece(fns[j], x0, x1, cf);
+                    for (int tidx = 0; tidx <= 16; ++tidx) {
+                        ld tau = -1.0L + 2.0L * tidx / 16.0L;
+                        ld xx = 0.5L * (x0 + x1) + 0.5L * (x1 - x0) * tau;
+                        ld truth = fns[j](xx);
+                        ld approx = eval_piece(cf, tau);
+                        double rel = double(std::fabs(approx - truth) / std::max(std::fabs(truth), 1e-300L));
+                        worst_err = std::max(worst_err, rel);
+                        if (rel > 6e-16) good = false;
+                    }
+                }
+            }
+            if (good) {
+                ok = true;
+                break;
+            }
+        }
+        if (!ok) {
+            out->dir[b] = kDirectMarker;  // evaluate E_p directly in this bin
+            continue;
+        }
+        out->max_rel_err = std::max(out->max_rel_err, worst_err);
+        out->dir[b] = (npieces << 4) | level;
+        out->coef.insert(out->coef.end(), coefs.begin(), coefs.end());
+        npieces += 1 << level;
+    }
+    out->npieces = npieces;
+}
+
+// Gauss-Legendre nodes/weights on [-1, 1] by Newton iteration on P_n (long double).
+void gauss_legendre(int n, std::vector<double>* xs, std::vector<double>* ws) {
+    xs->assign(n, 0.0);
+    ws->assign(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        ld x = std::cos(kPiL * (i + 0.75L) / (n + 0.5L));
+        ld dp = 0.0L;
+        for (int it = 0; it < 100; ++it) {
+            ld p0 = 1.0L, p1 = x;
+            for (int k = 2; k <= n; ++k) {
+                ld p2 = ((2.0L * k - 1.0L) * x * p1 - (k - 1.0L) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            if (n == 1) { p1 = x; p0 = 1.0L; }
+            dp = n * (x * p1 - p0) / (x * x - 1.0L);
+            ld dx = p1 / dp;
+            x -= dx;
+            if (std::fabs(dx) < 1e-21L) break;
+        }
+        ld p0 = 1.0L, p1 = x;
+        for (int k = 2; k <= n; ++k) {
+            ld p2 = ((2.0L * k - 1.0L) * x * p1 - (k - 1.0L) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        if (n == 1) { p1 = x; p0 = 1.0L; }
+        dp = n * (x * p1 - p0) / (x * x - 1.0L);
+        // ascending order (numpy leggauss order)
+        (*xs)[n - 1 - i] = double(x);
+        (*ws)[n - 1 - i] = double(2.0L / ((1.0L - x * x) * dp * dp));
+    }
+}
+
+}  // namespace lz

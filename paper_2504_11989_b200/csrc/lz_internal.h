@@ -1,0 +1,116 @@
+// Internal data structures shared by the host plan builder (context.cpp) and
+// the sm_100a kernels (kernels.cu).  Not part of the public C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace lz {
+
+// Branch labels of L/epstein.py:45-47.
+enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
+
+constexpr int kMaxDim = 4;     // L/lattice.py:20
+constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
+constexpr int kDeg = 10;       // degree of the piecewise polynomials (kDeg+1 coefficients)
+constexpr int kNC = kDeg + 1;
+constexpr int kNCP = 12;       // padded coefficient stride (16-byte aligned double2 loads)
+constexpr double kBinWidth = 0.5;   // directory bin width in x = c |y|^2
+constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
+
+// ---------------------------------------------------------------------------
+// Per-(lattice, nu) constants of the Crandall split (L/epstein.py:99-122, 202-259).
+struct CtxConst {
+    int branch;
+    int log_m;
+    int pole;            // |nu - d| < 1e-10: simple pole of the continuation at k in Lambda*
+    int d;
+    double nu, s;        // s = s_rec = (d - nu)/2
+    double pref, rfac, bconst;
+    double vol, inv_vol, split, c;   // c = pi / split
+    double log_t;        // log(split)
+    double pi_over_t_pow_s;          // (pi/t)^s, generic t0_reg prefactor
+    double sing_coef;
+    double const_value;  // trivial branch value
+};
+
+// Piecewise-polynomial table of up to 4 functions f_j(x) = scale_j E_{p_j}(x),
+// sharing one directory over x in [x_lo, x_hi).
+struct DevTable {
+    const int* dir;        // nbins entries: (first_piece << 4) | L ; L == 15 -> direct
+    const double* coef;    // [piece][nfunc][kNC], monomials in tau in [-1, 1]
+    int nbins, nfunc, npieces, pad_;
+    double x_lo, inv_hb, x_hi;
+    double p[4], scale[4]; // for the direct fallback
+};
+
+// A device-resident evaluation plan: union point sets of one lattice plus the
+// constants of the contexts that are evaluated together at every node.
+struct DevPlan {
+    int d;
+    int nctx;          // contexts (plain zeta) evaluated per node
+    int hess;          // 1 if context slot `hess_slot` also needs its Hessian
+    int hess_slot;
+    int n_dir, n_rec;
+    int nw;            // direct weight channels per point
+    int pad_;
+    double A[16];      // generator, row-major (columns = basis vectors)
+    double B[16];      // A^{-T}, row-major
+    const double* dir_n;   // [n_dir][d] integer coordinates (as double)
+    const double* dir_w;   // [n_dir][nw] weights: nctx plain channels, then (hess) d(d+1)/2
+    const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0
+    DevTable tab;          // functions: nctx plain F_j, then (hess) F', F''
+    CtxConst ctx[kMaxCtx];
+    CtxConst hctx;         // constants of the Hessian context
+};
+
+// Fixed Duffy grid description (device arrays + patch decomposition).
+struct DevGrid {
+    const double* u;   // radial nodes in (0, 1/2)
+    const double* wu;  // radial weights incl. grading Jacobian and u^{d-1}
+    const double* v;   // angular nodes on [0, 1/2]
+    const double* wv;  // angular weights
+    int n_u, n_v, n_cell, pu, pv, npu, npv, nv2;
+    int64_t tile_lo, tile_hi, n_patch;
+};
+
+// Host-side mirror of one context: constants + enumerated sets (host memory).
+struct HostCtx {
+    int d;
+    double A[16], B[16];
+    CtxConst k;
+    double kmax;
+    // plain evaluation sets (L/epstein.py:156-198)
+    std::vector<double> dir_n, dir_z, dir_w;   // n (int coords), z = A n, weights
+    std::vector<double> rec_n, rec_q;          // n, q = B n
+    // widened sets for the Hessian (poly_order = 2, gamma order s + 2)
+    int has_hess = 0;
+    std::vector<double> hdir_n, hdir_z, hdir_w;
+    std::vector<double> hrec_n, hrec_q;
+};
+
+struct HostTable {
+    std::vector<int> dir;
+    std::vector<double> coef;
+    int nbins = 0, nfunc = 0, npieces = 0;
+    double x_lo = 0, inv_hb = 0, x_hi = 0;
+    double p[4] = {0, 0, 0, 0}, scale[4] = {0, 0, 0, 0};
+    double max_rel_err = 0;   // measured during the build
+};
+
+// Errors raised by the host builder carry an lz status code.
+struct Error {
+    int code;
+    std::string msg;
+};
+
+// context.cpp
+void build_context(int d, const double* a, double nu, double splitting, int deriv_order,
+                   HostCtx* out);
+void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
+                 double rfac_pref, HostTable* out);
+double table_x_lo(const HostCtx& h);
+void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* w);  // on [-1, 1]
+
+}  // namespace lz

@@ -1,0 +1,301 @@
+"""Epstein zeta functions on Bravais lattices — drop-in for L/epstein.py.
+
+``Z(nu, k) = sum'_{z in Lambda} exp(-2 pi i z.k) |z|^-nu`` (meromorphically
+continued), evaluated with the reference's theta split (L/epstein.py:1-29):
+a direct sum of incomplete-gamma weights times phases, a reciprocal sum of
+``|k+q|^(nu-d) Gamma((d-nu)/2, pi |k+q|^2 / t)`` and the explicit singularity
+``shat``.  Context construction (point sets, constants, reciprocal-summand
+tables) happens once in the native library; every evaluation runs on the GPU
+through the C ABI (``lz_zeta*``).  The public names, signatures, branch
+semantics, error classes and scalar/batch conventions follow the reference.
+
+Beyond the reference: :meth:`EpsteinContext.zeta_hessian` and
+:meth:`EpsteinContext.polynomial_weighted` give the Cartesian-derivative
+(polynomial-weighted) zeta ``M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k}
+= -d_a d_b Z_nu(k) / (4 pi^2)`` needed for the ATM dot-product term.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+
+from . import _native as N
+from .lattice import Lattice
+
+GENERIC = "generic"
+LOG_CASE = "log_case"
+TRIVIAL = "trivial"
+_BRANCHES = {0: GENERIC, 1: LOG_CASE, 2: TRIVIAL}
+
+_BRANCH_TOL = 1e-12
+TWO_PI = 2.0 * math.pi
+
+
+def classify_exponent(nu: float, d: int):
+    """(branch, snapped nu, log index m or None), as L/epstein.py:58-70."""
+    if not np.isfinite(nu):
+        raise ValueError("exponent must be finite")
+    if abs(nu) > 100.0:
+        raise ValueError("exponent magnitude above 100 is not supported")
+    m = round((nu - d) / 2.0)
+    if m >= 0 and abs(nu - (d + 2 * m)) < _BRANCH_TOL:
+        return LOG_CASE, float(d + 2 * m), int(m)
+    j = round(-nu / 2.0)
+    if j >= 0 and abs(nu + 2 * j) < _BRANCH_TOL:
+        return TRIVIAL, float(-2 * j), None
+    return GENERIC, float(nu), None
+
+
+def _as_batch(k, d):
+    k = np.asarray(k, dtype=np.float64)
+    single = k.ndim == 1
+    k2 = np.ascontiguousarray(np.atleast_2d(k))
+    if k2.shape[-1] != d:
+        raise ValueError(f"k must have trailing dimension {d}, got shape {k.shape}")
+    if not np.all(np.isfinite(k2)):
+        raise ValueError("k contains non-finite entries")
+    return k2.reshape(-1, d), single, k.shape[:-1] if k.ndim > 1 else ()
+
+
+class EpsteinContext:
+    """Per-(lattice, exponent) device-resident evaluation data (L/epstein.py:93-122).
+
+    Construct through :func:`epstein_context`.  Immutable after construction;
+    safe to share between threads.
+    """
+
+    def __init__(self, lattice: Lattice, nu: float, splitting: float | None = None,
+                 deriv_order: int = 2, device: int | None = None):
+        self.lattice = lattice
+        d = lattice.d
+        self.d = d
+        p = N.CtxParams()
+        p.d = d
+        flat = np.ascontiguousarray(lattice.a, dtype=np.float64).ravel()
+        for i, v in enumerate(flat):
+            p.a[i] = float(v)
+        p.nu = float(nu)
+        p.splitting = float(splitting) if splitting is not None else -1.0
+        p.deriv_order = int(deriv_order)
+        self.device = N.current_device() if device is None else device
+        h = C.c_void_p()
+        N.check(N.lib().lz_ctx_create(C.byref(p), self.device, C.byref(h)), "epstein context")
+        self._h = h
+        info = N.CtxInfo()
+        N.lib().lz_ctx_get_info(h, C.byref(info))
+        self.info = info
+        self.branch = _BRANCHES[info.branch]
+        self.nu = info.nu
+        self.log_m = info.log_m if info.branch == 1 else None
+        self.vol = info.vol
+        self.split = info.split
+        self._lock = threading.Lock()
+        self._taylor_cache: dict = {}
+        if self.branch == TRIVIAL:
+            self.const_value = info.const_value
+            return
+        self.s_rec = info.s_rec
+        self.pref = info.pref
+        self.rfac = info.rfac
+        self.bconst = info.bconst
+        self.kmax = info.kmax
+        self._bz = lattice.brillouin_zone()
+        self.dir_pts = self._points(0).reshape(-1, d)
+        self.dir_w = self._points(1)
+        self.rec_pts = self._points(2).reshape(-1, d)
+        self.rec_norm2 = np.einsum("ij,ij->i", self.rec_pts, self.rec_pts)
+        self.has_hessian = info.n_rec_h > 0
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and N._lib is not None:
+            try:
+                N.lib().lz_ctx_destroy(h)
+            except Exception:
+                pass
+
+    def _points(self, which):
+        n = C.c_int64(0)
+        N.lib().lz_ctx_get_points(self._h, which, None, 0, C.byref(n))
+        out = np.empty(n.value, dtype=np.float64)
+        if n.value:
+            N.lib().lz_ctx_get_points(self._h, which, N.dptr(out), n.value, C.byref(n))
+        return out
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- evaluation (GPU) -------------------------------------------------------------
+    def _eval(self, k, flags):
+        kb, single, shape = _as_batch(k, self.d)
+        if self.branch == TRIVIAL:
+            out = np.full(len(kb), self.const_value) if not (flags & N.SINGULAR_ONLY) else np.zeros(len(kb))
+        else:
+            N.require_cuda("Epstein zeta evaluation")
+            out = np.empty(len(kb), dtype=np.float64)
+            if len(kb):
+                N.check(N.lib().lz_zeta_host(self._h, N.dptr(kb), len(kb), N.dptr(out), flags),
+                        "zeta")
+        if single:
+            return float(out[0])
+        return out.reshape(shape) if shape else out
+
+    def zeta_device(self, k, out=None, flags: int = 0, lanes_per_point: int = 0, stream=None):
+        """Zero-copy path: ``k`` a CUDA torch tensor (n, d) float64; returns a CUDA tensor."""
+        import torch
+        N.require_cuda("Epstein zeta evaluation")
+        k = k.contiguous()
+        n = k.shape[0]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=k.device)
+        status = torch.zeros(1, dtype=torch.int32, device=k.device)
+        st = stream if stream is not None else torch.cuda.current_stream(k.device).cuda_stream
+        N.check(N.lib().lz_zeta(self._h, k.data_ptr(), n, out.data_ptr(), flags, lanes_per_point,
+                                status.data_ptr(), st), "zeta")
+        return out, status
+
+    def singular_coef(self) -> float:
+        """Coefficient of shat without the |k| powers (L/epstein.py:202-215)."""
+        if self.branch == TRIVIAL:
+            return 0.0
+        return self.info.singular_coef
+
+    def singular(self, k) -> np.ndarray:
+        """shat(nu, k) (L/epstein.py:217-231); no BZ reduction, batch output."""
+        kb = np.atleast_2d(np.asarray(k, dtype=float))
+        rho = np.einsum("ij,ij->i", kb, kb)
+        if self.branch == TRIVIAL:
+            return np.zeros(len(rho))
+        if self.branch == LOG_CASE and np.any(rho == 0.0):
+            raise ValueError("singular part undefined at k = 0 in the log case")
+        if self.branch == GENERIC and self.nu < self.d and np.any(rho == 0.0):
+            raise ValueError("singular part diverges at k = 0 for nu < d")
+        out = self._eval(kb, N.NO_REDUCE | N.SINGULAR_ONLY)
+        return np.atleast_1d(out)
+
+    def reg_zeta(self, k):
+        """Z_reg(nu, k) on a batch (L/epstein.py:261-289); k is not reduced."""
+        return self._eval(k, N.NO_REDUCE | N.REG_ONLY)
+
+    def zeta(self, k):
+        """Z(nu, k) = Z_reg + shat/V with the k = 0 continuation convention (L/epstein.py:291-320)."""
+        return self._eval(k, 0)
+
+    def zeta_at_zero(self) -> float:
+        """Z(nu, 0) through the continuation in nu; pole at nu = d (L/epstein.py:322-324)."""
+        return float(self.zeta(np.zeros(self.d)))
+
+    # -- Cartesian-derivative (polynomial-weighted) zeta -----------------------------
+    def zeta_hessian(self, k) -> np.ndarray:
+        """d_a d_b Z_nu(k) as (..., d, d); k must not sit on the reciprocal lattice."""
+        if self.branch == TRIVIAL:
+            kb, single, shape = _as_batch(k, self.d)
+            out = np.zeros((len(kb), self.d, self.d))
+            return out[0] if single else out.reshape(shape + (self.d, self.d))
+        if not self.has_hessian:
+            raise ValueError("context built without Hessian tables (deriv_order < 2)")
+        kb, single, shape = _as_batch(k, self.d)
+        N.require_cuda("Epstein zeta Hessian")
+        ns = self.d * (self.d + 1) // 2
+        tri = np.empty((len(kb), ns), dtype=np.float64)
+        if len(kb):
+            N.check(N.lib().lz_zeta_hessian_host(self._h, N.dptr(kb), len(kb), N.dptr(tri)),
+                    "zeta hessian")
+        full = np.empty((len(kb), self.d, self.d))
+        c = 0
+        for a in range(self.d):
+            for b in range(a, self.d):
+                full[:, a, b] = tri[:, c]
+                full[:, b, a] = tri[:, c]
+                c += 1
+        if single:
+            return full[0]
+        return full.reshape(shape + (self.d, self.d)) if shape else full
+
+    def polynomial_weighted(self, k) -> np.ndarray:
+        """M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k} = -Hess Z_nu(k) / (4 pi^2)."""
+        return -self.zeta_hessian(k) / (4.0 * math.pi ** 2)
+
+    # -- derivatives of the regularized part at k = 0 (host tables, L/epstein.py:347-415)
+    def reg_derivatives(self, order: int) -> "RegZetaTaylor":
+        if order % 2 != 0:
+            raise ValueError("derivative order must be even")
+        if order > 12:
+            raise ValueError("derivative order above 12 is not supported")
+        with self._lock:
+            if order not in self._taylor_cache:
+                from .taylor import build_reg_derivatives
+                self._taylor_cache[order] = build_reg_derivatives(self, order)
+            return self._taylor_cache[order]
+
+
+@dataclass(frozen=True)
+class RegZetaTaylor:
+    """Partial derivatives of Z_reg at k = 0 up to an even total order (L/epstein.py:436-466)."""
+
+    lattice: Lattice
+    nu: float
+    order: int
+    derivs: dict
+
+    def directional_coeff(self, w, k: int):
+        """(w.grad)^{2k} Z_reg(0) / (2k)! for one direction or a batch of rows."""
+        if 2 * k > self.order:
+            raise ValueError(f"order {2 * k} exceeds table order {self.order}")
+        w = np.asarray(w, dtype=float)
+        single = w.ndim == 1
+        w = np.atleast_2d(w)
+        total = 2 * k
+        acc = np.zeros(len(w))
+        for alpha, val in self.derivs.items():
+            if sum(alpha) != total or val == 0.0:
+                continue
+            mult = math.factorial(total)
+            for a in alpha:
+                mult //= math.factorial(a)
+            acc += mult * np.prod(w ** np.array(alpha), axis=1) * val
+        acc /= math.factorial(total)
+        return acc[0] if single else acc
+
+
+@lru_cache(maxsize=4096)
+def epstein_context(lattice: Lattice, nu: float, splitting: float | None = None) -> EpsteinContext:
+    """Memoized evaluation context for (lattice, exponent) (L/epstein.py:469-472)."""
+    return EpsteinContext(lattice, float(nu), splitting)
+
+
+def epstein_zeta(lattice: Lattice, nu: float, k, reg: bool = False):
+    """Z(nu, k), or its regularized part with ``reg=True`` (L/epstein.py:478-481)."""
+    ctx = epstein_context(lattice, nu)
+    return ctx.reg_zeta(k) if reg else ctx.zeta(k)
+
+
+def singular_part(lattice: Lattice, nu: float, k):
+    """shat(nu, k) (no 1/V factor) (L/epstein.py:484-486)."""
+    return epstein_context(lattice, nu).singular(k)
+
+
+def regularized_zeta(lattice: Lattice, nu: float, k):
+    """Z_reg(nu, k) = Z(nu, k) - shat(nu, k)/V (L/epstein.py:489-491)."""
+    return epstein_context(lattice, nu).reg_zeta(k)
+
+
+def reg_zeta_derivatives(lattice: Lattice, nu: float, order: int) -> RegZetaTaylor:
+    """Partial derivatives of Z_reg at k = 0 (L/epstein.py:494-496)."""
+    return epstein_context(lattice, nu).reg_derivatives(order)
+
+
+def directional_taylor_coeff(taylor: RegZetaTaylor, w, k: int):
+    """Coefficient of u^(2k) in Z_reg(u w) around u = 0 (L/epstein.py:499-501)."""
+    return taylor.directional_coeff(w, k)
+
+
+def polynomial_weighted_zeta(lattice: Lattice, nu: float, k):
+    """M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k} (the ATM dot-product building block)."""
+    return epstein_context(lattice, nu).polynomial_weighted(k)

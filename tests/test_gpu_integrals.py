@@ -1,0 +1,140 @@
+"""GPU parity of the fused Duffy-grid integral kernels (product of zetas, ATM integrand)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2504_11989_b200 import named_lattice
+from paper_2504_11989_b200.manybody import ATMGrid, atm_cohesive_energy, atm_integrals, many_body_zeta
+from paper_2504_11989_b200.quadrature import QuadratureConfig, atm_plan, fixed_grid_integral, integrate_product
+
+pytestmark = pytest.mark.gpu
+SUM_TOL = 1e-10  # BASELINE north_star: <= 1e-10 relative on each lattice sum
+
+
+def test_fixed_grids_vs_reference_nodes(golden):
+    """Same node set as the reference zeta evaluated on it (golden): node-sum parity."""
+    for fg in golden["fixed_grid"]:
+        lat = named_lattice(fg["lattice"])
+        v = fixed_grid_integral(lat, fg["nus"], fg["n_u"], fg["n_v"], fg["grading"])
+        assert abs(v - fg["value"]) <= 1e-12 * abs(fg["value"]), (fg, v)
+
+
+def test_c2_three_body_square(golden):
+    """Config 2: zeta^(3)(3,3,3) on Z^2, Duffy 64 x 64 per cell, vs the reference's adaptive value."""
+    cfg = QuadratureConfig(grid_u=64, grid_v=64)
+    v, err = integrate_product(named_lattice("square"), (3, 3, 3), cfg)
+    ref = golden["c2"]["value"]
+    assert abs(v - ref) <= SUM_TOL * abs(ref), (v, ref)
+    assert err < 1e-9 * abs(v)
+
+
+def test_c2_direct_sum_crosscheck():
+    """Truncated direct summation |x|,|y| <= R by FFT convolution (BASELINE C2 cross-check)."""
+    R = 200
+    n = np.arange(-R, R + 1)
+    X, Y = np.meshgrid(n, n, indexing="ij")
+    r2 = (X * X + Y * Y).astype(float)
+    f = np.zeros_like(r2)
+    f[r2 > 0] = r2[r2 > 0] ** -1.5
+    size = 2 * (2 * R + 1)
+    F = np.fft.rfft2(f, s=(size, size))
+    conv = np.fft.irfft2(F * F, s=(size, size))
+    # sum_{x,y} f(x) f(y-x) f(y): conv[y] = sum_x f(x) f(y - x), shifted by 2R
+    g = conv[R:R + 2 * R + 1, R:R + 2 * R + 1]
+    direct = float(np.sum(g * f))
+    v, _ = integrate_product(named_lattice("square"), (3, 3, 3), QuadratureConfig(grid_u=64, grid_v=64))
+    assert abs(direct - v) / v < 2e-9  # truncation error of R = 200 (measured 1.35e-9)
+
+
+def test_c4_51_body_chain(golden_integrals):
+    """Config 4: 51-fold product of Z_4 on Z^2, Duffy 256 x 256."""
+    cfg = QuadratureConfig(grid_u=256, grid_v=256, estimate_error=False)
+    v, _ = integrate_product(named_lattice("square"), [4.0] * 51, cfg)
+    ref = golden_integrals["c4"]["value"]
+    assert abs(v - ref) <= SUM_TOL * abs(ref), (v, ref)
+
+
+def test_hex51_paper_case(golden_integrals):
+    cfg = QuadratureConfig(grid_u=256, grid_v=256, estimate_error=False)
+    v, _ = integrate_product(named_lattice("hex"), [3.0] * 51, cfg)
+    ref = golden_integrals["hex51"]["value"]
+    assert abs(v - ref) <= SUM_TOL * abs(ref), (v, ref)
+
+
+def test_small_products(golden):
+    for rec in golden["integrals_small"]:
+        lat = named_lattice(rec["lattice"])
+        cfg = QuadratureConfig(grid_u=96, grid_v=96, force_integral=True)
+        v, _ = integrate_product(lat, rec["nus"], cfg)
+        assert abs(v - rec["value"]) <= SUM_TOL * abs(rec["value"]), (rec, v)
+
+
+def test_two_body_identity():
+    lat = named_lattice("hex")
+    cfg = QuadratureConfig(grid_u=96, grid_v=96, force_integral=True)
+    res = many_body_zeta(lat, (4, 5), cfg)
+    ref = many_body_zeta(lat, (4, 5)).value  # Cor. 2.7 short-circuit Z(9, 0)
+    assert abs(res.value - ref) <= 1e-12 * abs(ref)
+    assert many_body_zeta(lat, (5,)).value == 0.0
+
+
+def test_atm_grid_vs_oracle():
+    """The fused ATM kernel against the long-double oracle on the same small grid."""
+    for name in ("fcc", "bcc", "square", "integer_1d"):
+        lat = named_lattice(name)
+        g = ATMGrid(8, 6, 3)
+        res = atm_integrals(lat, g)
+        s = O.atm_grid(lat.a, 8, 6, 3)
+        sc = 2.0 ** lat.d
+        assert abs(res.zeta333 - sc * s[0]) <= 1e-12 * abs(sc * s[0]), name
+        assert abs(res.dot_term - sc * s[1]) <= 1e-12 * max(1.0, abs(sc * s[1])), name
+
+
+@pytest.mark.parametrize("name,key", [("fcc", "fcc"), ("bcc", "bcc")])
+def test_c3_atm_energy(golden_integrals, name, key):
+    """Config 3 (fcc; bcc for the phase scan): 12 x 128 x 128^2 graded Duffy nodes."""
+    res = atm_integrals(named_lattice(name), ATMGrid(128, 128, 3))
+    ref = golden_integrals[key]
+    assert abs(res.energy - ref["atm"]) <= SUM_TOL * abs(ref["atm"]), (res.energy, ref["atm"])
+    assert abs(res.zeta333 - ref["z333"]) <= SUM_TOL * abs(ref["z333"])
+
+
+@pytest.mark.parametrize("name,key", [("integer_1d", "integer_1d"), ("square", "square")])
+def test_atm_low_dimensions(golden_integrals, name, key):
+    lat = named_lattice(name)
+    g = ATMGrid(256, 256, 3)
+    e = atm_cohesive_energy(lat, grid=g)
+    ref = golden_integrals[key]["atm"]
+    assert abs(e - ref) <= SUM_TOL * abs(ref), (e, ref)
+
+
+def test_atm_scaling_homogeneity():
+    lat = named_lattice("fcc")
+    g = ATMGrid(48, 24, 3)
+    e1 = atm_cohesive_energy(lat, grid=g)
+    e2 = atm_cohesive_energy(lat.scaled(1.3), grid=g)
+    assert abs(e2 * 1.3 ** 9 - e1) <= 1e-12 * abs(e1)
+
+
+def test_tile_sharding_bit_identical():
+    """Slot-disjoint partials: any split of the tile range gives bit-identical sums."""
+    import torch
+
+    from paper_2504_11989_b200.quadrature import Plan
+    lat = named_lattice("fcc")
+    plan = atm_plan(lat)
+    nn, nt = plan.tiles(32, 16, 3)
+    full = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
+    plan.integrate_device(full, 32, 16, 3)
+    for world in (2, 3, 8):
+        parts = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
+        for r in range(world):
+            lo, hi = nt * r // world, nt * (r + 1) // world
+            buf = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
+            plan.integrate_device(buf, 32, 16, 3, lo, hi)
+            parts += buf  # exact: disjoint slots
+        assert torch.equal(parts, full)
+    o1 = torch.zeros(2, dtype=torch.float64, device="cuda")
+    Plan.reduce_device(full, nt, 2, o1)
+    res = atm_integrals(lat, ATMGrid(32, 16, 3))
+    assert float(o1[0]) * 8 == res.zeta333

@@ -1,0 +1,161 @@
+"""GPU parity of the batched zeta / Hessian kernels through the C ABI (needs a B200)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import emetric
+from oracle import oracle as O
+from paper_2504_11989_b200 import PoleError, named_lattice
+from paper_2504_11989_b200 import _native as N
+from paper_2504_11989_b200.epstein import EpsteinContext, epstein_context, polynomial_weighted_zeta
+
+pytestmark = pytest.mark.gpu
+ZETA_TOL = 1e-12  # BASELINE north_star: <= 1e-12 per zeta value (E = min(abs, rel))
+
+
+def _ctx(name, nu):
+    return EpsteinContext(named_lattice(name), nu, device=0)
+
+
+def test_native_library_is_loaded():
+    assert N.device_count() >= 1
+    assert "sm_100a" in N.lib().lz_version().decode()
+
+
+def test_c1_parity_all_points(golden):
+    """Config 1: Z^2, nu = 3.5, 4096 seeded k; every point vs the reference (golden)."""
+    sq = named_lattice("square")
+    k = np.random.default_rng(0).uniform(-0.5, 0.5, size=(4096, 2))
+    z = _ctx("square", 3.5).zeta(k)
+    e = emetric(z, golden["c1"]["zeta"])
+    assert e.max() <= ZETA_TOL, e.max()
+    assert abs(math.fsum(z) - golden["c1"]["zeta_fsum"]) <= 1e-10 * abs(golden["c1"]["zeta_fsum"])
+    # and vs the long-double oracle
+    assert emetric(z, O.zeta(sq.a, 3.5, k)).max() <= ZETA_TOL
+
+
+@pytest.mark.parametrize("idx", range(29))
+def test_zeta_cases_vs_reference(golden, idx):
+    c = golden["cases"][idx]
+    lat = named_lattice(c["lattice"])
+    ctx = EpsteinContext(lat, c["nu"], device=0)
+    k = np.array(c["k"]).reshape(-1, lat.d)
+    z = ctx.zeta(k)
+    assert emetric(z, c["zeta"]).max() <= ZETA_TOL
+    inside = np.ones(len(k), bool)
+    inside[3] = False  # reg_zeta: k must lie in the BZ closure
+    zr = ctx.reg_zeta(k)
+    assert emetric(zr[inside], np.array(c["reg_zeta"])[inside]).max() <= ZETA_TOL
+    if c["branch"] != "trivial":
+        # out-of-contract point: same truncated sum as the oracle
+        assert emetric(zr[3:4], O.zeta(lat.a, c["nu"], k[3:4], 3)).max() <= 1e-9
+        if c.get("zeta_at_zero") == "pole":
+            with pytest.raises(PoleError):
+                ctx.zeta_at_zero()
+        else:
+            assert emetric(ctx.zeta_at_zero(), c["zeta_at_zero"]) <= ZETA_TOL
+
+
+def test_scalar_and_shapes():
+    ctx = _ctx("square", 3.5)
+    k = np.array([0.1, 0.2])
+    v = ctx.zeta(k)
+    assert isinstance(v, float)
+    assert ctx.zeta(np.zeros((0, 2))).shape == (0,)
+    kk = np.random.default_rng(5).uniform(-0.5, 0.5, size=(3, 7, 2))
+    out = ctx.zeta(kk)
+    assert out.shape == (3, 7)
+    assert np.array_equal(out.ravel(), ctx.zeta(kk.reshape(-1, 2)))
+    with pytest.raises(ValueError):
+        ctx.zeta(np.array([[np.nan, 0.0]]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 1000, 4097])
+def test_ragged_batches_bitwise(n):
+    """Batch size and lane split never change a point's value beyond rounding."""
+    ctx = _ctx("fcc", 3.0)
+    lat = named_lattice("fcc")
+    k = np.random.default_rng(n).uniform(-0.5, 0.5, size=(n, 3)) @ lat.a_inv_t.T
+    z = ctx.zeta(k)
+    zo = O.zeta(lat.a, 3.0, k)
+    assert emetric(z, zo).max() <= ZETA_TOL
+
+
+def test_lanes_per_point_agree():
+    import torch
+    ctx = _ctx("bcc", 5.0)
+    lat = named_lattice("bcc")
+    k = np.random.default_rng(3).uniform(-0.5, 0.5, size=(777, 3)) @ lat.a_inv_t.T
+    kt = torch.tensor(k, device="cuda")
+    outs = []
+    for lanes in (1, 2, 8, 32):
+        z, st = ctx.zeta_device(kt, lanes_per_point=lanes)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        outs.append(z.cpu().numpy())
+    for o in outs[1:]:
+        assert emetric(o, outs[0]).max() <= 1e-14
+
+
+def test_pole_and_singular_semantics():
+    c2 = _ctx("square", 2.0)
+    with pytest.raises(PoleError):
+        c2.zeta(np.zeros(2))
+    with pytest.raises(PoleError):
+        c2.zeta(np.array([[1.0, -1.0]]))  # reduces to k = 0
+    # log-case singular part undefined at 0; generic nu < d diverges at 0
+    with pytest.raises(ValueError):
+        c2.singular(np.zeros(2))
+    with pytest.raises(ValueError):
+        _ctx("square", 1.5).singular(np.zeros(2))
+    c = _ctx("square", 3.5)
+    k = np.array([[0.13, -0.21], [0.3, 0.4]])
+    rho = np.sum(k * k, axis=1)
+    assert np.allclose(c.singular(k), c.singular_coef() * rho ** 0.75, rtol=1e-14)
+    assert emetric(c.zeta(k), c.reg_zeta(k) + c.singular(k) / c.vol).max() <= 1e-14
+    # trivial branch: constant -1 at nu = 0, 0 at nu = -2
+    assert _ctx("square", 0.0).zeta(np.array([0.2, 0.1])) == -1.0
+    assert _ctx("square", -2.0).zeta(np.array([0.2, 0.1])) == 0.0
+
+
+def test_size_independent_properties_2pow20():
+    """Throughput-sized batch: evenness, periodicity and BZ reduction (no oracle needed)."""
+    ctx = _ctx("square", 3.5)
+    k = np.random.default_rng(1).uniform(-0.5, 0.5, size=(1 << 20, 2))
+    z = ctx.zeta(k)
+    assert np.all(np.isfinite(z))
+    zm = ctx.zeta(-k)
+    assert np.abs(z - zm).max() <= 1e-13 * max(1.0, np.abs(z).max())
+    shift = np.array([3.0, -2.0])
+    zs = ctx.zeta(k[:65536] + shift)
+    assert emetric(zs, z[:65536]).max() <= 1e-12
+    # sub-sample against the oracle
+    idx = np.random.default_rng(2).choice(len(k), 2048, replace=False)
+    assert emetric(z[idx], O.zeta(np.eye(2), 3.5, k[idx])).max() <= ZETA_TOL
+
+
+@pytest.mark.parametrize("name", ["fcc", "bcc", "square", "integer_1d", "hexagonal"])
+def test_hessian_vs_oracle_and_trace_identity(name):
+    lat = named_lattice(name)
+    d = lat.d
+    rng = np.random.default_rng(11)
+    kap = rng.uniform(-0.5, 0.5, size=(64, d))
+    k = kap @ lat.a_inv_t.T
+    ctx5 = EpsteinContext(lat, 5.0, device=0)
+    H = ctx5.zeta_hessian(k)
+    Ho = O.hessian(lat.a, 5.0, k)
+    scale = np.abs(Ho).max(axis=(1, 2), keepdims=True)
+    assert (np.abs(H - Ho) / np.maximum(scale, 1.0)).max() <= ZETA_TOL
+    # tr M_5 = Z_3 exactly (Laplacian of the lattice sum)
+    M = polynomial_weighted_zeta(lat, 5.0, k)
+    z3 = epstein_context(lat, 3.0).zeta(k)
+    assert emetric(np.trace(M, axis1=1, axis2=2), z3).max() <= 1e-12 * max(1.0, np.abs(z3).max())
+
+
+def test_hessian_vs_reference_fd(golden):
+    for h in golden["hessian_fd"]:
+        lat = named_lattice(h["lattice"])
+        M = polynomial_weighted_zeta(lat, 5.0, np.array(h["k"]))
+        assert abs(np.trace(M) - h["z3"]) <= 1e-12 * max(1.0, abs(h["z3"]))
+        assert np.abs(M - np.array(h["M_fd"]).reshape(3, 3)).max() < 1e-4
