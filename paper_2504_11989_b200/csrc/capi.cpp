@@ -78,7 +78,8 @@ void free_all(std::vector<void*>* allocs) {
 // Host-side description of a fused plan before upload.
 struct HostPlan {
     int d = 0, nctx = 0, hess = 0, nw = 0;
-    std::vector<double> dir_n, dir_w, rec_q;
+    double c = 0.0, r_cut = 0.0;
+    std::vector<double> dir_n, dir_w, rec_q, rec_norm;
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;
@@ -164,19 +165,35 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                 for (int b = a; b < d; ++b) hp->dir_w[i * hp->nw + hp->nctx + cidx++] = double(w * z[a] * z[b]);
         }
     }
+    // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
-    hp->rec_q.assign(nrec * d, 0.0);
-    for (size_t i = 0; i < nrec; ++i)
+    std::vector<double> q(nrec * d);
+    std::vector<ld> qn(nrec);
+    for (size_t i = 0; i < nrec; ++i) {
+        ld r2 = 0.0L;
         for (int a = 0; a < d; ++a) {
-            ld q = 0.0L;
-            for (int b = 0; b < d; ++b) q += ld(first->B[a * d + b]) * rec_n[i * d + b];
-            hp->rec_q[i * d + a] = double(q);
+            ld v = 0.0L;
+            for (int b = 0; b < d; ++b) v += ld(first->B[a * d + b]) * rec_n[i * d + b];
+            q[i * d + a] = double(v);
+            r2 += v * v;
         }
+        qn[i] = std::sqrt(r2);
+    }
+    std::vector<size_t> order(nrec);
+    for (size_t i = 0; i < nrec; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return qn[a] < qn[b]; });
+    hp->rec_q.assign(nrec * d, 0.0);
+    hp->rec_norm.assign(nrec, 0.0);
+    for (size_t i = 0; i < nrec; ++i) {
+        for (int a = 0; a < d; ++a) hp->rec_q[i * d + a] = q[order[i] * d + a];
+        hp->rec_norm[i] = double(qn[order[i]]);
+    }
     // table functions: plain F_j = c^s E_{1-s}; Hessian F' = -c^{s+1} E_{-s}, F'' = c^{s+2} E_{-s-1}
     double p[4], sc[4];
     int nf = 0;
     double rp = 0.0;
     const ld c = ld(lz::kPi) / ld(first->k.split);
+    hp->c = first->k.c;
     for (int j = 0; j < hp->nctx; ++j) {
         const lz::CtxConst& k = plain[j]->k;
         hp->ctx[j] = k;
@@ -203,6 +220,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->tab.nfunc = nf;
     } else {
         lz::build_table(p, sc, nf, double(c), lz::table_x_lo(*first), rp, &hp->tab);
+        // beyond x_hi every tabulated function is exactly zero in the kernel
+        hp->r_cut = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L + 1e-9L));
     }
 }
 
@@ -215,11 +234,14 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.n_dir = int(hp.dir_n.size() / hp.d);
     P.n_rec = int(hp.rec_q.size() / hp.d);
     P.nw = hp.nw;
+    P.c = hp.c;
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
     P.dir_n = upload(hp.dir_n, allocs);
     P.dir_w = upload(hp.dir_w, allocs);
     P.rec_q = upload(hp.rec_q, allocs);
+    P.rec_norm = upload(hp.rec_norm, allocs);
+    P.r_cut = hp.r_cut;
     P.tab.dir = upload(hp.tab.dir, allocs);
     P.tab.coef = upload(hp.tab.coef, allocs);
     P.tab.nbins = hp.tab.nbins;
@@ -243,6 +265,62 @@ struct GridArrays {
     double* v = nullptr;
     double* wv = nullptr;
 };
+
+// Per-device scratch for the host-buffer entry points: one non-blocking stream,
+// grow-only device memory and grow-only pinned staging, reused across calls so a
+// call costs copies + kernels only (no allocation, no stream creation).
+struct Arena {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    char* dbuf = nullptr;
+    size_t dcap = 0;
+    char* hbuf = nullptr;
+    size_t hcap = 0;
+    void ensure(size_t dbytes, size_t hbytes) {
+        if (!st) check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        if (dbytes > dcap) {
+            if (dbuf) cudaFree(dbuf);
+            dcap = std::max(dbytes, dcap * 2);
+            check_cuda(cudaMalloc((void**)&dbuf, dcap), "arena malloc");
+        }
+        if (hbytes > hcap) {
+            if (hbuf) cudaFreeHost(hbuf);
+            hcap = std::max(hbytes, hcap * 2);
+            check_cuda(cudaHostAlloc((void**)&hbuf, hcap, cudaHostAllocDefault), "arena pinned alloc");
+        }
+    }
+};
+
+Arena& arena(int device) {
+    static std::mutex m;
+    static std::map<int, Arena*> arenas;
+    std::lock_guard<std::mutex> lock(m);
+    Arena*& a = arenas[device];
+    if (!a) a = new Arena();
+    return *a;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// H2D from a host buffer: direct DMA when pinned, else through the arena's pinned staging.
+void h2d(void* dst, const void* src, size_t bytes, char* staging, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (is_pinned(src)) {
+        check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    } else {
+        std::memcpy(staging, src, bytes);
+        check_cuda(cudaMemcpyAsync(dst, staging, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    }
+}
 
 }  // namespace
 
@@ -487,26 +565,24 @@ int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint3
             if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
         if (n == 0) return;
         DeviceGuard dg(c->device);
-        cudaStream_t st;
-        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-        double *dk = nullptr, *dout = nullptr;
-        int* dstat = nullptr;
-        const size_t kb = sizeof(double) * size_t(n) * c->h.d;
-        check_cuda(cudaMallocAsync((void**)&dk, kb, st), "malloc");
-        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * size_t(n), st), "malloc");
-        check_cuda(cudaMallocAsync((void**)&dstat, sizeof(int), st), "malloc");
-        check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), st), "memset");
-        check_cuda(cudaMemcpyAsync(dk, k, kb, cudaMemcpyHostToDevice, st), "h2d");
-        check_cuda(lz::launch_batch(c->dplain, false, dk, n, dout, flags, auto_lanes(n), dstat, st), "zeta kernel");
-        int hstat = 0;
-        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st), "d2h");
-        check_cuda(cudaMemcpyAsync(&hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
-        cudaFreeAsync(dk, st);
-        cudaFreeAsync(dout, st);
-        cudaFreeAsync(dstat, st);
-        check_cuda(cudaStreamSynchronize(st), "sync");
-        cudaStreamDestroy(st);
-        if (hstat & 1)
+        Arena& A = arena(c->device);
+        std::lock_guard<std::mutex> lock(A.mu);
+        const size_t kb = sizeof(double) * size_t(n) * c->h.d, ob = sizeof(double) * size_t(n);
+        A.ensure(al256(kb) + al256(ob) + 256, std::max(kb, ob) + 256);
+        double* dk = reinterpret_cast<double*>(A.dbuf);
+        double* dout = reinterpret_cast<double*>(A.dbuf + al256(kb));
+        int* dstat = reinterpret_cast<int*>(A.dbuf + al256(kb) + al256(ob));
+        check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
+        h2d(dk, k, kb, A.hbuf, A.st);
+        check_cuda(lz::launch_batch(c->dplain, false, dk, n, dout, flags, auto_lanes(n), dstat, A.st), "zeta kernel");
+        const bool pinned_out = is_pinned(out);
+        check_cuda(cudaMemcpyAsync(pinned_out ? (void*)out : (void*)A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st),
+                   "d2h");
+        int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
+        check_cuda(cudaMemcpyAsync(hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, A.st), "d2h");
+        check_cuda(cudaStreamSynchronize(A.st), "sync");
+        if (!pinned_out) std::memcpy(out, A.hbuf, ob);
+        if (*hstat & 1)
             throw Error{LZ_EPOLE, "Epstein zeta has a simple pole at nu = d for k in the reciprocal lattice"};
     });
 }
@@ -531,18 +607,17 @@ int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* ou
         if (n == 0) return;
         DeviceGuard dg(c->device);
         const int d = c->h.d, ns = d * (d + 1) / 2;
-        cudaStream_t st;
-        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-        double *dk = nullptr, *dout = nullptr;
-        check_cuda(cudaMallocAsync((void**)&dk, sizeof(double) * size_t(n) * d, st), "malloc");
-        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * size_t(n) * ns, st), "malloc");
-        check_cuda(cudaMemcpyAsync(dk, k, sizeof(double) * size_t(n) * d, cudaMemcpyHostToDevice, st), "h2d");
-        check_cuda(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, st), "hessian kernel");
-        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * size_t(n) * ns, cudaMemcpyDeviceToHost, st), "d2h");
-        cudaFreeAsync(dk, st);
-        cudaFreeAsync(dout, st);
-        check_cuda(cudaStreamSynchronize(st), "sync");
-        cudaStreamDestroy(st);
+        Arena& A = arena(c->device);
+        std::lock_guard<std::mutex> lock(A.mu);
+        const size_t kb = sizeof(double) * size_t(n) * d, ob = sizeof(double) * size_t(n) * ns;
+        A.ensure(al256(kb) + al256(ob), std::max(kb, ob) + 256);
+        double* dk = reinterpret_cast<double*>(A.dbuf);
+        double* dout = reinterpret_cast<double*>(A.dbuf + al256(kb));
+        h2d(dk, k, kb, A.hbuf, A.st);
+        check_cuda(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, A.st), "hessian kernel");
+        check_cuda(cudaMemcpyAsync(A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st), "d2h");
+        check_cuda(cudaStreamSynchronize(A.st), "sync");
+        std::memcpy(out, A.hbuf, ob);
     });
 }
 
@@ -657,21 +732,21 @@ int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
         int rc = lz_grid_tiles(pl->d, g, &n_nodes, &n_tiles);
         if (rc != LZ_OK) throw Error{rc, g_last_error};
         const int ncomp = pl->kind == 0 ? 1 : 2;
-        cudaStream_t st;
-        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-        double *dp = nullptr, *dout = nullptr;
-        check_cuda(cudaMallocAsync((void**)&dp, sizeof(double) * size_t(n_tiles) * ncomp, st), "malloc");
-        check_cuda(cudaMallocAsync((void**)&dout, sizeof(double) * ncomp, st), "malloc");
-        check_cuda(cudaMemsetAsync(dp, 0, sizeof(double) * size_t(n_tiles) * ncomp, st), "memset");
+        Arena& A = arena(pl->device);
+        std::lock_guard<std::mutex> lock(A.mu);
+        const size_t pb = sizeof(double) * size_t(n_tiles) * ncomp;
+        A.ensure(al256(pb) + 256, 256);
+        double* dp = reinterpret_cast<double*>(A.dbuf);
+        double* dout = reinterpret_cast<double*>(A.dbuf + al256(pb));
         lz_grid gg = *g;
-        rc = lz_plan_integrate(pl, &gg, dp, 0, st);
+        gg.tile_lo = 0;
+        gg.tile_hi = 0;
+        rc = lz_plan_integrate(pl, &gg, dp, 0, A.st);
         if (rc != LZ_OK) throw Error{rc, g_last_error};
-        check_cuda(lz::launch_reduce(dp, n_tiles, ncomp, dout, st), "reduce");
-        check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * ncomp, cudaMemcpyDeviceToHost, st), "d2h");
-        cudaFreeAsync(dp, st);
-        cudaFreeAsync(dout, st);
-        check_cuda(cudaStreamSynchronize(st), "sync");
-        cudaStreamDestroy(st);
+        check_cuda(lz::launch_reduce(dp, n_tiles, ncomp, dout, A.st), "reduce");
+        check_cuda(cudaMemcpyAsync(A.hbuf, dout, sizeof(double) * ncomp, cudaMemcpyDeviceToHost, A.st), "d2h");
+        check_cuda(cudaStreamSynchronize(A.st), "sync");
+        std::memcpy(out, A.hbuf, sizeof(double) * ncomp);
     });
 }
 

@@ -14,6 +14,7 @@
 //   BrillouinZone.corner_radius L/lattice.py:131-136
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -394,7 +395,10 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     std::vector<Fn> fns;
     for (int j = 0; j < nfunc; ++j) fns.push_back(Fn{ld(p[j]), ld(scale[j])});
     // upper end: every function (times the |y|^2 factor of the Hessian terms) is
-    // below 1e-24 of the unit scale; terms past it are exactly zero in the kernel.
+    // below `cutoff` (default 1e-24) of the unit scale; terms past it are exactly
+    // zero in the kernel and culled per warp.
+    ld cutoff = 1e-24L;
+    if (const char* e = std::getenv("LATSUM_TABLE_CUTOFF")) cutoff = std::strtold(e, nullptr);
     const ld hb = kBinWidth;
     ld x_hi = x_lo;
     for (int b = 0; b < 1000; ++b) {
@@ -402,7 +406,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
         ld worst = 0.0L;
         for (const Fn& f : fns) worst = std::max(worst, std::fabs(f(x)) * (1.0L + 4.0L * x));
         x_hi = x;
-        if (worst * std::fabs(ld(rfac_pref)) < 1e-24L && x > 8.0L) break;
+        if (worst * std::fabs(ld(rfac_pref)) < cutoff && x > 8.0L) break;
     }
     const int nbins = int(std::lround((x_hi - ld(x_lo)) / hb));
     out->x_lo = x_lo;

@@ -36,11 +36,15 @@ constexpr int kTileNodes = 32 * kTileWarps;
 template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 
 // ---------------------------------------------------------------------------
-// Shared-memory staging of a plan
+// Shared-memory staging of a plan.  SMEM is a template parameter so that every
+// table load compiles to an explicit shared-space LDS (a runtime choice would
+// force generic LD through the L1 path); the global variant only serves plans
+// whose point sets exceed the 227 KB opt-in shared memory.
 struct View {
     const double* dir_n;
     const double* dir_w;
     const double* rec_q;
+    const double* rec_norm;
     const double* coef;
     const int* tdir;
 };
@@ -52,6 +56,7 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     b += align16(sizeof(double) * P.n_dir * P.d);
     b += align16(sizeof(double) * P.n_dir * P.nw);
     b += align16(sizeof(double) * P.n_rec * P.d);
+    b += align16(sizeof(double) * P.n_rec);
     b += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
     b += align16(sizeof(int) * P.tab.nbins);
     return b;
@@ -61,38 +66,56 @@ __device__ inline void copy_words(double* dst, const double* src, size_t n) {
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-__device__ inline View stage(const DevPlan& P, unsigned char* smem, bool use_smem) {
+template <bool SMEM>
+__device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
-    if (!use_smem) {
+    if constexpr (!SMEM) {
         v.dir_n = P.dir_n;
         v.dir_w = P.dir_w;
         v.rec_q = P.rec_q;
+        v.rec_norm = P.rec_norm;
         v.coef = P.tab.coef;
         v.tdir = P.tab.dir;
         return v;
+    } else {
+        size_t off = 0;
+        double* dn = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_dir * P.d);
+        double* dw = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_dir * P.nw);
+        double* rq = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_rec * P.d);
+        double* rn = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_rec);
+        double* cf = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
+        int* td = reinterpret_cast<int*>(smem + off);
+        copy_words(dn, P.dir_n, size_t(P.n_dir) * P.d);
+        copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
+        copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
+        copy_words(rn, P.rec_norm, size_t(P.n_rec));
+        copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
+        for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
+        __syncthreads();
+        v.dir_n = dn;
+        v.dir_w = dw;
+        v.rec_q = rq;
+        v.rec_norm = rn;
+        v.coef = cf;
+        v.tdir = td;
+        return v;
     }
-    size_t off = 0;
-    double* dn = reinterpret_cast<double*>(smem + off);
-    off += align16(sizeof(double) * P.n_dir * P.d);
-    double* dw = reinterpret_cast<double*>(smem + off);
-    off += align16(sizeof(double) * P.n_dir * P.nw);
-    double* rq = reinterpret_cast<double*>(smem + off);
-    off += align16(sizeof(double) * P.n_rec * P.d);
-    double* cf = reinterpret_cast<double*>(smem + off);
-    off += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
-    int* td = reinterpret_cast<int*>(smem + off);
-    copy_words(dn, P.dir_n, size_t(P.n_dir) * P.d);
-    copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
-    copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
-    copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
-    for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
-    __syncthreads();
-    v.dir_n = dn;
-    v.dir_w = dw;
-    v.rec_q = rq;
-    v.coef = cf;
-    v.tdir = td;
-    return v;
+}
+
+// Number of reciprocal points with |q| <= r (rec_norm ascending), binary search.
+__device__ __forceinline__ int count_le(const double* norm, int n, double r) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (norm[mid] <= r) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // Out-of-line E_p for the rare direct paths, so the hot loop stays small.
@@ -229,8 +252,18 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     double yy[NS > 0 ? NS : 1];
 #pragma unroll
     for (int c = 0; c < NS; ++c) yy[c] = 0.0;
-    const double cc = P.ctx[0].c;  // all contexts of a plan share the split
-    for (int i = gl; i < P.n_rec; i += G) {
+    const double cc = P.c;  // all contexts of a plan share the split
+    // Exact per-warp culling: |k+q| >= |q| - |k|, and every table function is
+    // identically zero beyond x_hi, i.e. for |k+q| > r_cut.  The points are
+    // sorted by |q|, so the warp stops after the last q with |q| <= r_cut + max|k|.
+    double kmag = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) kmag = fma(k[a], k[a], kmag);
+    kmag = sqrt(kmag);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
+    const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
+    for (int i = gl; i < n_eff; i += G) {
         double y[D], r = 0.0;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -316,12 +349,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 // ---------------------------------------------------------------------------
 // Batch kernel: G lanes per point, persistent grid-stride over points.
 // flags: 1 = NO_REDUCE, 2 = REG_ONLY, 4 = SINGULAR_ONLY.  status bit 1 = pole.
-template <int D, int NCTX, bool HESS>
+template <int D, int NCTX, bool HESS, bool SMEM>
 __global__ void __launch_bounds__(256) batch_kernel(DevPlan P, const double* __restrict__ kin, int64_t n,
                                                     double* __restrict__ out, uint32_t flags, int G,
-                                                    int use_smem, int* status) {
+                                                    int* status) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const View V = stage(P, smem, use_smem != 0);
+    const View V = stage<SMEM>(P, smem);
     const int64_t nslots = ((n * G + 31) / 32) * 32;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t slot = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; slot < nslots; slot += stride) {
@@ -413,13 +446,12 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
-template <int D, int NCTX, bool HESS, int MODE>
-__global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials,
-                                                   int use_smem) {
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM>
+__global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
     __shared__ double wsum[kTileWarps][NCOMP];
-    const View V = stage(P, smem, use_smem != 0);
+    const View V = stage<SMEM>(P, smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
     for (int64_t tile = g.tile_lo + blockIdx.x; tile < g.tile_hi; tile += gridDim.x) {
@@ -428,8 +460,15 @@ __global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mu
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
         double t[D], weight = 0.0, u = 0.0;
-        bool ok = patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
-        if (ok) {
+        const bool ok = patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
+        if (!ok) {  // padding lane: a harmless interior node with zero weight
+#pragma unroll
+            for (int a = 0; a < D; ++a) t[a] = 1.0;
+            u = 0.25;
+            weight = 0.0;
+        }
+        // every lane of the warp evaluates (the culling bound is a warp reduction)
+        {
             double k[D], kap[D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
@@ -455,7 +494,7 @@ __global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mu
                     }
                     prod *= r;
                 }
-                val[0] = weight * prod;
+                val[0] = ok ? weight * prod : 0.0;
             } else {
                 const double z = acc.z[0];
                 // M = -Hess / (4 pi^2); tr(M^3) over the symmetric matrix
@@ -480,8 +519,8 @@ __global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mu
                         for (int e = 0; e < D; ++e) m2 = fma(M[a][e], M[e][b], m2);
                         tr3 = fma(m2, M[b][a], tr3);
                     }
-                val[0] = weight * (z * z * z);
-                val[1] = weight * tr3;
+                val[0] = ok ? weight * (z * z * z) : 0.0;
+                val[1] = ok ? weight * tr3 : 0.0;
             }
         }
         // deterministic tile reduction: fixed xor tree per warp, fixed warp order
@@ -562,18 +601,11 @@ static int num_sms() {
     return g_num_sms;
 }
 
-template <class K>
-static cudaError_t prep_smem(K kernel, size_t bytes, int* use_smem) {
-    int dev = 0;
+static int smem_optin() {
+    int dev = 0, optin = 0;
     cudaGetDevice(&dev);
-    int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (bytes + 1024 > size_t(optin)) {
-        *use_smem = 0;
-        return cudaSuccess;
-    }
-    *use_smem = 1;
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    return optin;
 }
 
 template <class K>
@@ -584,22 +616,31 @@ static int blocks_for(K kernel, size_t smem, int threads) {
     return per_sm * num_sms();
 }
 
-template <int D, int NCTX, bool HESS>
-static cudaError_t launch_batch_t(const DevPlan& P, const double* k, int64_t n, double* out, uint32_t flags, int G,
-                                  int* status, cudaStream_t st) {
-    auto kern = batch_kernel<D, NCTX, HESS>;
-    int use = 0;
-    size_t bytes = plan_smem_bytes(P);
-    cudaError_t e = prep_smem(kern, bytes, &use);
-    if (e != cudaSuccess) return e;
-    size_t sm = use ? bytes : 0;
+template <int D, int NCTX, bool HESS, bool SMEM>
+static cudaError_t launch_batch_s(const DevPlan& P, const double* k, int64_t n, double* out, uint32_t flags, int G,
+                                  int* status, cudaStream_t st, size_t bytes) {
+    auto kern = batch_kernel<D, NCTX, HESS, SMEM>;
+    size_t sm = SMEM ? bytes : 0;
+    if (SMEM) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
     const int threads = 256;
     int64_t need = (n * G + threads - 1) / threads;
     int64_t cap = blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) blocks = 1;
-    kern<<<blocks, threads, sm, st>>>(P, k, n, out, flags, G, use, status);
+    kern<<<blocks, threads, sm, st>>>(P, k, n, out, flags, G, status);
     return cudaGetLastError();
+}
+
+template <int D, int NCTX, bool HESS>
+static cudaError_t launch_batch_t(const DevPlan& P, const double* k, int64_t n, double* out, uint32_t flags, int G,
+                                  int* status, cudaStream_t st) {
+    const size_t bytes = plan_smem_bytes(P);
+    if (bytes + 2048 <= size_t(smem_optin()))
+        return launch_batch_s<D, NCTX, HESS, true>(P, k, n, out, flags, G, status, st, bytes);
+    return launch_batch_s<D, NCTX, HESS, false>(P, k, n, out, flags, G, status, st, bytes);
 }
 
 cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n, double* out, uint32_t flags,
@@ -623,22 +664,31 @@ cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n
     return cudaErrorInvalidValue;
 }
 
-template <int D, int NCTX, bool HESS, int MODE>
-static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
-                                 cudaStream_t st) {
-    auto kern = tile_kernel<D, NCTX, HESS, MODE>;
-    int use = 0;
-    size_t bytes = plan_smem_bytes(P);
-    cudaError_t e = prep_smem(kern, bytes, &use);
-    if (e != cudaSuccess) return e;
-    size_t sm = use ? bytes : 0;
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM>
+static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
+                                 cudaStream_t st, size_t bytes) {
+    auto kern = tile_kernel<D, NCTX, HESS, MODE, SMEM>;
+    size_t sm = SMEM ? bytes : 0;
+    if (SMEM) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
     const int threads = 32 * kTileWarps;
     int64_t need = g.tile_hi - g.tile_lo;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
-    kern<<<blocks, threads, sm, st>>>(P, g, mult, partials, use);
+    kern<<<blocks, threads, sm, st>>>(P, g, mult, partials);
     return cudaGetLastError();
+}
+
+template <int D, int NCTX, bool HESS, int MODE>
+static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
+                                 cudaStream_t st) {
+    const size_t bytes = plan_smem_bytes(P);
+    if (bytes + 2048 <= size_t(smem_optin()))
+        return launch_tile_s<D, NCTX, HESS, MODE, true>(P, g, mult, partials, grid_blocks, st, bytes);
+    return launch_tile_s<D, NCTX, HESS, MODE, false>(P, g, mult, partials, grid_blocks, st, bytes);
 }
 
 cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, double* partials, int grid_blocks,

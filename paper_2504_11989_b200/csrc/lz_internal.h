@@ -55,11 +55,14 @@ struct DevPlan {
     int n_dir, n_rec;
     int nw;            // direct weight channels per point
     int pad_;
+    double c;          // pi / split, shared by every context of the plan
     double A[16];      // generator, row-major (columns = basis vectors)
     double B[16];      // A^{-T}, row-major
     const double* dir_n;   // [n_dir][d] integer coordinates (as double)
     const double* dir_w;   // [n_dir][nw] weights: nctx plain channels, then (hess) d(d+1)/2
-    const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0
+    const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0, sorted by |q|
+    const double* rec_norm;  // [n_rec] |q| ascending
+    double r_cut;          // |k+q| > r_cut  =>  every table function is exactly zero
     DevTable tab;          // functions: nctx plain F_j, then (hess) F', F''
     CtxConst ctx[kMaxCtx];
     CtxConst hctx;         // constants of the Hessian context

@@ -1,0 +1,163 @@
+"""Host-side logic of the drop-in (CPU only): C-ABI exports, lattice geometry, exponent
+classification, the native context/table builder vs the reference's point sets, configs,
+Duffy layout and the phase-scan arithmetic."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2504_11989_b200 import LatticeError, Lattice, named_lattice, parse_lattice_spec
+from paper_2504_11989_b200 import _native as N
+from paper_2504_11989_b200.epstein import EpsteinContext, classify_exponent
+from paper_2504_11989_b200.quadrature import (QuadratureConfig, angular_nodes, duffy_cells,
+                                              tail_primitive)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cabi_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "latsum_b200.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(lz_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 20
+    L = N.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(N.SIGNATURES), declared ^ set(N.SIGNATURES)
+    assert "sm_100a" in L.lz_version().decode()
+
+
+def test_lattice_geometry():
+    assert named_lattice("sq").volume == 1.0
+    assert abs(named_lattice("hex").volume - math.sqrt(3) / 2) < 1e-15
+    assert abs(named_lattice("fcc").volume - 1 / math.sqrt(2)) < 1e-15
+    for name in ("fcc", "bcc"):
+        assert abs(named_lattice(name).min_distance() - 1.0) < 1e-12
+    lat = named_lattice("hex", 2.5)
+    assert abs(lat.volume - 2.5 ** 2 * math.sqrt(3) / 2) < 1e-13
+    r = Lattice(np.diag([2.0, 1.0])).reciprocal()
+    assert np.allclose(r.a, np.diag([0.5, 1.0]))
+    assert np.allclose(named_lattice("hex").reciprocal().reciprocal().a, named_lattice("hex").a, atol=1e-14)
+    assert abs(named_lattice("bcc").brillouin_zone().volume * named_lattice("bcc").volume - 1) < 1e-14
+    assert parse_lattice_spec("hex:2.5") == lat
+    assert parse_lattice_spec("d=2;A=1,0;0,1") == named_lattice("square")
+    for bad in ("d=2;A=1,0", "nope", "d=x;A=1", "hex:abc"):
+        with pytest.raises(LatticeError):
+            parse_lattice_spec(bad)
+    with pytest.raises(LatticeError):
+        Lattice([[1.0, 2.0], [2.0, 4.0]])
+    with pytest.raises(LatticeError):
+        Lattice(np.eye(5))
+    with pytest.raises(LatticeError):
+        named_lattice("sq", -1.0)
+
+
+def test_bz_reduce_half_open():
+    bz = named_lattice("square").brillouin_zone()
+    k = np.array([[0.5, -0.5], [1.25, 0.75], [-0.5, 0.49]])
+    red = bz.reduce(k)
+    assert np.allclose(red, [[-0.5, -0.5], [0.25, -0.25], [-0.5, 0.49]])
+    assert bz.contains(red[0])
+
+
+def test_classify_exponent(golden):
+    for c in golden["cases"]:
+        d = named_lattice(c["lattice"]).d
+        branch, nu, m = classify_exponent(c["nu"], d)
+        assert branch == c["branch"]
+        assert nu == c["nu"]
+        assert m == c["log_m"]
+    assert classify_exponent(3.0 + 1e-13, 3)[0] == "log_case"
+    with pytest.raises(ValueError):
+        classify_exponent(101.0, 2)
+    with pytest.raises(ValueError):
+        classify_exponent(float("nan"), 2)
+
+
+@pytest.mark.parametrize("idx", range(29))
+def test_native_context_matches_reference(golden, idx):
+    """Constants, point counts and (d <= 2) the exact point sets in the reference's order."""
+    c = golden["cases"][idx]
+    lat = named_lattice(c["lattice"])
+    ctx = EpsteinContext(lat, c["nu"], device=-1)
+    assert ctx.branch == c["branch"]
+    if ctx.branch == "trivial":
+        assert ctx.const_value == c["const_value"]
+        return
+    for key in ("s_rec", "pref", "rfac", "bconst", "kmax", "split", "vol"):
+        assert abs(getattr(ctx, key) - c[key]) <= 2e-15 * abs(c[key]), key
+    assert abs(ctx.singular_coef() - c["singular_coef"]) <= 2e-15 * abs(c["singular_coef"])
+    assert (len(ctx.dir_w), len(ctx.rec_pts)) == (c["n_dir"], c["n_rec"])
+    assert abs(math.fsum(ctx.dir_w) - c["dir_w_fsum"]) <= 1e-14 * abs(c["dir_w_fsum"])
+    assert abs(math.fsum(ctx.rec_norm2) - c["rec_norm2_fsum"]) <= 1e-13 * c["rec_norm2_fsum"]
+    if "dir_pts" in c:
+        assert np.abs(ctx.dir_pts - np.array(c["dir_pts"]).reshape(-1, lat.d)).max() <= 1e-15
+        assert np.abs(ctx.rec_pts - np.array(c["rec_pts"]).reshape(-1, lat.d)).max() <= 2e-15
+        w = np.array(c["dir_w"])
+        assert np.abs(ctx.dir_w - w).max() <= 1e-13 * np.abs(w).max()  # reference Gamma(s<0) recurrence
+    # reciprocal-summand tables: Chebyshev-fitted pieces within 6e-16 relative of long double
+    assert ctx.info.table_max_rel_err < 6e-16
+    assert ctx.info.table_x_hi > 50.0
+
+
+def test_hessian_point_sets():
+    for name, nu, hd, hr in (("fcc", 5.0, 171, 1330), ("bcc", 5.0, 364, 2196)):
+        info = EpsteinContext(named_lattice(name), nu, device=-1).info
+        assert (info.n_dir_h, info.n_rec_h) == (hd, hr)
+
+
+def test_no_cpu_fallback():
+    ctx = EpsteinContext(named_lattice("square"), 3.5, device=-1)
+    with pytest.raises(RuntimeError):
+        ctx.zeta(np.array([[0.1, 0.2]]))
+
+
+def test_quadrature_config_roundtrip():
+    cfg = QuadratureConfig(gauss_order=10, epsilon=0.05, grid_u=96, grading=3, splitting=1.25)
+    assert QuadratureConfig.from_text(cfg.to_text()) == cfg
+    with pytest.raises(ValueError):
+        QuadratureConfig(epsilon=0.6)
+    with pytest.raises(ValueError):
+        QuadratureConfig(taylor_order=3)
+    with pytest.raises(ValueError):
+        QuadratureConfig.from_text("bogus=1")
+
+
+def test_duffy_layout():
+    for d in (1, 2, 3):
+        cells = duffy_cells(d)
+        assert len(cells) == 2 ** (d - 1) * d
+        v, w = angular_nodes(d, 14)
+        assert abs(w.sum() - 0.5 ** (d - 1)) < 1e-15
+    assert duffy_cells(3)[1].pyramid == 1 and duffy_cells(3)[3].signs == (1.0, -1.0)
+
+
+def test_tail_primitive_examples():
+    assert tail_primitive(2.0, 0, 1.0 / 16.0, 1.0) == -128.0
+    # log^1 closed form of PAPER.md:282
+    nu, eps, w2 = 1.5, 0.1, 0.7
+    ell = math.log(math.pi * eps * eps * w2)
+    assert abs(tail_primitive(nu, 1, eps, w2) + eps ** -nu * (2 + nu * ell) / nu ** 2) < 1e-12
+
+
+def test_phase_scan_from_reference_constants(golden, golden_integrals):
+    """lambda_c(p) from the reference's own constants (SURVEY 8(d) C5 values)."""
+    from paper_2504_11989_b200.phase import LatticeConstants, LJParams, critical_coupling, phase_scan
+    z = golden["zeta_at_zero"]
+    fcc = LatticeConstants("fcc", z["fcc_12"], z["fcc_6"], golden_integrals["fcc"]["atm"],
+                           named_lattice("fcc").volume)
+    bcc = LatticeConstants("bcc", z["bcc_12"], z["bcc_6"], golden_integrals["bcc"]["atm"],
+                           named_lattice("bcc").volume)
+    lj = LJParams()
+    expect = {0.0: 0.6347989463554651, 0.5: 0.6736514573960529, 1.0: 0.7088057861542634,
+              2.0: 0.7706881159724265}
+    for p, lc in expect.items():
+        got = critical_coupling(fcc, bcc, lj, p)
+        assert abs(got - lc) < 1e-9, (p, got, lc)
+    pts = phase_scan(fcc, bcc, lj, [0.0], np.linspace(0, 2, 64))
+    assert pts[0].winner == "fcc"      # fcc wins at lambda = 0
+    winners = [p.winner for p in pts]
+    assert winners.count("bcc") > 0 and winners[-1] == "bcc"
+    flips = sum(1 for a, b in zip(winners, winners[1:]) if a != b)
+    assert flips == 1

@@ -1,0 +1,64 @@
+"""Small, fixed GPU workloads for ncu (one process, one GPU).
+
+    python tools/profile_target.py atm      # one fused ATM integral, fcc, bench grid
+    python tools/profile_target.py c1       # C1 throughput batch (2^20 points)
+    python tools/profile_target.py e2e      # host-API overhead breakdown (no ncu)
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+from paper_2504_11989_b200 import named_lattice
+from paper_2504_11989_b200.epstein import EpsteinContext
+from paper_2504_11989_b200.manybody import ATMGrid, atm_integrals
+from paper_2504_11989_b200.quadrature import QuadratureConfig, atm_plan, integrate_product
+
+
+def atm():
+    fcc = named_lattice("fcc")
+    plan = atm_plan(fcc)
+    nn, nt = plan.tiles(128, 128, 3)
+    part = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
+    plan.integrate_device(part, 128, 128, 3)
+    torch.cuda.synchronize()
+    print("atm ok", nn, nt)
+
+
+def c1():
+    sq = named_lattice("square")
+    ctx = EpsteinContext(sq, 3.5, device=0)
+    k = torch.tensor(np.random.default_rng(1).uniform(-0.5, 0.5, size=(1 << 20, 2)), device="cuda")
+    z, st = ctx.zeta_device(k)
+    torch.cuda.synchronize()
+    print("c1 ok", float(z.sum()))
+
+
+def e2e():
+    sq = named_lattice("square")
+    ctx = EpsteinContext(sq, 3.5, device=0)
+    for n in (1, 4096, 1 << 20):
+        k = np.random.default_rng(0).uniform(-0.5, 0.5, size=(n, 2))
+        kp = torch.from_numpy(k).pin_memory().numpy()
+        ctx.zeta(k)
+        for label, arr in (("pageable", k), ("pinned", kp)):
+            t = time.perf_counter()
+            for _ in range(10):
+                ctx.zeta(arr)
+            print(f"zeta n={n} {label}: {(time.perf_counter() - t) / 10 * 1e3:.3f} ms/call")
+    cfg = QuadratureConfig(grid_u=256, grid_v=256, estimate_error=False)
+    integrate_product(sq, [4.0] * 51, cfg)
+    t = time.perf_counter()
+    integrate_product(sq, [4.0] * 51, cfg)
+    print(f"c4 integrate_product: {(time.perf_counter() - t) * 1e3:.3f} ms")
+    t = time.perf_counter()
+    atm_integrals(named_lattice("fcc"), ATMGrid(128, 128, 3))
+    print(f"c3 atm_integrals warm: {(time.perf_counter() - t) * 1e3:.3f} ms")
+
+
+if __name__ == "__main__":
+    {"atm": atm, "c1": c1, "e2e": e2e}[sys.argv[1]]()
