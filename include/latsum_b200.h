@@ -68,6 +68,9 @@ typedef struct {
 int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out);
 int lz_ctx_destroy(lz_ctx* ctx);
 int lz_ctx_get_info(const lz_ctx* ctx, lz_ctx_info* out);
+/* Build (host) and upload (device) the evaluation tables now instead of on first use.
+ * what: bit 1 = zeta tables, bit 2 = Hessian tables.  table_* info fields are zero until then. */
+int lz_ctx_prepare(const lz_ctx* ctx, int what);
 /* which: 0 dir_pts (z = A n), 1 dir_w, 2 rec_pts, 3 hdir_pts, 4 hdir_w, 5 rec_pts_h, 6 dir_n (int coords)
  * copies min(cap, size) doubles; returns the full size through *size.                        */
 int lz_ctx_get_points(const lz_ctx* ctx, int which, double* dst, int64_t cap, int64_t* size);
@@ -93,9 +96,11 @@ int lz_zeta_hessian_host(const lz_ctx* ctx, const double* k, int64_t n, double* 
  * on device; each 256-node tile writes one partial per component. */
 typedef struct {
     int n_u, n_v;
-    int grading;         /* q >= 1 in u = t^q / 2 */
+    int grading;         /* q >= 1 in u = u_lo + (1/2 - u_lo) t^q                     */
     int64_t tile_lo;     /* tile range of this call (multi-GPU shard); tile_hi <= 0: all */
     int64_t tile_hi;
+    double u_lo;         /* 0: whole radial range; epsilon: outer part of the split
+                            radial integral (L/quadrature.py:444-446)                 */
 } lz_grid;
 int lz_grid_tiles(int d, const lz_grid* g, int64_t* n_nodes, int64_t* n_tiles);
 
@@ -114,6 +119,14 @@ int lz_plan_integrate(const lz_plan* plan, const lz_grid* g, double* partials, i
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream);
 /* whole integral through host memory: out[ncomp] (value sums before the 2^d factor) */
 int lz_plan_integrate_host(const lz_plan* plan, const lz_grid* g, double* out);
+
+/* -- Taylor table of Z_reg at k = 0: EpsteinContext.reg_derivatives (L/epstein.py:347-415).
+ * Writes n multi-indices (alphas, n x d ints) with |alpha| even <= order and their values;
+ * copies min(cap, n) entries, returns n through *n. */
+int lz_ctx_reg_derivatives(const lz_ctx* ctx, int order, int* alphas, double* vals, int64_t cap, int64_t* n);
+
+/* -- host special function used by the tail algebra and tests: Gamma(s, x), x > 0 */
+double lz_upper_gamma(double s, double x);
 
 /* -- diagnostics */
 int lz_fp64_peak(double* tflops_out, double* ms_out);  /* DFMA-chain probe on the current device */

@@ -50,7 +50,7 @@ class CtxInfo(C.Structure):
 
 class Grid(C.Structure):
     _fields_ = [("n_u", C.c_int), ("n_v", C.c_int), ("grading", C.c_int),
-                ("tile_lo", C.c_int64), ("tile_hi", C.c_int64)]
+                ("tile_lo", C.c_int64), ("tile_hi", C.c_int64), ("u_lo", C.c_double)]
 
 
 # exported symbols and their signatures (every declaration of include/latsum_b200.h)
@@ -60,6 +60,7 @@ SIGNATURES = {
     "lz_ctx_create": (C.c_int, [C.POINTER(CtxParams), C.c_int, C.POINTER(_P)]),
     "lz_ctx_destroy": (C.c_int, [_P]),
     "lz_ctx_get_info": (C.c_int, [_P, C.POINTER(CtxInfo)]),
+    "lz_ctx_prepare": (C.c_int, [_P, C.c_int]),
     "lz_ctx_get_points": (C.c_int, [_P, C.c_int, _D, C.c_int64, C.POINTER(C.c_int64)]),
     "lz_zeta": (C.c_int, [_P, _P, C.c_int64, _P, C.c_uint32, C.c_int, _P, _P]),
     "lz_zeta_host": (C.c_int, [_P, _D, C.c_int64, _D, C.c_uint32]),
@@ -72,6 +73,9 @@ SIGNATURES = {
     "lz_plan_integrate": (C.c_int, [_P, C.POINTER(Grid), _P, C.c_int, _P]),
     "lz_reduce_partials": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
     "lz_plan_integrate_host": (C.c_int, [_P, C.POINTER(Grid), _D]),
+    "lz_ctx_reg_derivatives": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
+                                          C.POINTER(C.c_int64)]),
+    "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
     "lz_fp64_peak": (C.c_int, [_D, _D]),
     "lz_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "lz_strerror": (C.c_char_p, [C.c_int]),

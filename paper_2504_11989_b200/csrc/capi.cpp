@@ -327,6 +327,9 @@ void h2d(void* dst, const void* src, size_t bytes, char* staging, cudaStream_t s
 struct lz_ctx {
     lz::HostCtx h;
     int device = -1;
+    // evaluation tables are built on first use (plans of fused kernels build their own)
+    std::mutex mu;
+    bool plain_ready = false, hess_ready = false;
     HostPlan plain, hessp;
     lz::DevPlan dplain, dhess;
     std::vector<void*> allocs;
@@ -341,7 +344,7 @@ struct lz_plan {
     lz::DevPlan P;
     std::vector<void*> allocs;
     mutable std::mutex mu;
-    mutable std::map<std::tuple<int, int, int>, GridArrays> grids;
+    mutable std::map<std::tuple<int, int, int, double>, GridArrays> grids;
 };
 
 namespace {
@@ -349,6 +352,7 @@ namespace {
 void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
     if (g->n_u < 1 || (d > 1 && g->n_v < 1) || g->grading < 1)
         throw Error{LZ_EINVAL, "grid sizes must be positive and grading >= 1"};
+    if (!(g->u_lo >= 0.0 && g->u_lo < 0.5)) throw Error{LZ_EINVAL, "u_lo must lie in [0, 1/2)"};
     dg->n_u = g->n_u;
     dg->n_v = d > 1 ? g->n_v : 1;
     dg->n_cell = (1 << (d - 1)) * d;
@@ -365,21 +369,21 @@ void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
 
 const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
     std::lock_guard<std::mutex> lock(plan->mu);
-    auto key = std::make_tuple(g->n_u, plan->d > 1 ? g->n_v : 1, g->grading);
+    auto key = std::make_tuple(g->n_u, plan->d > 1 ? g->n_v : 1, g->grading, g->u_lo);
     auto it = plan->grids.find(key);
     if (it != plan->grids.end()) return it->second;
     const int d = plan->d;
     std::vector<double> x, w;
     lz::gauss_legendre(g->n_u, &x, &w);
     std::vector<double> u(g->n_u), wu(g->n_u);
-    const ld q = g->grading;
+    const ld q = g->grading, ulo = g->u_lo, span = 0.5L - ld(g->u_lo);
     for (int i = 0; i < g->n_u; ++i) {
-        // t = (x+1)/2 on (0,1); u = t^q / 2; du = q/2 t^{q-1} dt; times u^{d-1}
+        // t = (x+1)/2 on (0,1); u = u_lo + (1/2 - u_lo) t^q; du = (1/2 - u_lo) q t^{q-1} dt; times u^{d-1}
         const ld t = (ld(x[i]) + 1.0L) / 2.0L;
         const ld wt = ld(w[i]) / 2.0L;
-        const ld uu = 0.5L * std::pow(t, q);
+        const ld uu = ulo + span * std::pow(t, q);
         u[i] = double(uu);
-        wu[i] = double(wt * 0.5L * q * std::pow(t, q - 1.0L) * std::pow(uu, ld(d - 1)));
+        wu[i] = double(wt * span * q * std::pow(t, q - 1.0L) * std::pow(uu, ld(d - 1)));
     }
     std::vector<double> v, wv;
     if (d > 1) {
@@ -456,35 +460,70 @@ int lz_device_count(int* n) {
     return LZ_OK;
 }
 
+namespace {
+
+void ensure_plain(const lz_ctx* cc) {
+    lz_ctx* c = const_cast<lz_ctx*>(cc);
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (c->plain_ready) return;
+    if (c->h.k.branch != lz::kTrivial) {
+        build_host_plan({&c->h}, nullptr, &c->plain);
+    } else {
+        c->plain.d = c->h.d;
+        c->plain.nctx = 1;
+        c->plain.ctx[0] = c->h.k;
+        std::memcpy(c->plain.A, c->h.A, sizeof(c->plain.A));
+        std::memcpy(c->plain.B, c->h.B, sizeof(c->plain.B));
+    }
+    if (c->device >= 0) {
+        DeviceGuard dg(c->device);
+        c->dplain = upload_plan(c->plain, &c->allocs);
+    }
+    c->plain_ready = true;
+}
+
+void ensure_hess(const lz_ctx* cc) {
+    lz_ctx* c = const_cast<lz_ctx*>(cc);
+    if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+    std::lock_guard<std::mutex> lock(c->mu);
+    if (c->hess_ready) return;
+    build_host_plan({}, &c->h, &c->hessp);
+    if (c->device >= 0) {
+        DeviceGuard dg(c->device);
+        c->dhess = upload_plan(c->hessp, &c->allocs);
+    }
+    c->hess_ready = true;
+}
+
+}  // namespace
+
 int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out) {
     *out = nullptr;
     lz_ctx* c = new lz_ctx();
     int rc = guarded([&] {
         lz::build_context(p->d, p->a, p->nu, p->splitting, p->deriv_order, &c->h);
         c->device = device;
-        if (c->h.k.branch != lz::kTrivial) {
-            build_host_plan({&c->h}, nullptr, &c->plain);
-            if (c->h.has_hess) build_host_plan({}, &c->h, &c->hessp);
-        } else {
-            c->plain.d = p->d;
-            c->plain.nctx = 1;
-            c->plain.ctx[0] = c->h.k;
-            std::memcpy(c->plain.A, c->h.A, sizeof(c->plain.A));
-            std::memcpy(c->plain.B, c->h.B, sizeof(c->plain.B));
-        }
         if (device >= 0) {
-            DeviceGuard dg(device);
-            c->dplain = upload_plan(c->plain, &c->allocs);
-            if (c->h.has_hess) c->dhess = upload_plan(c->hessp, &c->allocs);
+            int n = 0;
+            if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n) {
+                cudaGetLastError();
+                throw Error{LZ_ECUDA, "no such CUDA device"};
+            }
         }
     });
     if (rc != LZ_OK) {
-        free_all(&c->allocs);
         delete c;
         return rc;
     }
     *out = c;
     return LZ_OK;
+}
+
+int lz_ctx_prepare(const lz_ctx* c, int what) {
+    return guarded([&] {
+        if (what & 1) ensure_plain(c);
+        if (what & 2) ensure_hess(c);
+    });
 }
 
 int lz_ctx_destroy(lz_ctx* c) {
@@ -521,6 +560,7 @@ int lz_ctx_get_info(const lz_ctx* c, lz_ctx_info* o) {
     o->n_rec = int64_t(c->h.rec_q.size() / c->h.d);
     o->n_dir_h = int64_t(c->h.hdir_w.size());
     o->n_rec_h = int64_t(c->h.hrec_q.size() / c->h.d);
+    // table statistics are reported once the tables exist (lz_ctx_prepare)
     o->table_x_lo = c->plain.tab.x_lo;
     o->table_x_hi = c->plain.tab.x_hi;
     o->table_max_rel_err = std::max(c->plain.tab.max_rel_err, c->hessp.tab.max_rel_err);
@@ -550,6 +590,7 @@ int lz_zeta(const lz_ctx* c, const double* k, int64_t n, double* out, uint32_t f
             void* stream) {
     return guarded([&] {
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables (created with device < 0)"};
+        ensure_plain(c);
         DeviceGuard dg(c->device);
         int G = lanes > 0 ? lanes : auto_lanes(n);
         if (G & (G - 1) || G > 32) throw Error{LZ_EINVAL, "lanes_per_point must be a power of two <= 32"};
@@ -564,6 +605,7 @@ int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint3
         for (int64_t i = 0; i < n * c->h.d; ++i)
             if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
         if (n == 0) return;
+        ensure_plain(c);
         DeviceGuard dg(c->device);
         Arena& A = arena(c->device);
         std::lock_guard<std::mutex> lock(A.mu);
@@ -590,7 +632,7 @@ int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint3
 int lz_zeta_hessian(const lz_ctx* c, const double* k, int64_t n, double* out, int lanes, void* stream) {
     return guarded([&] {
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
-        if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+        ensure_hess(c);
         DeviceGuard dg(c->device);
         int G = lanes > 0 ? lanes : auto_lanes(n);
         check_cuda(lz::launch_batch(c->dhess, true, k, n, out, 1u, G, nullptr, (cudaStream_t)stream),
@@ -605,6 +647,7 @@ int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* ou
         for (int64_t i = 0; i < n * c->h.d; ++i)
             if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
         if (n == 0) return;
+        ensure_hess(c);
         DeviceGuard dg(c->device);
         const int d = c->h.d, ns = d * (d + 1) / 2;
         Arena& A = arena(c->device);
@@ -748,6 +791,24 @@ int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, sizeof(double) * ncomp);
     });
+}
+
+int lz_ctx_reg_derivatives(const lz_ctx* c, int order, int* alphas, double* vals, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        if (order < 0 || order % 2 || order > 12) throw Error{LZ_EINVAL, "derivative order must be even and <= 12"};
+        std::vector<int> al;
+        std::vector<double> v;
+        lz::build_reg_derivatives(c->h, order, &al, &v);
+        *n = int64_t(v.size());
+        const int64_t m = std::min<int64_t>(cap, *n);
+        if (alphas && m > 0) std::memcpy(alphas, al.data(), sizeof(int) * size_t(m) * c->h.d);
+        if (vals && m > 0) std::memcpy(vals, v.data(), sizeof(double) * size_t(m));
+    });
+}
+
+double lz_upper_gamma(double s, double x) {
+    if (!(x > 0.0)) return std::nan("");
+    return double(lz::upper_gamma<long double>(s, x));
 }
 
 int lz_fp64_peak(double* tflops, double* ms_out) {

@@ -13,6 +13,8 @@
 //   singular_coef              L/epstein.py:202-215
 //   BrillouinZone.corner_radius L/lattice.py:131-136
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -376,10 +378,8 @@ void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
 }
 
 ld eval_piece(const double* c, ld tau) {
-    // evaluate as the device does: Horner in double
-    double t = double(tau), acc = c[kNC - 1];
-    for (int j = kNC - 2; j >= 0; --j) acc = std::fma(acc, t, c[j]);
-    return acc;
+    // evaluate exactly as the device does (Estrin form, double)
+    return estrin8(c, tau_powers(double(tau)));
 }
 
 }  // namespace
@@ -395,9 +395,9 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     std::vector<Fn> fns;
     for (int j = 0; j < nfunc; ++j) fns.push_back(Fn{ld(p[j]), ld(scale[j])});
     // upper end: every function (times the |y|^2 factor of the Hessian terms) is
-    // below `cutoff` (default 1e-24) of the unit scale; terms past it are exactly
+    // below `cutoff` (default 1e-20) of the unit scale; terms past it are exactly
     // zero in the kernel and culled per warp.
-    ld cutoff = 1e-24L;
+    ld cutoff = 1e-20L;
     if (const char* e = std::getenv("LATSUM_TABLE_CUTOFF")) cutoff = std::strtold(e, nullptr);
     const ld hb = kBinWidth;
     ld x_hi = x_lo;
@@ -416,18 +416,21 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     out->dir.assign(nbins, 0);
     out->coef.clear();
     out->max_rel_err = 0.0;
-    int npieces = 0;
-    const int kMaxLevel = 8;
-    for (int b = 0; b < nbins; ++b) {
-        ld b0 = ld(x_lo) + hb * b;
-        int level = 0;
-        bool ok = false;
+    // bins are independent: fit them on all host cores, then concatenate in order
+    struct BinFit {
+        int level = kDirectMarker;
+        double err = 0.0;
         std::vector<double> coefs;
-        double worst_err = 0.0;
-        for (level = 0; level <= kMaxLevel; ++level) {
+    };
+    std::vector<BinFit> fits(nbins);
+    const int kMaxLevel = 8;
+    auto fit_bin = [&](int b) {
+        const ld b0 = ld(x_lo) + hb * b;
+        BinFit& bf = fits[b];
+        for (int level = 0; level <= kMaxLevel; ++level) {
             const int nsub = 1 << level;
-            coefs.assign(size_t(nsub) * nfunc * kNCP, 0.0);
-            worst_err = 0.0;
+            std::vector<double> coefs(size_t(nsub) * nfunc * kNCP, 0.0);
+            double worst_err = 0.0;
             bool good = true;
             for (int sidx = 0; sidx < nsub && good; ++sidx) {
                 ld x0 = b0 + hb * sidx / nsub, x1 = b0 + hb * (sidx + 1) / nsub;
@@ -446,18 +449,35 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
                 }
             }
             if (good) {
-                ok = true;
-                break;
+                bf.level = level;
+                bf.err = worst_err;
+                bf.coefs.swap(coefs);
+                return;
             }
         }
-        if (!ok) {
-            out->dir[b] = kDirectMarker;  // evaluate E_p directly in this bin
+        bf.level = kDirectMarker;  // evaluate E_p directly in this bin
+    };
+    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (nbins < 8) nth = 1;
+    std::atomic<int> next(0);
+    auto worker = [&]() {
+        for (int b = next++; b < nbins; b = next++) fit_bin(b);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    int npieces = 0;
+    for (int b = 0; b < nbins; ++b) {
+        const BinFit& bf = fits[b];
+        if (bf.level == kDirectMarker) {
+            out->dir[b] = kDirectMarker;
             continue;
         }
-        out->max_rel_err = std::max(out->max_rel_err, worst_err);
-        out->dir[b] = (npieces << 4) | level;
-        out->coef.insert(out->coef.end(), coefs.begin(), coefs.end());
-        npieces += 1 << level;
+        out->max_rel_err = std::max(out->max_rel_err, bf.err);
+        out->dir[b] = (npieces << 4) | bf.level;
+        out->coef.insert(out->coef.end(), bf.coefs.begin(), bf.coefs.end());
+        npieces += 1 << bf.level;
     }
     out->npieces = npieces;
 }
@@ -493,6 +513,193 @@ void gauss_legendre(int n, std::vector<double>* xs, std::vector<double>* ws) {
         // ascending order (numpy leggauss order)
         (*xs)[n - 1 - i] = double(x);
         (*ws)[n - 1 - i] = double(2.0L / ((1.0L - x * x) * dp * dp));
+    }
+}
+
+}  // namespace lz
+
+namespace lz {
+
+// ---------------------------------------------------------------------------
+// Partial derivatives of Z_reg at k = 0 (reference: EpsteinContext.reg_derivatives,
+// L/epstein.py:328-415).  Derived here from the Gaussian representation
+//     F(|y|^2) = rho^{-s} Gamma(s, c rho) = int_c^inf tau^{s-1} exp(-tau |y|^2) d tau,
+// whose y-derivatives are Hermite polynomials:
+//     d^alpha F = (-1)^|alpha| sum_j prod_i h(alpha_i, j_i) y^{alpha-2j} |y|^{-2(s+p)} Gamma(s+p, c|y|^2),
+//     p = |alpha| - |j|,  h(n, j) = (-1)^j n! 2^{n-2j} / (j! (n-2j)!),
+// the direct sum gives (-1)^{|alpha|/2} (2 pi)^|alpha| 2 sum_z w_z z^alpha, and the
+// q = 0 regular part t0_reg(rho) = sum_n a_n rho^n gives a_n n!/prod (alpha_i/2)! prod alpha_i!.
+// All sums are compensated in long double.
+namespace {
+
+struct Acc {  // Neumaier summation in long double
+    ld s = 0.0L, c = 0.0L;
+    void add(ld x) {
+        ld t = s + x;
+        c += (std::fabs(s) >= std::fabs(x)) ? (s - t) + x : (x - t) + s;
+        s = t;
+    }
+    ld value() const { return s + c; }
+};
+
+ld factl(int n) {
+    ld f = 1.0L;
+    for (int i = 2; i <= n; ++i) f *= i;
+    return f;
+}
+
+ld hermite_coef(int n, int j) {
+    return ((j & 1) ? -1.0L : 1.0L) * factl(n) * std::pow(2.0L, ld(n - 2 * j)) / (factl(j) * factl(n - 2 * j));
+}
+
+// rho-series coefficient a_n of t0_reg (L/epstein.py:328-345)
+ld t0_series_coeff(const CtxConst& k, int n) {
+    const ld c = kPiL / ld(k.split);
+    if (k.branch == kLogCase) {
+        const int m = k.log_m;
+        ld val = 0.0L;
+        if (n == m) val += std::log(ld(k.split)) - ld(kEulerGamma);
+        if (n > m) {
+            const int l = n - m;
+            val += ((l + 1) % 2 ? -1.0L : 1.0L) * std::pow(c, ld(l)) / (ld(l) * factl(l));
+        }
+        ld acc = 0.0L;
+        for (int j = std::max(0, m - n - 1); j < m; ++j) acc += factl(j) / factl(n - m + j + 1);
+        val += (((n - m) % 2 != 0) ? -1.0L : 1.0L) * std::pow(c, ld(n - m)) * acc;
+        return ((m % 2) ? -1.0L : 1.0L) / factl(m) * val;
+    }
+    const ld s = k.s;
+    return -std::pow(c, s + n) * ((n % 2) ? -1.0L : 1.0L) / (factl(n) * (s + n));
+}
+
+void enumerate_alphas(int d, int total, std::vector<int>& cur, std::vector<int>* out) {
+    if (int(cur.size()) == d - 1) {
+        cur.push_back(total);
+        out->insert(out->end(), cur.begin(), cur.end());
+        cur.pop_back();
+        return;
+    }
+    for (int h = 0; h <= total; ++h) {
+        cur.push_back(h);
+        enumerate_alphas(d, total - h, cur, out);
+        cur.pop_back();
+    }
+}
+
+}  // namespace
+
+void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals) {
+    const int d = h.d;
+    alphas->clear();
+    vals->clear();
+    for (int total = 0; total <= order; total += 2) {
+        std::vector<int> cur;
+        enumerate_alphas(d, total, cur, alphas);
+    }
+    const size_t na = alphas->size() / d;
+    vals->assign(na, 0.0);
+    if (h.k.branch == kTrivial) {
+        for (size_t i = 0; i < na; ++i) {
+            int tot = 0;
+            for (int a = 0; a < d; ++a) tot += (*alphas)[i * d + a];
+            (*vals)[i] = tot == 0 ? h.k.const_value : 0.0;
+        }
+        return;
+    }
+    // widened point sets (L/epstein.py:376-377): z^alpha and shifted gamma orders
+    std::vector<double> dn, dz, dw, rn, rq;
+    enumerate_direct(h, order, 1e-20, &dn, &dz, &dw);
+    enumerate_reciprocal(h, h.k.s + order, 1e-20, &rn, &rq);
+    const CtxConst& k = h.k;
+    const ld c = kPiL / ld(k.split), s = k.s;
+    const size_t nd = dw.size(), nr = rq.size() / d;
+    // long-double copies; reciprocal gammas per order p
+    std::vector<ld> z(nd * d), q(nr * d), qn2(nr);
+    for (size_t i = 0; i < nd; ++i)
+        for (int a = 0; a < d; ++a) {
+            ld v = 0.0L;
+            for (int b = 0; b < d; ++b) v += ld(h.A[a * d + b]) * dn[i * d + b];
+            z[i * d + a] = v;
+        }
+    std::vector<ld> wz(nd);
+    for (size_t i = 0; i < nd; ++i) {
+        ld r2 = 0.0L;
+        for (int a = 0; a < d; ++a) r2 += z[i * d + a] * z[i * d + a];
+        wz[i] = upper_gamma<ld>(ld(k.nu) / 2.0L, kPiL * ld(k.split) * r2) * std::pow(r2, -ld(k.nu) / 2.0L);
+    }
+    for (size_t i = 0; i < nr; ++i) {
+        ld r2 = 0.0L;
+        for (int a = 0; a < d; ++a) {
+            ld v = 0.0L;
+            for (int b = 0; b < d; ++b) v += ld(h.B[a * d + b]) * rn[i * d + b];
+            q[i * d + a] = v;
+            r2 += v * v;
+        }
+        qn2[i] = r2;
+    }
+    std::vector<std::vector<ld>> gam(order + 1, std::vector<ld>(nr));
+    for (int p = 0; p <= order; ++p)
+        for (size_t i = 0; i < nr; ++i)
+            gam[p][i] = upper_gamma<ld>(s + p, c * qn2[i]) * std::pow(qn2[i], -(s + p));
+    auto ipow = [](ld x, int e) {
+        ld r = 1.0L;
+        for (int i = 0; i < e; ++i) r *= x;
+        return r;
+    };
+    for (size_t ia = 0; ia < na; ++ia) {
+        const int* al = &(*alphas)[ia * d];
+        int total = 0;
+        for (int a = 0; a < d; ++a) total += al[a];
+        Acc parts;
+        // direct space
+        {
+            Acc sd;
+            for (size_t i = 0; i < nd; ++i) {
+                ld zp = wz[i];
+                for (int a = 0; a < d; ++a) zp *= ipow(z[i * d + a], al[a]);
+                sd.add(zp);
+            }
+            parts.add(((total / 2) % 2 ? -1.0L : 1.0L) * std::pow(2.0L * kPiL, ld(total)) * 2.0L * sd.value());
+        }
+        if (total == 0) parts.add(ld(k.bconst));
+        // reciprocal space, Hermite expansion over j with 0 <= j_i <= alpha_i / 2
+        int jv[kMaxDim] = {0, 0, 0, 0};
+        for (;;) {
+            int jsum = 0;
+            ld coef = 1.0L;
+            for (int a = 0; a < d; ++a) {
+                jsum += jv[a];
+                coef *= hermite_coef(al[a], jv[a]);
+            }
+            const int p = total - jsum;
+            Acc sr;
+            for (size_t i = 0; i < nr; ++i) {
+                ld qp = gam[p][i];
+                for (int a = 0; a < d; ++a) qp *= ipow(q[i * d + a], al[a] - 2 * jv[a]);
+                sr.add(qp);
+            }
+            parts.add(ld(k.rfac) * coef * sr.value());
+            int a = 0;
+            while (a < d) {
+                if (++jv[a] <= al[a] / 2) break;
+                jv[a] = 0;
+                ++a;
+            }
+            if (a == d) break;
+        }
+        // q = 0 regular part: only all-even multi-indices survive
+        bool even = true;
+        for (int a = 0; a < d; ++a) even = even && (al[a] % 2 == 0);
+        if (even) {
+            const int n = total / 2;
+            ld mult = factl(n), fac = 1.0L;
+            for (int a = 0; a < d; ++a) {
+                mult /= factl(al[a] / 2);
+                fac *= factl(al[a]);
+            }
+            parts.add(ld(k.rfac) * t0_series_coeff(k, n) * mult * fac);
+        }
+        (*vals)[ia] = double(ld(k.pref) * parts.value());
     }
 }
 

@@ -145,24 +145,14 @@ __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, doubl
     const int L = e & 15;
     const double fs = (xb - double(b)) * double(1 << L);
     const int sub = int(fs);
-    const double tau = 2.0 * (fs - double(sub)) - 1.0;
+    const TauPowers tp = tau_powers(2.0 * (fs - double(sub)) - 1.0);
     const double2* c = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * NF * kNCP);
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
-        const double2 c01 = c[j * 6 + 0], c23 = c[j * 6 + 1], c45 = c[j * 6 + 2];
-        const double2 c67 = c[j * 6 + 3], c89 = c[j * 6 + 4], cab = c[j * 6 + 5];
-        double acc = cab.x;  // degree 10
-        acc = fma(acc, tau, c89.y);
-        acc = fma(acc, tau, c89.x);
-        acc = fma(acc, tau, c67.y);
-        acc = fma(acc, tau, c67.x);
-        acc = fma(acc, tau, c45.y);
-        acc = fma(acc, tau, c45.x);
-        acc = fma(acc, tau, c23.y);
-        acc = fma(acc, tau, c23.x);
-        acc = fma(acc, tau, c01.y);
-        acc = fma(acc, tau, c01.x);
-        f[j] = acc;
+        const double2 c01 = c[j * 5 + 0], c23 = c[j * 5 + 1], c45 = c[j * 5 + 2];
+        const double2 c67 = c[j * 5 + 3], c89 = c[j * 5 + 4];
+        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c89.x};
+        f[j] = estrin8(cc, tp);
     }
 }
 
@@ -263,6 +253,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
     const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
+#pragma unroll 2
     for (int i = gl; i < n_eff; i += G) {
         double y[D], r = 0.0;
 #pragma unroll

@@ -2,6 +2,7 @@
 // the sm_100a kernels (kernels.cu).  Not part of the public C ABI.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -13,10 +14,10 @@ enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
 
 constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
-constexpr int kDeg = 10;       // degree of the piecewise polynomials (kDeg+1 coefficients)
+constexpr int kDeg = 8;        // degree of the piecewise polynomials (kDeg+1 coefficients)
 constexpr int kNC = kDeg + 1;
-constexpr int kNCP = 12;       // padded coefficient stride (16-byte aligned double2 loads)
-constexpr double kBinWidth = 0.5;   // directory bin width in x = c |y|^2
+constexpr int kNCP = 10;       // padded coefficient stride (16-byte aligned double2 loads)
+constexpr double kBinWidth = 0.25;  // directory bin width in x = c |y|^2
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
 
 // ---------------------------------------------------------------------------
@@ -78,6 +79,7 @@ struct DevGrid {
     int64_t tile_lo, tile_hi, n_patch;
 };
 
+
 // Host-side mirror of one context: constants + enumerated sets (host memory).
 struct HostCtx {
     int d;
@@ -102,6 +104,37 @@ struct HostTable {
     double max_rel_err = 0;   // measured during the build
 };
 
+// Degree-8 polynomial in Estrin form: dependency depth 4 instead of 8, and the
+// powers tau^2, tau^4, tau^8 are shared by every function of a table row.
+// Host (table build check) and device evaluate with the same operation order.
+struct TauPowers {
+    double t1, t2, t4, t8;
+};
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline TauPowers tau_powers(double t) {
+    TauPowers p;
+    p.t1 = t;
+    p.t2 = t * t;
+    p.t4 = p.t2 * p.t2;
+    p.t8 = p.t4 * p.t4;
+    return p;
+}
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline double estrin8(const double* c, const TauPowers& p) {
+    const double a0 = fma(c[1], p.t1, c[0]);
+    const double a1 = fma(c[3], p.t1, c[2]);
+    const double a2 = fma(c[5], p.t1, c[4]);
+    const double a3 = fma(c[7], p.t1, c[6]);
+    const double b0 = fma(a1, p.t2, a0);
+    const double b1 = fma(a3, p.t2, a2);
+    const double e0 = fma(b1, p.t4, b0);
+    return fma(c[8], p.t8, e0);
+}
+
 // Errors raised by the host builder carry an lz status code.
 struct Error {
     int code;
@@ -114,6 +147,7 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
                  double rfac_pref, HostTable* out);
 double table_x_lo(const HostCtx& h);
+void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals);
 void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* w);  // on [-1, 1]
 
 }  // namespace lz

@@ -96,6 +96,7 @@ class EpsteinContext:
         self.split = info.split
         self._lock = threading.Lock()
         self._taylor_cache: dict = {}
+        self.has_hessian = False
         if self.branch == TRIVIAL:
             self.const_value = info.const_value
             return
@@ -118,6 +119,14 @@ class EpsteinContext:
                 N.lib().lz_ctx_destroy(h)
             except Exception:
                 pass
+
+    def table_stats(self, hessian: bool = False) -> "N.CtxInfo":
+        """Build the evaluation tables now (normally lazy) and return the context info with the
+        table statistics (pieces, bins, x range, measured max relative fit error)."""
+        N.check(N.lib().lz_ctx_prepare(self._h, 3 if (hessian and self.has_hessian) else 1), "prepare")
+        info = N.CtxInfo()
+        N.lib().lz_ctx_get_info(self._h, C.byref(info))
+        return info
 
     def _points(self, which):
         n = C.c_int64(0)

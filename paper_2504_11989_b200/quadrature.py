@@ -182,19 +182,19 @@ class Plan:
         N.check(N.lib().lz_grid_tiles(self.d, C.byref(g), C.byref(nn), C.byref(nt)), "grid")
         return nn.value, nt.value
 
-    def integrate(self, n_u: int, n_v: int, grading: int) -> np.ndarray:
+    def integrate(self, n_u: int, n_v: int, grading: int, u_lo: float = 0.0) -> np.ndarray:
         """Sum over all nodes (before the 2^d factor), through host memory."""
         N.require_cuda("BZ quadrature")
-        g = N.Grid(n_u, n_v, grading, 0, 0)
+        g = N.Grid(n_u, n_v, grading, 0, 0, float(u_lo))
         out = np.zeros(self.ncomp, dtype=np.float64)
         N.check(N.lib().lz_plan_integrate_host(self._h, C.byref(g), N.dptr(out)), "integral")
         return out
 
     def integrate_device(self, partials, n_u: int, n_v: int, grading: int, tile_lo: int = 0,
-                         tile_hi: int = 0, stream=None, grid_blocks: int = 0):
+                         tile_hi: int = 0, stream=None, grid_blocks: int = 0, u_lo: float = 0.0):
         """Write the tile partials of [tile_lo, tile_hi) into a CUDA tensor (n_tiles x ncomp)."""
         import torch
-        g = N.Grid(n_u, n_v, grading, tile_lo, tile_hi)
+        g = N.Grid(n_u, n_v, grading, tile_lo, tile_hi, float(u_lo))
         st = stream if stream is not None else torch.cuda.current_stream(partials.device).cuda_stream
         N.check(N.lib().lz_plan_integrate(self._h, C.byref(g), partials.data_ptr(), grid_blocks, st),
                 "integral")

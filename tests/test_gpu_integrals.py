@@ -138,3 +138,22 @@ def test_tile_sharding_bit_identical():
     Plan.reduce_device(full, nt, 2, o1)
     res = atm_integrals(lat, ATMGrid(32, 16, 3))
     assert float(o1[0]) * 8 == res.zeta333
+
+
+@pytest.mark.parametrize("name", ["integer_1d", "square", "fcc", "bcc"])
+def test_meromorphic_continuation_path(golden_integrals, name):
+    """zeta(-1,5,5) and zeta(1,3,5) (some nu <= d): analytic tail on (0, eps) from the native
+    Taylor tables + device grid on (eps, 1/2); vs the reference's integrate_product."""
+    lat = named_lattice(name)
+    ref = golden_integrals[name]
+    cfg = QuadratureConfig(grid_u=64, grid_v=48 if lat.d == 3 else 64)
+    vals = {}
+    for key, nus in (("zm155", (-1, 5, 5)), ("z135", (1, 3, 5))):
+        v, err = integrate_product(lat, nus, cfg)
+        vals[key] = v
+        assert abs(v - ref[key]) <= SUM_TOL * abs(ref[key]), (name, key, v, ref[key])
+    # Prop. 2.4 recombination vs the Hessian-form ATM energy
+    z333 = integrate_product(lat, (3, 3, 3), QuadratureConfig(grid_u=128, grid_v=64, grading=3))[0] \
+        if lat.d == 3 else ref["z333"]
+    e24 = z333 / 24 - 3 * vals["zm155"] / 16 + 3 * vals["z135"] / 8
+    assert abs(e24 - ref["atm"]) <= SUM_TOL * abs(ref["atm"])
