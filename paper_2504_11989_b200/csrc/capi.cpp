@@ -77,9 +77,12 @@ void free_all(std::vector<void*>* allocs) {
 
 // Host-side description of a fused plan before upload.
 struct HostPlan {
-    int d = 0, nctx = 0, hess = 0, nw = 0;
-    double c = 0.0, r_cut = 0.0;
-    std::vector<double> dir_n, dir_w, rec_q, rec_norm;
+    int d = 0, nctx = 0, hess = 0, nw = 0, alias_fp = 0;
+    double c = 0.0, r_cut = 0.0, alias_ratio = 0.0;
+    std::vector<double> dir_n, dir_w, rec_q, rec_norm, run_n, t0c;
+    int n_t0 = 0;
+    double t0_rho_max = -1.0;
+    std::vector<int> run_info;
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;
@@ -145,6 +148,37 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     union_points(d, dsets, &hp->dir_n);
     std::vector<double> rec_n;
     union_points(d, rsets, &rec_n);
+    // Direct points as runs of consecutive last coordinates: the kernel evaluates one
+    // sincospi per run and rotates by exp(2 pi i kappa_d) along it.
+    {
+        const size_t np = hp->dir_n.size() / d;
+        std::vector<size_t> ord(np);
+        for (size_t i = 0; i < np; ++i) ord[i] = i;
+        auto key = [&](size_t i, int a) { return std::lround(hp->dir_n[i * d + a]); };
+        std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+            for (int j = 0; j < d; ++j)
+                if (key(a, j) != key(b, j)) return key(a, j) < key(b, j);
+            return false;
+        });
+        std::vector<double> pts(np * d);
+        for (size_t i = 0; i < np; ++i)
+            for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[ord[i] * d + a];
+        hp->dir_n.swap(pts);
+        hp->run_n.clear();
+        hp->run_info.clear();
+        for (size_t i = 0; i < np; ++i) {
+            bool cont = i > 0;
+            for (int a = 0; cont && a < d - 1; ++a) cont = key(i, a) == key(i - 1, a);
+            cont = cont && key(i, d - 1) == key(i - 1, d - 1) + 1;
+            if (cont) {
+                hp->run_info.back() += 1;
+            } else {
+                hp->run_n.insert(hp->run_n.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
+                hp->run_info.push_back(int(i));
+                hp->run_info.push_back(1);
+            }
+        }
+    }
     const int nsym = d * (d + 1) / 2;
     hp->nw = hp->nctx + (hess ? nsym : 0);
     const size_t ndir = hp->dir_n.size() / d;
@@ -203,18 +237,61 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         rp = std::max(rp, std::fabs(k.rfac * k.pref));
     }
     std::memset(&hp->hctx, 0, sizeof(hp->hctx));
+    hp->alias_fp = 0;
+    hp->alias_ratio = 0.0;
     if (hess) {
         const lz::CtxConst& k = hess->k;
         hp->hctx = k;
-        p[nf] = -k.s;
-        sc[nf] = -double(std::pow(c, ld(k.s) + 1.0L));
-        ++nf;
+        // F' = -c^{s+1} E_{-s}: when plain context 0 has s0 = s + 1 its table is the same E_p
+        // (ATM: Z_3 and the Hessian of Z_5); then F' = ratio * F_0 and is not tabulated
+        if (hp->nctx == 1 && std::fabs(plain[0]->k.s - (k.s + 1.0)) < 1e-14) {
+            hp->alias_fp = 1;
+            hp->alias_ratio = double(-std::pow(c, ld(k.s) + 1.0L) / std::pow(c, ld(plain[0]->k.s)));
+        } else {
+            p[nf] = -k.s;
+            sc[nf] = -double(std::pow(c, ld(k.s) + 1.0L));
+            ++nf;
+        }
         p[nf] = -k.s - 1.0;
         sc[nf] = double(std::pow(c, ld(k.s) + 2.0L));
         ++nf;
         rp = std::max(rp, std::fabs(k.rfac * k.pref));
     }
     if (nf > 4) throw Error{LZ_EINVAL, "too many functions in one plan"};
+    // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives)
+    {
+        const int rows = hp->nctx + (hess ? 2 : 0);
+        hp->t0c.assign(size_t(std::max(rows, 1)) * lz::kT0, 0.0);
+        std::vector<ld> a(lz::kT0 + 2);
+        ld rho_max = ld(first->kmax) * ld(first->kmax) * (1.0L + 1e-9L);
+        int need = 0;
+        bool ok = true;
+        auto fill = [&](const lz::CtxConst& k, int row, int deriv) {
+            for (int n = 0; n < lz::kT0 + 2; ++n) a[n] = lz::t0_coeff(k, n);
+            ld big = 0.0L;
+            std::vector<ld> cf(lz::kT0);
+            for (int n = 0; n < lz::kT0; ++n) {
+                ld v = a[n + deriv];
+                for (int j = 1; j <= deriv; ++j) v *= ld(n + j);
+                cf[n] = v;
+                big = std::max(big, std::fabs(v) * std::pow(rho_max, ld(n)));
+            }
+            int used = lz::kT0;
+            while (used > 1 && std::fabs(cf[used - 1]) * std::pow(rho_max, ld(used - 1)) <= 1e-22L * std::max(big, 1.0L))
+                --used;
+            if (used >= lz::kT0 - 2) ok = false;  // not converged within kT0 terms: disable
+            need = std::max(need, used + 2);
+            for (int n = 0; n < lz::kT0; ++n) hp->t0c[size_t(row) * lz::kT0 + n] = double(cf[n]);
+        };
+        for (int j = 0; j < hp->nctx; ++j)
+            if (plain[j]->k.branch != lz::kTrivial) fill(plain[j]->k, j, 0);
+        if (hess) {
+            fill(hess->k, hp->nctx, 1);
+            fill(hess->k, hp->nctx + 1, 2);
+        }
+        hp->n_t0 = std::min(need, lz::kT0);
+        hp->t0_rho_max = ok ? double(rho_max) : -1.0;
+    }
     if (hp->rec_q.empty()) {
         hp->tab = lz::HostTable();
         hp->tab.nfunc = nf;
@@ -235,9 +312,16 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.n_rec = int(hp.rec_q.size() / hp.d);
     P.nw = hp.nw;
     P.c = hp.c;
+    P.alias_fp = hp.alias_fp;
+    P.t0c = upload(hp.t0c, allocs);
+    P.n_t0 = hp.n_t0;
+    P.t0_rho_max = hp.t0_rho_max;
+    P.alias_ratio = hp.alias_ratio;
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
-    P.dir_n = upload(hp.dir_n, allocs);
+    P.dir_n = upload(hp.run_n, allocs);
+    P.run_info = upload(hp.run_info, allocs);
+    P.n_runs = int(hp.run_info.size() / 2);
     P.dir_w = upload(hp.dir_w, allocs);
     P.rec_q = upload(hp.rec_q, allocs);
     P.rec_norm = upload(hp.rec_norm, allocs);
@@ -720,7 +804,10 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
         pl->d = z3->h.d;
         if (pl->d > 3) throw Error{LZ_EINVAL, "ATM is defined for d <= 3"};
         pl->kind = 1;
+        if (std::fabs(z5->h.k.nu - z3->h.k.nu - 2.0) > 1e-12)
+            throw Error{LZ_EINVAL, "ATM plan needs exponents nu and nu + 2 (Z_3 and the Hessian of Z_5)"};
         build_host_plan({&z3->h}, &z5->h, &pl->hp);
+        if (!pl->hp.alias_fp) throw Error{LZ_EINVAL, "ATM plan: F' alias expected"};
         DeviceGuard dg(pl->device);
         pl->P = upload_plan(pl->hp, &pl->allocs);
     });

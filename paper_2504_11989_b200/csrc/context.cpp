@@ -588,6 +588,8 @@ void enumerate_alphas(int d, int total, std::vector<int>& cur, std::vector<int>*
 
 }  // namespace
 
+long double t0_coeff(const CtxConst& k, int n) { return t0_series_coeff(k, n); }
+
 void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals) {
     const int d = h.d;
     alphas->clear();

@@ -31,6 +31,7 @@
 namespace lz {
 
 constexpr int kTileWarps = 8;
+constexpr int kTilesPerCta = 2;
 constexpr int kTileNodes = 32 * kTileWarps;
 
 template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
@@ -41,24 +42,28 @@ template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 // force generic LD through the L1 path); the global variant only serves plans
 // whose point sets exceed the 227 KB opt-in shared memory.
 struct View {
-    const double* dir_n;
+    const double* dir_n;   // run starts
+    const int* run_info;
     const double* dir_w;
     const double* rec_q;
     const double* rec_norm;
     const double* coef;
     const int* tdir;
+    const double* t0c;
 };
 
 __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
 
 __host__ size_t plan_smem_bytes(const DevPlan& P) {
     size_t b = 0;
-    b += align16(sizeof(double) * P.n_dir * P.d);
+    b += align16(sizeof(double) * P.n_runs * P.d);
+    b += align16(sizeof(int) * P.n_runs * 2);
     b += align16(sizeof(double) * P.n_dir * P.nw);
     b += align16(sizeof(double) * P.n_rec * P.d);
     b += align16(sizeof(double) * P.n_rec);
     b += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
     b += align16(sizeof(int) * P.tab.nbins);
+    b += align16(sizeof(double) * size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
     return b;
 }
 
@@ -71,16 +76,20 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
     if constexpr (!SMEM) {
         v.dir_n = P.dir_n;
+        v.run_info = P.run_info;
         v.dir_w = P.dir_w;
         v.rec_q = P.rec_q;
         v.rec_norm = P.rec_norm;
         v.coef = P.tab.coef;
         v.tdir = P.tab.dir;
+        v.t0c = P.t0c;
         return v;
     } else {
         size_t off = 0;
         double* dn = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * P.n_dir * P.d);
+        off += align16(sizeof(double) * P.n_runs * P.d);
+        int* ri = reinterpret_cast<int*>(smem + off);
+        off += align16(sizeof(int) * P.n_runs * 2);
         double* dw = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_dir * P.nw);
         double* rq = reinterpret_cast<double*>(smem + off);
@@ -90,19 +99,25 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* cf = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
         int* td = reinterpret_cast<int*>(smem + off);
-        copy_words(dn, P.dir_n, size_t(P.n_dir) * P.d);
+        off += align16(sizeof(int) * P.tab.nbins);
+        double* tc = reinterpret_cast<double*>(smem + off);
+        copy_words(dn, P.dir_n, size_t(P.n_runs) * P.d);
+        for (int i = threadIdx.x; i < 2 * P.n_runs; i += blockDim.x) ri[i] = P.run_info[i];
         copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
         copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
         copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
         for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
+        copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
         __syncthreads();
         v.dir_n = dn;
+        v.run_info = ri;
         v.dir_w = dw;
         v.rec_q = rq;
         v.rec_norm = rn;
         v.coef = cf;
         v.tdir = td;
+        v.t0c = tc;
         return v;
     }
 }
@@ -191,6 +206,13 @@ __device__ inline double t0_reg(const CtxConst& C, double rho) {
     return -C.pi_over_t_pow_s * acc;
 }
 
+// Horner over the first n coefficients of a power series in rho (shared-memory row).
+__device__ __forceinline__ double series(const double* c, int n, double rho) {
+    double acc = 0.0;
+    for (int i = n - 1; i >= 0; --i) acc = fma(acc, rho, c[i]);
+    return acc;
+}
+
 // Singular part shat(nu, k) (L/epstein.py:217-231).
 __device__ inline double singular(const CtxConst& C, double rho) {
     if (C.branch == kTrivial) return 0.0;
@@ -206,33 +228,49 @@ __device__ inline double singular(const CtxConst& C, double rho) {
 // Node evaluation.  kap = fractional coordinates (A^T k), k Cartesian.
 // Lanes gl = 0..G-1 of a group split the point loops; the result is complete
 // (identical) on every lane of the group.
-template <int D, int NCTX, bool HESS> struct NodeAcc {
+template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
     static constexpr int NS = HESS ? Sym<D>::n : 0;
     static constexpr int NW = NCTX + NS;
-    static constexpr int NF = NCTX + (HESS ? 2 : 0);
+    // ALIAS: F' of the Hessian context is a multiple of plain table 0 (ATM: nu_plain = nu_hess - 2,
+    // both E_{1-s}); only F'' is tabulated for the Hessian
+    static constexpr int NF = NCTX + (HESS ? (ALIAS ? 1 : 2) : 0);
+    static constexpr int FPP = NCTX + (ALIAS ? 0 : 1);
     double z[NCTX > 0 ? NCTX : 1];
     double h[HESS ? Sym<D>::n : 1];
 };
 
-template <int D, int NCTX, bool HESS>
+template <int D, int NCTX, bool HESS, bool ALIAS = false>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
-                                          NodeAcc<D, NCTX, HESS>& out) {
-    using Acc = NodeAcc<D, NCTX, HESS>;
+                                          NodeAcc<D, NCTX, HESS, ALIAS>& out) {
+    using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
     constexpr int NW = Acc::NW;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
     double dacc[NW];
 #pragma unroll
     for (int c = 0; c < NW; ++c) dacc[c] = 0.0;
-    // direct space: sum over half-lattice points of w * cos(2 pi kappa.n)
-    for (int i = gl; i < P.n_dir; i += G) {
-        double ph = 0.0;
+    // direct space: sum over half-lattice points of w * cos(2 pi kappa.n), walked as runs of
+    // consecutive n_d: one sincospi per run, then rotation by exp(2 pi i kappa_d) per point
+    {
+        double sd, cd;
+        sincospi(2.0 * kap[D - 1], &sd, &cd);
+        for (int r = gl; r < P.n_runs; r += G) {
+            double ph = 0.0;
 #pragma unroll
-        for (int a = 0; a < D; ++a) ph = fma(kap[a], V.dir_n[i * D + a], ph);
-        const double cs = cospi(2.0 * ph);
+            for (int a = 0; a < D; ++a) ph = fma(kap[a], V.dir_n[r * D + a], ph);
+            double sn, cs;
+            sincospi(2.0 * ph, &sn, &cs);
+            const int first = V.run_info[2 * r], len = V.run_info[2 * r + 1];
+            const double* w = V.dir_w + size_t(first) * NW;
+            for (int l = 0; l < len; ++l) {
 #pragma unroll
-        for (int c = 0; c < NW; ++c) dacc[c] = fma(V.dir_w[i * NW + c], cs, dacc[c]);
+                for (int c = 0; c < NW; ++c) dacc[c] = fma(w[l * NW + c], cs, dacc[c]);
+                const double c2 = fma(cs, cd, -sn * sd);
+                sn = fma(sn, cd, cs * sd);
+                cs = c2;
+            }
+        }
     }
     // reciprocal space: sum over q != 0 of F(|k+q|^2) (and F', F'' y_a y_b)
     double racc[NCTX > 0 ? NCTX : 1];
@@ -266,10 +304,10 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
         if constexpr (HESS) {
-            g1 += f[NCTX];
+            if constexpr (!ALIAS) g1 += f[NCTX];
             double fy[D];
 #pragma unroll
-            for (int a = 0; a < D; ++a) fy[a] = f[NCTX + 1] * y[a];
+            for (int a = 0; a < D; ++a) fy[a] = f[Acc::FPP] * y[a];
             int c = 0;
 #pragma unroll
             for (int a = 0; a < D; ++a)
@@ -309,7 +347,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         } else {
             zv = C.bconst;
             zv += 2.0 * dacc[j];
-            zv += C.rfac * (t0_reg(C, rho) + racc[j]);
+            const double t0 = rho <= P.t0_rho_max ? series(V.t0c + j * kT0, P.n_t0, rho) : t0_reg(C, rho);
+            zv += C.rfac * (t0 + racc[j]);
             zv *= C.pref;
             if (!reg_only && rho >= 1e-28) zv += singular(C, rho) * C.inv_vol;
         }
@@ -319,10 +358,33 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         const CtxConst& C = P.hctx;
         // q = 0 term of the unsplit reciprocal sum, evaluated directly:
         //   F'(rho) = -c^{s+1} E_{-s}(c rho),  F''(rho) = c^{s+2} E_{-s-1}(c rho)
-        const double x0 = C.c * rho;
-        const double fp = -pow(C.c, C.s + 1.0) * expint_dev(-C.s, x0);
-        const double fpp = pow(C.c, C.s + 2.0) * expint_dev(-C.s - 1.0, x0);
-        const double G1 = g1 + fp;
+        // F = t0_reg + shat / (V pref rfac): its rho-derivatives from the series of t0_reg and
+        // the closed-form singular part (k in the BZ), else E_p directly
+        double fp, fpp;
+        if (rho <= P.t0_rho_max && rho > 0.0) {
+            const double kk = C.sing_coef * C.inv_vol / (C.pref * C.rfac);
+            double s1, s2;
+            if (C.branch == kLogCase) {
+                const int m = C.log_m;
+                double rm1 = 1.0;  // rho^{m-1}
+                if (m == 0) rm1 = 1.0 / rho;
+                for (int i = 1; i < m; ++i) rm1 *= rho;
+                const double L = log(kPi * rho);
+                s1 = kk * rm1 * (double(m) * L + 1.0);
+                s2 = kk * (rm1 / rho) * (double(m * (m - 1)) * L + double(2 * m - 1));
+            } else {
+                const double p1 = pow(rho, -C.s - 1.0);
+                s1 = -kk * C.s * p1;
+                s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
+            }
+            fp = series(V.t0c + NCTX * kT0, P.n_t0, rho) + s1;
+            fpp = series(V.t0c + (NCTX + 1) * kT0, P.n_t0, rho) + s2;
+        } else {
+            const double x0 = C.c * rho;
+            fp = -pow(C.c, C.s + 1.0) * expint_dev(-C.s, x0);
+            fpp = pow(C.c, C.s + 2.0) * expint_dev(-C.s - 1.0, x0);
+        }
+        const double G1 = (ALIAS ? P.alias_ratio * racc[0] : g1) + fp;
         constexpr double k8pi2 = 8.0 * kPi * kPi;
         int c = 0;
 #pragma unroll
@@ -437,21 +499,27 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
+// One CTA = kTilesPerCta tiles of 8 warps sharing ONE staged copy of the plan
+// (the ATM plan is ~115 KB, so two 256-thread CTAs no longer fit one SM).
 template <int D, int NCTX, bool HESS, int MODE, bool SMEM>
-__global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
+__global__ void __launch_bounds__(32 * kTileWarps * kTilesPerCta, 1)
+    tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
-    __shared__ double wsum[kTileWarps][NCOMP];
+    __shared__ double wsum[kTilesPerCta][kTileWarps][NCOMP];
     const View V = stage<SMEM>(P, smem);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = warp_all / kTileWarps, warp = warp_all % kTileWarps;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
-    for (int64_t tile = g.tile_lo + blockIdx.x; tile < g.tile_hi; tile += gridDim.x) {
+    for (int64_t base = g.tile_lo + int64_t(blockIdx.x) * kTilesPerCta; base < g.tile_hi;
+         base += int64_t(gridDim.x) * kTilesPerCta) {
+        const int64_t tile = base + sub;
         const int64_t patch = tile * kTileWarps + warp;
         double val[NCOMP];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
         double t[D], weight = 0.0, u = 0.0;
-        const bool ok = patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
+        const bool ok = tile < g.tile_hi && patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
         if (!ok) {  // padding lane: a harmless interior node with zero weight
 #pragma unroll
             for (int a = 0; a < D; ++a) t[a] = 1.0;
@@ -469,8 +537,8 @@ __global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mu
                 k[a] = u * s;       // k = u * w, w = A^{-T} t   (L/quadrature.py:143-152, 417)
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
-            NodeAcc<D, NCTX, HESS> acc;
-            eval_node<D, NCTX, HESS>(P, V, kap, k, 0, 1, 0u, acc);
+            NodeAcc<D, NCTX, HESS, MODE == 1> acc;
+            eval_node<D, NCTX, HESS, MODE == 1>(P, V, kap, k, 0, 1, 0u, acc);
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll
@@ -520,13 +588,14 @@ __global__ void __launch_bounds__(256) tile_kernel(DevPlan P, DevGrid g, int4 mu
             double v = val[c];
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            if (lane == 0) wsum[warp][c] = v;
+            if (lane == 0) wsum[sub][warp][c] = v;
         }
         __syncthreads();
-        if (threadIdx.x < NCOMP) {
+        if (threadIdx.x < NCOMP * kTilesPerCta) {
+            const int ts = threadIdx.x / NCOMP, c = threadIdx.x % NCOMP;
             double s = 0.0;
-            for (int w = 0; w < kTileWarps; ++w) s += wsum[w][threadIdx.x];
-            partials[tile * NCOMP + threadIdx.x] = s;
+            for (int w = 0; w < kTileWarps; ++w) s += wsum[ts][w][c];
+            if (base + ts < g.tile_hi) partials[(base + ts) * NCOMP + c] = s;
         }
         __syncthreads();
     }
@@ -664,8 +733,8 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
     }
-    const int threads = 32 * kTileWarps;
-    int64_t need = g.tile_hi - g.tile_lo;
+    const int threads = 32 * kTileWarps * kTilesPerCta;
+    int64_t need = (g.tile_hi - g.tile_lo + kTilesPerCta - 1) / kTilesPerCta;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;

@@ -19,6 +19,7 @@ constexpr int kNC = kDeg + 1;
 constexpr int kNCP = 10;       // padded coefficient stride (16-byte aligned double2 loads)
 constexpr double kBinWidth = 0.25;  // directory bin width in x = c |y|^2
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
+constexpr int kT0 = 64;             // max terms of the q = 0 power series
 
 // ---------------------------------------------------------------------------
 // Per-(lattice, nu) constants of the Crandall split (L/epstein.py:99-122, 202-259).
@@ -57,10 +58,22 @@ struct DevPlan {
     int nw;            // direct weight channels per point
     int pad_;
     double c;          // pi / split, shared by every context of the plan
+    // q = 0 term as power series in rho = |k|^2 (valid for rho <= t0_rho_max, i.e. k in the BZ):
+    // rows [0, nctx): t0_reg of each plain context; rows nctx, nctx+1: d/drho and d2/drho2 of
+    // the Hessian context's t0_reg.  kT0 coefficients per row, n_t0 of them used.
+    const double* t0c;
+    int n_t0;
+    int pad4_;
+    double t0_rho_max;
+    int alias_fp;      // 1: the Hessian's F' equals alias_ratio * (plain table 0); F' not tabulated
+    int pad2_;
+    double alias_ratio;
     double A[16];      // generator, row-major (columns = basis vectors)
     double B[16];      // A^{-T}, row-major
-    const double* dir_n;   // [n_dir][d] integer coordinates (as double)
-    const double* dir_w;   // [n_dir][nw] weights: nctx plain channels, then (hess) d(d+1)/2
+    const double* dir_n;   // [n_runs][d] integer coordinates of the first point of each run
+    const int* run_info;   // [n_runs][2] (first point, length): runs of consecutive n_d
+    int n_runs, pad3_;
+    const double* dir_w;   // [n_dir][nw] weights (run order): nctx plain channels, then (hess) d(d+1)/2
     const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0, sorted by |q|
     const double* rec_norm;  // [n_rec] |q| ascending
     double r_cut;          // |k+q| > r_cut  =>  every table function is exactly zero
@@ -147,6 +160,7 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
                  double rfac_pref, HostTable* out);
 double table_x_lo(const HostCtx& h);
+long double t0_coeff(const CtxConst& k, int n);   // rho-series coefficient of t0_reg
 void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals);
 void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* w);  // on [-1, 1]
 
