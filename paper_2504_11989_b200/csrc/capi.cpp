@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -440,8 +441,13 @@ void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
     dg->n_u = g->n_u;
     dg->n_v = d > 1 ? g->n_v : 1;
     dg->n_cell = (1 << (d - 1)) * d;
-    dg->pu = d > 1 ? 4 : 32;
-    dg->pv = d > 1 ? 8 : 1;
+    // warp patch: pu radial x pv angular nodes (pu * pv = 32); compact patches keep the
+    // per-warp culling radius and the table pieces of the 32 lanes close together
+    int pu = 4;
+    if (const char* e = std::getenv("LATSUM_PATCH_U")) pu = std::atoi(e);
+    if (pu != 1 && pu != 2 && pu != 4 && pu != 8 && pu != 16 && pu != 32) pu = 4;
+    dg->pu = d > 1 ? pu : 32;
+    dg->pv = d > 1 ? 32 / pu : 1;
     dg->npu = (dg->n_u + dg->pu - 1) / dg->pu;
     dg->npv = d > 1 ? (dg->n_v + dg->pv - 1) / dg->pv : 1;
     dg->nv2 = d > 2 ? dg->n_v : 1;

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from collections import Counter
 from dataclasses import dataclass
 from functools import lru_cache
@@ -218,9 +219,18 @@ def product_plan(lattice: Lattice, nus_key: tuple, splitting: float | None = Non
     return Plan(h, lattice.d, 1, ctxs)
 
 
+# Theta-split used by the fused ATM plan, as a multiple of the reference's V^(-2/d)
+# (L/epstein.py:107).  The lattice sum is split-invariant; a smaller split moves work from the
+# reciprocal sum (table lookups, ~64 instructions per term) to the direct sum (phase rotations,
+# ~18 per point).  Measured on B200: see DESIGN.md section 3.2.
+ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "1.0"))
+
+
 @lru_cache(maxsize=64)
 def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
     """Plan for the ATM integrand [Z_3^3, tr(M_5^3)], M_5 = polynomial-weighted zeta at nu = 5."""
+    if splitting is None and ATM_SPLIT_SCALE != 1.0:
+        splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
     z3 = epstein_context(lattice, 3.0, splitting)
     z5 = epstein_context(lattice, 5.0, splitting)
     h = C.c_void_p()
