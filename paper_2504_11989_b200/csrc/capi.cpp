@@ -335,6 +335,9 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.x_lo = hp.tab.x_lo;
     P.tab.inv_hb = hp.tab.inv_hb;
     P.tab.x_hi = hp.tab.x_hi;
+    P.tab.c = hp.c;
+    P.tab.r_scale = hp.c * hp.tab.inv_hb;
+    P.tab.x_off = hp.tab.x_lo * hp.tab.inv_hb;
     for (int j = 0; j < 4; ++j) {
         P.tab.p[j] = hp.tab.p[j];
         P.tab.scale[j] = hp.tab.scale[j];
@@ -443,9 +446,9 @@ void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
     dg->n_cell = (1 << (d - 1)) * d;
     // warp patch: pu radial x pv angular nodes (pu * pv = 32); compact patches keep the
     // per-warp culling radius and the table pieces of the 32 lanes close together
-    int pu = 4;
+    int pu = 1;  // measured best on B200 for the fcc ATM grid
     if (const char* e = std::getenv("LATSUM_PATCH_U")) pu = std::atoi(e);
-    if (pu != 1 && pu != 2 && pu != 4 && pu != 8 && pu != 16 && pu != 32) pu = 4;
+    if (pu != 1 && pu != 2 && pu != 4 && pu != 8 && pu != 16 && pu != 32) pu = 1;
     dg->pu = d > 1 ? pu : 32;
     dg->pv = d > 1 ? 32 / pu : 1;
     dg->npu = (dg->n_u + dg->pu - 1) / dg->pu;

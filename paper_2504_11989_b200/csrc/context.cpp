@@ -467,6 +467,13 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     for (unsigned t = 1; t < nth; ++t) pool.emplace_back(worker);
     worker();
     for (auto& th : pool) th.join();
+    // Direct (unfitted) bins must form a prefix: the kernel's conversion-free floor may step one
+    // piece past a bin's last piece at an exact bin boundary, which is then the next bin's first
+    // piece evaluated at the same x -- valid only if that next bin has pieces.
+    int last_direct = -1;
+    for (int b = 0; b < nbins; ++b)
+        if (fits[b].level == kDirectMarker) last_direct = b;
+    for (int b = 0; b < last_direct; ++b) fits[b].level = kDirectMarker;
     int npieces = 0;
     for (int b = 0; b < nbins; ++b) {
         const BinFit& bf = fits[b];

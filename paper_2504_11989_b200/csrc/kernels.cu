@@ -138,29 +138,38 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 
 // ---------------------------------------------------------------------------
 // Table lookup: NF functions of x sharing one directory.
+// floor(y) for 0 <= y < 2^31 without FP64<->int conversions: y - 1/2 + 1.5*2^52 rounds to the
+// integer in the low word.  At exact integers the tie may yield y - 1 with fractional part 1,
+// i.e. tau = +1 at the end of the previous piece -- equally valid.
+constexpr double kMagic = 6755399441055744.0;
+
 template <int NF>
-__device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, double x, double (&f)[NF]) {
-    const double xb = (x - T.x_lo) * T.inv_hb;
+__device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, double r, double (&f)[NF]) {
+    const double xb = fma(r, T.r_scale, -T.x_off);  // (c r - x_lo) / h
     if (xb >= double(T.nbins)) {
 #pragma unroll
         for (int j = 0; j < NF; ++j) f[j] = 0.0;
         return;
     }
     int e = kDirectMarker;
-    int b = 0;
+    double tb = 0.0;
     if (xb >= 0.0) {
-        b = int(xb);
-        e = V.tdir[b];
+        tb = (xb - 0.5) + kMagic;
+        e = V.tdir[__double2loint(tb)];
     }
     if ((e & 15) == kDirectMarker) {
+        const double x = r * T.c;
 #pragma unroll
         for (int j = 0; j < NF; ++j) f[j] = T.scale[j] * expint_dev(T.p[j], x);
         return;
     }
     const int L = e & 15;
-    const double fs = (xb - double(b)) * double(1 << L);
-    const int sub = int(fs);
-    const TauPowers tp = tau_powers(2.0 * (fs - double(sub)) - 1.0);
+    // 2^L assembled from its exponent bits (no conversion)
+    const double two_l = __hiloint2double((1023 + L) << 20, 0);
+    const double fs = (xb - (tb - kMagic)) * two_l;
+    const double ts = (fs - 0.5) + kMagic;
+    const int sub = __double2loint(ts);
+    const TauPowers tp = tau_powers(2.0 * (fs - (ts - kMagic)) - 1.0);
     const double2* c = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * NF * kNCP);
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
@@ -300,7 +309,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             r = fma(y[a], y[a], r);
         }
         double f[NF];
-        tab_eval<NF>(P.tab, V, cc * r, f);
+        tab_eval<NF>(P.tab, V, r, f);
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
         if constexpr (HESS) {

@@ -44,6 +44,7 @@ struct DevTable {
     const double* coef;    // [piece][nfunc][kNC], monomials in tau in [-1, 1]
     int nbins, nfunc, npieces, pad_;
     double x_lo, inv_hb, x_hi;
+    double c, r_scale, x_off;  // x = c rho;  bin coordinate xb = rho * r_scale - x_off
     double p[4], scale[4]; // for the direct fallback
 };
 
