@@ -338,6 +338,11 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.c = hp.c;
     P.tab.r_scale = hp.c * hp.tab.inv_hb;
     P.tab.x_off = hp.tab.x_lo * hp.tab.inv_hb;
+    P.tab.xb_max = double(hp.tab.nbins) - 1.0 / 1048576.0;
+    P.tab.any_direct = 0;
+    for (int e : hp.tab.dir)
+        if ((e & 15) == lz::kDirectMarker) P.tab.any_direct = 1;
+    if (hp.tab.nbins == 0) P.tab.any_direct = 1;  // no table: never evaluated (no q points)
     for (int j = 0; j < 4; ++j) {
         P.tab.p[j] = hp.tab.p[j];
         P.tab.scale[j] = hp.tab.scale[j];

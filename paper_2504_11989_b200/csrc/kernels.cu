@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "lz_internal.h"
 #include "special.cuh"
@@ -142,6 +143,33 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 // integer in the low word.  At exact integers the tie may yield y - 1 with fractional part 1,
 // i.e. tau = +1 at the end of the previous piece -- equally valid.
 constexpr double kMagic = 6755399441055744.0;
+
+// Branch-free variant for tables without direct-evaluation bins (every practical lattice):
+// out-of-range lanes evaluate the last piece and are zeroed by a select, so the unrolled
+// q-loop is one basic block and two terms' Estrin chains interleave.
+template <int NF>
+__device__ __forceinline__ void tab_eval_fast(const DevTable& T, const View& V, double r, double (&f)[NF]) {
+    const double xb_raw = fma(r, T.r_scale, -T.x_off);
+    const bool far = xb_raw >= T.xb_max;
+    const double xb = far ? T.xb_max : xb_raw;
+    const double tb = (xb - 0.5) + kMagic;
+    const int e = V.tdir[__double2loint(tb)];
+    const int L = e & 15;
+    const double two_l = __hiloint2double((1023 + L) << 20, 0);
+    const double fs = (xb - (tb - kMagic)) * two_l;
+    const double ts = (fs - 0.5) + kMagic;
+    const int sub = __double2loint(ts);
+    const TauPowers tp = tau_powers(2.0 * (fs - (ts - kMagic)) - 1.0);
+    const double2* c = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * NF * kNCP);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        const double2 c01 = c[j * 5 + 0], c23 = c[j * 5 + 1], c45 = c[j * 5 + 2];
+        const double2 c67 = c[j * 5 + 3], c89 = c[j * 5 + 4];
+        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c89.x};
+        const double v = estrin8(cc, tp);
+        f[j] = far ? 0.0 : v;
+    }
+}
 
 template <int NF>
 __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, double r, double (&f)[NF]) {
@@ -300,8 +328,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
     const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
-#pragma unroll 2
-    for (int i = gl; i < n_eff; i += G) {
+    auto term = [&](int i, auto fast) {
         double y[D], r = 0.0;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -309,7 +336,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             r = fma(y[a], y[a], r);
         }
         double f[NF];
-        tab_eval<NF>(P.tab, V, r, f);
+        if constexpr (decltype(fast)::value) tab_eval_fast<NF>(P.tab, V, r, f);
+        else tab_eval<NF>(P.tab, V, r, f);
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
         if constexpr (HESS) {
@@ -326,6 +354,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                     ++c;
                 }
         }
+    };
+    if (P.tab.any_direct) {
+        for (int i = gl; i < n_eff; i += G) term(i, std::false_type{});
+    } else {
+#pragma unroll 2
+        for (int i = gl; i < n_eff; i += G) term(i, std::true_type{});
     }
     if (G > 1) {
         for (int off = G >> 1; off > 0; off >>= 1) {

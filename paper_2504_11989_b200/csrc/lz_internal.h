@@ -45,6 +45,8 @@ struct DevTable {
     int nbins, nfunc, npieces, pad_;
     double x_lo, inv_hb, x_hi;
     double c, r_scale, x_off;  // x = c rho;  bin coordinate xb = rho * r_scale - x_off
+    double xb_max;             // largest bin coordinate evaluated (nbins - 2^-20)
+    int any_direct, pad5_;     // 1 if some bin is evaluated directly (slow, branchy path)
     double p[4], scale[4]; // for the direct fallback
 };
 
