@@ -339,7 +339,10 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.r_scale = hp.c * hp.tab.inv_hb;
     P.tab.x_off = hp.tab.x_lo * hp.tab.inv_hb;
     P.tab.xb_max = double(hp.tab.nbins) - 1.0 / 1048576.0;
-    P.tab.any_direct = 0;
+    // branch-free lookup is opt-in (LATSUM_BRANCHFREE=1): measured 6% slower on the fcc ATM grid,
+    // where lanes beyond the cutoff would otherwise skip the polynomial entirely
+    const char* bf = std::getenv("LATSUM_BRANCHFREE");
+    P.tab.any_direct = (bf && std::atoi(bf) == 1) ? 0 : 1;
     for (int e : hp.tab.dir)
         if ((e & 15) == lz::kDirectMarker) P.tab.any_direct = 1;
     if (hp.tab.nbins == 0) P.tab.any_direct = 1;  // no table: never evaluated (no q points)
@@ -580,9 +583,16 @@ void ensure_plain(const lz_ctx* cc) {
     c->plain_ready = true;
 }
 
+void ensure_hess_sets(const lz_ctx* cc) {
+    lz_ctx* c = const_cast<lz_ctx*>(cc);
+    if (!c->h.want_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+    std::lock_guard<std::mutex> lock(c->mu);
+    lz::build_hess_sets(c->h);
+}
+
 void ensure_hess(const lz_ctx* cc) {
     lz_ctx* c = const_cast<lz_ctx*>(cc);
-    if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
+    ensure_hess_sets(cc);
     std::lock_guard<std::mutex> lock(c->mu);
     if (c->hess_ready) return;
     build_host_plan({}, &c->h, &c->hessp);
@@ -656,7 +666,7 @@ int lz_ctx_get_info(const lz_ctx* c, lz_ctx_info* o) {
     o->const_value = k.const_value;
     o->n_dir = int64_t(c->h.dir_w.size());
     o->n_rec = int64_t(c->h.rec_q.size() / c->h.d);
-    o->n_dir_h = int64_t(c->h.hdir_w.size());
+    o->n_dir_h = int64_t(c->h.hdir_w.size());  // 0 until the Hessian sets are built (lazy)
     o->n_rec_h = int64_t(c->h.hrec_q.size() / c->h.d);
     // table statistics are reported once the tables exist (lz_ctx_prepare)
     o->table_x_lo = c->plain.tab.x_lo;
@@ -668,6 +678,10 @@ int lz_ctx_get_info(const lz_ctx* c, lz_ctx_info* o) {
 }
 
 int lz_ctx_get_points(const lz_ctx* c, int which, double* dst, int64_t cap, int64_t* size) {
+    if (which >= 3 && which <= 5) {
+        int rc = guarded([&] { ensure_hess_sets(c); });
+        if (rc != LZ_OK) return rc;
+    }
     const std::vector<double>* v = nullptr;
     switch (which) {
         case 0: v = &c->h.dir_z; break;
@@ -741,7 +755,6 @@ int lz_zeta_hessian(const lz_ctx* c, const double* k, int64_t n, double* out, in
 int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* out) {
     return guarded([&] {
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
-        if (!c->h.has_hess) throw Error{LZ_EINVAL, "context was created without Hessian tables (deriv_order < 2)"};
         for (int64_t i = 0; i < n * c->h.d; ++i)
             if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
         if (n == 0) return;
@@ -810,7 +823,8 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
     *out = nullptr;
     lz_plan* pl = new lz_plan();
     int rc = guarded([&] {
-        if (!z5->h.has_hess) throw Error{LZ_EINVAL, "the nu = 5 context needs deriv_order >= 2"};
+        if (!z5->h.want_hess) throw Error{LZ_EINVAL, "the nu = 5 context needs deriv_order >= 2"};
+        ensure_hess_sets(z5);
         if (z3->h.k.branch == lz::kTrivial || z5->h.k.branch == lz::kTrivial)
             throw Error{LZ_EINVAL, "ATM contexts cannot be trivial"};
         pl->device = z3->device;

@@ -290,13 +290,16 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
     }
     enumerate_direct(*h, 0, kTermCutoff, &h->dir_n, &h->dir_z, &h->dir_w);
     enumerate_reciprocal(*h, k.s, kTermCutoff, &h->rec_n, &h->rec_q);
-    if (deriv_order >= 2) {
-        // Hessian sets: the derivative-table enumerators of L/epstein.py:376-377
-        // specialised to second order (z^alpha weight |z|^2, gamma order s + 2).
-        h->has_hess = 1;
-        enumerate_direct(*h, 2, kTermCutoff, &h->hdir_n, &h->hdir_z, &h->hdir_w);
-        enumerate_reciprocal(*h, k.s + 2.0, kTermCutoff, &h->hrec_n, &h->hrec_q);
-    }
+    h->want_hess = deriv_order >= 2 ? 1 : 0;  // Hessian sets are enumerated on first use
+}
+
+void build_hess_sets(HostCtx& h) {
+    if (h.has_hess || !h.want_hess || h.k.branch == kTrivial) return;
+    // Hessian sets: the derivative-table enumerators of L/epstein.py:376-377
+    // specialised to second order (z^alpha weight |z|^2, gamma order s + 2).
+    enumerate_direct(h, 2, kTermCutoff, &h.hdir_n, &h.hdir_z, &h.hdir_w);
+    enumerate_reciprocal(h, h.k.s + 2.0, kTermCutoff, &h.hrec_n, &h.hrec_q);
+    h.has_hess = 1;
 }
 
 // Rigorous lower bound of x = c |k + q|^2 over k in the BZ box and q != 0:

@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "lz_internal.h"
@@ -276,7 +278,7 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
     double h[HESS ? Sym<D>::n : 1];
 };
 
-template <int D, int NCTX, bool HESS, bool ALIAS = false>
+template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out) {
@@ -356,9 +358,10 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         }
     };
     if (P.tab.any_direct) {
+#pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::false_type{});
     } else {
-#pragma unroll 2
+#pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::true_type{});
     }
     if (G > 1) {
@@ -542,11 +545,12 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
-// One CTA = kTilesPerCta tiles of 8 warps sharing ONE staged copy of the plan
+// One CTA = TPC tiles of 8 warps sharing ONE staged copy of the plan
 // (the ATM plan is ~115 KB, so two 256-thread CTAs no longer fit one SM).
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM>
-__global__ void __launch_bounds__(32 * kTileWarps * kTilesPerCta, 1)
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC = kTilesPerCta, int UNR = 2>
+__global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
     tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
+    constexpr int kTilesPerCta = TPC;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
     __shared__ double wsum[kTilesPerCta][kTileWarps][NCOMP];
@@ -581,7 +585,7 @@ __global__ void __launch_bounds__(32 * kTileWarps * kTilesPerCta, 1)
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
-            eval_node<D, NCTX, HESS, MODE == 1>(P, V, kap, k, 0, 1, 0u, acc);
+            eval_node<D, NCTX, HESS, MODE == 1, UNR>(P, V, kap, k, 0, 1, 0u, acc);
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll
@@ -767,17 +771,17 @@ cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n
     return cudaErrorInvalidValue;
 }
 
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM>
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC, int UNR>
 static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
-    auto kern = tile_kernel<D, NCTX, HESS, MODE, SMEM>;
+    auto kern = tile_kernel<D, NCTX, HESS, MODE, SMEM, TPC, UNR>;
     size_t sm = SMEM ? bytes : 0;
     if (SMEM) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
     }
-    const int threads = 32 * kTileWarps * kTilesPerCta;
-    int64_t need = (g.tile_hi - g.tile_lo + kTilesPerCta - 1) / kTilesPerCta;
+    const int threads = 32 * kTileWarps * TPC;
+    int64_t need = (g.tile_hi - g.tile_lo + TPC - 1) / TPC;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
@@ -785,13 +789,38 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
     return cudaGetLastError();
 }
 
+// ATM kernel shape (tiles per CTA x q-unroll), overridable for tuning sweeps: LATSUM_ATM_SHAPE
+// in {"2x2" (default), "2x1", "3x1", "3x2"}.
+static int atm_shape() {
+    static int shape = -1;
+    if (shape < 0) {
+        shape = 22;
+        if (const char* e = std::getenv("LATSUM_ATM_SHAPE")) {
+            if (!std::strcmp(e, "2x1")) shape = 21;
+            if (!std::strcmp(e, "3x1")) shape = 31;
+            if (!std::strcmp(e, "3x2")) shape = 32;
+        }
+    }
+    return shape;
+}
+
 template <int D, int NCTX, bool HESS, int MODE>
 static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st) {
     const size_t bytes = plan_smem_bytes(P);
-    if (bytes + 2048 <= size_t(smem_optin()))
-        return launch_tile_s<D, NCTX, HESS, MODE, true>(P, g, mult, partials, grid_blocks, st, bytes);
-    return launch_tile_s<D, NCTX, HESS, MODE, false>(P, g, mult, partials, grid_blocks, st, bytes);
+    const bool smem = bytes + 2048 <= size_t(smem_optin());
+    if constexpr (MODE == 1 && D == 3) {
+        if (smem) {
+            switch (atm_shape()) {
+                case 21: return launch_tile_s<D, NCTX, HESS, MODE, true, 2, 1>(P, g, mult, partials, grid_blocks, st, bytes);
+                case 31: return launch_tile_s<D, NCTX, HESS, MODE, true, 3, 1>(P, g, mult, partials, grid_blocks, st, bytes);
+                case 32: return launch_tile_s<D, NCTX, HESS, MODE, true, 3, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                default: break;
+            }
+        }
+    }
+    if (smem) return launch_tile_s<D, NCTX, HESS, MODE, true, kTilesPerCta, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+    return launch_tile_s<D, NCTX, HESS, MODE, false, kTilesPerCta, 2>(P, g, mult, partials, grid_blocks, st, bytes);
 }
 
 cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, double* partials, int grid_blocks,

@@ -106,7 +106,8 @@ struct HostCtx {
     std::vector<double> dir_n, dir_z, dir_w;   // n (int coords), z = A n, weights
     std::vector<double> rec_n, rec_q;          // n, q = B n
     // widened sets for the Hessian (poly_order = 2, gamma order s + 2)
-    int has_hess = 0;
+    int want_hess = 0;   // requested at creation (deriv_order >= 2)
+    int has_hess = 0;    // sets enumerated
     std::vector<double> hdir_n, hdir_z, hdir_w;
     std::vector<double> hrec_n, hrec_q;
 };
@@ -163,6 +164,7 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
                  double rfac_pref, HostTable* out);
 double table_x_lo(const HostCtx& h);
+void build_hess_sets(HostCtx& h);
 long double t0_coeff(const CtxConst& k, int n);   // rho-series coefficient of t0_reg
 void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals);
 void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* w);  // on [-1, 1]

@@ -110,7 +110,7 @@ class EpsteinContext:
         self.dir_w = self._points(1)
         self.rec_pts = self._points(2).reshape(-1, d)
         self.rec_norm2 = np.einsum("ij,ij->i", self.rec_pts, self.rec_pts)
-        self.has_hessian = info.n_rec_h > 0
+        self.has_hessian = deriv_order >= 2  # Hessian point sets and tables are built on first use
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -104,7 +104,7 @@ def test_native_context_matches_reference(golden, idx):
 
 def test_hessian_point_sets():
     for name, nu, hd, hr in (("fcc", 5.0, 171, 1330), ("bcc", 5.0, 364, 2196)):
-        info = EpsteinContext(named_lattice(name), nu, device=-1).info
+        info = EpsteinContext(named_lattice(name), nu, device=-1).table_stats(hessian=True)
         assert (info.n_dir_h, info.n_rec_h) == (hd, hr)
 
 
