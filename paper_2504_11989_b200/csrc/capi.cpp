@@ -194,7 +194,10 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             hp->dir_w[i * hp->nw + j] = double(direct_weight(*c, n, z));
         }
         if (hess) {
-            ld w = direct_weight(*hess, n, z);
+            // direct Hessian term -8 pi^2 w z_a z_b cos(.), stored divided by 4 rfac so that it
+            // shares the kernel's reciprocal accumulators (sum of y_a y_b F'')
+            const ld scale = -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac);
+            ld w = direct_weight(*hess, n, z) * scale;
             int cidx = 0;
             for (int a = 0; a < d; ++a)
                 for (int b = a; b < d; ++b) hp->dir_w[i * hp->nw + hp->nctx + cidx++] = double(w * z[a] * z[b]);

@@ -34,7 +34,7 @@
 namespace lz {
 
 constexpr int kTileWarps = 8;
-constexpr int kTilesPerCta = 2;
+constexpr int kTilesPerCta = 3;
 constexpr int kTileNodes = 32 * kTileWarps;
 
 template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
@@ -316,9 +316,11 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
     for (int j = 0; j < NCTX; ++j) racc[j] = 0.0;
     double g1 = 0.0;
+    // The Hessian's direct-space channels arrive pre-scaled by -2 pi^2 / rfac (host), so they
+    // seed the reciprocal accumulators: one register set of d(d+1)/2 instead of two.
     double yy[NS > 0 ? NS : 1];
 #pragma unroll
-    for (int c = 0; c < NS; ++c) yy[c] = 0.0;
+    for (int c = 0; c < NS; ++c) yy[c] = dacc[NCTX + c];
     const double cc = P.c;  // all contexts of a plan share the split
     // Exact per-warp culling: |k+q| >= |q| - |k|, and every table function is
     // identically zero beyond x_hi, i.e. for |k+q| > r_cut.  The points are
@@ -367,7 +369,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     if (G > 1) {
         for (int off = G >> 1; off > 0; off >>= 1) {
 #pragma unroll
-            for (int c = 0; c < NW; ++c) dacc[c] += __shfl_xor_sync(0xffffffffu, dacc[c], off);
+            for (int c = 0; c < NCTX; ++c) dacc[c] += __shfl_xor_sync(0xffffffffu, dacc[c], off);
 #pragma unroll
             for (int j = 0; j < NCTX; ++j) racc[j] += __shfl_xor_sync(0xffffffffu, racc[j], off);
             if constexpr (HESS) {
@@ -431,15 +433,14 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             fpp = pow(C.c, C.s + 2.0) * expint_dev(-C.s - 1.0, x0);
         }
         const double G1 = (ALIAS ? P.alias_ratio * racc[0] : g1) + fp;
-        constexpr double k8pi2 = 8.0 * kPi * kPi;
         int c = 0;
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b) {
+                // yy = sum_z (-2 pi^2 / rfac) w z_a z_b cos + sum_{q != 0} y_a y_b F''
                 const double Y = fma(k[a] * k[b], fpp, yy[c]);
-                double hv = -k8pi2 * dacc[NCTX + c] + C.rfac * (4.0 * Y + (a == b ? 2.0 * G1 : 0.0));
-                out.h[c] = C.pref * hv;
+                out.h[c] = C.pref * C.rfac * (4.0 * Y + (a == b ? 2.0 * G1 : 0.0));
                 ++c;
             }
     }
@@ -794,11 +795,12 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
 static int atm_shape() {
     static int shape = -1;
     if (shape < 0) {
-        shape = 22;
+        shape = 32;  // measured best on B200
         if (const char* e = std::getenv("LATSUM_ATM_SHAPE")) {
-            if (!std::strcmp(e, "2x1")) shape = 21;
+            if (!std::strcmp(e, "2x2")) shape = 22;
             if (!std::strcmp(e, "3x1")) shape = 31;
-            if (!std::strcmp(e, "3x2")) shape = 32;
+            if (!std::strcmp(e, "4x1")) shape = 41;
+            if (!std::strcmp(e, "4x2")) shape = 42;
         }
     }
     return shape;
@@ -812,9 +814,10 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if constexpr (MODE == 1 && D == 3) {
         if (smem) {
             switch (atm_shape()) {
-                case 21: return launch_tile_s<D, NCTX, HESS, MODE, true, 2, 1>(P, g, mult, partials, grid_blocks, st, bytes);
+                case 22: return launch_tile_s<D, NCTX, HESS, MODE, true, 2, 2>(P, g, mult, partials, grid_blocks, st, bytes);
                 case 31: return launch_tile_s<D, NCTX, HESS, MODE, true, 3, 1>(P, g, mult, partials, grid_blocks, st, bytes);
-                case 32: return launch_tile_s<D, NCTX, HESS, MODE, true, 3, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                case 41: return launch_tile_s<D, NCTX, HESS, MODE, true, 4, 1>(P, g, mult, partials, grid_blocks, st, bytes);
+                case 42: return launch_tile_s<D, NCTX, HESS, MODE, true, 4, 2>(P, g, mult, partials, grid_blocks, st, bytes);
                 default: break;
             }
         }
