@@ -32,9 +32,10 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_atm_ncu.md); used to turn kernel time into achieved FLOP/s.
-FLOPS_PER_NODE = 130_000.0
-FLOPS_SOURCE = "static source count (DESIGN.md) pending ncu"
+# bench grid (profiles/r01_summary.md, v6); used to turn the live kernel time into FLOP/s.
+FLOPS_PER_NODE = 22214.8
+FLOPS_SOURCE = "ncu r01 v6: 5.5905e11 FP64 FLOPs per launch / 25,165,824 nodes"
+TRAFFIC_PER_LAUNCH = 691_200 + 21_248  # ncu r01 v6 dram__bytes_read.sum + dram__bytes_write.sum
 
 
 def parse():
@@ -284,7 +285,7 @@ def run_ours(args):
                 "call": "paper_2504_11989_b200.distributed.atm_energy_distributed(fcc, ATMGrid(128,128,3)) "
                         "from cold caches", "energy": res.energy},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
-                     "frac": achieved / pk.value, "traffic": None,
+                     "frac": achieved / pk.value, "traffic": TRAFFIC_PER_LAUNCH,
                      "kernel": "lz::tile_kernel<3,1,true,1> (fused ATM integrand)",
                      "kernel_ms": kern_ms, "flops_per_node": FLOPS_PER_NODE, "flops_source": FLOPS_SOURCE,
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "

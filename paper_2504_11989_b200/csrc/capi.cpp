@@ -149,6 +149,33 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     union_points(d, dsets, &hp->dir_n);
     std::vector<double> rec_n;
     union_points(d, rsets, &rec_n);
+    // Ball truncation of the direct set: the reference appends whole max-norm shells
+    // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
+    // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-20) times
+    // the summed weights are dropped (|z|^2 factor covers the Hessian channels).
+    {
+        ld dcut = 1e-20L;
+        if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
+        const size_t np = hp->dir_n.size() / d;
+        std::vector<ld> mag(np, 0.0L);
+        ld total = 0.0L;
+        std::vector<const lz::HostCtx*> all(plain.begin(), plain.end());
+        if (hess) all.push_back(hess);
+        for (size_t i = 0; i < np; ++i) {
+            ld z[lz::kMaxDim];
+            for (const lz::HostCtx* c : all) {
+                ld w = std::fabs(direct_weight(*c, &hp->dir_n[i * d], z));
+                ld r2 = 0.0L;
+                for (int a = 0; a < d; ++a) r2 += z[a] * z[a];
+                mag[i] = std::max(mag[i], w * std::max(1.0L, r2));
+                total += w;
+            }
+        }
+        std::vector<double> kept;
+        for (size_t i = 0; i < np; ++i)
+            if (mag[i] > dcut * total) kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
+        hp->dir_n.swap(kept);
+    }
     // Direct points as runs of consecutive last coordinates: the kernel evaluates one
     // sincospi per run and rotates by exp(2 pi i kappa_d) along it.
     {
