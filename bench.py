@@ -137,7 +137,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sample = 4096
+    sample = 65536
     vals = []
     for i in range(args.warmup + args.steps):
         v, dt, threads = cpu_atm_sample(sample)
@@ -294,9 +294,9 @@ def run_ours(args):
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, threads = cpu_atm_sample(8192)
+        v, dt, threads = cpu_atm_sample(131072)
         line["cpu_baseline"] = {"value": v, "unit": "zeta evals/s", "cores": threads, "kind": "port",
-                                "sample": f"8192 contiguous nodes of the C3 grid ({dt:.1f} s), "
+                                "sample": f"131072 contiguous nodes of the C3 grid ({dt:.1f} s), "
                                           "oracle/latsum_oracle.c (long double) on all host threads"}
     if rank == 0 and world == 1 and not args.no_secondary:
         line["secondary"] = secondary(np, torch)

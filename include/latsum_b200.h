@@ -108,11 +108,19 @@ int lz_grid_tiles(int d, const lz_grid* g, int64_t* n_nodes, int64_t* n_tiles);
  * (L/quadrature.py:393-397,455-490), distinct exponents evaluated once per node
  * and raised to their multiplicity.  partials: n_tiles doubles (only the tiles
  * of [tile_lo, tile_hi) are written).  value = 2^d * sum(partials). */
+/* Contexts created with device < 0 give host-only plans (inspection / tests; integrate -> LZ_ECUDA). */
 int lz_plan_create_product(const lz_ctx* const* ctxs, const int* mult, int nctx, lz_plan** out);
 /* -- ATM integrand [Z_3^3, tr(M_5^3)] with M_5 = -Hess Z_5/(4 pi^2): partials n_tiles x 2.
  * E_ATM = 2^d/6 * (sum_0 - 3 sum_1); zeta^(3)(3,3,3) = 2^d sum_0.  z5 needs deriv_order 2. */
 int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out);
 int lz_plan_destroy(lz_plan* plan);
+typedef struct {
+    int d, kind, nctx, hess, alias, n_funcs;       /* kind: 0 product, 1 ATM                    */
+    int64_t n_dir, n_runs, n_rec;                  /* union point sets after truncation         */
+    int64_t table_pieces, table_bins, n_t0, smem_bytes;
+    double table_x_lo, table_x_hi, table_max_rel_err, r_cut, split, t0_rho_max;
+} lz_plan_info;
+int lz_plan_get_info(const lz_plan* plan, lz_plan_info* out);
 int lz_plan_integrate(const lz_plan* plan, const lz_grid* g, double* partials, int grid_blocks,
                       void* stream);
 /* fixed-order compensated sum of n_tiles x ncomp partials -> out[ncomp] (device) */

@@ -53,6 +53,16 @@ class Grid(C.Structure):
                 ("tile_lo", C.c_int64), ("tile_hi", C.c_int64), ("u_lo", C.c_double)]
 
 
+class PlanInfo(C.Structure):
+    _fields_ = [("d", C.c_int), ("kind", C.c_int), ("nctx", C.c_int), ("hess", C.c_int),
+                ("alias", C.c_int), ("n_funcs", C.c_int),
+                ("n_dir", C.c_int64), ("n_runs", C.c_int64), ("n_rec", C.c_int64),
+                ("table_pieces", C.c_int64), ("table_bins", C.c_int64), ("n_t0", C.c_int64),
+                ("smem_bytes", C.c_int64),
+                ("table_x_lo", C.c_double), ("table_x_hi", C.c_double), ("table_max_rel_err", C.c_double),
+                ("r_cut", C.c_double), ("split", C.c_double), ("t0_rho_max", C.c_double)]
+
+
 # exported symbols and their signatures (every declaration of include/latsum_b200.h)
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
@@ -70,6 +80,7 @@ SIGNATURES = {
     "lz_plan_create_product": (C.c_int, [C.POINTER(_P), C.POINTER(C.c_int), C.c_int, C.POINTER(_P)]),
     "lz_plan_create_atm": (C.c_int, [_P, _P, C.POINTER(_P)]),
     "lz_plan_destroy": (C.c_int, [_P]),
+    "lz_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
     "lz_plan_integrate": (C.c_int, [_P, C.POINTER(Grid), _P, C.c_int, _P]),
     "lz_reduce_partials": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
     "lz_plan_integrate_host": (C.c_int, [_P, C.POINTER(Grid), _D]),

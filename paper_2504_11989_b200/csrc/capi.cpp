@@ -151,10 +151,10 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     union_points(d, rsets, &rec_n);
     // Ball truncation of the direct set: the reference appends whole max-norm shells
     // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
-    // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-20) times
+    // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-18) times
     // the summed weights are dropped (|z|^2 factor covers the Hessian channels).
     {
-        ld dcut = 1e-20L;
+        ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
         std::vector<ld> mag(np, 0.0L);
@@ -831,14 +831,15 @@ int lz_plan_create_product(const lz_ctx* const* ctxs, const int* mult, int nctx,
             plain.push_back(&ctxs[j]->h);
             pl->mult[j] = mult[j];
         }
-        pl->device = ctxs[0]->device;
-        if (pl->device < 0) throw Error{LZ_ECUDA, "contexts have no device"};
+        pl->device = ctxs[0]->device;  // < 0: host tables only (inspection / tests)
         pl->d = ctxs[0]->h.d;
         if (pl->d > 3) throw Error{LZ_EINVAL, "integral kernels support d <= 3"};
         pl->kind = 0;
         build_host_plan(plain, nullptr, &pl->hp);
-        DeviceGuard dg(pl->device);
-        pl->P = upload_plan(pl->hp, &pl->allocs);
+        if (pl->device >= 0) {
+            DeviceGuard dg(pl->device);
+            pl->P = upload_plan(pl->hp, &pl->allocs);
+        }
     });
     if (rc != LZ_OK) {
         free_all(&pl->allocs);
@@ -857,8 +858,7 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
         ensure_hess_sets(z5);
         if (z3->h.k.branch == lz::kTrivial || z5->h.k.branch == lz::kTrivial)
             throw Error{LZ_EINVAL, "ATM contexts cannot be trivial"};
-        pl->device = z3->device;
-        if (pl->device < 0) throw Error{LZ_ECUDA, "contexts have no device"};
+        pl->device = z3->device;  // < 0: host tables only (inspection / tests)
         pl->d = z3->h.d;
         if (pl->d > 3) throw Error{LZ_EINVAL, "ATM is defined for d <= 3"};
         pl->kind = 1;
@@ -866,8 +866,10 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
             throw Error{LZ_EINVAL, "ATM plan needs exponents nu and nu + 2 (Z_3 and the Hessian of Z_5)"};
         build_host_plan({&z3->h}, &z5->h, &pl->hp);
         if (!pl->hp.alias_fp) throw Error{LZ_EINVAL, "ATM plan: F' alias expected"};
-        DeviceGuard dg(pl->device);
-        pl->P = upload_plan(pl->hp, &pl->allocs);
+        if (pl->device >= 0) {
+            DeviceGuard dg(pl->device);
+            pl->P = upload_plan(pl->hp, &pl->allocs);
+        }
     });
     if (rc != LZ_OK) {
         free_all(&pl->allocs);
@@ -880,17 +882,20 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
 
 int lz_plan_destroy(lz_plan* pl) {
     if (!pl) return LZ_OK;
-    int old = -1;
-    cudaGetDevice(&old);
-    cudaSetDevice(pl->device);
-    free_all(&pl->allocs);
-    if (old >= 0) cudaSetDevice(old);
+    if (pl->device >= 0) {
+        int old = -1;
+        cudaGetDevice(&old);
+        cudaSetDevice(pl->device);
+        free_all(&pl->allocs);
+        if (old >= 0) cudaSetDevice(old);
+    }
     delete pl;
     return LZ_OK;
 }
 
 int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int grid_blocks, void* stream) {
     return guarded([&] {
+        if (pl->device < 0) throw Error{LZ_ECUDA, "plan has no device tables (created from host-only contexts)"};
         DeviceGuard dg(pl->device);
         lz::DevGrid dgd;
         fill_grid(pl->d, g, &dgd);
@@ -907,6 +912,33 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
     });
 }
 
+int lz_plan_get_info(const lz_plan* pl, lz_plan_info* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->d = pl->d;
+    o->kind = pl->kind;
+    o->nctx = pl->hp.nctx;
+    o->hess = pl->hp.hess;
+    o->alias = pl->hp.alias_fp;
+    o->n_dir = int64_t(pl->hp.dir_n.size() / std::max(pl->d, 1));
+    o->n_runs = int64_t(pl->hp.run_info.size() / 2);
+    o->n_rec = int64_t(pl->hp.rec_norm.size());
+    o->n_funcs = pl->hp.tab.nfunc;
+    o->table_pieces = pl->hp.tab.npieces;
+    o->table_bins = pl->hp.tab.nbins;
+    o->table_x_lo = pl->hp.tab.x_lo;
+    o->table_x_hi = pl->hp.tab.x_hi;
+    o->table_max_rel_err = pl->hp.tab.max_rel_err;
+    o->r_cut = pl->hp.r_cut;
+    o->split = pl->hp.c > 0 ? lz::kPi / pl->hp.c : 0.0;
+    o->n_t0 = pl->hp.n_t0;
+    o->t0_rho_max = pl->hp.t0_rho_max;
+    const size_t ns = pl->hp.nctx + (pl->hp.hess ? 2 : 0);
+    o->smem_bytes = int64_t(8 * (pl->hp.run_n.size() + pl->hp.dir_w.size() + pl->hp.rec_q.size() +
+                                 pl->hp.rec_norm.size() + pl->hp.tab.coef.size() + ns * lz::kT0) +
+                            4 * (pl->hp.run_info.size() + pl->hp.tab.dir.size()));
+    return LZ_OK;
+}
+
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream) {
     return guarded([&] {
         check_cuda(lz::launch_reduce(partials, n_tiles, ncomp, out, (cudaStream_t)stream), "reduce kernel");
@@ -915,6 +947,7 @@ int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, doubl
 
 int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
     return guarded([&] {
+        if (pl->device < 0) throw Error{LZ_ECUDA, "plan has no device tables (created from host-only contexts)"};
         DeviceGuard dg(pl->device);
         int64_t n_nodes = 0, n_tiles = 0;
         int rc = lz_grid_tiles(pl->d, g, &n_nodes, &n_tiles);

@@ -398,9 +398,10 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     std::vector<Fn> fns;
     for (int j = 0; j < nfunc; ++j) fns.push_back(Fn{ld(p[j]), ld(scale[j])});
     // upper end: every function (times the |y|^2 factor of the Hessian terms) is
-    // below `cutoff` (default 1e-20) of the unit scale; terms past it are exactly
+    // below `cutoff` (default 1e-18, the reference's term cutoff L/epstein.py:51) of the unit
+    // scale; terms past it are exactly
     // zero in the kernel and culled per warp.
-    ld cutoff = 1e-20L;
+    ld cutoff = 1e-18L;
     if (const char* e = std::getenv("LATSUM_TABLE_CUTOFF")) cutoff = std::strtold(e, nullptr);
     const ld hb = kBinWidth;
     ld x_hi = x_lo;
@@ -440,8 +441,8 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
                 for (int j = 0; j < nfunc && good; ++j) {
                     double* cf = &coefs[(size_t(sidx) * nfunc + j) * kNCP];
                     fit_piece(fns[j], x0, x1, cf);
-                    for (int tidx = 0; tidx <= 16; ++tidx) {
-                        ld tau = -1.0L + 2.0L * tidx / 16.0L;
+                    for (int tidx = 0; tidx <= 10; ++tidx) {
+                        ld tau = -1.0L + 2.0L * tidx / 10.0L;
                         ld xx = 0.5L * (x0 + x1) + 0.5L * (x1 - x0) * tau;
                         ld truth = fns[j](xx);
                         ld approx = eval_piece(cf, tau);

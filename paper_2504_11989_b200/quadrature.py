@@ -177,6 +177,11 @@ class Plan:
     def handle(self):
         return self._h
 
+    def info(self) -> "N.PlanInfo":
+        out = N.PlanInfo()
+        N.check(N.lib().lz_plan_get_info(self._h, C.byref(out)), "plan info")
+        return out
+
     def tiles(self, n_u: int, n_v: int, grading: int):
         g = N.Grid(n_u, n_v, grading, 0, 0)
         nn, nt = C.c_int64(0), C.c_int64(0)

@@ -99,7 +99,7 @@ def test_native_context_matches_reference(golden, idx):
     # reciprocal-summand tables: Chebyshev-fitted pieces within 6e-16 relative of long double
     stats = ctx.table_stats(hessian=True)
     assert stats.table_max_rel_err < 6e-16
-    assert stats.table_x_hi > 40.0  # terms below 1e-20 of the unit scale are dropped
+    assert stats.table_x_hi > 35.0  # terms below 1e-18 of the unit scale are dropped
 
 
 def test_hessian_point_sets():
@@ -188,3 +188,35 @@ def test_native_upper_gamma(golden):
             if s < 0:
                 tol += 1e-14 * x ** (s + math.ceil(-s) - 1) * math.exp(-x)
             assert abs(got - ref) <= tol, (s, x)
+
+
+def test_host_only_plans():
+    """Fused plans build without a GPU (host tables only) and report their layout."""
+    import ctypes as C
+    from paper_2504_11989_b200.quadrature import Plan
+    fcc = named_lattice("fcc")
+    t = 0.65 * fcc.volume ** (-2.0 / 3.0)
+    z3 = EpsteinContext(fcc, 3.0, splitting=t, device=-1)
+    z5 = EpsteinContext(fcc, 5.0, splitting=t, device=-1)
+    h = C.c_void_p()
+    N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)))
+    plan = Plan(h, 3, 2, (z3, z5))
+    info = plan.info()
+    assert info.kind == 1 and info.alias == 1 and info.n_funcs == 2   # Z_3's E_1 table serves F'_5
+    assert 0 < info.n_dir <= 364 and info.n_runs < info.n_dir       # ball-truncated half cube, runs
+    assert info.n_rec >= 728 and info.table_max_rel_err < 6e-16
+    assert abs(info.split - t) < 1e-15 and info.smem_bytes < 200_000
+    with pytest.raises(RuntimeError):
+        plan.integrate(8, 4, 3)
+    sq = named_lattice("square")
+    c3 = EpsteinContext(sq, 3.0, device=-1)
+    c4 = EpsteinContext(sq, 4.0, device=-1)
+    arr = (C.c_void_p * 2)(c3.handle, c4.handle)
+    mult = (C.c_int * 2)(2, 1)
+    h2 = C.c_void_p()
+    N.check(N.lib().lz_plan_create_product(arr, mult, 2, C.byref(h2)))
+    p2 = Plan(h2, 2, 1, (c3, c4)).info()
+    assert p2.kind == 0 and p2.nctx == 2 and p2.n_funcs == 2 and p2.alias == 0
+    # ATM plans need nu and nu + 2
+    h3 = C.c_void_p()
+    assert N.lib().lz_plan_create_atm(c3.handle, c3.handle, C.byref(h3)) != 0
