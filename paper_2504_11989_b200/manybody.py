@@ -65,6 +65,20 @@ def normalized_many_body(lattice: Lattice, nu: float, n: int, cfg: QuadratureCon
     return many_body_zeta(lattice, [nu] * n, cfg).value / z0 ** n
 
 
+def table_square(n_list=(2, 3, 4, 5, 6, 7, 8), nu_list=(2.0, 3.0), cfg: QuadratureConfig | None = None):
+    """Table 1 of the paper (SPEC.md: table_square): zeta^(n)(nu, ..., nu) on the square lattice.
+
+    Rows (n, nu, value, error_estimate); nu = 2 = d runs through the continuation path."""
+    from .lattice import named_lattice
+    sq = named_lattice("square")
+    rows = []
+    for nu in nu_list:
+        for n in n_list:
+            res = many_body_zeta(sq, [nu] * n, cfg)
+            rows.append((n, float(nu), res.value, res.error_estimate))
+    return rows
+
+
 @dataclass(frozen=True)
 class ATMGrid:
     """Fixed Duffy grid of the ATM integral: n_u radial (graded u = t^q/2) x n_v^(d-1) angular."""
@@ -113,5 +127,5 @@ def atm_energy_scaled(lattice: Lattice, scale: float, **kw) -> float:
     return atm_cohesive_energy(lattice.scaled(scale), **kw)
 
 
-__all__ = ["ManyBodyResult", "many_body_zeta", "normalized_many_body", "ATMGrid", "ATMResult",
+__all__ = ["ManyBodyResult", "many_body_zeta", "normalized_many_body", "table_square", "ATMGrid", "ATMResult",
            "atm_integrals", "atm_cohesive_energy", "atm_energy_scaled", "math"]

@@ -157,3 +157,15 @@ def test_meromorphic_continuation_path(golden_integrals, name):
         if lat.d == 3 else ref["z333"]
     e24 = z333 / 24 - 3 * vals["zm155"] / 16 + 3 * vals["z135"] / 8
     assert abs(e24 - ref["atm"]) <= SUM_TOL * abs(ref["atm"])
+
+
+def test_table_square_and_normalized(golden_integrals, golden):
+    from paper_2504_11989_b200.manybody import normalized_many_body, table_square
+    rows = {(n, nu): v for n, nu, v, _ in table_square(n_list=(2, 3, 5), nu_list=(3.0,))}
+    sq_z6 = [c for c in golden["cases"] if c["lattice"] == "square" and c["nu"] == 6.0][0]["zeta_at_zero"]
+    assert abs(rows[(2, 3.0)] - sq_z6) <= 1e-12 * abs(sq_z6)          # Cor. 2.7
+    assert abs(rows[(3, 3.0)] - golden["c2"]["value"]) <= 1e-10 * golden["c2"]["value"]
+    five = [r for r in golden["integrals_small"] if r["lattice"] == "square" and len(r["nus"]) == 5][0]
+    assert abs(rows[(5, 3.0)] - five["value"]) <= 1e-10 * abs(five["value"])
+    hexl = named_lattice("hex")
+    assert abs(normalized_many_body(hexl, 3.0, 4)) <= 1.0                # PAPER section 4.3 bound

@@ -38,6 +38,32 @@ def c1():
     print("c1 ok", float(z.sum()))
 
 
+def e2e_breakdown():
+    """Where the cold-cache time of atm_energy_distributed goes (host vs device)."""
+    import ctypes as C
+    from paper_2504_11989_b200 import _native as N
+    from paper_2504_11989_b200.distributed import ShardedIntegral
+    from paper_2504_11989_b200.epstein import epstein_context
+    from paper_2504_11989_b200.quadrature import atm_plan, product_plan
+    fcc = named_lattice("fcc")
+    for rep in range(3):
+        epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        t = 0.65 * fcc.volume ** (-2.0 / 3.0)
+        z3 = epstein_context(fcc, 3.0, t)
+        z5 = epstein_context(fcc, 5.0, t)
+        t1 = time.perf_counter()
+        plan = atm_plan(fcc)
+        t2 = time.perf_counter()
+        s = ShardedIntegral(plan, 128, 128, 3)
+        t3 = time.perf_counter()
+        out = s.run().cpu().numpy()
+        t4 = time.perf_counter()
+        print(f"rep {rep}: contexts {1e3*(t1-t0):.1f} ms, plan {1e3*(t2-t1):.1f} ms, "
+              f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms")
+
+
 def e2e():
     sq = named_lattice("square")
     ctx = EpsteinContext(sq, 3.5, device=0)
@@ -61,4 +87,4 @@ def e2e():
 
 
 if __name__ == "__main__":
-    {"atm": atm, "c1": c1, "e2e": e2e}[sys.argv[1]]()
+    {"atm": atm, "c1": c1, "e2e": e2e, "e2e_breakdown": e2e_breakdown}[sys.argv[1]]()
