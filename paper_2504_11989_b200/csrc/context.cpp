@@ -511,7 +511,8 @@ void gauss_legendre(int n, std::vector<double>* xs, std::vector<double>* ws) {
             dp = n * (x * p1 - p0) / (x * x - 1.0L);
             ld dx = p1 / dp;
             x -= dx;
-            if (std::fabs(dx) < 1e-21L) break;
+            // relative test: an absolute one never triggers near +-1 in long double
+            if (std::fabs(dx) <= 4e-19L * std::fabs(x) || it > 20) break;
         }
         ld p0 = 1.0L, p1 = x;
         for (int k = 2; k <= n; ++k) {
