@@ -60,8 +60,10 @@ def e2e_breakdown():
         t3 = time.perf_counter()
         out = s.run().cpu().numpy()
         t4 = time.perf_counter()
+        out = s.run().cpu().numpy()
+        t5 = time.perf_counter()
         print(f"rep {rep}: contexts {1e3*(t1-t0):.1f} ms, plan {1e3*(t2-t1):.1f} ms, "
-              f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms")
+              f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms, warm run+d2h {1e3*(t5-t4):.1f} ms")
 
 
 def e2e():
