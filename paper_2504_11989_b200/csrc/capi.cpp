@@ -30,7 +30,6 @@ cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int
                        cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st);
 cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cudaStream_t st);
-int tile_nodes();
 
 }  // namespace lz
 

@@ -35,7 +35,6 @@ namespace lz {
 
 constexpr int kTileWarps = 8;
 constexpr int kTilesPerCta = 3;
-constexpr int kTileNodes = 32 * kTileWarps;
 
 template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 
@@ -858,7 +857,5 @@ cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cu
     return cudaGetLastError();
 }
 
-int tile_nodes() { return kTileNodes; }
-int coef_stride() { return kNCP; }
 
 }  // namespace lz

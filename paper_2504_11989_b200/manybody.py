@@ -20,7 +20,6 @@ per node (csrc/kernels.cu, tile_kernel MODE 1).
 """
 from __future__ import annotations
 
-import math
 import time
 from dataclasses import dataclass, field
 
@@ -128,4 +127,4 @@ def atm_energy_scaled(lattice: Lattice, scale: float, **kw) -> float:
 
 
 __all__ = ["ManyBodyResult", "many_body_zeta", "normalized_many_body", "table_square", "ATMGrid", "ATMResult",
-           "atm_integrals", "atm_cohesive_energy", "atm_energy_scaled", "math"]
+           "atm_integrals", "atm_cohesive_energy", "atm_energy_scaled"]

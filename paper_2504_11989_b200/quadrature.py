@@ -26,7 +26,7 @@ from functools import lru_cache
 import numpy as np
 
 from . import _native as N
-from .epstein import GENERIC, LOG_CASE, TRIVIAL, EpsteinContext, epstein_context
+from .epstein import TRIVIAL, epstein_context
 from .errors import PoleError
 from .lattice import Lattice
 
