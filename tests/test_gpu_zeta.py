@@ -159,3 +159,18 @@ def test_hessian_vs_reference_fd(golden):
         M = polynomial_weighted_zeta(lat, 5.0, np.array(h["k"]))
         assert abs(np.trace(M) - h["z3"]) <= 1e-12 * max(1.0, abs(h["z3"]))
         assert np.abs(M - np.array(h["M_fd"]).reshape(3, 3)).max() < 1e-4
+
+
+@pytest.mark.parametrize("scale", [0.35, 0.5, 0.65, 1.0, 1.6])
+def test_split_invariance(scale):
+    """Z and its Hessian do not depend on the theta split (the fused ATM plan uses a tuned one)."""
+    fcc = named_lattice("fcc")
+    t = scale * fcc.volume ** (-2.0 / 3.0)
+    kap = np.random.default_rng(7).uniform(-0.5, 0.5, size=(256, 3))
+    k = kap @ fcc.a_inv_t.T
+    z = EpsteinContext(fcc, 3.0, splitting=t, device=0).zeta(k)
+    assert emetric(z, O.zeta(fcc.a, 3.0, k)).max() <= ZETA_TOL
+    H = EpsteinContext(fcc, 5.0, splitting=t, device=0).zeta_hessian(k)
+    Ho = O.hessian(fcc.a, 5.0, k)
+    scale_h = np.maximum(np.abs(Ho).max(axis=(1, 2), keepdims=True), 1.0)
+    assert (np.abs(H - Ho) / scale_h).max() <= ZETA_TOL
