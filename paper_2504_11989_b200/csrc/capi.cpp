@@ -592,12 +592,31 @@ int lz_device_count(int* n) {
 
 namespace {
 
+// Theta split of the per-context evaluation tables, as a multiple of the context's own split
+// (LATSUM_ZETA_SPLIT_SCALE, default 1).  The value of Z is split-invariant; the context keeps
+// reporting the reference's split and point sets.
+double zeta_split_scale() {
+    static double v = [] {
+        const char* e = std::getenv("LATSUM_ZETA_SPLIT_SCALE");
+        double x = e ? std::atof(e) : 1.0;
+        return (x > 0.0 && x < 10.0) ? x : 1.0;
+    }();
+    return v;
+}
+
 void ensure_plain(const lz_ctx* cc) {
     lz_ctx* c = const_cast<lz_ctx*>(cc);
     std::lock_guard<std::mutex> lock(c->mu);
     if (c->plain_ready) return;
     if (c->h.k.branch != lz::kTrivial) {
-        build_host_plan({&c->h}, nullptr, &c->plain);
+        const double sc = zeta_split_scale();
+        if (sc != 1.0) {
+            lz::HostCtx eval;
+            lz::build_context(c->h.d, c->h.A, c->h.k.nu, c->h.k.split * sc, 0, &eval);
+            build_host_plan({&eval}, nullptr, &c->plain);
+        } else {
+            build_host_plan({&c->h}, nullptr, &c->plain);
+        }
     } else {
         c->plain.d = c->h.d;
         c->plain.nctx = 1;

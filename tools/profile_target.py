@@ -66,6 +66,25 @@ def e2e_breakdown():
               f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms, warm run+d2h {1e3*(t5-t4):.1f} ms")
 
 
+def c1_time():
+    """Device time of the C1 zeta batches (4096 and 2^20 points), CUDA events."""
+    sq = named_lattice("square")
+    ctx = EpsteinContext(sq, 3.5, device=0)
+    for n, seed in ((4096, 0), (1 << 20, 1)):
+        k = torch.tensor(np.random.default_rng(seed).uniform(-0.5, 0.5, size=(n, 2)), device="cuda")
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            ctx.zeta_device(k, out=out)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            ctx.zeta_device(k, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 20
+        print(f"n={n}: {ms:.4f} ms, {n / ms * 1e3:.3e} evals/s")
+
+
 def e2e():
     sq = named_lattice("square")
     ctx = EpsteinContext(sq, 3.5, device=0)
@@ -89,4 +108,5 @@ def e2e():
 
 
 if __name__ == "__main__":
-    {"atm": atm, "c1": c1, "e2e": e2e, "e2e_breakdown": e2e_breakdown}[sys.argv[1]]()
+    {"atm": atm, "c1": c1, "c1_time": c1_time, "e2e": e2e,
+     "e2e_breakdown": e2e_breakdown}[sys.argv[1]]()
