@@ -83,6 +83,14 @@ def c1_time():
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 20
         print(f"n={n}: {ms:.4f} ms, {n / ms * 1e3:.3e} evals/s")
+        if n == 4096:
+            for lanes in (1, 2, 4, 8, 16, 32):
+                a.record()
+                for _ in range(20):
+                    ctx.zeta_device(k, out=out, lanes_per_point=lanes)
+                b.record()
+                torch.cuda.synchronize()
+                print(f"   lanes={lanes}: {a.elapsed_time(b) / 20:.4f} ms")
 
 
 def e2e():
