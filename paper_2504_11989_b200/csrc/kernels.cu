@@ -383,6 +383,15 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     for (int a = 0; a < D; ++a) rho = fma(k[a], k[a], rho);
     const bool reg_only = flags & 2u;
     const bool sing_only = flags & 4u;
+    // q = 0 term: power series in rho for x = c rho <= max(2, x_lo) (t0_rho_max); beyond it the
+    // alternating series would cancel, so the full F comes from the tables (x >= x_lo there)
+    // and t0_reg = F - shat / (V pref rfac) (no cancellation: F is the small part).
+    const bool q0_series = rho <= P.t0_rho_max;
+    const bool q0_table = !q0_series && P.n_rec > 0;
+    double f0[NF];
+#pragma unroll
+    for (int j = 0; j < NF; ++j) f0[j] = 0.0;
+    if (q0_table) tab_eval<NF>(P.tab, V, rho, f0);
 #pragma unroll
     for (int j = 0; j < NCTX; ++j) {
         const CtxConst& C = P.ctx[j];
@@ -394,7 +403,9 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         } else {
             zv = C.bconst;
             zv += 2.0 * dacc[j];
-            const double t0 = rho <= P.t0_rho_max ? series(V.t0c + j * kT0, P.n_t0, rho) : t0_reg(C, rho);
+            const double t0 = q0_series ? series(V.t0c + j * kT0, P.n_t0, rho)
+                              : q0_table ? f0[j] - singular(C, rho) * C.inv_vol / (C.pref * C.rfac)
+                                         : t0_reg(C, rho);
             zv += C.rfac * (t0 + racc[j]);
             zv *= C.pref;
             if (!reg_only && rho >= 1e-28) zv += singular(C, rho) * C.inv_vol;
@@ -408,7 +419,10 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         // F = t0_reg + shat / (V pref rfac): its rho-derivatives from the series of t0_reg and
         // the closed-form singular part (k in the BZ), else E_p directly
         double fp, fpp;
-        if (rho <= P.t0_rho_max && rho > 0.0) {
+        if (q0_table) {
+            fp = ALIAS ? P.alias_ratio * f0[0] : f0[NCTX];
+            fpp = f0[Acc::FPP];
+        } else if (q0_series && rho > 0.0) {
             const double kk = C.sing_coef * C.inv_vol / (C.pref * C.rfac);
             double s1, s2;
             if (C.branch == kLogCase) {
