@@ -327,10 +327,13 @@ def secondary(np, torch):
         kt = torch.tensor(k, device="cuda")
         zt = torch.empty(n, dtype=torch.float64, device="cuda")
         ms = _time_cuda(lambda: ctx.zeta_device(kt, out=zt), 20, torch)
+        kp = torch.from_numpy(k).pin_memory().numpy()   # pinned host input (contract: pinned H2D)
+        zp = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+        ctx._eval_into(kp, zp)
         t0 = time.perf_counter()
         reps = 5
         for _ in range(reps):
-            ctx.zeta(k)
+            ctx._eval_into(kp, zp)
         e2e = (time.perf_counter() - t0) / reps
         out[f"c1_{n}"] = {"evals_per_s": n / (ms * 1e-3), "ms": ms, "e2e_evals_per_s": n / e2e,
                           "terms_per_s": n * 105 / (ms * 1e-3)}

@@ -155,6 +155,15 @@ class EpsteinContext:
             return float(out[0])
         return out.reshape(shape) if shape else out
 
+    def _eval_into(self, k: np.ndarray, out: np.ndarray, flags: int = 0) -> np.ndarray:
+        """Z into a caller-provided host buffer (no allocation; pinned buffers skip staging)."""
+        N.require_cuda("Epstein zeta evaluation")
+        assert k.dtype == np.float64 and k.flags.c_contiguous and out.dtype == np.float64
+        n = k.shape[0]
+        if n:
+            N.check(N.lib().lz_zeta_host(self._h, N.dptr(k), n, N.dptr(out), flags), "zeta")
+        return out
+
     def zeta_device(self, k, out=None, flags: int = 0, lanes_per_point: int = 0, stream=None):
         """Zero-copy path: ``k`` a CUDA torch tensor (n, d) float64; returns a CUDA tensor."""
         import torch

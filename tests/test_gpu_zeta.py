@@ -174,3 +174,19 @@ def test_split_invariance(scale):
     Ho = O.hessian(fcc.a, 5.0, k)
     scale_h = np.maximum(np.abs(Ho).max(axis=(1, 2), keepdims=True), 1.0)
     assert (np.abs(H - Ho) / scale_h).max() <= ZETA_TOL
+
+
+@pytest.mark.parametrize("nu", [5.0, 6.0, 4.5, 2.5])
+def test_four_dimensional_lattice(nu):
+    """d = 4 (L/lattice.py:20 upper limit): batch zeta and Hessian vs the oracle."""
+    from paper_2504_11989_b200 import Lattice
+    a = np.array([[1.0, 0.2, 0.0, 0.1], [0.0, 1.1, 0.3, 0.0], [0.0, 0.0, 0.9, 0.2], [0.1, 0.0, 0.0, 1.0]])
+    lat = Lattice(a)
+    kap = np.random.default_rng(3).uniform(-0.5, 0.5, size=(64, 4))
+    k = kap @ lat.a_inv_t.T
+    ctx = EpsteinContext(lat, nu, device=0)
+    assert emetric(ctx.zeta(k), O.zeta(lat.a, nu, k)).max() <= ZETA_TOL
+    H = ctx.zeta_hessian(k)
+    Ho = O.hessian(lat.a, nu, k)
+    sc = np.maximum(np.abs(Ho).max(axis=(1, 2), keepdims=True), 1.0)
+    assert (np.abs(H - Ho) / sc).max() <= ZETA_TOL
