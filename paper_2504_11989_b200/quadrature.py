@@ -50,6 +50,7 @@ class QuadratureConfig:
     grid_v: int = 64
     grading: int = 1
     estimate_error: bool = True
+    method: str = "grid"   # "grid": fixed device grid; "adaptive": reference GK strategy, GPU panels
 
     def __post_init__(self):
         if not 0.0 < self.epsilon < 0.5:
@@ -60,15 +61,18 @@ class QuadratureConfig:
             raise ValueError("taylor_order must be a nonnegative even integer")
         if self.grid_u < 2 or self.grid_v < 1 or self.grading < 1:
             raise ValueError("grid_u >= 2, grid_v >= 1 and grading >= 1 required")
+        if self.method not in ("grid", "adaptive"):
+            raise ValueError("method must be 'grid' or 'adaptive'")
 
     _INT = ("gauss_order", "taylor_order", "adaptive_max_depth", "grid_u", "grid_v", "grading")
     _FLOAT = ("epsilon", "adaptive_rel_tol", "splitting")
     _BOOL = ("force_integral", "allow_high_log_power", "estimate_error")
+    _STR = ("method",)
 
     def to_text(self) -> str:
         keys = ("gauss_order", "epsilon", "taylor_order", "adaptive_rel_tol", "adaptive_max_depth",
                 "force_integral", "allow_high_log_power", "grid_u", "grid_v", "grading",
-                "estimate_error")
+                "estimate_error", "method")
         out = []
         for k in keys:
             v = getattr(self, k)
@@ -92,6 +96,8 @@ class QuadratureConfig:
                 kwargs[key] = float(value)
             elif key in cls._BOOL:
                 kwargs[key] = value.lower() in ("1", "true", "yes")
+            elif key in cls._STR:
+                kwargs[key] = value
             else:
                 raise ValueError(f"unknown config key {key!r}")
         return cls(**kwargs)
@@ -295,6 +301,10 @@ def integrate_product(lattice: Lattice, nus, cfg: QuadratureConfig | None = None
     contexts = [epstein_context(lattice, nu, cfg.splitting) for nu in nus]
     min_nu = min(ctx.nu for ctx in contexts if ctx.branch != TRIVIAL) if any(
         c.branch != TRIVIAL for c in contexts) else math.inf
+    if cfg.method == "adaptive":
+        N.require_cuda("BZ quadrature")
+        from .adaptive import integrate_product_adaptive
+        return integrate_product_adaptive(lattice, contexts, cfg)
     if min_nu <= d:
         from .tail import integrate_product_continued
         return integrate_product_continued(lattice, contexts, cfg)

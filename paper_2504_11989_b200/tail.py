@@ -76,14 +76,23 @@ def _tail_primitive(nu, m, eps, wsq, allow_high):
     return tail_primitive(nu, m, eps, wsq, allow_high)
 
 
-def tail_values(contexts, taylors, w, cfg):
-    """Continuation value of int_0^eps u^(d-1) prod Z(nu_i, u w) du for every row of w."""
-    d = contexts[0].d
+def ray_series(contexts, taylors, w, cfg):
+    """Monomials of prod_i Z(nu_i, u w) near u = 0 (above the u^(d-1) factor), per row of w."""
     ell = cfg.taylor_order
     wsq = np.einsum("ij,ij->i", w, w)
     series = {(0.0, 0): np.ones(len(w))}
     for ctx, tab in zip(contexts, taylors):
         series = _multiply(series, _ray_expansion(ctx, tab, w, wsq, ell), ell + _EXTRA_ORDER)
+    return series
+
+
+def tail_values(contexts, taylors, w, cfg, series=None):
+    """Continuation value of int_0^eps u^(d-1) prod Z(nu_i, u w) du for every row of w."""
+    d = contexts[0].d
+    ell = cfg.taylor_order
+    wsq = np.einsum("ij,ij->i", w, w)
+    if series is None:
+        series = ray_series(contexts, taylors, w, cfg)
     total = np.zeros(len(w))
     top = np.zeros(len(w))
     for (e, m), c in sorted(series.items()):

@@ -169,3 +169,16 @@ def test_table_square_and_normalized(golden_integrals, golden):
     assert abs(rows[(5, 3.0)] - five["value"]) <= 1e-10 * abs(five["value"])
     hexl = named_lattice("hex")
     assert abs(normalized_many_body(hexl, 3.0, 4)) <= 1.0                # PAPER section 4.3 bound
+
+
+@pytest.mark.parametrize("name,nus,key", [("square", (3, 3, 3), None), ("square", (1, 3, 5), "z135"),
+                                          ("integer_1d", (-1, 5, 5), "zm155"), ("fcc", (-1, 5, 5), "zm155")])
+def test_adaptive_method_matches_reference(golden, golden_integrals, name, nus, key):
+    """method='adaptive': the reference's GK15/G7 refinement with GPU panels (drop-in fidelity)."""
+    lat = named_lattice(name)
+    cfg = QuadratureConfig(method="adaptive")
+    v, err = integrate_product(lat, nus, cfg)
+    ref = golden["c2"]["value"] if key is None else golden_integrals[name][key]
+    ref_err = golden["c2"]["err"] if key is None else golden_integrals[name][key + "_err"]
+    assert abs(v - ref) <= max(1e-12 * abs(ref), 2 * ref_err), (v, ref)
+    assert 0.0 < err < 1e-9 * abs(v)
