@@ -50,7 +50,10 @@ class QuadratureConfig:
     grid_v: int = 64
     grading: int = 1
     estimate_error: bool = True
-    method: str = "grid"   # "grid": fixed device grid; "adaptive": reference GK strategy, GPU panels
+    # "auto": fixed device grid when every exponent exceeds d, else the adaptive path;
+    # "grid": fixed device grid (continuation tail on the host for nu <= d);
+    # "adaptive": the reference's GK15/G7 strategy with GPU panel evaluation
+    method: str = "auto"
 
     def __post_init__(self):
         if not 0.0 < self.epsilon < 0.5:
@@ -61,8 +64,8 @@ class QuadratureConfig:
             raise ValueError("taylor_order must be a nonnegative even integer")
         if self.grid_u < 2 or self.grid_v < 1 or self.grading < 1:
             raise ValueError("grid_u >= 2, grid_v >= 1 and grading >= 1 required")
-        if self.method not in ("grid", "adaptive"):
-            raise ValueError("method must be 'grid' or 'adaptive'")
+        if self.method not in ("auto", "grid", "adaptive"):
+            raise ValueError("method must be 'auto', 'grid' or 'adaptive'")
 
     _INT = ("gauss_order", "taylor_order", "adaptive_max_depth", "grid_u", "grid_v", "grading")
     _FLOAT = ("epsilon", "adaptive_rel_tol", "splitting")
@@ -301,7 +304,7 @@ def integrate_product(lattice: Lattice, nus, cfg: QuadratureConfig | None = None
     contexts = [epstein_context(lattice, nu, cfg.splitting) for nu in nus]
     min_nu = min(ctx.nu for ctx in contexts if ctx.branch != TRIVIAL) if any(
         c.branch != TRIVIAL for c in contexts) else math.inf
-    if cfg.method == "adaptive":
+    if cfg.method == "adaptive" or (cfg.method == "auto" and min_nu <= d):
         N.require_cuda("BZ quadrature")
         from .adaptive import integrate_product_adaptive
         return integrate_product_adaptive(lattice, contexts, cfg)
