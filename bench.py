@@ -350,6 +350,24 @@ def secondary(np, torch):
         e2e = time.perf_counter() - t0
         out[name] = {"value": v, "nodes": nn, "kernel_ms": ms, "api_ms": e2e * 1e3,
                      "evals_per_s": nn / (ms * 1e-3)}
+    # config 5: fcc/bcc LJ(12,6) + lambda ATM phase scan (two ATM sums + four zeta_at_zero on the
+    # GPU, then the host enthalpy scan on the 64 x 64 (lambda, R) grids and lambda_c for 4 pressures)
+    import numpy as np
+    from paper_2504_11989_b200.manybody import ATMGrid
+    from paper_2504_11989_b200.phase import LJParams, critical_coupling, lattice_constants, phase_scan
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lj = LJParams()
+    fc = lattice_constants("fcc", lj, ATMGrid(128, 128, 3))
+    bc = lattice_constants("bcc", lj, ATMGrid(128, 128, 3))
+    t1 = time.perf_counter()
+    lam = np.linspace(0.0, 2.0, 64)
+    pts = phase_scan(fc, bc, lj, [0.0, 0.5, 1.0, 2.0], lam, np.linspace(0.9, 1.7, 64))
+    crit = {p: critical_coupling(fc, bc, lj, p) for p in (0.0, 0.5, 1.0, 2.0)}
+    t2 = time.perf_counter()
+    out["c5_phase_scan"] = {"constants_ms": (t1 - t0) * 1e3, "scan_ms": (t2 - t1) * 1e3,
+                            "lambda_c": crit, "k_atm_fcc": fc.k_atm, "k_atm_bcc": bc.k_atm,
+                            "points": len(pts)}
     return out
 
 

@@ -182,3 +182,21 @@ def test_adaptive_method_matches_reference(golden, golden_integrals, name, nus, 
     ref_err = golden["c2"]["err"] if key is None else golden_integrals[name][key + "_err"]
     assert abs(v - ref) <= max(1e-12 * abs(ref), 2 * ref_err), (v, ref)
     assert 0.0 < err < 1e-9 * abs(v)
+
+
+def test_c5_phase_scan_from_gpu_constants(golden, golden_integrals):
+    """Config 5: LJ(12,6) + lambda ATM, fcc vs bcc; constants Z(6,0), Z(12,0), K_ATM on the GPU."""
+    from paper_2504_11989_b200.phase import LJParams, critical_coupling, lattice_constants, phase_scan
+    lj = LJParams()
+    fcc = lattice_constants("fcc", lj, ATMGrid(128, 128, 3))
+    bcc = lattice_constants("bcc", lj, ATMGrid(128, 128, 3))
+    z = golden["zeta_at_zero"]
+    assert abs(fcc.z_n - z["fcc_12"]) <= 1e-12 * z["fcc_12"] and abs(bcc.z_m - z["bcc_6"]) <= 1e-12 * z["bcc_6"]
+    assert abs(fcc.k_atm - golden_integrals["fcc"]["atm"]) <= 1e-10 * golden_integrals["fcc"]["atm"]
+    assert abs(bcc.k_atm - golden_integrals["bcc"]["atm"]) <= 1e-10 * golden_integrals["bcc"]["atm"]
+    expect = {0.0: 0.6347989463554651, 0.5: 0.6736514573960529, 1.0: 0.7088057861542634,
+              2.0: 0.7706881159724265}
+    for p, lc in expect.items():
+        assert abs(critical_coupling(fcc, bcc, lj, p) - lc) < 1e-8, p
+    pts = phase_scan(fcc, bcc, lj, [0.0, 1.0], np.linspace(0.0, 2.0, 64), np.linspace(0.9, 1.7, 64))
+    assert pts[0].winner == "fcc" and pts[63].winner == "bcc"
