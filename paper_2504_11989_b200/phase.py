@@ -58,70 +58,108 @@ def total_enthalpy(c: LatticeConstants, lj: LJParams, lam: float, p: float, r):
     return lj_cohesive(c, lj, r) + lam * c.k_atm / r ** 9 + p * c.v_unit * r ** 3
 
 
+def _enthalpy_derivs(c, lj, lam, p, r):
+    """dH/dR and d2H/dR2 of total_enthalpy (closed form)."""
+    n, m = lj.n, lj.m
+    pre = n * m / (2.0 * (n - m))
+    a_, b_ = pre * c.z_n / n, pre * c.z_m / m        # H = a R^-n - b R^-m + lam K R^-9 + p V R^3
+    k_, v_ = lam * c.k_atm, p * c.v_unit
+    d1 = -n * a_ * r ** (-n - 1) + m * b_ * r ** (-m - 1) - 9.0 * k_ * r ** -10 + 3.0 * v_ * r ** 2
+    d2 = (n * (n + 1) * a_ * r ** (-n - 2) - m * (m + 1) * b_ * r ** (-m - 2) + 90.0 * k_ * r ** -11
+          + 6.0 * v_ * r)
+    return d1, d2
+
+
+def _golden_min(c, lj, lam, p, r_grid, tol=1e-13, iters=12):
+    """Vectorised global minimum of H(R) over R for arrays of (lambda, p): best point of the R grid,
+    then safeguarded Newton on dH/dR = 0 inside the bracketing grid cells (quadratic convergence;
+    a golden-section step replaces any Newton step that leaves the bracket)."""
+    lam = np.asarray(lam, dtype=float)
+    p = np.asarray(p, dtype=float)
+    lam, p = np.broadcast_arrays(lam, p)
+    r_grid = np.asarray(r_grid, dtype=float)
+    h = total_enthalpy(c, lj, lam[..., None], p[..., None], r_grid)
+    i = np.argmin(h, axis=-1)
+    if np.any((i == 0) | (i == len(r_grid) - 1)):
+        raise ValueError("enthalpy minimum hits the R bracket boundary")
+    lo, hi = r_grid[i - 1], r_grid[i + 1]
+    r = r_grid[i].astype(float)
+    active = np.ones(r.shape, dtype=bool)
+    for _ in range(iters + 40):
+        d1, d2 = _enthalpy_derivs(c, lj, lam, p, r)
+        step = np.where(d2 > 0.0, d1 / np.where(d2 > 0.0, d2, 1.0), 0.0)
+        rn = r - step
+        bad = (d2 <= 0.0) | (rn <= lo) | (rn >= hi)
+        rn = np.where(bad, np.where(d1 > 0.0, lo + _GOLD * (r - lo), r + (1.0 - _GOLD) * (hi - r)), rn)
+        # shrink the bracket around the root of dH/dR (converged entries are frozen)
+        lo = np.where(active & (d1 <= 0.0), np.maximum(lo, r), lo)
+        hi = np.where(active & (d1 > 0.0), np.minimum(hi, r), hi)
+        done = np.abs(rn - r) <= tol * np.abs(r)
+        r = np.where(active, rn, r)
+        active &= ~done
+        if not np.any(active):
+            break
+    return r, total_enthalpy(c, lj, lam, p, r)
+
+
 def optimize_scale(c: LatticeConstants, lj: LJParams, lam: float, p: float,
                    r_grid=None, tol: float = 1e-13):
-    """Global minimum of H(R): best point of a coarse grid, then golden-section refinement."""
+    """Global minimum of H(R): best point of a coarse grid, then golden-section refinement
+    (SPEC.md: optimize_scale).  Returns (R*, H*)."""
     if r_grid is None:
         r_grid = np.linspace(0.5, 3.0, 200)
-    r_grid = np.asarray(r_grid, dtype=float)
-    h = total_enthalpy(c, lj, lam, p, r_grid)
-    i = int(np.argmin(h))
-    if i == 0 or i == len(r_grid) - 1:
-        raise ValueError("enthalpy minimum hits the R bracket boundary")
-    a, b = r_grid[i - 1], r_grid[i + 1]
-    x1 = b - _GOLD * (b - a)
-    x2 = a + _GOLD * (b - a)
-    f1 = float(total_enthalpy(c, lj, lam, p, x1))
-    f2 = float(total_enthalpy(c, lj, lam, p, x2))
-    while b - a > tol * max(1.0, abs(a)):
-        if f1 < f2:
-            b, x2, f2 = x2, x1, f1
-            x1 = b - _GOLD * (b - a)
-            f1 = float(total_enthalpy(c, lj, lam, p, x1))
-        else:
-            a, x1, f1 = x1, x2, f2
-            x2 = a + _GOLD * (b - a)
-            f2 = float(total_enthalpy(c, lj, lam, p, x2))
-    r = 0.5 * (a + b)
-    return r, float(total_enthalpy(c, lj, lam, p, r))
-
-
-def _delta_h(fcc, bcc, lj, lam, p, r_grid):
-    return optimize_scale(fcc, lj, lam, p, r_grid)[1] - optimize_scale(bcc, lj, lam, p, r_grid)[1]
+    r, h = _golden_min(c, lj, lam, p, r_grid, tol)
+    return float(r), float(h)
 
 
 def phase_scan(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams, p_grid, lam_grid,
                r_grid=None):
     """Winner of min_R H for every (p, lambda) of the grids, ordered by (p, lambda)."""
+    if r_grid is None:
+        r_grid = np.linspace(0.5, 3.0, 200)
+    P, L = np.meshgrid(np.asarray(p_grid, float), np.asarray(lam_grid, float), indexing="ij")
+    rf, hf = _golden_min(fcc, lj, L, P, r_grid)
+    rb, hb = _golden_min(bcc, lj, L, P, r_grid)
     pts = []
-    for p in p_grid:
-        for lam in lam_grid:
-            rf, hf = optimize_scale(fcc, lj, float(lam), float(p), r_grid)
-            rb, hb = optimize_scale(bcc, lj, float(lam), float(p), r_grid)
-            pts.append(PhasePoint(float(p), float(lam), "fcc" if hf <= hb else "bcc", rf, rb, hf, hb))
+    for idx in np.ndindex(P.shape):
+        pts.append(PhasePoint(float(P[idx]), float(L[idx]), "fcc" if hf[idx] <= hb[idx] else "bcc",
+                              float(rf[idx]), float(rb[idx]), float(hf[idx]), float(hb[idx])))
     return pts
 
 
-def critical_coupling(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams, p: float,
+def critical_coupling(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams, p,
                       lam_grid=None, r_grid=None, tol: float = 1e-14):
-    """lambda_c(p): first fcc -> bcc sign change of min_R H_fcc - min_R H_bcc on the lambda
-    grid, refined by bisection (SPEC.md: 'bisection on lambda ... between bracketing points')."""
+    """lambda_c(p): first fcc -> bcc sign change of min_R H_fcc - min_R H_bcc on the lambda grid,
+    refined by bisection (SPEC.md: 'bisection on lambda ... between bracketing points').
+    ``p`` may be a scalar or an array (vectorised over pressures)."""
     if lam_grid is None:
         lam_grid = np.linspace(0.0, 2.0, 64)
-    vals = [_delta_h(fcc, bcc, lj, float(l), p, r_grid) for l in lam_grid]
-    for i in range(len(lam_grid) - 1):
-        if vals[i] <= 0.0 < vals[i + 1]:
-            a, b = float(lam_grid[i]), float(lam_grid[i + 1])
-            fa = vals[i]
-            while b - a > tol:
-                mid = 0.5 * (a + b)
-                fm = _delta_h(fcc, bcc, lj, mid, p, r_grid)
-                if (fm <= 0.0) == (fa <= 0.0):
-                    a, fa = mid, fm
-                else:
-                    b = mid
-            return 0.5 * (a + b)
-    return math.nan
+    if r_grid is None:
+        r_grid = np.linspace(0.5, 3.0, 200)
+    scalar = np.ndim(p) == 0
+    p = np.atleast_1d(np.asarray(p, float))
+    lam_grid = np.asarray(lam_grid, float)
+
+    def delta(lam, pp):
+        return _golden_min(fcc, lj, lam, pp, r_grid)[1] - _golden_min(bcc, lj, lam, pp, r_grid)[1]
+
+    dv = delta(lam_grid[None, :], p[:, None])
+    out = np.full(len(p), np.nan)
+    flip = (dv[:, :-1] <= 0.0) & (dv[:, 1:] > 0.0)
+    has = flip.any(axis=1)
+    first = np.argmax(flip, axis=1)
+    a = lam_grid[first].astype(float)
+    b = lam_grid[np.minimum(first + 1, len(lam_grid) - 1)].astype(float)
+    for _ in range(200):
+        if np.all(b - a <= tol):
+            break
+        mid = 0.5 * (a + b)
+        fm = delta(mid, p)
+        go_right = fm <= 0.0
+        a = np.where(go_right, mid, a)
+        b = np.where(go_right, b, mid)
+    out[has] = 0.5 * (a + b)[has]
+    return float(out[0]) if scalar else out
 
 
 def lattice_constants(name: str, lj: LJParams = LJParams(), atm_grid=None) -> LatticeConstants:

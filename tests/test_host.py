@@ -156,6 +156,8 @@ def test_phase_scan_from_reference_constants(golden, golden_integrals):
     for p, lc in expect.items():
         got = critical_coupling(fcc, bcc, lj, p)
         assert abs(got - lc) < 1e-9, (p, got, lc)
+    vec = critical_coupling(fcc, bcc, lj, list(expect))   # vectorised over pressures
+    assert np.allclose(vec, list(expect.values()), rtol=0, atol=1e-9)
     pts = phase_scan(fcc, bcc, lj, [0.0], np.linspace(0, 2, 64))
     assert pts[0].winner == "fcc"      # fcc wins at lambda = 0
     winners = [p.winner for p in pts]
