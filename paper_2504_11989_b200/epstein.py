@@ -113,12 +113,12 @@ class EpsteinContext:
         self.has_hessian = deriv_order >= 2  # Hessian point sets and tables are built on first use
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and N._lib is not None:
-            try:
-                N.lib().lz_ctx_destroy(h)
-            except Exception:
-                pass
+        try:  # also reached at interpreter shutdown, when module globals may be gone
+            h = getattr(self, "_h", None)
+            if h is not None and N is not None and N._lib is not None:
+                N._lib.lz_ctx_destroy(h)
+        except Exception:
+            pass
 
     def table_stats(self, hessian: bool = False) -> "N.CtxInfo":
         """Build the evaluation tables now (normally lazy) and return the context info with the

@@ -175,12 +175,12 @@ class Plan:
         self._keep = keepalive  # contexts must outlive the plan
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and N._lib is not None:
-            try:
-                N.lib().lz_plan_destroy(h)
-            except Exception:
-                pass
+        try:  # also reached at interpreter shutdown, when module globals may be gone
+            h = getattr(self, "_h", None)
+            if h is not None and N is not None and N._lib is not None:
+                N._lib.lz_plan_destroy(h)
+        except Exception:
+            pass
 
     @property
     def handle(self):
