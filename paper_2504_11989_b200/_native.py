@@ -21,7 +21,7 @@ LIB_DIR = os.path.join(_HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblatsum_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
-SOURCES = ["kernels.cu", "context.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "direct.cu", "context.cpp", "capi.cpp"]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -87,6 +87,7 @@ SIGNATURES = {
     "lz_ctx_reg_derivatives": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
                                           C.POINTER(C.c_int64)]),
     "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
+    "lz_direct_sum3": (C.c_int, [C.c_int, _D, C.c_int64, C.c_int, _D, C.c_double, _D]),
     "lz_fp64_peak": (C.c_int, [_D, _D]),
     "lz_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "lz_strerror": (C.c_char_p, [C.c_int]),

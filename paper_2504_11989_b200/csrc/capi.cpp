@@ -30,6 +30,9 @@ cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int
                        cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st);
 cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cudaStream_t st);
+cudaError_t launch_direct(int d, int kind, int64_t L, int64_t npts, const double* A, const double* nus,
+                          double* partials, int64_t nblocks, cudaStream_t st);
+int direct_tile();
 
 }  // namespace lz
 
@@ -1018,6 +1021,41 @@ int lz_ctx_reg_derivatives(const lz_ctx* c, int order, int* alphas, double* vals
 double lz_upper_gamma(double s, double x) {
     if (!(x > 0.0)) return std::nan("");
     return double(lz::upper_gamma<long double>(s, x));
+}
+
+int lz_direct_sum3(int d, const double* a, int64_t L, int kind, const double* nus, double max_pairs,
+                   double* out) {
+    return guarded([&] {
+        if (d < 1 || d > 3) throw Error{LZ_EINVAL, "direct sums support d = 1..3"};
+        if (L < 1) throw Error{LZ_EINVAL, "truncation L must be >= 1"};
+        if (kind != 0 && kind != 1) throw Error{LZ_EINVAL, "kind: 0 three-body zeta, 1 ATM energy"};
+        int64_t npts = 1;
+        for (int i = 0; i < d; ++i) npts *= 2 * L + 1;
+        const double pairs = double(npts) * double(npts);
+        if (max_pairs > 0 && pairs > max_pairs)
+            throw Error{LZ_EINVAL, "direct sum exceeds the term guard (pass a larger max_pairs)"};
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "device");
+        Arena& ar = arena(dev);
+        std::lock_guard<std::mutex> lock(ar.mu);
+        const int64_t nblocks = (npts + lz::direct_tile() - 1) / lz::direct_tile();
+        ar.ensure(al256(sizeof(double) * 16) + al256(sizeof(double) * size_t(nblocks)) + 256, 256);
+        double* dA = reinterpret_cast<double*>(ar.dbuf);
+        double* dp = reinterpret_cast<double*>(ar.dbuf + al256(sizeof(double) * 16));
+        double* dout = reinterpret_cast<double*>(ar.dbuf + al256(sizeof(double) * 16) +
+                                                 al256(sizeof(double) * size_t(nblocks)));
+        double hA[16] = {0};
+        for (int i = 0; i < d * d; ++i) hA[i] = a[i];
+        check_cuda(cudaMemcpyAsync(dA, hA, sizeof(hA), cudaMemcpyHostToDevice, ar.st), "h2d");
+        const double nz[3] = {nus ? nus[0] : 0.0, nus ? nus[1] : 0.0, nus ? nus[2] : 0.0};
+        check_cuda(lz::launch_direct(d, kind, L, npts, dA, nz, dp, nblocks, ar.st), "direct kernel");
+        check_cuda(lz::launch_reduce(dp, nblocks, 1, dout, ar.st), "reduce");
+        check_cuda(cudaMemcpyAsync(ar.hbuf, dout, sizeof(double), cudaMemcpyDeviceToHost, ar.st), "d2h");
+        check_cuda(cudaStreamSynchronize(ar.st), "sync");
+        double v;
+        std::memcpy(&v, ar.hbuf, sizeof(double));
+        *out = kind == 1 ? v / 6.0 : v;
+    });
 }
 
 int lz_fp64_peak(double* tflops, double* ms_out) {

@@ -200,3 +200,23 @@ def test_c5_phase_scan_from_gpu_constants(golden, golden_integrals):
         assert abs(critical_coupling(fcc, bcc, lj, p) - lc) < 1e-8, p
     pts = phase_scan(fcc, bcc, lj, [0.0, 1.0], np.linspace(0.0, 2.0, 64), np.linspace(0.9, 1.7, 64))
     assert pts[0].winner == "fcc" and pts[63].winner == "bcc"
+
+
+def test_direct_sums_reproduce_paper_and_epstein(golden, golden_integrals):
+    """GPU direct summation (SPEC oracle module): the paper's own direct-sum values, and the
+    algebraic convergence of direct sums to the Epstein-method results."""
+    from paper_2504_11989_b200.direct import direct_sum_atm, direct_sum_zeta
+    # PAPER.md:338 -- 1D ATM by direct summation at L = 5000
+    e1 = direct_sum_atm(named_lattice("Z"), 5000)
+    assert abs(e1 - (-0.2723018495076886)) <= 2e-15
+    # PAPER.md:355 -- 2D square-lattice ATM at L = 250 ("over 10^10 summands", ~6 h on one core)
+    e2 = direct_sum_atm(named_lattice("square"), 250)
+    assert abs(e2 - 0.7700936511489661) <= 1e-13 * abs(e2)
+    # the truncated sums approach the Epstein values
+    ref2 = golden_integrals["square"]["atm"]
+    assert abs(e2 - ref2) < 1e-8 * ref2
+    z = direct_sum_zeta(named_lattice("square"), (3, 3, 3), 200)
+    assert abs(z - golden["c2"]["value"]) < 3e-9 * golden["c2"]["value"]
+    fcc = named_lattice("fcc")
+    errs = [abs(direct_sum_atm(fcc, L) - golden_integrals["fcc"]["atm"]) for L in (4, 8, 16)]
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 5e-4 * golden_integrals["fcc"]["atm"]
