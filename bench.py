@@ -32,10 +32,10 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v8); used to turn the live kernel time into FLOP/s.
-FLOPS_PER_NODE = 14537.2
-FLOPS_SOURCE = "ncu r01 v8: 3.6584e11 FP64 FLOPs per launch / 25,165,824 nodes"
-TRAFFIC_PER_LAUNCH = 598_016 + 34_048  # ncu r01 v8 dram__bytes_read.sum + dram__bytes_write.sum
+# bench grid (profiles/r01_summary.md, v9); used to turn the live kernel time into FLOP/s.
+FLOPS_PER_NODE = 13667.2
+FLOPS_SOURCE = "ncu r01 v9: 3.4395e+11 FP64 FLOPs per launch / 25,165,824 nodes"
+TRAFFIC_PER_LAUNCH = 631_040 + 30_464  # ncu r01 v9 dram__bytes_read.sum + dram__bytes_write.sum
 
 
 def parse():
