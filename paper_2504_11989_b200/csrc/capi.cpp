@@ -201,34 +201,11 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             for (int a = 0; cont && a < d - 1; ++a) cont = key(i, a) == key(i - 1, a);
             cont = cont && key(i, d - 1) == key(i - 1, d - 1) + 1;
             if (cont) {
-                hp->run_info[hp->run_info.size() - 3] += 1;
+                hp->run_info.back() += 1;
             } else {
                 hp->run_n.insert(hp->run_n.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
                 hp->run_info.push_back(int(i));
                 hp->run_info.push_back(1);
-                hp->run_info.push_back(1);   // anchor flag (set below)
-                hp->run_info.push_back(0);   // packed start-to-start delta
-            }
-        }
-        // Run-start phases chain: start_r = start_{r-1} * exp(2 pi i kappa . dn) with small integer
-        // dn (one rotation per unit step, warp-uniform); a true sincospi re-anchors every
-        // kAnchor runs and whenever the step is long, bounding the rounding growth.
-        const int kAnchor = 6;
-        const int nr = int(hp->run_info.size() / 4);
-        for (int r = 0; r < nr; ++r) {
-            int* info = &hp->run_info[size_t(r) * 4];
-            if (r % kAnchor == 0) continue;
-            int packed = 0, l1 = 0;
-            bool ok = true;
-            for (int a = 0; a < d; ++a) {
-                const long dn = std::lround(hp->run_n[size_t(r) * d + a] - hp->run_n[size_t(r - 1) * d + a]);
-                if (dn < -127 || dn > 127) ok = false;
-                l1 += int(std::labs(dn));
-                packed |= (int(dn) & 0xff) << (8 * a);
-            }
-            if (ok && l1 <= 6) {
-                info[2] = 0;
-                info[3] = packed;
             }
         }
     }
@@ -381,7 +358,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     std::memcpy(P.B, hp.B, sizeof(P.B));
     P.dir_n = upload(hp.run_n, allocs);
     P.run_info = upload(hp.run_info, allocs);
-    P.n_runs = int(hp.run_info.size() / 4);
+    P.n_runs = int(hp.run_info.size() / 2);
     P.dir_w = upload(hp.dir_w, allocs);
     P.rec_q = upload(hp.rec_q, allocs);
     P.rec_norm = upload(hp.rec_norm, allocs);
@@ -977,7 +954,7 @@ int lz_plan_get_info(const lz_plan* pl, lz_plan_info* o) {
     o->hess = pl->hp.hess;
     o->alias = pl->hp.alias_fp;
     o->n_dir = int64_t(pl->hp.dir_n.size() / std::max(pl->d, 1));
-    o->n_runs = int64_t(pl->hp.run_info.size() / 4);
+    o->n_runs = int64_t(pl->hp.run_info.size() / 2);
     o->n_rec = int64_t(pl->hp.rec_norm.size());
     o->n_funcs = pl->hp.tab.nfunc;
     o->table_pieces = pl->hp.tab.npieces;

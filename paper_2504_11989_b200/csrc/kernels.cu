@@ -59,7 +59,7 @@ __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(
 __host__ size_t plan_smem_bytes(const DevPlan& P) {
     size_t b = 0;
     b += align16(sizeof(double) * P.n_runs * P.d);
-    b += align16(sizeof(int) * P.n_runs * 4);
+    b += align16(sizeof(int) * P.n_runs * 2);
     b += align16(sizeof(double) * P.n_dir * P.nw);
     b += align16(sizeof(double) * P.n_rec * P.d);
     b += align16(sizeof(double) * P.n_rec);
@@ -91,7 +91,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* dn = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_runs * P.d);
         int* ri = reinterpret_cast<int*>(smem + off);
-        off += align16(sizeof(int) * P.n_runs * 4);
+        off += align16(sizeof(int) * P.n_runs * 2);
         double* dw = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_dir * P.nw);
         double* rq = reinterpret_cast<double*>(smem + off);
@@ -104,7 +104,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
         copy_words(dn, P.dir_n, size_t(P.n_runs) * P.d);
-        for (int i = threadIdx.x; i < 4 * P.n_runs; i += blockDim.x) ri[i] = P.run_info[i];
+        for (int i = threadIdx.x; i < 2 * P.n_runs; i += blockDim.x) ri[i] = P.run_info[i];
         copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
         copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
@@ -293,35 +293,17 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     // cos((l+1) th) = 2 cos(th) cos(l th) - cos((l-1) th), th = 2 pi kappa_d (one DFMA per point;
     // runs are short, so the O(l^2 eps) error growth stays at the 1e-15 level)
     {
-        double ec[D], es[D];  // exp(2 pi i kappa_a)
-#pragma unroll
-        for (int a = 0; a < D; ++a) sincospi(2.0 * kap[a], &es[a], &ec[a]);
-        const double sd = es[D - 1], cd = ec[D - 1];
+        double sd, cd;
+        sincospi(2.0 * kap[D - 1], &sd, &cd);
         const double two_cd = 2.0 * cd;
-        double c0 = 1.0, s0 = 0.0;  // phase at the start of the current run
         for (int r = gl; r < P.n_runs; r += G) {
-            const int4 info = reinterpret_cast<const int4*>(V.run_info)[r];
-            if (G > 1 || info.z) {
-                double ph = 0.0;
+            double ph = 0.0;
 #pragma unroll
-                for (int a = 0; a < D; ++a) ph = fma(kap[a], V.dir_n[r * D + a], ph);
-                sincospi(2.0 * ph, &s0, &c0);
-            } else {
-                // chain from the previous run start: rotate by exp(2 pi i kappa_a) per unit step
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    const int m = static_cast<signed char>((info.w >> (8 * a)) & 0xff);
-                    const double sa = m < 0 ? -es[a] : es[a];
-                    for (int t = 0; t < (m < 0 ? -m : m); ++t) {
-                        const double cn = fma(c0, ec[a], -s0 * sa);
-                        s0 = fma(s0, ec[a], c0 * sa);
-                        c0 = cn;
-                    }
-                }
-            }
-            double cs = c0;
-            double cprev = fma(cs, cd, s0 * sd);  // cos(phi - th)
-            const int first = info.x, len = info.y;
+            for (int a = 0; a < D; ++a) ph = fma(kap[a], V.dir_n[r * D + a], ph);
+            double sn, cs;
+            sincospi(2.0 * ph, &sn, &cs);
+            double cprev = fma(cs, cd, sn * sd);  // cos(phi - th)
+            const int first = V.run_info[2 * r], len = V.run_info[2 * r + 1];
             const double* w = V.dir_w + size_t(first) * NW;
             for (int l = 0; l < len; ++l) {
 #pragma unroll

@@ -74,7 +74,7 @@ struct DevPlan {
     double A[16];      // generator, row-major (columns = basis vectors)
     double B[16];      // A^{-T}, row-major
     const double* dir_n;   // [n_runs][d] integer coordinates of the first point of each run
-    const int* run_info;   // [n_runs][4] (first point, length, anchor, packed int8 start delta)
+    const int* run_info;   // [n_runs][2] (first point, length): runs of consecutive n_d
     int n_runs, pad3_;
     const double* dir_w;   // [n_dir][nw] weights (run order): nctx plain channels, then (hess) d(d+1)/2
     const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0, sorted by |q|
