@@ -261,7 +261,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (the fused ATM tile kernel)
     import ctypes as C
     pk, pms = C.c_double(0.0), C.c_double(0.0)
-    N.check(N.lib().lz_fp64_peak(C.byref(pk), C.byref(pms)), "fp64 peak probe")
+    N.check(N.lib().lz_fp64_peak(local, C.byref(pk), C.byref(pms)), "fp64 peak probe")
     local_nodes = min(S.local_nodes, S.n_nodes)
     achieved = FLOPS_PER_NODE * local_nodes / (kern_ms * 1e-3) / 1e12
 

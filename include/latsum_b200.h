@@ -140,10 +140,11 @@ double lz_upper_gamma(double s, double x);
  * (SPEC.md:354-406): kind 0 -> sum' |x|^-nu0 |y-x|^-nu1 |y|^-nu2,
  * kind 1 -> the ATM energy (1/6) sum' U_ATM(x, y).  max_pairs > 0 guards the (2L+1)^{2d} pair
  * count (SPEC guard 1e10 on a CPU; a B200 does ~1e11 pairs/s).  Synchronous, result on host. */
-int lz_direct_sum3(int d, const double* a, int64_t L, int kind, const double* nus, double max_pairs, double* out);
+int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, const double* nus, double max_pairs,
+                   double* out);
 
 /* -- diagnostics */
-int lz_fp64_peak(double* tflops_out, double* ms_out);  /* DFMA-chain probe on the current device */
+int lz_fp64_peak(int device, double* tflops_out, double* ms_out);  /* DFMA-chain probe on `device` */
 int lz_device_count(int* n);
 const char* lz_strerror(int code);
 const char* lz_last_error(void);   /* thread-local message of the last failure */

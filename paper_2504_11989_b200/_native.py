@@ -87,8 +87,8 @@ SIGNATURES = {
     "lz_ctx_reg_derivatives": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
                                           C.POINTER(C.c_int64)]),
     "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
-    "lz_direct_sum3": (C.c_int, [C.c_int, _D, C.c_int64, C.c_int, _D, C.c_double, _D]),
-    "lz_fp64_peak": (C.c_int, [_D, _D]),
+    "lz_direct_sum3": (C.c_int, [C.c_int, C.c_int, _D, C.c_int64, C.c_int, _D, C.c_double, _D]),
+    "lz_fp64_peak": (C.c_int, [C.c_int, _D, _D]),
     "lz_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "lz_strerror": (C.c_char_p, [C.c_int]),
     "lz_last_error": (C.c_char_p, []),

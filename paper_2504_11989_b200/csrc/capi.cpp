@@ -973,8 +973,20 @@ int lz_plan_get_info(const lz_plan* pl, lz_plan_info* o) {
     return LZ_OK;
 }
 
+// Device that owns a device pointer (multi-GPU processes: the library's own current device
+// may differ from the caller's).
+static int device_of(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return at.type == cudaMemoryTypeDevice ? at.device : -1;
+}
+
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream) {
     return guarded([&] {
+        DeviceGuard dg(device_of(partials));
         check_cuda(lz::launch_reduce(partials, n_tiles, ncomp, out, (cudaStream_t)stream), "reduce kernel");
     });
 }
@@ -1023,7 +1035,7 @@ double lz_upper_gamma(double s, double x) {
     return double(lz::upper_gamma<long double>(s, x));
 }
 
-int lz_direct_sum3(int d, const double* a, int64_t L, int kind, const double* nus, double max_pairs,
+int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, const double* nus, double max_pairs,
                    double* out) {
     return guarded([&] {
         if (d < 1 || d > 3) throw Error{LZ_EINVAL, "direct sums support d = 1..3"};
@@ -1034,6 +1046,7 @@ int lz_direct_sum3(int d, const double* a, int64_t L, int kind, const double* nu
         const double pairs = double(npts) * double(npts);
         if (max_pairs > 0 && pairs > max_pairs)
             throw Error{LZ_EINVAL, "direct sum exceeds the term guard (pass a larger max_pairs)"};
+        DeviceGuard guard(device);
         int dev = 0;
         check_cuda(cudaGetDevice(&dev), "device");
         Arena& ar = arena(dev);
@@ -1058,8 +1071,9 @@ int lz_direct_sum3(int d, const double* a, int64_t L, int kind, const double* nu
     });
 }
 
-int lz_fp64_peak(double* tflops, double* ms_out) {
+int lz_fp64_peak(int device, double* tflops, double* ms_out) {
     return guarded([&] {
+        DeviceGuard guard(device);
         int dev = 0, sms = 0;
         check_cuda(cudaGetDevice(&dev), "device");
         check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");

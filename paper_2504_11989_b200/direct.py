@@ -25,8 +25,8 @@ def _run(lattice: Lattice, L: int, kind: int, nus, max_pairs: float) -> float:
     a = np.ascontiguousarray(lattice.a, dtype=np.float64)
     nu = np.ascontiguousarray(np.asarray(nus if nus is not None else (0.0, 0.0, 0.0), dtype=np.float64))
     out = C.c_double(0.0)
-    N.check(N.lib().lz_direct_sum3(lattice.d, N.dptr(a), int(L), kind, N.dptr(nu), float(max_pairs),
-                                   C.byref(out)), "direct sum")
+    N.check(N.lib().lz_direct_sum3(N.current_device(), lattice.d, N.dptr(a), int(L), kind, N.dptr(nu),
+                                   float(max_pairs), C.byref(out)), "direct sum")
     return out.value
 
 
