@@ -13,6 +13,9 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <unordered_map>
+#include <unordered_set>
+#include <future>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -95,16 +98,25 @@ struct HostPlan {
 using ld = long double;
 
 // Union of integer point sets (keeps the order of the first, appends the rest).
+// lattice coordinates packed into one 64-bit key (16 bits per axis, d <= 4)
+uint64_t pack_key(int d, const double* n) {
+    uint64_t key = 0;
+    for (int a = 0; a < d; ++a) {
+        const long v = std::lround(n[a]);
+        if (v < -32767 || v > 32767) throw Error{LZ_EINVAL, "lattice point index out of range"};
+        key = (key << 16) | uint64_t(v + 32768);
+    }
+    return key;
+}
+
 void union_points(int d, const std::vector<const std::vector<double>*>& sets, std::vector<double>* out) {
     out->clear();
-    std::set<std::vector<long>> seen;
+    std::unordered_set<uint64_t> seen;
     for (const auto* s : sets) {
         const size_t cnt = s->size() / d;
-        for (size_t i = 0; i < cnt; ++i) {
-            std::vector<long> key(d);
-            for (int a = 0; a < d; ++a) key[a] = std::lround((*s)[i * d + a]);
-            if (seen.insert(key).second) out->insert(out->end(), s->begin() + i * d, s->begin() + (i + 1) * d);
-        }
+        for (size_t i = 0; i < cnt; ++i)
+            if (seen.insert(pack_key(d, &(*s)[i * d])).second)
+                out->insert(out->end(), s->begin() + i * d, s->begin() + (i + 1) * d);
     }
 }
 
@@ -120,6 +132,12 @@ ld direct_weight(const lz::HostCtx& h, const double* n, ld* z) {
     const ld nu = h.k.nu;
     const ld x = ld(lz::kPi) * ld(h.k.split) * r2;
     return lz::upper_gamma<ld>(nu / 2.0L, x) * std::pow(r2, -nu / 2.0L);
+}
+
+bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
+    for (const auto* v : sets)
+        if (!v->empty()) return false;
+    return true;
 }
 
 // Build a fused plan from plain contexts (+ optionally one Hessian context).
@@ -148,6 +166,50 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     auto by_size = [](const std::vector<double>* a, const std::vector<double>* b) { return a->size() > b->size(); };
     std::stable_sort(dsets.begin(), dsets.end(), by_size);
     std::stable_sort(rsets.begin(), rsets.end(), by_size);
+    // table functions: plain F_j = c^s E_{1-s}; Hessian F' = -c^{s+1} E_{-s}, F'' = c^{s+2} E_{-s-1}
+    double p[4], sc[4];
+    int nf = 0;
+    double rp = 0.0;
+    const ld c = ld(lz::kPi) / ld(first->k.split);
+    hp->c = first->k.c;
+    for (int j = 0; j < hp->nctx; ++j) {
+        const lz::CtxConst& k = plain[j]->k;
+        hp->ctx[j] = k;
+        p[nf] = 1.0 - k.s;
+        sc[nf] = double(std::pow(c, ld(k.s)));
+        ++nf;
+        rp = std::max(rp, std::fabs(k.rfac * k.pref));
+    }
+    std::memset(&hp->hctx, 0, sizeof(hp->hctx));
+    hp->alias_fp = 0;
+    hp->alias_ratio = 0.0;
+    if (hess) {
+        const lz::CtxConst& k = hess->k;
+        hp->hctx = k;
+        // F' = -c^{s+1} E_{-s}: when plain context 0 has s0 = s + 1 its table is the same E_p
+        // (ATM: Z_3 and the Hessian of Z_5); then F' = ratio * F_0 and is not tabulated
+        if (hp->nctx == 1 && std::fabs(plain[0]->k.s - (k.s + 1.0)) < 1e-14) {
+            hp->alias_fp = 1;
+            hp->alias_ratio = double(-std::pow(c, ld(k.s) + 1.0L) / std::pow(c, ld(plain[0]->k.s)));
+        } else {
+            p[nf] = -k.s;
+            sc[nf] = -double(std::pow(c, ld(k.s) + 1.0L));
+            ++nf;
+        }
+        p[nf] = -k.s - 1.0;
+        sc[nf] = double(std::pow(c, ld(k.s) + 2.0L));
+        ++nf;
+        rp = std::max(rp, std::fabs(k.rfac * k.pref));
+    }
+    if (nf > 4) throw Error{LZ_EINVAL, "too many functions in one plan"};
+    // the piecewise tables depend only on the contexts' constants: fit them on a helper thread
+    // (which fans out over the host cores) while the point sets are prepared
+    std::future<void> table_job;
+    const double x_lo_tab = lz::table_x_lo(*first);
+    if (!rec_n_empty(rsets))
+        table_job = std::async(std::launch::async, [&hp, p, sc, nf, c, x_lo_tab, rp] {
+            lz::build_table(p, sc, nf, double(c), x_lo_tab, rp, &hp->tab);
+        });
     union_points(d, dsets, &hp->dir_n);
     std::vector<double> rec_n;
     union_points(d, rsets, &rec_n);
@@ -155,27 +217,36 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
     // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-18) times
     // the summed weights are dropped (|z|^2 factor covers the Hessian channels).
+    // weights of every context at every union point (long double), reused for the ball
+    // truncation and the kernel's weight channels
+    std::vector<const lz::HostCtx*> wctx(plain.begin(), plain.end());
+    if (hess) wctx.push_back(hess);
+    std::unordered_map<uint64_t, std::vector<ld>> wmap;
     {
         ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
+        std::vector<std::vector<ld>> wall(np, std::vector<ld>(wctx.size()));
         std::vector<ld> mag(np, 0.0L);
-        ld total = 0.0L;
-        std::vector<const lz::HostCtx*> all(plain.begin(), plain.end());
-        if (hess) all.push_back(hess);
-        for (size_t i = 0; i < np; ++i) {
+        lz::parallel_for(int64_t(np), 64, [&](int64_t i) {
             ld z[lz::kMaxDim];
-            for (const lz::HostCtx* c : all) {
-                ld w = std::fabs(direct_weight(*c, &hp->dir_n[i * d], z));
+            for (size_t j = 0; j < wctx.size(); ++j) {
+                const ld w = direct_weight(*wctx[j], &hp->dir_n[i * d], z);
+                wall[i][j] = w;
                 ld r2 = 0.0L;
                 for (int a = 0; a < d; ++a) r2 += z[a] * z[a];
-                mag[i] = std::max(mag[i], w * std::max(1.0L, r2));
-                total += w;
+                mag[i] = std::max(mag[i], std::fabs(w) * std::max(1.0L, r2));
             }
-        }
-        std::vector<double> kept;
+        });
+        ld total = 0.0L;  // fixed summation order: independent of the thread count
         for (size_t i = 0; i < np; ++i)
-            if (mag[i] > dcut * total) kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
+            for (size_t j = 0; j < wctx.size(); ++j) total += std::fabs(wall[i][j]);
+        std::vector<double> kept;
+        for (size_t i = 0; i < np; ++i) {
+            if (!(mag[i] > dcut * total)) continue;
+            kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
+            wmap.emplace(pack_key(d, &hp->dir_n[i * d]), std::move(wall[i]));
+        }
         hp->dir_n.swap(kept);
     }
     // Direct points as runs of consecutive last coordinates: the kernel evaluates one
@@ -215,18 +286,18 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     hp->dir_w.assign(ndir * hp->nw, 0.0);
     for (size_t i = 0; i < ndir; ++i) {
         const double* n = &hp->dir_n[i * d];
+        const std::vector<ld>& wts = wmap.at(pack_key(d, n));
         ld z[lz::kMaxDim];
-        for (int j = 0; j < hp->nctx; ++j) {
-            // reuse the context's own rounded weight when the point is in its set (bit-identical
-            // single-context plans), else compute it
-            const lz::HostCtx* c = plain[j];
-            hp->dir_w[i * hp->nw + j] = double(direct_weight(*c, n, z));
+        for (int a = 0; a < d; ++a) {
+            z[a] = 0.0L;
+            for (int b = 0; b < d; ++b) z[a] += ld(first->A[a * d + b]) * n[b];
         }
+        for (int j = 0; j < hp->nctx; ++j) hp->dir_w[i * hp->nw + j] = double(wts[j]);
         if (hess) {
             // direct Hessian term -8 pi^2 w z_a z_b cos(.), stored divided by 4 rfac so that it
             // shares the kernel's reciprocal accumulators (sum of y_a y_b F'')
             const ld scale = -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac);
-            ld w = direct_weight(*hess, n, z) * scale;
+            ld w = wts[hp->nctx] * scale;
             int cidx = 0;
             for (int a = 0; a < d; ++a)
                 for (int b = a; b < d; ++b) hp->dir_w[i * hp->nw + hp->nctx + cidx++] = double(w * z[a] * z[b]);
@@ -255,42 +326,6 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         for (int a = 0; a < d; ++a) hp->rec_q[i * d + a] = q[order[i] * d + a];
         hp->rec_norm[i] = double(qn[order[i]]);
     }
-    // table functions: plain F_j = c^s E_{1-s}; Hessian F' = -c^{s+1} E_{-s}, F'' = c^{s+2} E_{-s-1}
-    double p[4], sc[4];
-    int nf = 0;
-    double rp = 0.0;
-    const ld c = ld(lz::kPi) / ld(first->k.split);
-    hp->c = first->k.c;
-    for (int j = 0; j < hp->nctx; ++j) {
-        const lz::CtxConst& k = plain[j]->k;
-        hp->ctx[j] = k;
-        p[nf] = 1.0 - k.s;
-        sc[nf] = double(std::pow(c, ld(k.s)));
-        ++nf;
-        rp = std::max(rp, std::fabs(k.rfac * k.pref));
-    }
-    std::memset(&hp->hctx, 0, sizeof(hp->hctx));
-    hp->alias_fp = 0;
-    hp->alias_ratio = 0.0;
-    if (hess) {
-        const lz::CtxConst& k = hess->k;
-        hp->hctx = k;
-        // F' = -c^{s+1} E_{-s}: when plain context 0 has s0 = s + 1 its table is the same E_p
-        // (ATM: Z_3 and the Hessian of Z_5); then F' = ratio * F_0 and is not tabulated
-        if (hp->nctx == 1 && std::fabs(plain[0]->k.s - (k.s + 1.0)) < 1e-14) {
-            hp->alias_fp = 1;
-            hp->alias_ratio = double(-std::pow(c, ld(k.s) + 1.0L) / std::pow(c, ld(plain[0]->k.s)));
-        } else {
-            p[nf] = -k.s;
-            sc[nf] = -double(std::pow(c, ld(k.s) + 1.0L));
-            ++nf;
-        }
-        p[nf] = -k.s - 1.0;
-        sc[nf] = double(std::pow(c, ld(k.s) + 2.0L));
-        ++nf;
-        rp = std::max(rp, std::fabs(k.rfac * k.pref));
-    }
-    if (nf > 4) throw Error{LZ_EINVAL, "too many functions in one plan"};
     // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives)
     {
         const int rows = hp->nctx + (hess ? 2 : 0);
@@ -329,11 +364,11 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->n_t0 = std::min(need, lz::kT0);
         hp->t0_rho_max = ok ? double(rho_max) : -1.0;
     }
-    if (hp->rec_q.empty()) {
+    if (!table_job.valid()) {
         hp->tab = lz::HostTable();
         hp->tab.nfunc = nf;
     } else {
-        lz::build_table(p, sc, nf, double(c), lz::table_x_lo(*first), rp, &hp->tab);
+        table_job.get();
         // beyond x_hi every tabulated function is exactly zero in the kernel
         hp->r_cut = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L + 1e-9L));
     }

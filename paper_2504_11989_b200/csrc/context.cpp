@@ -99,8 +99,6 @@ bool lex_positive(const int* n, int d) {
     return false;
 }
 
-// Gamma(s, x) on the host (long double), any real s, x > 0.
-ld upper_gamma_l(ld s, ld x) { return upper_gamma<ld>(s, x); }
 
 }  // namespace
 
@@ -152,9 +150,11 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
                 for (int b = 0; b < d; ++b) z[a] += ld(h.A[a * d + b]) * n[b];
                 r2 += z[a] * z[a];
             }
-            ld x = kPiL * t * r2;
-            ld w = upper_gamma_l(nu / 2.0L, x) * std::pow(r2, -nu / 2.0L);
-            mag = std::max(mag, std::fabs(w) * std::pow(r2, ld(poly_order) / 2.0L));
+            // truncation decisions and the reported weights need double precision only (the
+            // reference computes them in double); plan weights are recomputed in long double
+            const double xd = double(kPiL * t * r2), r2d = double(r2), nud = double(nu);
+            ld w = upper_gamma<double>(nud / 2.0, xd) * std::pow(r2d, -nud / 2.0);
+            mag = std::max(mag, std::fabs(w) * ld(std::pow(r2d, double(poly_order) / 2.0)));
             wsum += std::fabs(w);
             for (int a = 0; a < d; ++a) {
                 sn.push_back(double(n[a]));
@@ -208,7 +208,8 @@ static void enumerate_reciprocal(const HostCtx& h, double gamma_order, double to
                 ld r_low = rq[i] - kmax;
                 ld x_low = kPiL * r_low * r_low / t;
                 ld r_pow = (nu >= d) ? rq[i] + kmax : r_low;
-                ld bound = std::fabs(upper_gamma_l(ld(gamma_order), x_low)) * std::pow(r_pow, nu - d);
+                ld bound = std::fabs(upper_gamma<double>(gamma_order, double(x_low))) *
+                           std::pow(double(r_pow), double(nu) - d);
                 mag = std::max(mag, bound);
             }
         }
@@ -461,16 +462,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
         }
         bf.level = kDirectMarker;  // evaluate E_p directly in this bin
     };
-    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    if (nbins < 8) nth = 1;
-    std::atomic<int> next(0);
-    auto worker = [&]() {
-        for (int b = next++; b < nbins; b = next++) fit_bin(b);
-    };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(worker);
-    worker();
-    for (auto& th : pool) th.join();
+    parallel_for(nbins, 1, [&](int64_t b) { fit_bin(int(b)); });
     // Direct (unfitted) bins must form a prefix: the kernel's conversion-free floor may step one
     // piece past a bin's last piece at an exact bin boundary, which is then the next bin's first
     // piece evaluated at the same x -- valid only if that next bin has pieces.
@@ -491,6 +483,21 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
         npieces += 1 << bf.level;
     }
     out->npieces = npieces;
+}
+
+void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t)>& body) {
+    grain = std::max<int64_t>(1, grain);
+    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n < 2 * grain || n < 8) nth = 1;
+    std::atomic<int64_t> next(0);
+    auto worker = [&]() {
+        for (int64_t b = next.fetch_add(grain); b < n; b = next.fetch_add(grain))
+            for (int64_t i = b; i < std::min(n, b + grain); ++i) body(i);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
 }
 
 // Gauss-Legendre nodes/weights on [-1, 1] by Newton iteration on P_n (long double).

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -168,5 +169,8 @@ void build_hess_sets(HostCtx& h);
 long double t0_coeff(const CtxConst& k, int n);   // rho-series coefficient of t0_reg
 void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals);
 void gauss_legendre(int n, std::vector<double>* x, std::vector<double>* w);  // on [-1, 1]
+// body(i) for i in [0, n) on up to 32 host threads (dynamic chunks of `grain`); serial when
+// n < 2 * grain.  Host setup only (table fits, plan weights).
+void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t)>& body);
 
 }  // namespace lz

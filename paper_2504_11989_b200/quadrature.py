@@ -245,8 +245,12 @@ def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
     """Plan for the ATM integrand [Z_3^3, tr(M_5^3)], M_5 = polynomial-weighted zeta at nu = 5."""
     if splitting is None and ATM_SPLIT_SCALE != 1.0:
         splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
-    z3 = epstein_context(lattice, 3.0, splitting)
-    z5 = epstein_context(lattice, 5.0, splitting)
+    # the two contexts' host enumerations are independent native calls (GIL released): overlap them
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        f5 = pool.submit(epstein_context, lattice, 5.0, splitting)
+        z3 = epstein_context(lattice, 3.0, splitting)
+        z5 = f5.result()
     h = C.c_void_p()
     N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)), "atm plan")
     return Plan(h, lattice.d, 2, (z3, z5))
