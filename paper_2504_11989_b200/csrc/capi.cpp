@@ -85,7 +85,8 @@ void free_all(std::vector<void*>* allocs) {
 struct HostPlan {
     int d = 0, nctx = 0, hess = 0, nw = 0, alias_fp = 0;
     double c = 0.0, r_cut = 0.0, alias_ratio = 0.0;
-    std::vector<double> dir_n, dir_w, rec_q, rec_norm, run_n, t0c;
+    std::vector<double> dir_n, dir_w, rec_q, rec_norm, run_n, run_rec, t0c;
+    double estep[4] = {0, 0, 0, 0};
     int n_t0 = 0;
     double t0_rho_max = -1.0;
     std::vector<int> run_info;
@@ -280,27 +281,50 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             }
         }
     }
-    const int nsym = d * (d + 1) / 2;
-    hp->nw = hp->nctx + (hess ? nsym : 0);
-    const size_t ndir = hp->dir_n.size() / d;
-    hp->dir_w.assign(ndir * hp->nw, 0.0);
-    for (size_t i = 0; i < ndir; ++i) {
-        const double* n = &hp->dir_n[i * d];
-        const std::vector<ld>& wts = wmap.at(pack_key(d, n));
-        ld z[lz::kMaxDim];
+    // Weight rows per run, padded to even length (the kernel walks runs two points at a time).
+    // Hessian: the direct term -8 pi^2 w z_a z_b cos(.) is stored divided by 4 rfac so that it
+    // shares the kernel's reciprocal accumulators (sum of y_a y_b F''), and factorised along the
+    // run: z = z0 + l e (z0 at the run center, e = A e_d), so three channels w l^m (m = 0, 1, 2)
+    // replace the d(d+1)/2 channels w z_a z_b.
+    const int nh = hess ? 3 : 0;
+    hp->nw = (hp->nctx + nh == 1) ? 1 : ((hp->nctx + nh + 1) & ~1);
+    const int rs = 2 * d + 2;
+    ld e[lz::kMaxDim];
+    for (int a = 0; a < d; ++a) {
+        e[a] = ld(first->A[a * d + d - 1]);
+        hp->estep[a] = double(e[a]);
+    }
+    const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
+    const size_t nruns = hp->run_info.size() / 2;
+    hp->run_rec.assign(nruns * rs, 0.0);
+    hp->dir_w.clear();
+    for (size_t r = 0; r < nruns; ++r) {
+        const int f = hp->run_info[2 * r], len = hp->run_info[2 * r + 1];
+        const int lenp = len + (len & 1);
+        const int row0 = int(hp->dir_w.size() / hp->nw);
+        const ld center = ld(len - 1) / 2.0L;
+        double* rec = &hp->run_rec[r * rs];
+        const double* n0 = &hp->dir_n[size_t(f) * d];
         for (int a = 0; a < d; ++a) {
-            z[a] = 0.0L;
-            for (int b = 0; b < d; ++b) z[a] += ld(first->A[a * d + b]) * n[b];
+            ld z0 = center * e[a];
+            for (int b = 0; b < d; ++b) z0 += ld(first->A[a * d + b]) * n0[b];
+            rec[a] = n0[a];
+            rec[d + a] = double(z0);
         }
-        for (int j = 0; j < hp->nctx; ++j) hp->dir_w[i * hp->nw + j] = double(wts[j]);
-        if (hess) {
-            // direct Hessian term -8 pi^2 w z_a z_b cos(.), stored divided by 4 rfac so that it
-            // shares the kernel's reciprocal accumulators (sum of y_a y_b F'')
-            const ld scale = -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac);
-            ld w = wts[hp->nctx] * scale;
-            int cidx = 0;
-            for (int a = 0; a < d; ++a)
-                for (int b = a; b < d; ++b) hp->dir_w[i * hp->nw + hp->nctx + cidx++] = double(w * z[a] * z[b]);
+        const int32_t info[2] = {row0, lenp};
+        std::memcpy(&rec[2 * d], info, sizeof(info));
+        for (int l = 0; l < lenp; ++l) {
+            const size_t base = hp->dir_w.size();
+            hp->dir_w.resize(base + hp->nw, 0.0);
+            if (l >= len) continue;
+            const std::vector<ld>& wts = wmap.at(pack_key(d, &hp->dir_n[size_t(f + l) * d]));
+            for (int j = 0; j < hp->nctx; ++j) hp->dir_w[base + j] = double(wts[j]);
+            if (hess) {
+                const ld wh = wts[hp->nctx] * hscale, lc = ld(l) - center;
+                hp->dir_w[base + hp->nctx] = double(wh);
+                hp->dir_w[base + hp->nctx + 1] = double(wh * lc);
+                hp->dir_w[base + hp->nctx + 2] = double(wh * lc * lc);
+            }
         }
     }
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
@@ -380,7 +404,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.d = hp.d;
     P.nctx = hp.nctx;
     P.hess = hp.hess;
-    P.n_dir = int(hp.dir_n.size() / hp.d);
+    P.n_dir = int(hp.dir_w.size() / std::max(hp.nw, 1));  // padded rows
     P.n_rec = int(hp.rec_q.size() / hp.d);
     P.nw = hp.nw;
     P.c = hp.c;
@@ -391,9 +415,9 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.alias_ratio = hp.alias_ratio;
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
-    P.dir_n = upload(hp.run_n, allocs);
-    P.run_info = upload(hp.run_info, allocs);
+    P.run_rec = upload(hp.run_rec, allocs);
     P.n_runs = int(hp.run_info.size() / 2);
+    std::memcpy(P.estep, hp.estep, sizeof(P.estep));
     P.dir_w = upload(hp.dir_w, allocs);
     P.rec_q = upload(hp.rec_q, allocs);
     P.rec_norm = upload(hp.rec_norm, allocs);
@@ -1002,9 +1026,9 @@ int lz_plan_get_info(const lz_plan* pl, lz_plan_info* o) {
     o->n_t0 = pl->hp.n_t0;
     o->t0_rho_max = pl->hp.t0_rho_max;
     const size_t ns = pl->hp.nctx + (pl->hp.hess ? 2 : 0);
-    o->smem_bytes = int64_t(8 * (pl->hp.run_n.size() + pl->hp.dir_w.size() + pl->hp.rec_q.size() +
+    o->smem_bytes = int64_t(8 * (pl->hp.run_rec.size() + pl->hp.dir_w.size() + pl->hp.rec_q.size() +
                                  pl->hp.rec_norm.size() + pl->hp.tab.coef.size() + ns * lz::kT0) +
-                            4 * (pl->hp.run_info.size() + pl->hp.tab.dir.size()));
+                            4 * pl->hp.tab.dir.size());
     return LZ_OK;
 }
 

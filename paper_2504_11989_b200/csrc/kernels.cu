@@ -44,8 +44,7 @@ template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 // force generic LD through the L1 path); the global variant only serves plans
 // whose point sets exceed the 227 KB opt-in shared memory.
 struct View {
-    const double* dir_n;   // run starts
-    const int* run_info;
+    const double* run;     // run records (DevPlan::run_rec)
     const double* dir_w;
     const double* rec_q;
     const double* rec_norm;
@@ -58,8 +57,7 @@ __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(
 
 __host__ size_t plan_smem_bytes(const DevPlan& P) {
     size_t b = 0;
-    b += align16(sizeof(double) * P.n_runs * P.d);
-    b += align16(sizeof(int) * P.n_runs * 2);
+    b += align16(sizeof(double) * P.n_runs * (2 * P.d + 2));
     b += align16(sizeof(double) * P.n_dir * P.nw);
     b += align16(sizeof(double) * P.n_rec * P.d);
     b += align16(sizeof(double) * P.n_rec);
@@ -77,8 +75,7 @@ template <bool SMEM>
 __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
     if constexpr (!SMEM) {
-        v.dir_n = P.dir_n;
-        v.run_info = P.run_info;
+        v.run = P.run_rec;
         v.dir_w = P.dir_w;
         v.rec_q = P.rec_q;
         v.rec_norm = P.rec_norm;
@@ -88,10 +85,8 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         return v;
     } else {
         size_t off = 0;
-        double* dn = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * P.n_runs * P.d);
-        int* ri = reinterpret_cast<int*>(smem + off);
-        off += align16(sizeof(int) * P.n_runs * 2);
+        double* rr = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_runs * (2 * P.d + 2));
         double* dw = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_dir * P.nw);
         double* rq = reinterpret_cast<double*>(smem + off);
@@ -103,8 +98,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
-        copy_words(dn, P.dir_n, size_t(P.n_runs) * P.d);
-        for (int i = threadIdx.x; i < 2 * P.n_runs; i += blockDim.x) ri[i] = P.run_info[i];
+        copy_words(rr, P.run_rec, size_t(P.n_runs) * (2 * P.d + 2));
         copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
         copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
@@ -112,8 +106,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
         copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
         __syncthreads();
-        v.dir_n = dn;
-        v.run_info = ri;
+        v.run = rr;
         v.dir_w = dw;
         v.rec_q = rq;
         v.rec_norm = rn;
@@ -133,6 +126,39 @@ __device__ __forceinline__ int count_le(const double* norm, int n, double r) {
         else hi = mid;
     }
     return lo;
+}
+
+// sin(2 pi x), cos(2 pi x) for the direct-space run starts (|x| < 2^50): y = 2x = j + r with
+// j = rint(y), |r| <= 1/2, then sin(pi r) = r P(r^2), cos(pi r) = Q(r^2) (degree-8 near-minimax
+// fits on r^2 in [0, 1/4], |error| < 5e-16 and 2.5e-16; tools/sincos_coeffs.py) and the sign
+// (-1)^j.  About 25 instructions, no quadrant selects (the library sincospi takes ~60).
+__device__ __forceinline__ void sincos2pi(double x, double& sn, double& cs) {
+    constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52: rint via the low word
+    const double y = x + x;
+    const double t = y + kM;
+    const double r = y - (t - kM);
+    const double u = r * r;
+    double p = 7.697826768224191e-07, q = 4.149564353942586e-06;
+    p = fma(p, u, -2.1903497074626018e-05);
+    q = fma(q, u, -0.00010456655338748738);
+    p = fma(p, u, 0.0004662998161898394);
+    q = fma(q, u, 0.0019295562724817132);
+    p = fma(p, u, -0.007370430505916944);
+    q = fma(q, u, -0.025806888737002202);
+    p = fma(p, u, 0.0821458865731029);
+    q = fma(q, u, 0.23533063012953284);
+    p = fma(p, u, -0.5992645293189447);
+    q = fma(q, u, -1.335262768843447);
+    p = fma(p, u, 2.5501640398773007);
+    q = fma(q, u, 4.058712126416497);
+    p = fma(p, u, -5.167712780049969);
+    q = fma(q, u, -4.934802200544676);
+    p = fma(p, u, 3.141592653589793);
+    q = fma(q, u, 1.0);
+    const double s0 = r * p;
+    const int flip = __double2loint(t) << 31;  // sign bit of (-1)^j
+    sn = __hiloint2double(__double2hiint(s0) ^ flip, __double2loint(s0));
+    cs = __hiloint2double(__double2hiint(q) ^ flip, __double2loint(q));
 }
 
 // Out-of-line E_p for the rare direct paths, so the hot loop stays small.
@@ -282,35 +308,86 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out) {
     using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
-    constexpr int NW = Acc::NW;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
-    double dacc[NW];
-#pragma unroll
-    for (int c = 0; c < NW; ++c) dacc[c] = 0.0;
     // direct space: sum over half-lattice points of w * cos(2 pi kappa.n), walked as runs of
-    // consecutive n_d: one sincospi per run, then the Chebyshev recurrence
+    // consecutive n_d: one sincos2pi per run, then the Chebyshev recurrence
     // cos((l+1) th) = 2 cos(th) cos(l th) - cos((l-1) th), th = 2 pi kappa_d (one DFMA per point;
-    // runs are short, so the O(l^2 eps) error growth stays at the 1e-15 level)
+    // runs are short, so the O(l^2 eps) error growth stays at the 1e-15 level).
+    // Hessian: per run S_m = sum_l w l^m cos (m = 0, 1, 2), folded at the run end into
+    // H_ab += z0a z0b S_0, U_a += z0a S_1, T += S_2; after all runs
+    // sum w z_a z_b cos = H_ab + U_a e_b + e_a U_b + e_a e_b T.
+    constexpr int NH = HESS ? 3 : 0;
+    constexpr int NWP = (NCTX + NH == 1) ? 1 : ((NCTX + NH + 1) & ~1);
+    constexpr int RS = 2 * D + 2;
+    double dacc[NCTX > 0 ? NCTX : 1];
+#pragma unroll
+    for (int c = 0; c < NCTX; ++c) dacc[c] = 0.0;
+    double hh[NS > 0 ? NS : 1], uu[D], tt = 0.0;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) hh[c] = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) uu[a] = 0.0;
     {
         double sd, cd;
-        sincospi(2.0 * kap[D - 1], &sd, &cd);
+        sincos2pi(kap[D - 1], sd, cd);
         const double two_cd = 2.0 * cd;
         for (int r = gl; r < P.n_runs; r += G) {
+            const double* rec = V.run + r * RS;
             double ph = 0.0;
 #pragma unroll
-            for (int a = 0; a < D; ++a) ph = fma(kap[a], V.dir_n[r * D + a], ph);
+            for (int a = 0; a < D; ++a) ph = fma(kap[a], rec[a], ph);
             double sn, cs;
-            sincospi(2.0 * ph, &sn, &cs);
+            sincos2pi(ph, sn, cs);
             double cprev = fma(cs, cd, sn * sd);  // cos(phi - th)
-            const int first = V.run_info[2 * r], len = V.run_info[2 * r + 1];
-            const double* w = V.dir_w + size_t(first) * NW;
-            for (int l = 0; l < len; ++l) {
+            const double info = rec[2 * D];
+            const int first = __double2loint(info), len = __double2hiint(info);
+            const double* w = V.dir_w + size_t(first) * NWP;
+            double S[NH > 0 ? NH : 1];
 #pragma unroll
-                for (int c = 0; c < NW; ++c) dacc[c] = fma(w[l * NW + c], cs, dacc[c]);
+            for (int m = 0; m < NH; ++m) S[m] = 0.0;
+            auto point = [&](const double* wp) {
+                double wv[NWP];
+                if constexpr (NWP % 2 == 0) {
+#pragma unroll
+                    for (int c = 0; c < NWP; c += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(wp + c);
+                        wv[c] = v2.x;
+                        wv[c + 1] = v2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NWP; ++c) wv[c] = wp[c];
+                }
+#pragma unroll
+                for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
+#pragma unroll
+                for (int m = 0; m < NH; ++m) S[m] = fma(wv[NCTX + m], cs, S[m]);
                 const double cnext = fma(two_cd, cs, -cprev);
                 cprev = cs;
                 cs = cnext;
+            };
+            for (int l = 0; l < len; l += 2) {
+                point(w);
+                point(w + NWP);
+                w += 2 * NWP;
+            }
+            if constexpr (HESS) {
+                double v[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    v[a] = rec[D + a] * S[0];
+                    uu[a] = fma(rec[D + a], S[1], uu[a]);
+                }
+                tt += S[2];
+                int c = 0;
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int b = a; b < D; ++b) {
+                        hh[c] = fma(v[a], rec[D + b], hh[c]);
+                        ++c;
+                    }
             }
         }
     }
@@ -322,8 +399,17 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     // The Hessian's direct-space channels arrive pre-scaled by -2 pi^2 / rfac (host), so they
     // seed the reciprocal accumulators: one register set of d(d+1)/2 instead of two.
     double yy[NS > 0 ? NS : 1];
+    if constexpr (HESS) {
+        int c = 0;
 #pragma unroll
-    for (int c = 0; c < NS; ++c) yy[c] = dacc[NCTX + c];
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) {
+                const double eu = fma(uu[a], P.estep[b], uu[b] * P.estep[a]);
+                yy[c] = hh[c] + fma(P.estep[a] * P.estep[b], tt, eu);
+                ++c;
+            }
+    }
     const double cc = P.c;  // all contexts of a plan share the split
     // Exact per-warp culling: |k+q| >= |q| - |k|, and every table function is
     // identically zero beyond x_hi, i.e. for |k+q| > r_cut.  The points are

@@ -59,7 +59,7 @@ struct DevPlan {
     int hess;          // 1 if context slot `hess_slot` also needs its Hessian
     int hess_slot;
     int n_dir, n_rec;
-    int nw;            // direct weight channels per point
+    int nw;            // direct weight channels per point (see dir_w)
     int pad_;
     double c;          // pi / split, shared by every context of the plan
     // q = 0 term as power series in rho = |k|^2 (valid for rho <= t0_rho_max, i.e. k in the BZ):
@@ -74,10 +74,16 @@ struct DevPlan {
     double alias_ratio;
     double A[16];      // generator, row-major (columns = basis vectors)
     double B[16];      // A^{-T}, row-major
-    const double* dir_n;   // [n_runs][d] integer coordinates of the first point of each run
-    const int* run_info;   // [n_runs][2] (first point, length): runs of consecutive n_d
+    // Direct space as runs of consecutive n_d.  Run record (2d + 2 doubles): integer coordinates
+    // of the first point [d], Cartesian reference point z0 = A n(center) [d], (first weight row,
+    // even length) packed as two int32 in one double, pad.
+    const double* run_rec;
     int n_runs, pad3_;
-    const double* dir_w;   // [n_dir][nw] weights (run order): nctx plain channels, then (hess) d(d+1)/2
+    // [n_dir][nw] weights (run order, runs padded to even length with zero rows): nctx plain
+    // channels, then (hess) the Hessian weight times l^0, l^1, l^2 with l = point - run center
+    // (z_a z_b = z0a z0b + l (z0a e_b + e_a z0b) + l^2 e_a e_b along the run), zero-padded to even nw
+    const double* dir_w;
+    double estep[4];       // e = A e_d: Cartesian step along a run
     const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0, sorted by |q|
     const double* rec_norm;  // [n_rec] |q| ascending
     double r_cut;          // |k+q| > r_cut  =>  every table function is exactly zero
