@@ -419,7 +419,15 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.n_runs = int(hp.run_info.size() / 2);
     std::memcpy(P.estep, hp.estep, sizeof(P.estep));
     P.dir_w = upload(hp.dir_w, allocs);
-    P.rec_q = upload(hp.rec_q, allocs);
+    {
+        // reciprocal vectors padded to an even stride (16-byte aligned double2 loads)
+        const int qs = (hp.d + 1) & ~1;
+        const size_t nrec = hp.rec_q.size() / hp.d;
+        std::vector<double> rq(nrec * qs, 0.0);
+        for (size_t i = 0; i < nrec; ++i)
+            for (int a = 0; a < hp.d; ++a) rq[i * qs + a] = hp.rec_q[i * hp.d + a];
+        P.rec_q = upload(rq, allocs);
+    }
     P.rec_norm = upload(hp.rec_norm, allocs);
     P.r_cut = hp.r_cut;
     P.tab.dir = upload(hp.tab.dir, allocs);
@@ -434,6 +442,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.r_scale = hp.c * hp.tab.inv_hb;
     P.tab.x_off = hp.tab.x_lo * hp.tab.inv_hb;
     P.tab.xb_max = double(hp.tab.nbins) - 1.0 / 1048576.0;
+    P.tab.nbins_d = double(hp.tab.nbins);
     // branch-free lookup is opt-in (LATSUM_BRANCHFREE=1): measured 6% slower on the fcc ATM grid,
     // where lanes beyond the cutoff would otherwise skip the polynomial entirely
     const char* bf = std::getenv("LATSUM_BRANCHFREE");

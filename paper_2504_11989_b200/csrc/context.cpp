@@ -352,7 +352,9 @@ struct Fn {
     ld operator()(ld x) const { return scale * expint<ld>(p, x); }
 };
 
-// Chebyshev interpolation at kNC first-kind nodes, converted to monomials in tau.
+// Chebyshev interpolation at kNC first-kind nodes, converted to monomials in delta = tau / 2
+// in [-1/2, 1/2] (c_j tau^j = (2^j c_j) delta^j: exact rescaling, same conditioning; the device
+// gets delta = (fs - 1/2) - floor(fs) without the extra 2 x - 1 step).
 void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
     const int N = kNC;
     ld fv[kNC];
@@ -377,13 +379,13 @@ void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
     for (int j = 0; j < N; ++j) {
         ld c = 0.0L;
         for (int k = 0; k < N; ++k) c += ak[k] * tk[k][j];
-        out[j] = double(c);
+        out[j] = double(std::ldexp(c, j));
     }
 }
 
 ld eval_piece(const double* c, ld tau) {
     // evaluate exactly as the device does (Estrin form, double)
-    return estrin8(c, tau_powers(double(tau)));
+    return estrin8(c, tau_powers(double(tau) * 0.5));
 }
 
 }  // namespace

@@ -44,6 +44,9 @@ template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 // force generic LD through the L1 path); the global variant only serves plans
 // whose point sets exceed the 227 KB opt-in shared memory.
 struct View {
+    // 32-bit shared-window addresses of the staged arrays (SMEM variant): the hot loops load
+    // through ld.shared with these, so no generic->shared conversion is re-derived per access
+    uint32_t s_run, s_dir_w, s_rec_q, s_coef, s_tdir;
     const double* run;     // run records (DevPlan::run_rec)
     const double* dir_w;
     const double* rec_q;
@@ -59,7 +62,7 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     size_t b = 0;
     b += align16(sizeof(double) * P.n_runs * (2 * P.d + 2));
     b += align16(sizeof(double) * P.n_dir * P.nw);
-    b += align16(sizeof(double) * P.n_rec * P.d);
+    b += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
     b += align16(sizeof(double) * P.n_rec);
     b += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
     b += align16(sizeof(int) * P.tab.nbins);
@@ -74,6 +77,7 @@ __device__ inline void copy_words(double* dst, const double* src, size_t n) {
 template <bool SMEM>
 __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
+    v.s_run = v.s_dir_w = v.s_rec_q = v.s_coef = v.s_tdir = 0;
     if constexpr (!SMEM) {
         v.run = P.run_rec;
         v.dir_w = P.dir_w;
@@ -90,7 +94,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* dw = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_dir * P.nw);
         double* rq = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * P.n_rec * P.d);
+        off += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
         double* rn = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_rec);
         double* cf = reinterpret_cast<double*>(smem + off);
@@ -100,12 +104,17 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* tc = reinterpret_cast<double*>(smem + off);
         copy_words(rr, P.run_rec, size_t(P.n_runs) * (2 * P.d + 2));
         copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
-        copy_words(rq, P.rec_q, size_t(P.n_rec) * P.d);
+        copy_words(rq, P.rec_q, size_t(P.n_rec) * ((P.d + 1) & ~1));
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
         copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
         for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
         copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
         __syncthreads();
+        v.s_run = uint32_t(__cvta_generic_to_shared(rr));
+        v.s_dir_w = uint32_t(__cvta_generic_to_shared(dw));
+        v.s_rec_q = uint32_t(__cvta_generic_to_shared(rq));
+        v.s_coef = uint32_t(__cvta_generic_to_shared(cf));
+        v.s_tdir = uint32_t(__cvta_generic_to_shared(td));
         v.run = rr;
         v.dir_w = dw;
         v.rec_q = rq;
@@ -115,6 +124,39 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         v.t0c = tc;
         return v;
     }
+}
+
+// Plan-array loads: ld.shared at a 32-bit window address (SMEM) or a plain global load.
+// Indices are in elements of the array.
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+template <bool SMEM>
+__device__ __forceinline__ double ld_f64(const double* g, uint32_t s, int i) {
+    if constexpr (SMEM) return lds_f64(s + 8u * uint32_t(i));
+    else return g[i];
+}
+template <bool SMEM>
+__device__ __forceinline__ double2 ld_f64x2(const double* g, uint32_t s, int i) {  // i even
+    if constexpr (SMEM) return lds_f64x2(s + 8u * uint32_t(i));
+    else return *reinterpret_cast<const double2*>(g + i);
+}
+template <bool SMEM>
+__device__ __forceinline__ int ld_s32(const int* g, uint32_t s, int i) {
+    if constexpr (SMEM) return lds_s32(s + 4u * uint32_t(i));
+    else return g[i];
 }
 
 // Number of reciprocal points with |q| <= r (rec_norm ascending), binary search.
@@ -171,37 +213,49 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 // i.e. tau = +1 at the end of the previous piece -- equally valid.
 constexpr double kMagic = 6755399441055744.0;
 
-// Branch-free variant for tables without direct-evaluation bins (every practical lattice):
-// out-of-range lanes evaluate the last piece and are zeroed by a select, so the unrolled
-// q-loop is one basic block and two terms' Estrin chains interleave.
-template <int NF>
+// Piece lookup shared by both variants: bin b = floor(xb) from the directory, sub-piece
+// floor(fs) of fs = (xb - b) 2^L, and the local coordinate delta = (fs - 1/2) - floor(fs) in
+// [-1/2, 1/2] (coefficients are stored for delta, see context.cpp fit_piece).
+template <int NF, bool SMEM>
+__device__ __forceinline__ void tab_piece(const View& V, double xb, double tb, int e, double (&f)[NF]) {
+    const int L = e & 15;
+    // 2^L assembled from its exponent bits (no conversion)
+    const double two_l = __hiloint2double((1023 + L) << 20, 0);
+    const double a = fma(xb - (tb - kMagic), two_l, -0.5);  // fs - 1/2
+    const double ts = a + kMagic;
+    const int sub = __double2loint(ts);
+    const TauPowers tp = tau_powers(a - (ts - kMagic));
+    const int base = ((e >> 4) + sub) * (NF * kNCP);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        const double2 c01 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 0);
+        const double2 c23 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 2);
+        const double2 c45 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 4);
+        const double2 c67 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 6);
+        const double c8 = ld_f64<SMEM>(V.coef, V.s_coef, base + j * kNCP + 8);
+        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c8};
+        f[j] = estrin8(cc, tp);
+    }
+}
+
+// Branch-free variant for tables without direct-evaluation bins: out-of-range lanes evaluate
+// the last piece and are zeroed by a select (opt-in, LATSUM_BRANCHFREE=1).
+template <int NF, bool SMEM>
 __device__ __forceinline__ void tab_eval_fast(const DevTable& T, const View& V, double r, double (&f)[NF]) {
     const double xb_raw = fma(r, T.r_scale, -T.x_off);
     const bool far = xb_raw >= T.xb_max;
     const double xb = far ? T.xb_max : xb_raw;
     const double tb = (xb - 0.5) + kMagic;
-    const int e = V.tdir[__double2loint(tb)];
-    const int L = e & 15;
-    const double two_l = __hiloint2double((1023 + L) << 20, 0);
-    const double fs = (xb - (tb - kMagic)) * two_l;
-    const double ts = (fs - 0.5) + kMagic;
-    const int sub = __double2loint(ts);
-    const TauPowers tp = tau_powers(2.0 * (fs - (ts - kMagic)) - 1.0);
-    const double2* c = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * NF * kNCP);
+    const int e = ld_s32<SMEM>(V.tdir, V.s_tdir, __double2loint(tb));
+    tab_piece<NF, SMEM>(V, xb, tb, e, f);
 #pragma unroll
-    for (int j = 0; j < NF; ++j) {
-        const double2 c01 = c[j * 5 + 0], c23 = c[j * 5 + 1], c45 = c[j * 5 + 2];
-        const double2 c67 = c[j * 5 + 3], c89 = c[j * 5 + 4];
-        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c89.x};
-        const double v = estrin8(cc, tp);
-        f[j] = far ? 0.0 : v;
-    }
+    for (int j = 0; j < NF; ++j) f[j] = far ? 0.0 : f[j];
 }
 
-template <int NF>
+template <int NF, bool SMEM>
 __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, double r, double (&f)[NF]) {
     const double xb = fma(r, T.r_scale, -T.x_off);  // (c r - x_lo) / h
-    if (xb >= double(T.nbins)) {
+    if (xb >= T.nbins_d) {
 #pragma unroll
         for (int j = 0; j < NF; ++j) f[j] = 0.0;
         return;
@@ -210,7 +264,7 @@ __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, doubl
     double tb = 0.0;
     if (xb >= 0.0) {
         tb = (xb - 0.5) + kMagic;
-        e = V.tdir[__double2loint(tb)];
+        e = ld_s32<SMEM>(V.tdir, V.s_tdir, __double2loint(tb));
     }
     if ((e & 15) == kDirectMarker) {
         const double x = r * T.c;
@@ -218,21 +272,7 @@ __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, doubl
         for (int j = 0; j < NF; ++j) f[j] = T.scale[j] * expint_dev(T.p[j], x);
         return;
     }
-    const int L = e & 15;
-    // 2^L assembled from its exponent bits (no conversion)
-    const double two_l = __hiloint2double((1023 + L) << 20, 0);
-    const double fs = (xb - (tb - kMagic)) * two_l;
-    const double ts = (fs - 0.5) + kMagic;
-    const int sub = __double2loint(ts);
-    const TauPowers tp = tau_powers(2.0 * (fs - (ts - kMagic)) - 1.0);
-    const double2* c = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * NF * kNCP);
-#pragma unroll
-    for (int j = 0; j < NF; ++j) {
-        const double2 c01 = c[j * 5 + 0], c23 = c[j * 5 + 1], c45 = c[j * 5 + 2];
-        const double2 c67 = c[j * 5 + 3], c89 = c[j * 5 + 4];
-        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c89.x};
-        f[j] = estrin8(cc, tp);
-    }
+    tab_piece<NF, SMEM>(V, xb, tb, e, f);
 }
 
 // ---------------------------------------------------------------------------
@@ -303,7 +343,7 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
     double h[HESS ? Sym<D>::n : 1];
 };
 
-template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2>
+template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out) {
@@ -333,7 +373,14 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         sincos2pi(kap[D - 1], sd, cd);
         const double two_cd = 2.0 * cd;
         for (int r = gl; r < P.n_runs; r += G) {
-            const double* rec = V.run + r * RS;
+            double rec[RS - 1];  // n_start, z0, info
+#pragma unroll
+            for (int c = 0; c + 1 < RS - 1; c += 2) {
+                const double2 v2 = ld_f64x2<SMEM>(V.run, V.s_run, r * RS + c);
+                rec[c] = v2.x;
+                rec[c + 1] = v2.y;
+            }
+            if constexpr ((RS - 1) % 2 == 1) rec[RS - 2] = ld_f64<SMEM>(V.run, V.s_run, r * RS + RS - 2);
             double ph = 0.0;
 #pragma unroll
             for (int a = 0; a < D; ++a) ph = fma(kap[a], rec[a], ph);
@@ -342,22 +389,22 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             double cprev = fma(cs, cd, sn * sd);  // cos(phi - th)
             const double info = rec[2 * D];
             const int first = __double2loint(info), len = __double2hiint(info);
-            const double* w = V.dir_w + size_t(first) * NWP;
+            int w = first * NWP;  // element index of the run's first weight row
             double S[NH > 0 ? NH : 1];
 #pragma unroll
             for (int m = 0; m < NH; ++m) S[m] = 0.0;
-            auto point = [&](const double* wp) {
+            auto point = [&](int wp) {
                 double wv[NWP];
                 if constexpr (NWP % 2 == 0) {
 #pragma unroll
                     for (int c = 0; c < NWP; c += 2) {
-                        const double2 v2 = *reinterpret_cast<const double2*>(wp + c);
+                        const double2 v2 = ld_f64x2<SMEM>(V.dir_w, V.s_dir_w, wp + c);
                         wv[c] = v2.x;
                         wv[c + 1] = v2.y;
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < NWP; ++c) wv[c] = wp[c];
+                    for (int c = 0; c < NWP; ++c) wv[c] = ld_f64<SMEM>(V.dir_w, V.s_dir_w, wp + c);
                 }
 #pragma unroll
                 for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
@@ -422,15 +469,22 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
     const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
     auto term = [&](int i, auto fast) {
-        double y[D], r = 0.0;
+        constexpr int QS = (D + 1) & ~1;
+        double y[QS], r = 0.0;
+#pragma unroll
+        for (int a = 0; a < QS; a += 2) {
+            const double2 q2 = ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, i * QS + a);
+            y[a] = q2.x;
+            y[a + 1] = q2.y;
+        }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-            y[a] = k[a] + V.rec_q[i * D + a];
+            y[a] += k[a];
             r = fma(y[a], y[a], r);
         }
         double f[NF];
-        if constexpr (decltype(fast)::value) tab_eval_fast<NF>(P.tab, V, r, f);
-        else tab_eval<NF>(P.tab, V, r, f);
+        if constexpr (decltype(fast)::value) tab_eval_fast<NF, SMEM>(P.tab, V, r, f);
+        else tab_eval<NF, SMEM>(P.tab, V, r, f);
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
         if constexpr (HESS) {
@@ -481,7 +535,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     double f0[NF];
 #pragma unroll
     for (int j = 0; j < NF; ++j) f0[j] = 0.0;
-    if (q0_table) tab_eval<NF>(P.tab, V, rho, f0);
+    if (q0_table) tab_eval<NF, SMEM>(P.tab, V, rho, f0);
 #pragma unroll
     for (int j = 0; j < NCTX; ++j) {
         const CtxConst& C = P.ctx[j];
@@ -588,7 +642,7 @@ __global__ void __launch_bounds__(256) batch_kernel(DevPlan P, const double* __r
             }
         }
         NodeAcc<D, NCTX, HESS> acc;
-        eval_node<D, NCTX, HESS>(P, V, kap, k, gl, G, flags, acc);
+        eval_node<D, NCTX, HESS, false, 2, SMEM>(P, V, kap, k, gl, G, flags, acc);
         if (valid && gl == 0) {
             if constexpr (NCTX > 0) {
                 out[pt] = acc.z[0];
@@ -689,7 +743,7 @@ __global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
-            eval_node<D, NCTX, HESS, MODE == 1, UNR>(P, V, kap, k, 0, 1, 0u, acc);
+            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM>(P, V, kap, k, 0, 1, 0u, acc);
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll

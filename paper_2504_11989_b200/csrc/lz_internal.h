@@ -42,11 +42,12 @@ struct CtxConst {
 // sharing one directory over x in [x_lo, x_hi).
 struct DevTable {
     const int* dir;        // nbins entries: (first_piece << 4) | L ; L == 15 -> direct
-    const double* coef;    // [piece][nfunc][kNC], monomials in tau in [-1, 1]
+    const double* coef;    // [piece][nfunc][kNCP], monomials in delta in [-1/2, 1/2] (piece center 0)
     int nbins, nfunc, npieces, pad_;
     double x_lo, inv_hb, x_hi;
     double c, r_scale, x_off;  // x = c rho;  bin coordinate xb = rho * r_scale - x_off
     double xb_max;             // largest bin coordinate evaluated (nbins - 2^-20)
+    double nbins_d;            // nbins as a double (no int->FP64 conversion in the hot loop)
     int any_direct, pad5_;     // 1 if some bin is evaluated directly (slow, branchy path)
     double p[4], scale[4]; // for the direct fallback
 };
@@ -84,7 +85,7 @@ struct DevPlan {
     // (z_a z_b = z0a z0b + l (z0a e_b + e_a z0b) + l^2 e_a e_b along the run), zero-padded to even nw
     const double* dir_w;
     double estep[4];       // e = A e_d: Cartesian step along a run
-    const double* rec_q;   // [n_rec][d] Cartesian reciprocal vectors q != 0, sorted by |q|
+    const double* rec_q;   // [n_rec][(d+1)&~1] Cartesian reciprocal vectors q != 0 (zero-padded), sorted by |q|
     const double* rec_norm;  // [n_rec] |q| ascending
     double r_cut;          // |k+q| > r_cut  =>  every table function is exactly zero
     DevTable tab;          // functions: nctx plain F_j, then (hess) F', F''

@@ -3,6 +3,7 @@
     python tools/profile_target.py atm      # one fused ATM integral, fcc, bench grid
     python tools/profile_target.py c1       # C1 throughput batch (2^20 points)
     python tools/profile_target.py e2e      # host-API overhead breakdown (no ncu)
+    SWEEP=0.45,0.6 python tools/profile_target.py atm_sweep   # kernel ms vs theta split
 """
 import os
 import sys
@@ -27,6 +28,29 @@ def atm():
     plan.integrate_device(part, 128, 128, 3)
     torch.cuda.synchronize()
     print("atm ok", nn, nt)
+
+
+def atm_sweep():
+    """Kernel time and energy of the fcc ATM sum vs the theta split (CUDA events, 5 reps)."""
+    fcc = named_lattice("fcc")
+    scales = [float(v) for v in os.environ.get("SWEEP", "0.35,0.45,0.55,0.65,0.8").split(",")]
+    for sc in scales:
+        plan = atm_plan(fcc, sc * fcc.volume ** (-2.0 / 3.0))
+        nn, nt = plan.tiles(128, 128, 3)
+        part = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
+        plan.integrate_device(part, 128, 128, 3)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            plan.integrate_device(part, 128, 128, 3)
+        b.record()
+        torch.cuda.synchronize()
+        s2 = plan.integrate(128, 128, 3)
+        e = 8.0 * (s2[0] - 3.0 * s2[1]) / 6.0
+        info = plan.info()
+        print(f"split {sc:.2f}: {a.elapsed_time(b) / 5:.3f} ms  n_dir {info.n_dir} runs {info.n_runs} "
+              f"n_rec {info.n_rec} pieces {info.table_pieces} smem {info.smem_bytes}  E {e:.15f}")
 
 
 def c1():
@@ -117,4 +141,4 @@ def e2e():
 
 if __name__ == "__main__":
     {"atm": atm, "c1": c1, "c1_time": c1_time, "e2e": e2e,
-     "e2e_breakdown": e2e_breakdown}[sys.argv[1]]()
+     "e2e_breakdown": e2e_breakdown, "atm_sweep": atm_sweep}[sys.argv[1]]()
