@@ -442,14 +442,16 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.r_scale = hp.c * hp.tab.inv_hb;
     P.tab.x_off = hp.tab.x_lo * hp.tab.inv_hb;
     P.tab.xb_max = double(hp.tab.nbins) - 1.0 / 1048576.0;
+    P.tab.r_off = hp.c > 0.0 ? double((long double)hp.tab.x_lo / (long double)hp.c) : 0.0;
     P.tab.nbins_d = double(hp.tab.nbins);
-    // branch-free lookup is opt-in (LATSUM_BRANCHFREE=1): measured 6% slower on the fcc ATM grid,
-    // where lanes beyond the cutoff would otherwise skip the polynomial entirely
+    // branch-free lookup is opt-in (LATSUM_BRANCHFREE=1): measured slower on the fcc ATM grid,
+    // where warps beyond the cutoff otherwise skip the polynomial entirely
     const char* bf = std::getenv("LATSUM_BRANCHFREE");
-    P.tab.any_direct = (bf && std::atoi(bf) == 1) ? 0 : 1;
+    P.tab.branchfree = (bf && std::atoi(bf) == 1) ? 1 : 0;
+    P.tab.has_marker = 0;
     for (int e : hp.tab.dir)
-        if ((e & 15) == lz::kDirectMarker) P.tab.any_direct = 1;
-    if (hp.tab.nbins == 0) P.tab.any_direct = 1;  // no table: never evaluated (no q points)
+        if ((e & 15) == lz::kDirectMarker) P.tab.has_marker = 1;
+    if (hp.tab.nbins == 0) P.tab.has_marker = 1;  // no table: never evaluated (no q points)
     for (int j = 0; j < 4; ++j) {
         P.tab.p[j] = hp.tab.p[j];
         P.tab.scale[j] = hp.tab.scale[j];

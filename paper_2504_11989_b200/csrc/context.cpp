@@ -481,7 +481,17 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
         }
         out->max_rel_err = std::max(out->max_rel_err, bf.err);
         out->dir[b] = (npieces << 4) | bf.level;
-        out->coef.insert(out->coef.end(), bf.coefs.begin(), bf.coefs.end());
+        // fit arrays [sub][func][kNCP] -> device layout [sub][piece_stride(nfunc)]
+        const int ps = piece_stride(nfunc);
+        for (int sidx = 0; sidx < (1 << bf.level); ++sidx) {
+            const size_t base = out->coef.size();
+            out->coef.resize(base + ps, 0.0);
+            for (int j = 0; j < nfunc; ++j) {
+                const double* cf = &bf.coefs[(size_t(sidx) * nfunc + j) * kNCP];
+                for (int m = 0; m < 8; ++m) out->coef[base + j * 8 + m] = cf[m];
+                out->coef[base + nfunc * 8 + j] = cf[8];
+            }
+        }
         npieces += 1 << bf.level;
     }
     out->npieces = npieces;

@@ -64,7 +64,7 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     b += align16(sizeof(double) * P.n_dir * P.nw);
     b += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
     b += align16(sizeof(double) * P.n_rec);
-    b += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
+    b += align16(sizeof(double) * size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
     b += align16(sizeof(int) * P.tab.nbins);
     b += align16(sizeof(double) * size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
     return b;
@@ -98,7 +98,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* rn = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_rec);
         double* cf = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
+        off += align16(sizeof(double) * size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
@@ -106,8 +106,15 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
         copy_words(rq, P.rec_q, size_t(P.n_rec) * ((P.d + 1) & ~1));
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
-        copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * P.tab.nfunc * kNCP);
-        for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) td[i] = P.tab.dir[i];
+        copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
+        // directory relocated for the shared copy: the high word of 2^L in bits 20-30 and the
+        // shared byte address of the bin's first piece in bits 0-19 (the 227 KB window fits)
+        const uint32_t cf_addr = uint32_t(__cvta_generic_to_shared(cf));
+        const uint32_t pbytes = uint32_t(sizeof(double) * piece_stride(P.tab.nfunc));
+        for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) {
+            const int e = P.tab.dir[i];
+            td[i] = int((uint32_t(1023 + (e & 15)) << 20) | (cf_addr + uint32_t(e >> 4) * pbytes));
+        }
         copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
         __syncthreads();
         v.s_run = uint32_t(__cvta_generic_to_shared(rr));
@@ -174,29 +181,26 @@ __device__ __forceinline__ int count_le(const double* norm, int n, double r) {
 // j = rint(y), |r| <= 1/2, then sin(pi r) = r P(r^2), cos(pi r) = Q(r^2) (degree-8 near-minimax
 // fits on r^2 in [0, 1/4], |error| < 5e-16 and 2.5e-16; tools/sincos_coeffs.py) and the sign
 // (-1)^j.  About 25 instructions, no quadrant selects (the library sincospi takes ~60).
+__constant__ double kSinP[9] = {3.141592653589793, -5.167712780049969, 2.5501640398773007,
+                                 -0.5992645293189447, 0.0821458865731029, -0.007370430505916944,
+                                 0.0004662998161898394, -2.1903497074626018e-05, 7.697826768224191e-07};
+__constant__ double kCosQ[9] = {1.0, -4.934802200544676, 4.058712126416497, -1.335262768843447,
+                                0.23533063012953284, -0.025806888737002202, 0.0019295562724817132,
+                                -0.00010456655338748738, 4.149564353942586e-06};
 __device__ __forceinline__ void sincos2pi(double x, double& sn, double& cs) {
     constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52: rint via the low word
     const double y = x + x;
     const double t = y + kM;
     const double r = y - (t - kM);
     const double u = r * r;
-    double p = 7.697826768224191e-07, q = 4.149564353942586e-06;
-    p = fma(p, u, -2.1903497074626018e-05);
-    q = fma(q, u, -0.00010456655338748738);
-    p = fma(p, u, 0.0004662998161898394);
-    q = fma(q, u, 0.0019295562724817132);
-    p = fma(p, u, -0.007370430505916944);
-    q = fma(q, u, -0.025806888737002202);
-    p = fma(p, u, 0.0821458865731029);
-    q = fma(q, u, 0.23533063012953284);
-    p = fma(p, u, -0.5992645293189447);
-    q = fma(q, u, -1.335262768843447);
-    p = fma(p, u, 2.5501640398773007);
-    q = fma(q, u, 4.058712126416497);
-    p = fma(p, u, -5.167712780049969);
-    q = fma(q, u, -4.934802200544676);
-    p = fma(p, u, 3.141592653589793);
-    q = fma(q, u, 1.0);
+    // coefficients from constant memory: DFMA takes them as c[][] operands (64-bit immediates
+    // would cost two uniform moves each)
+    double p = kSinP[8], q = kCosQ[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+        p = fma(p, u, kSinP[i]);
+        q = fma(q, u, kCosQ[i]);
+    }
     const double s0 = r * p;
     const int flip = __double2loint(t) << 31;  // sign bit of (-1)^j
     sn = __hiloint2double(__double2hiint(s0) ^ flip, __double2loint(s0));
@@ -218,24 +222,37 @@ constexpr double kMagic = 6755399441055744.0;
 // [-1/2, 1/2] (coefficients are stored for delta, see context.cpp fit_piece).
 template <int NF, bool SMEM>
 __device__ __forceinline__ void tab_piece(const View& V, double xb, double tb, int e, double (&f)[NF]) {
-    const int L = e & 15;
-    // 2^L assembled from its exponent bits (no conversion)
-    const double two_l = __hiloint2double((1023 + L) << 20, 0);
+    constexpr int PS = piece_stride(NF);
+    // 2^L from its exponent bits (no conversion); SMEM directory entries carry them pre-shifted
+    const int hi = SMEM ? (e & 0x7ff00000) : ((1023 + (e & 15)) << 20);
+    const double two_l = __hiloint2double(hi, 0);
     const double a = fma(xb - (tb - kMagic), two_l, -0.5);  // fs - 1/2
     const double ts = a + kMagic;
     const int sub = __double2loint(ts);
     const TauPowers tp = tau_powers(a - (ts - kMagic));
-    const int base = ((e >> 4) + sub) * (NF * kNCP);
+    double2 c[PS / 2];
+    if constexpr (SMEM) {
+        const uint32_t addr = uint32_t(e & 0xfffff) + uint32_t(sub) * uint32_t(PS * 8);
+#pragma unroll
+        for (int m = 0; m < PS / 2; ++m) c[m] = lds_f64x2(addr + 16u * m);
+    } else {
+        const double2* g = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * PS);
+#pragma unroll
+        for (int m = 0; m < PS / 2; ++m) c[m] = g[m];
+    }
+    const double* cd = reinterpret_cast<const double*>(c);
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
-        const double2 c01 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 0);
-        const double2 c23 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 2);
-        const double2 c45 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 4);
-        const double2 c67 = ld_f64x2<SMEM>(V.coef, V.s_coef, base + j * kNCP + 6);
-        const double c8 = ld_f64<SMEM>(V.coef, V.s_coef, base + j * kNCP + 8);
-        const double cc[9] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c8};
+        const double cc[9] = {cd[j * 8 + 0], cd[j * 8 + 1], cd[j * 8 + 2], cd[j * 8 + 3], cd[j * 8 + 4],
+                              cd[j * 8 + 5], cd[j * 8 + 6], cd[j * 8 + 7], cd[NF * 8 + j]};
         f[j] = estrin8(cc, tp);
     }
+}
+
+template <bool SMEM>
+__device__ __forceinline__ bool is_marker(int e) {
+    if constexpr (SMEM) return (e & 0x7ff00000) == ((1023 + kDirectMarker) << 20);
+    else return (e & 15) == kDirectMarker;
 }
 
 // Branch-free variant for tables without direct-evaluation bins: out-of-range lanes evaluate
@@ -252,6 +269,17 @@ __device__ __forceinline__ void tab_eval_fast(const DevTable& T, const View& V, 
     for (int j = 0; j < NF; ++j) f[j] = far ? 0.0 : f[j];
 }
 
+// In-cell variant: k in the reduced cell guarantees xb >= 0 (x_lo = c lambda_min / 4, see
+// context.cpp table_x_lo), and a table without marker bins needs no direct branch; only lanes
+// past the cutoff branch out (warp-uniform for most q, which are sorted by |q|).
+template <int NF, bool SMEM>
+__device__ __forceinline__ void tab_eval_cell(const View& V, double xb, double (&f)[NF]) {
+    const double tb = (xb - 0.5) + kMagic;
+    const int e = ld_s32<SMEM>(V.tdir, V.s_tdir, __double2loint(tb));
+    tab_piece<NF, SMEM>(V, xb, tb, e, f);
+}
+
+// Checked variant: arbitrary k (xb < 0 possible) and marker bins (E_p evaluated directly).
 template <int NF, bool SMEM>
 __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, double r, double (&f)[NF]) {
     const double xb = fma(r, T.r_scale, -T.x_off);  // (c r - x_lo) / h
@@ -260,13 +288,13 @@ __device__ __forceinline__ void tab_eval(const DevTable& T, const View& V, doubl
         for (int j = 0; j < NF; ++j) f[j] = 0.0;
         return;
     }
-    int e = kDirectMarker;
+    int e = SMEM ? ((1023 + kDirectMarker) << 20) : kDirectMarker;  // xb < 0: evaluate directly
     double tb = 0.0;
     if (xb >= 0.0) {
         tb = (xb - 0.5) + kMagic;
         e = ld_s32<SMEM>(V.tdir, V.s_tdir, __double2loint(tb));
     }
-    if ((e & 15) == kDirectMarker) {
+    if (is_marker<SMEM>(e)) {
         const double x = r * T.c;
 #pragma unroll
         for (int j = 0; j < NF; ++j) f[j] = T.scale[j] * expint_dev(T.p[j], x);
@@ -414,6 +442,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 cprev = cs;
                 cs = cnext;
             };
+            // runs are short (~6 points): no unrolling beyond the pair, so no remainder set-up
+#pragma unroll 1
             for (int l = 0; l < len; l += 2) {
                 point(w);
                 point(w + NWP);
@@ -468,23 +498,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
     const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
-    auto term = [&](int i, auto fast) {
-        constexpr int QS = (D + 1) & ~1;
-        double y[QS], r = 0.0;
-#pragma unroll
-        for (int a = 0; a < QS; a += 2) {
-            const double2 q2 = ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, i * QS + a);
-            y[a] = q2.x;
-            y[a + 1] = q2.y;
-        }
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            y[a] += k[a];
-            r = fma(y[a], y[a], r);
-        }
-        double f[NF];
-        if constexpr (decltype(fast)::value) tab_eval_fast<NF, SMEM>(P.tab, V, r, f);
-        else tab_eval<NF, SMEM>(P.tab, V, r, f);
+    auto accumulate = [&](const double (&y)[(D + 1) & ~1], const double (&f)[NF]) {
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
         if constexpr (HESS) {
@@ -502,12 +516,49 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 }
         }
     };
-    if (P.tab.any_direct) {
+    auto term = [&](int i, auto fast) {
+        constexpr int QS = (D + 1) & ~1;
+        constexpr int mode = decltype(fast)::value;
+        double y[QS];
+#pragma unroll
+        for (int a = 0; a < QS; a += 2) {
+            const double2 q2 = ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, i * QS + a);
+            y[a] = q2.x;
+            y[a + 1] = q2.y;
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) y[a] += k[a];
+        double f[NF];
+        if constexpr (mode == 1) {
+            // in-cell: xb = (|k+q|^2 - x_lo / c) * r_scale; lanes past the cutoff skip the
+            // lookup and the accumulation (no zero-fill)
+            double r = -P.tab.r_off;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) r = fma(y[a], y[a], r);
+            const double xb = r * P.tab.r_scale;
+            if (xb < P.tab.nbins_d) {
+                tab_eval_cell<NF, SMEM>(V, xb, f);
+                accumulate(y, f);
+            }
+        } else {
+            double r = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) r = fma(y[a], y[a], r);
+            if constexpr (mode == 2) tab_eval_fast<NF, SMEM>(P.tab, V, r, f);
+            else tab_eval<NF, SMEM>(P.tab, V, r, f);
+            accumulate(y, f);
+        }
+    };
+    // lookup variant: checked (marker bins, or k not reduced into the cell), in-cell, branch-free
+    if (P.tab.has_marker || (flags & 1u)) {
 #pragma unroll UNR
-        for (int i = gl; i < n_eff; i += G) term(i, std::false_type{});
+        for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 0>{});
+    } else if (!P.tab.branchfree) {
+#pragma unroll UNR
+        for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 1>{});
     } else {
 #pragma unroll UNR
-        for (int i = gl; i < n_eff; i += G) term(i, std::true_type{});
+        for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 2>{});
     }
     if (G > 1) {
         for (int off = G >> 1; off > 0; off >>= 1) {

@@ -17,7 +17,13 @@ constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
 constexpr int kDeg = 8;        // degree of the piecewise polynomials (kDeg+1 coefficients)
 constexpr int kNC = kDeg + 1;
-constexpr int kNCP = 10;       // padded coefficient stride (16-byte aligned double2 loads)
+constexpr int kNCP = 10;       // per-function stride of the host fit arrays
+// Device piece layout for nf functions: c0..c7 of each function (8 doubles each), then c8 of
+// every function, padded to an even count (every double2 load 16-byte aligned; NF = 2: 9 loads).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int piece_stride(int nf) { return nf * 8 + ((nf + 1) & ~1); }
 constexpr double kBinWidth = 0.25;  // directory bin width in x = c |y|^2
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
 constexpr int kT0 = 64;             // max terms of the q = 0 power series
@@ -42,13 +48,15 @@ struct CtxConst {
 // sharing one directory over x in [x_lo, x_hi).
 struct DevTable {
     const int* dir;        // nbins entries: (first_piece << 4) | L ; L == 15 -> direct
-    const double* coef;    // [piece][nfunc][kNCP], monomials in delta in [-1/2, 1/2] (piece center 0)
+    const double* coef;    // [piece][piece_stride(nfunc)], monomials in delta in [-1/2, 1/2]
     int nbins, nfunc, npieces, pad_;
     double x_lo, inv_hb, x_hi;
     double c, r_scale, x_off;  // x = c rho;  bin coordinate xb = rho * r_scale - x_off
+    double r_off;              // x_lo / c:  xb = (rho - r_off) * r_scale (in-cell lookup)
     double xb_max;             // largest bin coordinate evaluated (nbins - 2^-20)
     double nbins_d;            // nbins as a double (no int->FP64 conversion in the hot loop)
-    int any_direct, pad5_;     // 1 if some bin is evaluated directly (slow, branchy path)
+    int has_marker;            // 1 if some bin is evaluated directly (E_p; checked lookup path)
+    int branchfree;            // opt-in (LATSUM_BRANCHFREE=1): select instead of the far branch
     double p[4], scale[4]; // for the direct fallback
 };
 
