@@ -84,9 +84,12 @@ void free_all(std::vector<void*>* allocs) {
 // Host-side description of a fused plan before upload.
 struct HostPlan {
     int d = 0, nctx = 0, hess = 0, nw = 0, alias_fp = 0;
-    double c = 0.0, r_cut = 0.0, alias_ratio = 0.0;
-    std::vector<double> dir_n, dir_w, rec_q, rec_norm, run_n, run_rec, t0c;
-    double estep[4] = {0, 0, 0, 0};
+    double c = 0.0, r_cut = 0.0, r_in = 0.0, alias_ratio = 0.0;
+    std::vector<double> dir_n, rec_q, rec_norm, t0c;
+    // direct space: [slab records][row records][weight rows] (see build_host_plan)
+    std::vector<double> direct;
+    int n_slabs = 0, n_rows = 0, rows_off = 0, w_off = 0, n_wrows = 0;
+    double e2[4] = {0, 0, 0, 0}, e3[4] = {0, 0, 0, 0};
     int n_t0 = 0;
     double t0_rho_max = -1.0;
     std::vector<int> run_info;
@@ -250,8 +253,16 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         }
         hp->dir_n.swap(kept);
     }
-    // Direct points as runs of consecutive last coordinates: the kernel evaluates one
-    // sincospi per run and rotates by exp(2 pi i kappa_d) along it.
+    // Direct points as 2D slabs: slab = fixed (n_1 .. n_{d-2}), rows along n_{d-1}, columns along
+    // n_d.  The kernel evaluates one sincos per slab; row starts follow by a complex rotation
+    // exp(2 pi i kappa_{d-1}) and points along a row by the Chebyshev cosine recurrence in
+    // kappa_d.  Rows are stored from their first point (skip = columns after the slab's l0),
+    // padded to even length with zero weights (the kernel walks rows two points at a time).
+    // Hessian: the direct term -8 pi^2 w z_a z_b cos(.) is stored divided by 4 rfac so that it
+    // shares the kernel's reciprocal accumulators (sum of y_a y_b F''), and factorised over the
+    // slab: z = zc + j' e2 + l' e3 (zc = slab center, e2 = A e_{d-1}, e3 = A e_d), so three
+    // channels w l'^m (m = 0, 1, 2) replace the d(d+1)/2 channels w z_a z_b and the row and
+    // slab folds carry the j' and zc parts.
     {
         const size_t np = hp->dir_n.size() / d;
         std::vector<size_t> ord(np);
@@ -266,7 +277,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         for (size_t i = 0; i < np; ++i)
             for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[ord[i] * d + a];
         hp->dir_n.swap(pts);
-        hp->run_n.clear();
+        // maximal runs (for plan info only)
         hp->run_info.clear();
         for (size_t i = 0; i < np; ++i) {
             bool cont = i > 0;
@@ -275,57 +286,107 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             if (cont) {
                 hp->run_info.back() += 1;
             } else {
-                hp->run_n.insert(hp->run_n.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
                 hp->run_info.push_back(int(i));
                 hp->run_info.push_back(1);
             }
         }
     }
-    // Weight rows per run, padded to even length (the kernel walks runs two points at a time).
-    // Hessian: the direct term -8 pi^2 w z_a z_b cos(.) is stored divided by 4 rfac so that it
-    // shares the kernel's reciprocal accumulators (sum of y_a y_b F''), and factorised along the
-    // run: z = z0 + l e (z0 at the run center, e = A e_d), so three channels w l^m (m = 0, 1, 2)
-    // replace the d(d+1)/2 channels w z_a z_b.
     const int nh = hess ? 3 : 0;
     hp->nw = (hp->nctx + nh == 1) ? 1 : ((hp->nctx + nh + 1) & ~1);
-    const int rs = 2 * d + 2;
-    ld e[lz::kMaxDim];
+    for (int a = 0; a < 4; ++a) hp->e2[a] = hp->e3[a] = 0.0;
     for (int a = 0; a < d; ++a) {
-        e[a] = ld(first->A[a * d + d - 1]);
-        hp->estep[a] = double(e[a]);
+        hp->e3[a] = first->A[a * d + d - 1];
+        if (d >= 2) hp->e2[a] = first->A[a * d + d - 2];
     }
     const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
-    const size_t nruns = hp->run_info.size() / 2;
-    hp->run_rec.assign(nruns * rs, 0.0);
-    hp->dir_w.clear();
-    for (size_t r = 0; r < nruns; ++r) {
-        const int f = hp->run_info[2 * r], len = hp->run_info[2 * r + 1];
-        const int lenp = len + (len & 1);
-        const int row0 = int(hp->dir_w.size() / hp->nw);
-        const ld center = ld(len - 1) / 2.0L;
-        double* rec = &hp->run_rec[r * rs];
-        const double* n0 = &hp->dir_n[size_t(f) * d];
-        for (int a = 0; a < d; ++a) {
-            ld z0 = center * e[a];
-            for (int b = 0; b < d; ++b) z0 += ld(first->A[a * d + b]) * n0[b];
-            rec[a] = n0[a];
-            rec[d + a] = double(z0);
+    {
+        const size_t np = hp->dir_n.size() / d;
+        const int ns = std::max(d - 2, 0);   // slab key length
+        struct Row { long j; std::vector<std::pair<long, size_t>> pts; };
+        std::vector<std::pair<std::vector<long>, std::vector<Row>>> slabs;
+        for (size_t i = 0; i < np; ++i) {
+            const double* n = &hp->dir_n[i * d];
+            std::vector<long> sk(ns);
+            for (int a = 0; a < ns; ++a) sk[a] = std::lround(n[a]);
+            const long j = d >= 2 ? std::lround(n[d - 2]) : 0;
+            const long l = std::lround(n[d - 1]);
+            if (slabs.empty() || slabs.back().first != sk) slabs.push_back({sk, {}});
+            auto& rows = slabs.back().second;
+            if (rows.empty() || rows.back().j != j) rows.push_back({j, {}});
+            rows.back().pts.push_back({l, i});
         }
-        const int32_t info[2] = {row0, lenp};
-        std::memcpy(&rec[2 * d], info, sizeof(info));
-        for (int l = 0; l < lenp; ++l) {
-            const size_t base = hp->dir_w.size();
-            hp->dir_w.resize(base + hp->nw, 0.0);
-            if (l >= len) continue;
-            const std::vector<ld>& wts = wmap.at(pack_key(d, &hp->dir_n[size_t(f + l) * d]));
-            for (int j = 0; j < hp->nctx; ++j) hp->dir_w[base + j] = double(wts[j]);
-            if (hess) {
-                const ld wh = wts[hp->nctx] * hscale, lc = ld(l) - center;
-                hp->dir_w[base + hp->nctx] = double(wh);
-                hp->dir_w[base + hp->nctx + 1] = double(wh * lc);
-                hp->dir_w[base + hp->nctx + 2] = double(wh * lc * lc);
+        const int sr = 2 * d + 2;
+        std::vector<double> srec, rrec, wts_out;
+        int n_rows = 0;
+        for (const auto& sl : slabs) {
+            const auto& rows = sl.second;
+            const long jmin = rows.front().j, jmax = rows.back().j;
+            long l0 = rows.front().pts.front().first, l1 = l0;
+            for (const Row& r : rows) {
+                l0 = std::min(l0, r.pts.front().first);
+                l1 = std::max(l1, r.pts.back().first);
+            }
+            const ld jc = ld(jmin + jmax) / 2.0L, lc = ld(l0 + l1) / 2.0L;
+            std::vector<double> rec(sr, 0.0);
+            ld ncen[lz::kMaxDim];
+            for (int a = 0; a < ns; ++a) {
+                rec[a] = double(sl.first[a]);
+                ncen[a] = ld(sl.first[a]);
+            }
+            if (d >= 2) {
+                rec[d - 2] = double(jmin);
+                ncen[d - 2] = jc;
+            }
+            rec[d - 1] = double(l0);
+            ncen[d - 1] = lc;
+            for (int a = 0; a < d; ++a) {
+                ld zc = 0.0L;
+                for (int b = 0; b < d; ++b) zc += ld(first->A[a * d + b]) * ncen[b];
+                rec[d + a] = double(zc);
+            }
+            rec[2 * d] = double(ld(jmin) - jc);
+            const int32_t sinfo[2] = {n_rows, int32_t(jmax - jmin + 1)};
+            std::memcpy(&rec[2 * d + 1], sinfo, sizeof(sinfo));
+            srec.insert(srec.end(), rec.begin(), rec.end());
+            size_t ri = 0;
+            for (long j = jmin; j <= jmax; ++j, ++n_rows) {
+                int32_t rinfo[2] = {0, 0};
+                if (ri < rows.size() && rows[ri].j == j) {
+                    const Row& r = rows[ri++];
+                    const long lo = r.pts.front().first, hi = r.pts.back().first;
+                    const long len = hi - lo + 1, lenp = len + (len & 1), skip = lo - l0;
+                    if (lenp > 65535 || skip > 65535) throw Error{LZ_EINVAL, "direct row too long"};
+                    const size_t row0 = wts_out.size() / hp->nw;
+                    if (row0 > size_t(INT32_MAX)) throw Error{LZ_EINVAL, "direct set too large"};
+                    rinfo[0] = int32_t(row0);
+                    rinfo[1] = int32_t((skip << 16) | lenp);
+                    wts_out.resize(wts_out.size() + size_t(lenp) * hp->nw, 0.0);
+                    for (const auto& pt : r.pts) {
+                        const size_t base = (row0 + size_t(pt.first - lo)) * hp->nw;
+                        const std::vector<ld>& w = wmap.at(pack_key(d, &hp->dir_n[pt.second * d]));
+                        for (int c = 0; c < hp->nctx; ++c) wts_out[base + c] = double(w[c]);
+                        if (hess) {
+                            const ld wh = w[hp->nctx] * hscale, lp = ld(pt.first) - lc;
+                            wts_out[base + hp->nctx] = double(wh);
+                            wts_out[base + hp->nctx + 1] = double(wh * lp);
+                            wts_out[base + hp->nctx + 2] = double(wh * lp * lp);
+                        }
+                    }
+                }
+                double rd;
+                std::memcpy(&rd, rinfo, sizeof(rd));
+                rrec.push_back(rd);
             }
         }
+        hp->n_slabs = int(slabs.size());
+        hp->n_rows = n_rows;
+        if (rrec.size() & 1) rrec.push_back(0.0);
+        hp->direct = srec;
+        hp->rows_off = int(srec.size());
+        hp->direct.insert(hp->direct.end(), rrec.begin(), rrec.end());
+        hp->w_off = int(hp->direct.size());
+        hp->direct.insert(hp->direct.end(), wts_out.begin(), wts_out.end());
+        hp->n_wrows = int(wts_out.size() / hp->nw);
     }
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
@@ -395,6 +456,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         table_job.get();
         // beyond x_hi every tabulated function is exactly zero in the kernel
         hp->r_cut = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L + 1e-9L));
+        hp->r_in = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L - 1e-9L));
     }
 }
 
@@ -404,7 +466,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.d = hp.d;
     P.nctx = hp.nctx;
     P.hess = hp.hess;
-    P.n_dir = int(hp.dir_w.size() / std::max(hp.nw, 1));  // padded rows
+    P.n_dir = hp.n_wrows;  // padded weight rows
     P.n_rec = int(hp.rec_q.size() / hp.d);
     P.nw = hp.nw;
     P.c = hp.c;
@@ -415,10 +477,14 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.alias_ratio = hp.alias_ratio;
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
-    P.run_rec = upload(hp.run_rec, allocs);
-    P.n_runs = int(hp.run_info.size() / 2);
-    std::memcpy(P.estep, hp.estep, sizeof(P.estep));
-    P.dir_w = upload(hp.dir_w, allocs);
+    P.direct = upload(hp.direct, allocs);
+    P.n_direct = int(hp.direct.size());
+    P.n_slabs = hp.n_slabs;
+    P.n_rows = hp.n_rows;
+    P.rows_off = hp.rows_off;
+    P.w_off = hp.w_off;
+    std::memcpy(P.e2, hp.e2, sizeof(P.e2));
+    std::memcpy(P.e3, hp.e3, sizeof(P.e3));
     {
         // reciprocal vectors padded to an even stride (16-byte aligned double2 loads)
         const int qs = (hp.d + 1) & ~1;
@@ -430,6 +496,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     }
     P.rec_norm = upload(hp.rec_norm, allocs);
     P.r_cut = hp.r_cut;
+    P.r_in = hp.r_in;
     P.tab.dir = upload(hp.tab.dir, allocs);
     P.tab.coef = upload(hp.tab.coef, allocs);
     P.tab.nbins = hp.tab.nbins;
@@ -1037,7 +1104,7 @@ int lz_plan_get_info(const lz_plan* pl, lz_plan_info* o) {
     o->n_t0 = pl->hp.n_t0;
     o->t0_rho_max = pl->hp.t0_rho_max;
     const size_t ns = pl->hp.nctx + (pl->hp.hess ? 2 : 0);
-    o->smem_bytes = int64_t(8 * (pl->hp.run_rec.size() + pl->hp.dir_w.size() + pl->hp.rec_q.size() +
+    o->smem_bytes = int64_t(8 * (pl->hp.direct.size() + pl->hp.rec_q.size() +
                                  pl->hp.rec_norm.size() + pl->hp.tab.coef.size() + ns * lz::kT0) +
                             4 * pl->hp.tab.dir.size());
     return LZ_OK;

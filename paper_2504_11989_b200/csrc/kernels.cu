@@ -46,9 +46,8 @@ template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 struct View {
     // 32-bit shared-window addresses of the staged arrays (SMEM variant): the hot loops load
     // through ld.shared with these, so no generic->shared conversion is re-derived per access
-    uint32_t s_run, s_dir_w, s_rec_q, s_coef, s_tdir;
-    const double* run;     // run records (DevPlan::run_rec)
-    const double* dir_w;
+    uint32_t s_dir, s_rec_q, s_coef, s_tdir;
+    const double* dir;     // direct-space block (DevPlan::direct)
     const double* rec_q;
     const double* rec_norm;
     const double* coef;
@@ -60,8 +59,7 @@ __host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(
 
 __host__ size_t plan_smem_bytes(const DevPlan& P) {
     size_t b = 0;
-    b += align16(sizeof(double) * P.n_runs * (2 * P.d + 2));
-    b += align16(sizeof(double) * P.n_dir * P.nw);
+    b += align16(sizeof(double) * P.n_direct);
     b += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
     b += align16(sizeof(double) * P.n_rec);
     b += align16(sizeof(double) * size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
@@ -77,10 +75,9 @@ __device__ inline void copy_words(double* dst, const double* src, size_t n) {
 template <bool SMEM>
 __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
-    v.s_run = v.s_dir_w = v.s_rec_q = v.s_coef = v.s_tdir = 0;
+    v.s_dir = v.s_rec_q = v.s_coef = v.s_tdir = 0;
     if constexpr (!SMEM) {
-        v.run = P.run_rec;
-        v.dir_w = P.dir_w;
+        v.dir = P.direct;
         v.rec_q = P.rec_q;
         v.rec_norm = P.rec_norm;
         v.coef = P.tab.coef;
@@ -89,10 +86,8 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         return v;
     } else {
         size_t off = 0;
-        double* rr = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * P.n_runs * (2 * P.d + 2));
-        double* dw = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * P.n_dir * P.nw);
+        double* dd = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * P.n_direct);
         double* rq = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
         double* rn = reinterpret_cast<double*>(smem + off);
@@ -102,8 +97,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
-        copy_words(rr, P.run_rec, size_t(P.n_runs) * (2 * P.d + 2));
-        copy_words(dw, P.dir_w, size_t(P.n_dir) * P.nw);
+        copy_words(dd, P.direct, size_t(P.n_direct));
         copy_words(rq, P.rec_q, size_t(P.n_rec) * ((P.d + 1) & ~1));
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
         copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
@@ -117,13 +111,11 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         }
         copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
         __syncthreads();
-        v.s_run = uint32_t(__cvta_generic_to_shared(rr));
-        v.s_dir_w = uint32_t(__cvta_generic_to_shared(dw));
+        v.s_dir = uint32_t(__cvta_generic_to_shared(dd));
         v.s_rec_q = uint32_t(__cvta_generic_to_shared(rq));
         v.s_coef = uint32_t(__cvta_generic_to_shared(cf));
         v.s_tdir = uint32_t(__cvta_generic_to_shared(td));
-        v.run = rr;
-        v.dir_w = dw;
+        v.dir = dd;
         v.rec_q = rq;
         v.rec_norm = rn;
         v.coef = cf;
@@ -378,91 +370,121 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
-    // direct space: sum over half-lattice points of w * cos(2 pi kappa.n), walked as runs of
-    // consecutive n_d: one sincos2pi per run, then the Chebyshev recurrence
-    // cos((l+1) th) = 2 cos(th) cos(l th) - cos((l-1) th), th = 2 pi kappa_d (one DFMA per point;
-    // runs are short, so the O(l^2 eps) error growth stays at the 1e-15 level).
-    // Hessian: per run S_m = sum_l w l^m cos (m = 0, 1, 2), folded at the run end into
-    // H_ab += z0a z0b S_0, U_a += z0a S_1, T += S_2; after all runs
-    // sum w z_a z_b cos = H_ab + U_a e_b + e_a U_b + e_a e_b T.
+    // direct space: sum over half-lattice points of w * cos(2 pi kappa.n) in 2D slabs (host:
+    // build_host_plan).  One sincos2pi per slab gives exp(i phi) at (first row, column l0);
+    // row starts follow by the rotation exp(2 pi i kappa_{d-1}) (error linear in the row count),
+    // points along a row by the Chebyshev recurrence cos((l+1) th) = 2 cos th cos(l th) -
+    // cos((l-1) th), th = 2 pi kappa_d (rows are short: O(l^2 eps) stays at 1e-15).
+    // Hessian: per row S_m = sum_l w l'^m cos (m = 0, 1, 2); per slab A0 = sum S0, A1 = sum j' S0,
+    // A2 = sum j'^2 S0, B0 = sum S1, B1 = sum j' S1, T = sum S2; with z = zc + j' e2 + l' e3,
+    // sum w z_a z_b cos = zc_a X_b + e2_a Y_b + e3_a W_b, X = zc A0 + e2 A1 + e3 B0,
+    // Y = zc A1 + e2 A2 + e3 B1, W = zc B0 + e2 B1 + e3 T.
     constexpr int NH = HESS ? 3 : 0;
     constexpr int NWP = (NCTX + NH == 1) ? 1 : ((NCTX + NH + 1) & ~1);
-    constexpr int RS = 2 * D + 2;
+    constexpr int SR = 2 * D + 2;
     double dacc[NCTX > 0 ? NCTX : 1];
 #pragma unroll
     for (int c = 0; c < NCTX; ++c) dacc[c] = 0.0;
-    double hh[NS > 0 ? NS : 1], uu[D], tt = 0.0;
+    double hh[NS > 0 ? NS : 1];
 #pragma unroll
     for (int c = 0; c < NS; ++c) hh[c] = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) uu[a] = 0.0;
     {
-        double sd, cd;
-        sincos2pi(kap[D - 1], sd, cd);
-        const double two_cd = 2.0 * cd;
-        for (int r = gl; r < P.n_runs; r += G) {
-            double rec[RS - 1];  // n_start, z0, info
+        double s3, c3, s2 = 0.0, c2 = 1.0;
+        sincos2pi(kap[D - 1], s3, c3);
+        if constexpr (D >= 2) sincos2pi(kap[D - 2], s2, c2);
+        const double two_c3 = 2.0 * c3;
+        int row = 0;  // global row index (lane split for G > 1)
+        for (int sl = 0; sl < P.n_slabs; ++sl) {
+            double rec[SR];
 #pragma unroll
-            for (int c = 0; c + 1 < RS - 1; c += 2) {
-                const double2 v2 = ld_f64x2<SMEM>(V.run, V.s_run, r * RS + c);
+            for (int c = 0; c < SR; c += 2) {
+                const double2 v2 = ld_f64x2<SMEM>(V.dir, V.s_dir, sl * SR + c);
                 rec[c] = v2.x;
                 rec[c + 1] = v2.y;
             }
-            if constexpr ((RS - 1) % 2 == 1) rec[RS - 2] = ld_f64<SMEM>(V.run, V.s_run, r * RS + RS - 2);
             double ph = 0.0;
 #pragma unroll
             for (int a = 0; a < D; ++a) ph = fma(kap[a], rec[a], ph);
-            double sn, cs;
-            sincos2pi(ph, sn, cs);
-            double cprev = fma(cs, cd, sn * sd);  // cos(phi - th)
-            const double info = rec[2 * D];
-            const int first = __double2loint(info), len = __double2hiint(info);
-            int w = first * NWP;  // element index of the run's first weight row
-            double S[NH > 0 ? NH : 1];
-#pragma unroll
-            for (int m = 0; m < NH; ++m) S[m] = 0.0;
-            auto point = [&](int wp) {
-                double wv[NWP];
-                if constexpr (NWP % 2 == 0) {
-#pragma unroll
-                    for (int c = 0; c < NWP; c += 2) {
-                        const double2 v2 = ld_f64x2<SMEM>(V.dir_w, V.s_dir_w, wp + c);
-                        wv[c] = v2.x;
-                        wv[c + 1] = v2.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < NWP; ++c) wv[c] = ld_f64<SMEM>(V.dir_w, V.s_dir_w, wp + c);
-                }
-#pragma unroll
-                for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
-#pragma unroll
-                for (int m = 0; m < NH; ++m) S[m] = fma(wv[NCTX + m], cs, S[m]);
-                const double cnext = fma(two_cd, cs, -cprev);
-                cprev = cs;
-                cs = cnext;
-            };
-            // runs are short (~6 points): no unrolling beyond the pair, so no remainder set-up
+            double ps, pc;  // exp(i phi) at (row, l0)
+            sincos2pi(ph, ps, pc);
+            const int nrows = __double2hiint(rec[2 * D + 1]);
+            double jd = rec[2 * D];
+            double A0 = 0.0, A1 = 0.0, A2 = 0.0, B0 = 0.0, B1 = 0.0, T = 0.0;
+            for (int rr = 0; rr < nrows; ++rr, ++row) {
+                const double rinfo = ld_f64<SMEM>(V.dir, V.s_dir, P.rows_off + row);
+                const int len = __double2hiint(rinfo) & 0xffff;
+                if (len > 0 && (G == 1 || row % G == gl)) {
+                    const int skip = __double2hiint(rinfo) >> 16;
+                    double cs = pc;
+                    double cprev = fma(pc, c3, ps * s3);  // cos(phi - th)
 #pragma unroll 1
-            for (int l = 0; l < len; l += 2) {
-                point(w);
-                point(w + NWP);
-                w += 2 * NWP;
+                    for (int t = 0; t < skip; ++t) {
+                        const double cn = fma(two_c3, cs, -cprev);
+                        cprev = cs;
+                        cs = cn;
+                    }
+                    int w = P.w_off + __double2loint(rinfo) * NWP;  // element index of the row
+                    double S[NH > 0 ? NH : 1];
+#pragma unroll
+                    for (int m = 0; m < NH; ++m) S[m] = 0.0;
+                    auto point = [&](int wp) {
+                        double wv[NWP];
+                        if constexpr (NWP % 2 == 0) {
+#pragma unroll
+                            for (int c = 0; c < NWP; c += 2) {
+                                const double2 v2 = ld_f64x2<SMEM>(V.dir, V.s_dir, wp + c);
+                                wv[c] = v2.x;
+                                wv[c + 1] = v2.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < NWP; ++c) wv[c] = ld_f64<SMEM>(V.dir, V.s_dir, wp + c);
+                        }
+#pragma unroll
+                        for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
+#pragma unroll
+                        for (int m = 0; m < NH; ++m) S[m] = fma(wv[NCTX + m], cs, S[m]);
+                        const double cnext = fma(two_c3, cs, -cprev);
+                        cprev = cs;
+                        cs = cnext;
+                    };
+                    // rows are short (~6 points): no unrolling beyond the pair
+#pragma unroll 1
+                    for (int l = 0; l < len; l += 2) {
+                        point(w);
+                        point(w + NWP);
+                        w += 2 * NWP;
+                    }
+                    if constexpr (HESS) {
+                        A0 += S[0];
+                        A1 = fma(jd, S[0], A1);
+                        A2 = fma(jd * jd, S[0], A2);
+                        B0 += S[1];
+                        B1 = fma(jd, S[1], B1);
+                        T += S[2];
+                    }
+                }
+                // next row: exp(i phi) *= exp(2 pi i kappa_{d-1})
+                const double pcn = fma(pc, c2, -ps * s2);
+                ps = fma(ps, c2, pc * s2);
+                pc = pcn;
+                jd += 1.0;
             }
             if constexpr (HESS) {
-                double v[D];
+                const double* zc = rec + D;
+                double X[D], Y[D], W[D];
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    v[a] = rec[D + a] * S[0];
-                    uu[a] = fma(rec[D + a], S[1], uu[a]);
+                for (int b = 0; b < D; ++b) {
+                    X[b] = fma(zc[b], A0, fma(P.e2[b], A1, P.e3[b] * B0));
+                    Y[b] = fma(zc[b], A1, fma(P.e2[b], A2, P.e3[b] * B1));
+                    W[b] = fma(zc[b], B0, fma(P.e2[b], B1, P.e3[b] * T));
                 }
-                tt += S[2];
                 int c = 0;
 #pragma unroll
                 for (int a = 0; a < D; ++a)
 #pragma unroll
                     for (int b = a; b < D; ++b) {
-                        hh[c] = fma(v[a], rec[D + b], hh[c]);
+                        hh[c] = fma(zc[a], X[b], fma(P.e2[a], Y[b], fma(P.e3[a], W[b], hh[c])));
                         ++c;
                     }
             }
@@ -476,17 +498,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     // The Hessian's direct-space channels arrive pre-scaled by -2 pi^2 / rfac (host), so they
     // seed the reciprocal accumulators: one register set of d(d+1)/2 instead of two.
     double yy[NS > 0 ? NS : 1];
-    if constexpr (HESS) {
-        int c = 0;
 #pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = a; b < D; ++b) {
-                const double eu = fma(uu[a], P.estep[b], uu[b] * P.estep[a]);
-                yy[c] = hh[c] + fma(P.estep[a] * P.estep[b], tt, eu);
-                ++c;
-            }
-    }
+    for (int c = 0; c < NS; ++c) yy[c] = hh[c];
     const double cc = P.c;  // all contexts of a plan share the split
     // Exact per-warp culling: |k+q| >= |q| - |k|, and every table function is
     // identically zero beyond x_hi, i.e. for |k+q| > r_cut.  The points are
@@ -529,14 +542,15 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
         for (int a = 0; a < D; ++a) y[a] += k[a];
         double f[NF];
-        if constexpr (mode == 1) {
-            // in-cell: xb = (|k+q|^2 - x_lo / c) * r_scale; lanes past the cutoff skip the
-            // lookup and the accumulation (no zero-fill)
+        if constexpr (mode == 1 || mode == 3) {
+            // in-cell: xb = (|k+q|^2 - x_lo / c) * r_scale.  mode 1: lanes past the cutoff skip
+            // the lookup and the accumulation; mode 3: every lane is inside (|q| + max|k| <= r_in),
+            // no branch, so consecutive terms interleave
             double r = -P.tab.r_off;
 #pragma unroll
             for (int a = D - 1; a >= 0; --a) r = fma(y[a], y[a], r);
             const double xb = r * P.tab.r_scale;
-            if (xb < P.tab.nbins_d) {
+            if (mode == 3 || xb < P.tab.nbins_d) {
                 tab_eval_cell<NF, SMEM>(V, xb, f);
                 accumulate(y, f);
             }
@@ -554,8 +568,13 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 0>{});
     } else if (!P.tab.branchfree) {
+        // q with |q| <= r_in - max|k| are inside the table for every lane of the warp
+        const int n_in = min(n_eff, count_le(V.rec_norm, P.n_rec, P.r_in - kmag));
+        int i = gl;
 #pragma unroll UNR
-        for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 1>{});
+        for (; i < n_in; i += G) term(i, std::integral_constant<int, 3>{});
+#pragma unroll UNR
+        for (; i < n_eff; i += G) term(i, std::integral_constant<int, 1>{});
     } else {
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 2>{});

@@ -83,19 +83,18 @@ struct DevPlan {
     double alias_ratio;
     double A[16];      // generator, row-major (columns = basis vectors)
     double B[16];      // A^{-T}, row-major
-    // Direct space as runs of consecutive n_d.  Run record (2d + 2 doubles): integer coordinates
-    // of the first point [d], Cartesian reference point z0 = A n(center) [d], (first weight row,
-    // even length) packed as two int32 in one double, pad.
-    const double* run_rec;
-    int n_runs, pad3_;
-    // [n_dir][nw] weights (run order, runs padded to even length with zero rows): nctx plain
-    // channels, then (hess) the Hessian weight times l^0, l^1, l^2 with l = point - run center
-    // (z_a z_b = z0a z0b + l (z0a e_b + e_a z0b) + l^2 e_a e_b along the run), zero-padded to even nw
-    const double* dir_w;
-    double estep[4];       // e = A e_d: Cartesian step along a run
+    // Direct space (one array, staged as a block): slab records [n_slabs][2d + 2] = integer
+    // coordinates of (slab, first row, l0) [d], Cartesian slab center zc [d], j' of the first row,
+    // (first row, row count) as two int32; row records [n_rows] = (weight row, (skip << 16) | even
+    // length) as two int32; weight rows [n_dir][nw] from w_off: nctx plain channels, then (hess)
+    // the Hessian weight times l'^0, l'^1, l'^2 (l' = column - slab center column).
+    const double* direct;
+    int n_direct, n_slabs, n_rows, rows_off, w_off, pad3_;
+    double e2[4], e3[4];   // A e_{d-1}, A e_d: Cartesian row and column steps
     const double* rec_q;   // [n_rec][(d+1)&~1] Cartesian reciprocal vectors q != 0 (zero-padded), sorted by |q|
     const double* rec_norm;  // [n_rec] |q| ascending
     double r_cut;          // |k+q| > r_cut  =>  every table function is exactly zero
+    double r_in;           // |k+q| <= r_in  =>  inside the table (xb < nbins, no far check)
     DevTable tab;          // functions: nctx plain F_j, then (hess) F', F''
     CtxConst ctx[kMaxCtx];
     CtxConst hctx;         // constants of the Hessian context
