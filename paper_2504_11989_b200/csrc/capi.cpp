@@ -478,6 +478,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
     P.direct = upload(hp.direct, allocs);
+    P.direct_host = hp.direct.empty() ? nullptr : hp.direct.data();
     P.n_direct = int(hp.direct.size());
     P.n_slabs = hp.n_slabs;
     P.n_rows = hp.n_rows;

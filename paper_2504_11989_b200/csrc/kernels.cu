@@ -72,7 +72,7 @@ __device__ inline void copy_words(double* dst, const double* src, size_t n) {
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-template <bool SMEM>
+template <bool SMEM, bool SKIP_DIR = false>
 __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
     View v;
     v.s_dir = v.s_rec_q = v.s_coef = v.s_tdir = 0;
@@ -97,7 +97,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
-        copy_words(dd, P.direct, size_t(P.n_direct));
+        if (!SKIP_DIR) copy_words(dd, P.direct, size_t(P.n_direct));
         copy_words(rq, P.rec_q, size_t(P.n_rec) * ((P.d + 1) & ~1));
         copy_words(rn, P.rec_norm, size_t(P.n_rec));
         copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
@@ -156,6 +156,19 @@ template <bool SMEM>
 __device__ __forceinline__ int ld_s32(const int* g, uint32_t s, int i) {
     if constexpr (SMEM) return lds_s32(s + 4u * uint32_t(i));
     else return g[i];
+}
+
+// Direct-space block loads: shared memory (SMEM), global, or (CDIR) the kernel's parameter
+// space (a __grid_constant__ copy: warp-uniform LDC loads that bypass the LSU/shared pipe).
+template <bool SMEM, bool CDIR>
+__device__ __forceinline__ double2 ld_dir2(const View& V, int i) {
+    if constexpr (CDIR) return *reinterpret_cast<const double2*>(V.dir + i);
+    else return ld_f64x2<SMEM>(V.dir, V.s_dir, i);
+}
+template <bool SMEM, bool CDIR>
+__device__ __forceinline__ double ld_dir(const View& V, int i) {
+    if constexpr (CDIR) return V.dir[i];
+    else return ld_f64<SMEM>(V.dir, V.s_dir, i);
 }
 
 // Number of reciprocal points with |q| <= r (rec_norm ascending), binary search.
@@ -363,7 +376,7 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
     double h[HESS ? Sym<D>::n : 1];
 };
 
-template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true>
+template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true, bool CDIR = false>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out) {
@@ -398,7 +411,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             double rec[SR];
 #pragma unroll
             for (int c = 0; c < SR; c += 2) {
-                const double2 v2 = ld_f64x2<SMEM>(V.dir, V.s_dir, sl * SR + c);
+                const double2 v2 = ld_dir2<SMEM, CDIR>(V, sl * SR + c);
                 rec[c] = v2.x;
                 rec[c + 1] = v2.y;
             }
@@ -411,7 +424,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             double jd = rec[2 * D];
             double A0 = 0.0, A1 = 0.0, A2 = 0.0, B0 = 0.0, B1 = 0.0, T = 0.0;
             for (int rr = 0; rr < nrows; ++rr, ++row) {
-                const double rinfo = ld_f64<SMEM>(V.dir, V.s_dir, P.rows_off + row);
+                const double rinfo = ld_dir<SMEM, CDIR>(V, P.rows_off + row);
                 const int len = __double2hiint(rinfo) & 0xffff;
                 if (len > 0 && (G == 1 || row % G == gl)) {
                     const int skip = __double2hiint(rinfo) >> 16;
@@ -432,13 +445,13 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                         if constexpr (NWP % 2 == 0) {
 #pragma unroll
                             for (int c = 0; c < NWP; c += 2) {
-                                const double2 v2 = ld_f64x2<SMEM>(V.dir, V.s_dir, wp + c);
+                                const double2 v2 = ld_dir2<SMEM, CDIR>(V, wp + c);
                                 wv[c] = v2.x;
                                 wv[c + 1] = v2.y;
                             }
                         } else {
 #pragma unroll
-                            for (int c = 0; c < NWP; ++c) wv[c] = ld_f64<SMEM>(V.dir, V.s_dir, wp + c);
+                            for (int c = 0; c < NWP; ++c) wv[c] = ld_dir<SMEM, CDIR>(V, wp + c);
                         }
 #pragma unroll
                         for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
@@ -775,14 +788,22 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
 // One CTA = TPC tiles of 8 warps sharing ONE staged copy of the plan
 // (the ATM plan is ~115 KB, so two 256-thread CTAs no longer fit one SM).
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC = kTilesPerCta, int UNR = 2>
-__global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
-    tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
+// Direct-space block passed by value in the kernel parameters (CDIR variant; 28 KB leaves room
+// for DevPlan and DevGrid within the 32764-byte parameter limit).
+constexpr int kDirParam = 3584;
+struct __align__(16) DirBlock {
+    double w[kDirParam];
+};
+
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC, int UNR, bool CDIR>
+__device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
+                                          double* __restrict__ partials, const double* cdir) {
     constexpr int kTilesPerCta = TPC;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
     __shared__ double wsum[kTilesPerCta][kTileWarps][NCOMP];
-    const View V = stage<SMEM>(P, smem);
+    View V = stage<SMEM, CDIR>(P, smem);
+    if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = warp_all / kTileWarps, warp = warp_all % kTileWarps;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
@@ -813,7 +834,7 @@ __global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
-            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM>(P, V, kap, k, 0, 1, 0u, acc);
+            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM, CDIR>(P, V, kap, k, 0, 1, 0u, acc);
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll
@@ -874,6 +895,19 @@ __global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
         }
         __syncthreads();
     }
+}
+
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC = kTilesPerCta, int UNR = 2>
+__global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
+    tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
+    tile_body<D, NCTX, HESS, MODE, SMEM, TPC, UNR, false>(P, g, mult, partials, nullptr);
+}
+
+template <int D, int NCTX, bool HESS, int MODE, int TPC = kTilesPerCta, int UNR = 2>
+__global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
+    tile_kernel_c(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials,
+                  const __grid_constant__ DirBlock B) {
+    tile_body<D, NCTX, HESS, MODE, true, TPC, UNR, true>(P, g, mult, partials, B.w);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -1017,6 +1051,39 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
     return cudaGetLastError();
 }
 
+template <int D, int NCTX, bool HESS, int MODE, int TPC, int UNR>
+static cudaError_t launch_tile_c(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
+                                 cudaStream_t st, size_t bytes) {
+    static_assert(sizeof(DevPlan) + sizeof(DevGrid) + sizeof(int4) + sizeof(double*) + 16 + sizeof(DirBlock) <= 32764,
+                  "kernel parameters exceed the 32 KB limit");
+    auto kern = tile_kernel_c<D, NCTX, HESS, MODE, TPC, UNR>;
+    const size_t sm = bytes - ((sizeof(double) * size_t(P.n_direct) + 15) & ~size_t(15));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+    (void)sm;  // the direct region stays reserved (offsets unchanged) but is not staged
+    thread_local DirBlock blk;  // host staging of the parameter copy (copied at launch)
+    std::memcpy(blk.w, P.direct_host, sizeof(double) * size_t(P.n_direct));
+    const int threads = 32 * kTileWarps * TPC;
+    int64_t need = (g.tile_hi - g.tile_lo + TPC - 1) / TPC;
+    int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, bytes, threads);
+    int blocks = int(need < cap ? need : cap);
+    if (blocks < 1) return cudaSuccess;
+    kern<<<blocks, threads, bytes, st>>>(P, g, mult, partials, blk);
+    return cudaGetLastError();
+}
+
+// Parameter-space direct block for the ATM kernel: default on (measured 15.7 -> 14.4 ms on the
+// fcc bench grid: the broadcast weight loads leave the LSU pipe to the table lookups);
+// LATSUM_CDIR=0 stages it in shared memory instead.
+static bool cdir_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("LATSUM_CDIR");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // ATM kernel shape (tiles per CTA x q-unroll), overridable for tuning sweeps: LATSUM_ATM_SHAPE
 // in {"2x2" (default), "2x1", "3x1", "3x2"}.
 static int atm_shape() {
@@ -1038,6 +1105,10 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
                                  cudaStream_t st) {
     const size_t bytes = plan_smem_bytes(P);
     const bool smem = bytes + 2048 <= size_t(smem_optin());
+    if constexpr (MODE == 1) {
+        if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host)
+            return launch_tile_c<D, NCTX, HESS, MODE, kTilesPerCta, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+    }
     if constexpr (MODE == 1 && D == 3) {
         if (smem) {
             switch (atm_shape()) {

@@ -89,6 +89,7 @@ struct DevPlan {
     // length) as two int32; weight rows [n_dir][nw] from w_off: nctx plain channels, then (hess)
     // the Hessian weight times l'^0, l'^1, l'^2 (l' = column - slab center column).
     const double* direct;
+    const double* direct_host;  // host copy (plan-owned) for the parameter-space variant
     int n_direct, n_slabs, n_rows, rows_off, w_off, pad3_;
     double e2[4], e3[4];   // A e_{d-1}, A e_d: Cartesian row and column steps
     const double* rec_q;   // [n_rec][(d+1)&~1] Cartesian reciprocal vectors q != 0 (zero-padded), sorted by |q|
