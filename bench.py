@@ -32,10 +32,10 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v9); used to turn the live kernel time into FLOP/s.
-FLOPS_PER_NODE = 13667.2
-FLOPS_SOURCE = "ncu r01 v9: 3.4395e+11 FP64 FLOPs per launch / 25,165,824 nodes"
-TRAFFIC_PER_LAUNCH = 631_040 + 30_464  # ncu r01 v9 dram__bytes_read.sum + dram__bytes_write.sum
+# bench grid (profiles/r01_summary.md, v13); used to turn the live kernel time into FLOP/s.
+FLOPS_PER_NODE = 11020.0
+FLOPS_SOURCE = "ncu r01 v13: 2.7733e+11 FP64 FLOPs per launch / 25,165,824 nodes"
+TRAFFIC_PER_LAUNCH = 122_624 + 18_176  # ncu r01 v13 dram__bytes_read.sum + dram__bytes_write.sum
 
 
 def parse():
@@ -363,7 +363,8 @@ def secondary(np, torch):
     t1 = time.perf_counter()
     lam = np.linspace(0.0, 2.0, 64)
     pts = phase_scan(fc, bc, lj, [0.0, 0.5, 1.0, 2.0], lam, np.linspace(0.9, 1.7, 64))
-    crit = {p: critical_coupling(fc, bc, lj, p) for p in (0.0, 0.5, 1.0, 2.0)}
+    pres = (0.0, 0.5, 1.0, 2.0)
+    crit = dict(zip(pres, (float(v) for v in critical_coupling(fc, bc, lj, np.array(pres)))))
     t2 = time.perf_counter()
     out["c5_phase_scan"] = {"constants_ms": (t1 - t0) * 1e3, "scan_ms": (t2 - t1) * 1e3,
                             "lambda_c": crit, "k_atm_fcc": fc.k_atm, "k_atm_bcc": bc.k_atm,

@@ -130,7 +130,9 @@ def phase_scan(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams, p_gri
 def critical_coupling(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams, p,
                       lam_grid=None, r_grid=None, tol: float = 1e-14):
     """lambda_c(p): first fcc -> bcc sign change of min_R H_fcc - min_R H_bcc on the lambda grid,
-    refined by bisection (SPEC.md: 'bisection on lambda ... between bracketing points').
+    refined inside the bracketing points (SPEC.md: 'bisection on lambda ... between bracketing
+    points') by safeguarded Newton with the envelope-theorem slope K_fcc/R_fcc^9 - K_bcc/R_bcc^9,
+    falling back to bisection.
     ``p`` may be a scalar or an array (vectorised over pressures)."""
     if lam_grid is None:
         lam_grid = np.linspace(0.0, 2.0, 64)
@@ -143,6 +145,12 @@ def critical_coupling(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams
     def delta(lam, pp):
         return _golden_min(fcc, lj, lam, pp, r_grid)[1] - _golden_min(bcc, lj, lam, pp, r_grid)[1]
 
+    def delta_d(lam, pp):
+        # envelope theorem: d/dlambda min_R H(R; lambda) = K / R*^9 at the minimiser
+        rf, hf = _golden_min(fcc, lj, lam, pp, r_grid)
+        rb, hb = _golden_min(bcc, lj, lam, pp, r_grid)
+        return hf - hb, fcc.k_atm / rf ** 9 - bcc.k_atm / rb ** 9
+
     dv = delta(lam_grid[None, :], p[:, None])
     out = np.full(len(p), np.nan)
     flip = (dv[:, :-1] <= 0.0) & (dv[:, 1:] > 0.0)
@@ -150,14 +158,21 @@ def critical_coupling(fcc: LatticeConstants, bcc: LatticeConstants, lj: LJParams
     first = np.argmax(flip, axis=1)
     a = lam_grid[first].astype(float)
     b = lam_grid[np.minimum(first + 1, len(lam_grid) - 1)].astype(float)
-    for _ in range(200):
-        if np.all(b - a <= tol):
+    # safeguarded Newton on delta(lambda) = 0 inside the sign-change bracket (bisection fallback)
+    lam = 0.5 * (a + b)
+    for _ in range(100):
+        fm, dm = delta_d(lam, p)
+        a = np.where(fm <= 0.0, lam, a)
+        b = np.where(fm <= 0.0, b, lam)
+        step = np.where(dm != 0.0, fm / np.where(dm != 0.0, dm, 1.0), 0.0)
+        nxt = lam - step
+        bad = ~((nxt > a) & (nxt < b)) | (dm == 0.0)
+        nxt = np.where(bad, 0.5 * (a + b), nxt)
+        done = (np.abs(nxt - lam) <= tol) | (b - a <= tol)
+        lam = nxt
+        if np.all(done):
             break
-        mid = 0.5 * (a + b)
-        fm = delta(mid, p)
-        go_right = fm <= 0.0
-        a = np.where(go_right, mid, a)
-        b = np.where(go_right, b, mid)
+    a = b = lam
     out[has] = 0.5 * (a + b)[has]
     return float(out[0]) if scalar else out
 
