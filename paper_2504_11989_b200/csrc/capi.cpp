@@ -230,27 +230,37 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
-        std::vector<std::vector<ld>> wall(np, std::vector<ld>(wctx.size()));
-        std::vector<ld> mag(np, 0.0L);
-        lz::parallel_for(int64_t(np), 64, [&](int64_t i) {
-            ld z[lz::kMaxDim];
+        // keep/drop decisions in double precision (magnitudes only), final weights in long double
+        // for the kept points
+        std::vector<double> wabs(np * wctx.size()), mag(np, 0.0);
+        lz::parallel_for(int64_t(np), 128, [&](int64_t i) {
+            double r2 = 0.0;
+            for (int a = 0; a < d; ++a) {
+                double za = 0.0;
+                for (int b = 0; b < d; ++b) za += first->A[a * d + b] * hp->dir_n[i * d + b];
+                r2 += za * za;
+            }
             for (size_t j = 0; j < wctx.size(); ++j) {
-                const ld w = direct_weight(*wctx[j], &hp->dir_n[i * d], z);
-                wall[i][j] = w;
-                ld r2 = 0.0L;
-                for (int a = 0; a < d; ++a) r2 += z[a] * z[a];
-                mag[i] = std::max(mag[i], std::fabs(w) * std::max(1.0L, r2));
+                const double nu = wctx[j]->k.nu;
+                const double w = std::fabs(lz::upper_gamma<double>(nu / 2.0, lz::kPi * wctx[j]->k.split * r2) *
+                                           std::pow(r2, -nu / 2.0));
+                wabs[i * wctx.size() + j] = w;
+                mag[i] = std::max(mag[i], w * std::max(1.0, r2));
             }
         });
-        ld total = 0.0L;  // fixed summation order: independent of the thread count
-        for (size_t i = 0; i < np; ++i)
-            for (size_t j = 0; j < wctx.size(); ++j) total += std::fabs(wall[i][j]);
+        double total = 0.0;  // fixed summation order: independent of the thread count
+        for (double w : wabs) total += w;
         std::vector<double> kept;
-        for (size_t i = 0; i < np; ++i) {
-            if (!(mag[i] > dcut * total)) continue;
-            kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
-            wmap.emplace(pack_key(d, &hp->dir_n[i * d]), std::move(wall[i]));
-        }
+        for (size_t i = 0; i < np; ++i)
+            if (mag[i] > double(dcut) * total)
+                kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
+        const size_t nk = kept.size() / d;
+        std::vector<std::vector<ld>> wall(nk, std::vector<ld>(wctx.size()));
+        lz::parallel_for(int64_t(nk), 32, [&](int64_t i) {
+            ld z[lz::kMaxDim];
+            for (size_t j = 0; j < wctx.size(); ++j) wall[i][j] = direct_weight(*wctx[j], &kept[i * d], z);
+        });
+        for (size_t i = 0; i < nk; ++i) wmap.emplace(pack_key(d, &kept[i * d]), std::move(wall[i]));
         hp->dir_n.swap(kept);
     }
     // Direct points as 2D slabs: slab = fixed (n_1 .. n_{d-2}), rows along n_{d-1}, columns along
@@ -460,9 +470,40 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     }
 }
 
+// All device arrays of a plan in one allocation and one copy (16-byte aligned sections).
+struct Blob {
+    std::vector<unsigned char> host;
+    template <class T> size_t add(const T* p, size_t n) {
+        const size_t off = (host.size() + 15) & ~size_t(15);
+        host.resize(off + n * sizeof(T));
+        if (n) std::memcpy(host.data() + off, p, n * sizeof(T));
+        return off;
+    }
+};
+
 lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     lz::DevPlan P;
     std::memset(&P, 0, sizeof(P));
+    // reciprocal vectors padded to an even stride (16-byte aligned double2 loads)
+    const int qs = (hp.d + 1) & ~1;
+    const size_t nrec = hp.rec_q.size() / hp.d;
+    std::vector<double> rq(nrec * qs, 0.0);
+    for (size_t i = 0; i < nrec; ++i)
+        for (int a = 0; a < hp.d; ++a) rq[i * qs + a] = hp.rec_q[i * hp.d + a];
+    Blob b;
+    const size_t o_t0 = b.add(hp.t0c.data(), hp.t0c.size());
+    const size_t o_dir = b.add(hp.direct.data(), hp.direct.size());
+    const size_t o_rq = b.add(rq.data(), rq.size());
+    const size_t o_rn = b.add(hp.rec_norm.data(), hp.rec_norm.size());
+    const size_t o_td = b.add(hp.tab.dir.data(), hp.tab.dir.size());
+    const size_t o_cf = b.add(hp.tab.coef.data(), hp.tab.coef.size());
+    unsigned char* dev = nullptr;
+    if (!b.host.empty()) {
+        check_cuda(cudaMalloc(reinterpret_cast<void**>(&dev), b.host.size()), "cudaMalloc");
+        allocs->push_back(dev);
+        check_cuda(cudaMemcpy(dev, b.host.data(), b.host.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
+    }
+    auto at = [&](size_t off, bool nonempty) -> unsigned char* { return nonempty ? dev + off : nullptr; };
     P.d = hp.d;
     P.nctx = hp.nctx;
     P.hess = hp.hess;
@@ -471,13 +512,13 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.nw = hp.nw;
     P.c = hp.c;
     P.alias_fp = hp.alias_fp;
-    P.t0c = upload(hp.t0c, allocs);
+    P.t0c = reinterpret_cast<const double*>(at(o_t0, !hp.t0c.empty()));
     P.n_t0 = hp.n_t0;
     P.t0_rho_max = hp.t0_rho_max;
     P.alias_ratio = hp.alias_ratio;
     std::memcpy(P.A, hp.A, sizeof(P.A));
     std::memcpy(P.B, hp.B, sizeof(P.B));
-    P.direct = upload(hp.direct, allocs);
+    P.direct = reinterpret_cast<const double*>(at(o_dir, !hp.direct.empty()));
     P.direct_host = hp.direct.empty() ? nullptr : hp.direct.data();
     P.n_direct = int(hp.direct.size());
     P.n_slabs = hp.n_slabs;
@@ -486,20 +527,12 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.w_off = hp.w_off;
     std::memcpy(P.e2, hp.e2, sizeof(P.e2));
     std::memcpy(P.e3, hp.e3, sizeof(P.e3));
-    {
-        // reciprocal vectors padded to an even stride (16-byte aligned double2 loads)
-        const int qs = (hp.d + 1) & ~1;
-        const size_t nrec = hp.rec_q.size() / hp.d;
-        std::vector<double> rq(nrec * qs, 0.0);
-        for (size_t i = 0; i < nrec; ++i)
-            for (int a = 0; a < hp.d; ++a) rq[i * qs + a] = hp.rec_q[i * hp.d + a];
-        P.rec_q = upload(rq, allocs);
-    }
-    P.rec_norm = upload(hp.rec_norm, allocs);
+    P.rec_q = reinterpret_cast<const double*>(at(o_rq, !rq.empty()));
+    P.rec_norm = reinterpret_cast<const double*>(at(o_rn, !hp.rec_norm.empty()));
     P.r_cut = hp.r_cut;
     P.r_in = hp.r_in;
-    P.tab.dir = upload(hp.tab.dir, allocs);
-    P.tab.coef = upload(hp.tab.coef, allocs);
+    P.tab.dir = reinterpret_cast<const int*>(at(o_td, !hp.tab.dir.empty()));
+    P.tab.coef = reinterpret_cast<const double*>(at(o_cf, !hp.tab.coef.empty()));
     P.tab.nbins = hp.tab.nbins;
     P.tab.nfunc = hp.tab.nfunc;
     P.tab.npieces = hp.tab.npieces;
@@ -676,10 +709,17 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
     }
     GridArrays ga;
     std::vector<void*>& allocs = const_cast<std::vector<void*>&>(plan->allocs);
-    ga.u = upload(u, &allocs);
-    ga.wu = upload(wu, &allocs);
-    ga.v = upload(v, &allocs);
-    ga.wv = upload(wv, &allocs);
+    std::vector<double> all;
+    all.reserve(2 * (u.size() + v.size()));
+    all.insert(all.end(), u.begin(), u.end());
+    all.insert(all.end(), wu.begin(), wu.end());
+    all.insert(all.end(), v.begin(), v.end());
+    all.insert(all.end(), wv.begin(), wv.end());
+    double* dev = upload(all, &allocs);  // one allocation, one copy
+    ga.u = dev;
+    ga.wu = dev + u.size();
+    ga.v = dev + 2 * u.size();
+    ga.wv = dev + 2 * u.size() + v.size();
     return plan->grids.emplace(key, ga).first->second;
 }
 

@@ -355,30 +355,45 @@ struct Fn {
 // Chebyshev interpolation at kNC first-kind nodes, converted to monomials in delta = tau / 2
 // in [-1/2, 1/2] (c_j tau^j = (2^j c_j) delta^j: exact rescaling, same conditioning; the device
 // gets delta = (fs - 1/2) - floor(fs) without the extra 2 x - 1 step).
+// Chebyshev nodes, the cosine (DCT) matrix and the monomial coefficients of T_k, computed once.
+struct ChebConsts {
+    ld tau[kNC];
+    ld cosm[kNC][kNC];   // cos(pi k (i + 1/2) / N)
+    ld tk[kNC][kNC];     // T_k(tau) = sum_j tk[k][j] tau^j
+    ChebConsts() {
+        const int N = kNC;
+        for (int i = 0; i < N; ++i) tau[i] = std::cos(kPiL * (i + 0.5L) / N);
+        for (int k = 0; k < N; ++k)
+            for (int i = 0; i < N; ++i) cosm[k][i] = std::cos(kPiL * k * (i + 0.5L) / N);
+        for (int k = 0; k < N; ++k)
+            for (int j = 0; j < N; ++j) tk[k][j] = 0.0L;
+        tk[0][0] = 1.0L;
+        if (N > 1) tk[1][1] = 1.0L;
+        for (int k = 2; k < N; ++k)
+            for (int j = 0; j < N; ++j)
+                tk[k][j] = (j > 0 ? 2.0L * tk[k - 1][j - 1] : 0.0L) - tk[k - 2][j];
+    }
+};
+const ChebConsts& cheb() {
+    static const ChebConsts c;
+    return c;
+}
+
 void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
     const int N = kNC;
+    const ChebConsts& C = cheb();
     ld fv[kNC];
     ld mid = 0.5L * (x0 + x1), half = 0.5L * (x1 - x0);
-    for (int i = 0; i < N; ++i) {
-        ld tau = std::cos(kPiL * (i + 0.5L) / N);
-        fv[i] = f(mid + half * tau);
-    }
+    for (int i = 0; i < N; ++i) fv[i] = f(mid + half * C.tau[i]);
     ld ak[kNC];
     for (int k = 0; k < N; ++k) {
         ld s = 0.0L;
-        for (int i = 0; i < N; ++i) s += fv[i] * std::cos(kPiL * k * (i + 0.5L) / N);
+        for (int i = 0; i < N; ++i) s += fv[i] * C.cosm[k][i];
         ak[k] = (k == 0 ? 1.0L : 2.0L) * s / N;
     }
-    // monomial coefficients of T_k
-    ld tk[kNC][kNC] = {};
-    tk[0][0] = 1.0L;
-    if (N > 1) tk[1][1] = 1.0L;
-    for (int k = 2; k < N; ++k)
-        for (int j = 0; j < N; ++j)
-            tk[k][j] = (j > 0 ? 2.0L * tk[k - 1][j - 1] : 0.0L) - tk[k - 2][j];
     for (int j = 0; j < N; ++j) {
         ld c = 0.0L;
-        for (int k = 0; k < N; ++k) c += ak[k] * tk[k][j];
+        for (int k = 0; k < N; ++k) c += ak[k] * C.tk[k][j];
         out[j] = double(std::ldexp(c, j));
     }
 }
