@@ -490,13 +490,18 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     std::vector<double> rq(nrec * qs, 0.0);
     for (size_t i = 0; i < nrec; ++i)
         for (int a = 0; a < hp.d; ++a) rq[i * qs + a] = hp.rec_q[i * hp.d + a];
+    // section order and 16-byte alignment = the kernel's shared-memory image (stage<true>), so the
+    // kernel stages the plan with one bulk copy
     Blob b;
-    const size_t o_t0 = b.add(hp.t0c.data(), hp.t0c.size());
     const size_t o_dir = b.add(hp.direct.data(), hp.direct.size());
     const size_t o_rq = b.add(rq.data(), rq.size());
     const size_t o_rn = b.add(hp.rec_norm.data(), hp.rec_norm.size());
-    const size_t o_td = b.add(hp.tab.dir.data(), hp.tab.dir.size());
     const size_t o_cf = b.add(hp.tab.coef.data(), hp.tab.coef.size());
+    const size_t o_td = b.add(hp.tab.dir.data(), hp.tab.dir.size());
+    std::vector<double> t0rows(size_t(hp.nctx + (hp.hess ? 2 : 0)) * lz::kT0, 0.0);
+    std::copy(hp.t0c.begin(), hp.t0c.begin() + std::min(hp.t0c.size(), t0rows.size()), t0rows.begin());
+    const size_t o_t0 = b.add(t0rows.data(), t0rows.size());
+    b.host.resize((b.host.size() + 15) & ~size_t(15), 0);
     unsigned char* dev = nullptr;
     if (!b.host.empty()) {
         check_cuda(cudaMalloc(reinterpret_cast<void**>(&dev), b.host.size()), "cudaMalloc");
@@ -504,6 +509,8 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
         check_cuda(cudaMemcpy(dev, b.host.data(), b.host.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
     }
     auto at = [&](size_t off, bool nonempty) -> unsigned char* { return nonempty ? dev + off : nullptr; };
+    P.blob = dev;
+    P.blob_bytes = b.host.size();
     P.d = hp.d;
     P.nctx = hp.nctx;
     P.hess = hp.hess;
@@ -512,7 +519,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.nw = hp.nw;
     P.c = hp.c;
     P.alias_fp = hp.alias_fp;
-    P.t0c = reinterpret_cast<const double*>(at(o_t0, !hp.t0c.empty()));
+    P.t0c = reinterpret_cast<const double*>(at(o_t0, !t0rows.empty()));
     P.n_t0 = hp.n_t0;
     P.t0_rho_max = hp.t0_rho_max;
     P.alias_ratio = hp.alias_ratio;

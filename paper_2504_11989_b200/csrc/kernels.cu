@@ -26,6 +26,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "lz_internal.h"
@@ -68,8 +71,31 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     return b;
 }
 
-__device__ inline void copy_words(double* dst, const double* src, size_t n) {
-    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+// Bulk asynchronous copy (TMA engine, 1D) of the plan image global -> shared, completing on an
+// mbarrier.  The device blob (capi.cpp upload_plan) has exactly the shared-memory layout, so one
+// elected thread issues the copy; chunks of <= 32 KB, all on one transaction count.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
 }
 
 template <bool SMEM, bool SKIP_DIR = false>
@@ -97,19 +123,36 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
-        if (!SKIP_DIR) copy_words(dd, P.direct, size_t(P.n_direct));
-        copy_words(rq, P.rec_q, size_t(P.n_rec) * ((P.d + 1) & ~1));
-        copy_words(rn, P.rec_norm, size_t(P.n_rec));
-        copy_words(cf, P.tab.coef, size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
+        // one TMA bulk copy of the plan image (minus the direct block when it travels in the
+        // kernel parameters), then the directory is relocated in place
+        __shared__ __align__(8) uint64_t bar_storage;
+        const uint32_t bar = uint32_t(__cvta_generic_to_shared(&bar_storage));
+        const size_t skip = SKIP_DIR ? align16(sizeof(double) * P.n_direct) : 0;
+        const uint32_t total = uint32_t(P.blob_bytes - skip);
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            if (total > 0) {
+                mbar_expect_tx(bar, total);
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(skip);
+                for (uint32_t o = 0; o < total; o += 32768u) {
+                    const uint32_t n = total - o < 32768u ? total - o : 32768u;
+                    bulk_g2s(dst + o, P.blob + skip + o, n, bar);
+                }
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+            }
+        }
+        __syncthreads();  // barrier initialised before anyone polls it
+        mbar_wait(bar, 0);
         // directory relocated for the shared copy: the high word of 2^L in bits 20-30 and the
         // shared byte address of the bin's first piece in bits 0-19 (the 227 KB window fits)
         const uint32_t cf_addr = uint32_t(__cvta_generic_to_shared(cf));
         const uint32_t pbytes = uint32_t(sizeof(double) * piece_stride(P.tab.nfunc));
         for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) {
-            const int e = P.tab.dir[i];
+            const int e = td[i];
             td[i] = int((uint32_t(1023 + (e & 15)) << 20) | (cf_addr + uint32_t(e >> 4) * pbytes));
         }
-        copy_words(tc, P.t0c, size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
+        (void)tc;
         __syncthreads();
         v.s_dir = uint32_t(__cvta_generic_to_shared(dd));
         v.s_rec_q = uint32_t(__cvta_generic_to_shared(rq));
@@ -513,7 +556,6 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     double yy[NS > 0 ? NS : 1];
 #pragma unroll
     for (int c = 0; c < NS; ++c) yy[c] = hh[c];
-    const double cc = P.c;  // all contexts of a plan share the split
     // Exact per-warp culling: |k+q| >= |q| - |k|, and every table function is
     // identically zero beyond x_hi, i.e. for |k+q| > r_cut.  The points are
     // sorted by |q|, so the warp stops after the last q with |q| <= r_cut + max|k|.
@@ -959,30 +1001,78 @@ __global__ void fp64_probe(double* out, int iters, double seed) {
 // ---------------------------------------------------------------------------
 // Launchers (host)
 
-static int g_num_sms = 0;
-static int num_sms() {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
-
-static int smem_optin() {
-    int dev = 0, optin = 0;
+// Per-device launch facts, cached: the host entry points are called per batch (C1: 4096 points
+// in ~5 us of device time), so the attribute / occupancy queries must not be repeated per call.
+struct DeviceFacts {
+    int sms = 0, optin = 0;
+};
+static std::mutex g_launch_mu;
+static DeviceFacts& facts() {
+    static DeviceFacts f[64];
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return optin;
+    DeviceFacts& d = f[dev & 63];
+    if (d.sms == 0) {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        if (d.sms == 0) {
+            int sms = 0, optin = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            d.optin = optin;
+            d.sms = sms > 0 ? sms : 148;
+        }
+    }
+    return d;
+}
+static int num_sms() { return facts().sms; }
+static int smem_optin() { return facts().optin; }
+
+// Occupancy per (kernel, dynamic smem, threads, device) and the largest dynamic-smem attribute
+// already set per (kernel, device), both cached.
+static std::map<std::tuple<const void*, size_t, int, int>, int>& occ_cache() {
+    static std::map<std::tuple<const void*, size_t, int, int>, int> m;
+    return m;
+}
+static std::map<std::pair<const void*, int>, size_t>& attr_cache() {
+    static std::map<std::pair<const void*, int>, size_t> m;
+    return m;
 }
 
 template <class K>
 static int blocks_for(K kernel, size_t smem, int threads) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), smem, threads, dev);
+    {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        auto it = occ_cache().find(key);
+        if (it != occ_cache().end()) return it->second;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (per_sm < 1) per_sm = 1;
-    return per_sm * num_sms();
+    const int blocks = per_sm * num_sms();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    occ_cache()[key] = blocks;
+    return blocks;
+}
+
+template <class K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+    {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        auto it = attr_cache().find(key);
+        if (it != attr_cache().end() && it->second >= bytes) return cudaSuccess;
+    }
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    size_t& v = attr_cache()[key];
+    v = std::max(v, bytes);
+    return cudaSuccess;
 }
 
 template <int D, int NCTX, bool HESS, bool SMEM>
@@ -991,7 +1081,7 @@ static cudaError_t launch_batch_s(const DevPlan& P, const double* k, int64_t n, 
     auto kern = batch_kernel<D, NCTX, HESS, SMEM>;
     size_t sm = SMEM ? bytes : 0;
     if (SMEM) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_smem(kern, sm);
         if (e != cudaSuccess) return e;
     }
     const int threads = 256;
@@ -1007,6 +1097,7 @@ template <int D, int NCTX, bool HESS>
 static cudaError_t launch_batch_t(const DevPlan& P, const double* k, int64_t n, double* out, uint32_t flags, int G,
                                   int* status, cudaStream_t st) {
     const size_t bytes = plan_smem_bytes(P);
+    if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     if (bytes + 2048 <= size_t(smem_optin()))
         return launch_batch_s<D, NCTX, HESS, true>(P, k, n, out, flags, G, status, st, bytes);
     return launch_batch_s<D, NCTX, HESS, false>(P, k, n, out, flags, G, status, st, bytes);
@@ -1039,7 +1130,7 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
     auto kern = tile_kernel<D, NCTX, HESS, MODE, SMEM, TPC, UNR>;
     size_t sm = SMEM ? bytes : 0;
     if (SMEM) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        cudaError_t e = set_smem(kern, sm);
         if (e != cudaSuccess) return e;
     }
     const int threads = 32 * kTileWarps * TPC;
@@ -1058,7 +1149,7 @@ static cudaError_t launch_tile_c(const DevPlan& P, const DevGrid& g, int4 mult, 
                   "kernel parameters exceed the 32 KB limit");
     auto kern = tile_kernel_c<D, NCTX, HESS, MODE, TPC, UNR>;
     const size_t sm = bytes - ((sizeof(double) * size_t(P.n_direct) + 15) & ~size_t(15));
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
     (void)sm;  // the direct region stays reserved (offsets unchanged) but is not staged
     thread_local DirBlock blk;  // host staging of the parameter copy (copied at launch)
@@ -1104,6 +1195,7 @@ template <int D, int NCTX, bool HESS, int MODE>
 static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st) {
     const size_t bytes = plan_smem_bytes(P);
+    if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1) {
         if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host)

@@ -88,6 +88,10 @@ struct DevPlan {
     // (first row, row count) as two int32; row records [n_rows] = (weight row, (skip << 16) | even
     // length) as two int32; weight rows [n_dir][nw] from w_off: nctx plain channels, then (hess)
     // the Hessian weight times l'^0, l'^1, l'^2 (l' = column - slab center column).
+    // device image of every staged array in the shared-memory layout (see kernels.cu stage):
+    // direct block, reciprocal vectors, norms, coefficients, directory, q=0 series
+    const unsigned char* blob;
+    unsigned long long blob_bytes;
     const double* direct;
     const double* direct_host;  // host copy (plan-owned) for the parameter-space variant
     int n_direct, n_slabs, n_rows, rows_off, w_off, pad3_;

@@ -32,7 +32,7 @@ def atm():
 
 def atm_sweep():
     """Kernel time and energy of the fcc ATM sum vs the theta split (CUDA events, 5 reps)."""
-    fcc = named_lattice("fcc")
+    fcc = named_lattice(os.environ.get("LATTICE", "fcc"))
     scales = [float(v) for v in os.environ.get("SWEEP", "0.35,0.45,0.55,0.65,0.8").split(",")]
     for sc in scales:
         plan = atm_plan(fcc, sc * fcc.volume ** (-2.0 / 3.0))
@@ -107,6 +107,25 @@ def c1_time():
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 20
         print(f"n={n}: {ms:.4f} ms, {n / ms * 1e3:.3e} evals/s")
+        # device time without host launch overhead: 20 launches replayed from a CUDA graph
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ctx.zeta_device(k, out=out)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(20):
+                    ctx.zeta_device(k, out=out)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        print(f"   graph replay: {a.elapsed_time(b) / 20:.4f} ms per batch")
         if n == 4096:
             for lanes in (1, 2, 4, 8, 16, 32):
                 a.record()
