@@ -255,6 +255,19 @@ __device__ __forceinline__ void sincos2pi(double x, double& sn, double& cs) {
     cs = __hiloint2double(__double2hiint(q) ^ flip, __double2loint(q));
 }
 
+// cos(2 pi x) alone (the lane-split direct path of small batches).
+__device__ __forceinline__ double cos2pi(double x) {
+    constexpr double kM = 6755399441055744.0;
+    const double y = x + x;
+    const double t = y + kM;
+    const double r = y - (t - kM);
+    const double u = r * r;
+    double q = kCosQ[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) q = fma(q, u, kCosQ[i]);
+    return __hiloint2double(__double2hiint(q) ^ (__double2loint(t) << 31), __double2loint(q));
+}
+
 // Out-of-line E_p for the rare direct paths, so the hot loop stays small.
 __device__ __noinline__ double expint_dev(double p, double x) { return expint<double>(p, x); }
 
@@ -469,22 +482,13 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             for (int rr = 0; rr < nrows; ++rr, ++row) {
                 const double rinfo = ld_dir<SMEM, CDIR>(V, P.rows_off + row);
                 const int len = __double2hiint(rinfo) & 0xffff;
-                if (len > 0 && (G == 1 || row % G == gl)) {
+                if (len > 0) {
                     const int skip = __double2hiint(rinfo) >> 16;
-                    double cs = pc;
-                    double cprev = fma(pc, c3, ps * s3);  // cos(phi - th)
-#pragma unroll 1
-                    for (int t = 0; t < skip; ++t) {
-                        const double cn = fma(two_c3, cs, -cprev);
-                        cprev = cs;
-                        cs = cn;
-                    }
                     int w = P.w_off + __double2loint(rinfo) * NWP;  // element index of the row
                     double S[NH > 0 ? NH : 1];
 #pragma unroll
                     for (int m = 0; m < NH; ++m) S[m] = 0.0;
-                    auto point = [&](int wp) {
-                        double wv[NWP];
+                    auto load_w = [&](int wp, double (&wv)[NWP]) {
                         if constexpr (NWP % 2 == 0) {
 #pragma unroll
                             for (int c = 0; c < NWP; c += 2) {
@@ -496,20 +500,47 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
                             for (int c = 0; c < NWP; ++c) wv[c] = ld_dir<SMEM, CDIR>(V, wp + c);
                         }
+                    };
+                    auto accum = [&](const double (&wv)[NWP], double cs) {
 #pragma unroll
                         for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
 #pragma unroll
                         for (int m = 0; m < NH; ++m) S[m] = fma(wv[NCTX + m], cs, S[m]);
-                        const double cnext = fma(two_c3, cs, -cprev);
-                        cprev = cs;
-                        cs = cnext;
                     };
-                    // rows are short (~6 points): no unrolling beyond the pair
+                    if (G == 1) {
+                        double cs = pc;
+                        double cprev = fma(pc, c3, ps * s3);  // cos(phi - th)
 #pragma unroll 1
-                    for (int l = 0; l < len; l += 2) {
-                        point(w);
-                        point(w + NWP);
-                        w += 2 * NWP;
+                        for (int t = 0; t < skip; ++t) {
+                            const double cn = fma(two_c3, cs, -cprev);
+                            cprev = cs;
+                            cs = cn;
+                        }
+                        auto point = [&](int wp) {
+                            double wv[NWP];
+                            load_w(wp, wv);
+                            accum(wv, cs);
+                            const double cnext = fma(two_c3, cs, -cprev);
+                            cprev = cs;
+                            cs = cnext;
+                        };
+                        // rows are short (~6 points): no unrolling beyond the pair
+#pragma unroll 1
+                        for (int l = 0; l < len; l += 2) {
+                            point(w);
+                            point(w + NWP);
+                            w += 2 * NWP;
+                        }
+                    } else {
+                        // G lanes per node (small batches): the row's points are spread over the
+                        // lanes, each cosine evaluated directly at phi_row + (skip + l) kappa_d
+                        double phr = ph;
+                        if constexpr (D >= 2) phr = fma(double(rr), kap[D - 2], ph);
+                        for (int l = gl; l < len; l += G) {
+                            double wv[NWP];
+                            load_w(w + l * NWP, wv);
+                            accum(wv, cos2pi(fma(double(skip + l), kap[D - 1], phr)));
+                        }
                     }
                     if constexpr (HESS) {
                         A0 += S[0];

@@ -53,6 +53,16 @@ def atm_sweep():
               f"n_rec {info.n_rec} pieces {info.table_pieces} smem {info.smem_bytes}  E {e:.15f}")
 
 
+def c1_small():
+    sq = named_lattice("square")
+    ctx = EpsteinContext(sq, 3.5, device=0)
+    k = torch.tensor(np.random.default_rng(0).uniform(-0.5, 0.5, size=(4096, 2)), device="cuda")
+    for _ in range(3):
+        z, st = ctx.zeta_device(k)
+    torch.cuda.synchronize()
+    print("c1_small ok", float(z.sum()))
+
+
 def c1():
     sq = named_lattice("square")
     ctx = EpsteinContext(sq, 3.5, device=0)
@@ -128,12 +138,21 @@ def c1_time():
         print(f"   graph replay: {a.elapsed_time(b) / 20:.4f} ms per batch")
         if n == 4096:
             for lanes in (1, 2, 4, 8, 16, 32):
-                a.record()
-                for _ in range(20):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
                     ctx.zeta_device(k, out=out, lanes_per_point=lanes)
+                    torch.cuda.synchronize()
+                    with torch.cuda.graph(g, stream=s):
+                        for _ in range(20):
+                            ctx.zeta_device(k, out=out, lanes_per_point=lanes)
+                torch.cuda.synchronize()
+                g.replay()
+                torch.cuda.synchronize()
+                a.record()
+                g.replay()
                 b.record()
                 torch.cuda.synchronize()
-                print(f"   lanes={lanes}: {a.elapsed_time(b) / 20:.4f} ms")
+                print(f"   lanes={lanes}: {a.elapsed_time(b) / 20:.4f} ms per batch (graph replay)")
 
 
 def e2e():
@@ -160,4 +179,4 @@ def e2e():
 
 if __name__ == "__main__":
     {"atm": atm, "c1": c1, "c1_time": c1_time, "e2e": e2e,
-     "e2e_breakdown": e2e_breakdown, "atm_sweep": atm_sweep}[sys.argv[1]]()
+     "e2e_breakdown": e2e_breakdown, "atm_sweep": atm_sweep, "c1_small": c1_small}[sys.argv[1]]()
