@@ -400,7 +400,7 @@ void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
 
 ld eval_piece(const double* c, ld tau) {
     // evaluate exactly as the device does (Estrin form, double)
-    return estrin8(c, tau_powers(double(tau) * 0.5));
+    return estrin(c, tau_powers(double(tau) * 0.5));
 }
 
 }  // namespace
@@ -504,7 +504,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
             for (int j = 0; j < nfunc; ++j) {
                 const double* cf = &bf.coefs[(size_t(sidx) * nfunc + j) * kNCP];
                 for (int m = 0; m < 8; ++m) out->coef[base + j * 8 + m] = cf[m];
-                out->coef[base + nfunc * 8 + j] = cf[8];
+                if (kDeg == 8) out->coef[base + nfunc * 8 + j] = cf[8];
             }
         }
         npieces += 1 << bf.level;

@@ -305,8 +305,8 @@ __device__ __forceinline__ void tab_piece(const View& V, double xb, double tb, i
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
         const double cc[9] = {cd[j * 8 + 0], cd[j * 8 + 1], cd[j * 8 + 2], cd[j * 8 + 3], cd[j * 8 + 4],
-                              cd[j * 8 + 5], cd[j * 8 + 6], cd[j * 8 + 7], cd[NF * 8 + j]};
-        f[j] = estrin8(cc, tp);
+                              cd[j * 8 + 5], cd[j * 8 + 6], cd[j * 8 + 7], kDeg == 8 ? cd[NF * 8 + j] : 0.0};
+        f[j] = estrin(cc, tp);
     }
 }
 

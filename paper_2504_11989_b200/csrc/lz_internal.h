@@ -15,16 +15,20 @@ enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
 
 constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
-constexpr int kDeg = 8;        // degree of the piecewise polynomials (kDeg+1 coefficients)
+// Degree of the piecewise polynomials (kDeg + 1 coefficients): 7 or 8.  Degree 7 on bins of
+// 0.125 in x saves two DFMA, one DMUL and one 16-byte load per function pair and term but needs
+// ~1.8x the pieces for the same 6e-16 bound; measured slower (fcc ATM 14.4 -> 20.8 ms, C1 2^20
+// 0.155 -> 0.204 ms: lanes of a warp spread over more pieces), so degree 8 is the default.
+constexpr int kDeg = 8;
 constexpr int kNC = kDeg + 1;
 constexpr int kNCP = 10;       // per-function stride of the host fit arrays
-// Device piece layout for nf functions: c0..c7 of each function (8 doubles each), then c8 of
-// every function, padded to an even count (every double2 load 16-byte aligned; NF = 2: 9 loads).
+// Device piece layout for nf functions: c0..c7 of each function (8 doubles each), then (degree 8)
+// c8 of every function, padded to an even count (every double2 load 16-byte aligned).
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-constexpr int piece_stride(int nf) { return nf * 8 + ((nf + 1) & ~1); }
-constexpr double kBinWidth = 0.25;  // directory bin width in x = c |y|^2
+constexpr int piece_stride(int nf) { return kDeg == 8 ? nf * 8 + ((nf + 1) & ~1) : nf * 8; }
+constexpr double kBinWidth = kDeg == 8 ? 0.25 : 0.125;  // directory bin width in x = c |y|^2
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
 constexpr int kT0 = 64;             // max terms of the q = 0 power series
 
@@ -141,8 +145,8 @@ struct HostTable {
     double max_rel_err = 0;   // measured during the build
 };
 
-// Degree-8 polynomial in Estrin form: dependency depth 4 instead of 8, and the
-// powers tau^2, tau^4, tau^8 are shared by every function of a table row.
+// Degree-kDeg polynomial in Estrin form: dependency depth 3-4 instead of 7-8, and the
+// powers tau^2, tau^4 (, tau^8) are shared by every function of a table row.
 // Host (table build check) and device evaluate with the same operation order.
 struct TauPowers {
     double t1, t2, t4, t8;
@@ -161,7 +165,7 @@ inline TauPowers tau_powers(double t) {
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-inline double estrin8(const double* c, const TauPowers& p) {
+inline double estrin(const double* c, const TauPowers& p) {
     const double a0 = fma(c[1], p.t1, c[0]);
     const double a1 = fma(c[3], p.t1, c[2]);
     const double a2 = fma(c[5], p.t1, c[4]);
@@ -169,7 +173,8 @@ inline double estrin8(const double* c, const TauPowers& p) {
     const double b0 = fma(a1, p.t2, a0);
     const double b1 = fma(a3, p.t2, a2);
     const double e0 = fma(b1, p.t4, b0);
-    return fma(c[8], p.t8, e0);
+    if (kDeg == 8) return fma(c[8], p.t8, e0);
+    return e0;
 }
 
 // Errors raised by the host builder carry an lz status code.
