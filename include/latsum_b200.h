@@ -145,6 +145,16 @@ int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, cons
 
 /* -- diagnostics */
 int lz_fp64_peak(int device, double* tflops_out, double* ms_out);  /* DFMA-chain probe on `device` */
+
+/* -- multi-GPU: sum the slot-disjoint tile partials of every rank in place (SURVEY.md 8(b)
+ * lz_allreduce_partials; replaces the reference's per-cell thread pool reduction,
+ * L/quadrature.py:475-488, and its fsum of panel results, L/quadrature.py:236).  One
+ * ncclAllReduce(double, sum) of n values on `stream` over the caller's communicator
+ * (`nccl_comm` is an ncclComm_t, e.g. ProcessGroupNCCL._comm_ptr()).  NCCL is resolved at run
+ * time from the copy already loaded in the process (the one that created the communicator), so
+ * the library has no link-time NCCL dependency.  Returns LZ_ENCCL when NCCL is unavailable or
+ * the collective fails. */
+int lz_allreduce_partials(double* partials, int64_t n, void* nccl_comm, void* stream);
 int lz_device_count(int* n);
 const char* lz_strerror(int code);
 const char* lz_last_error(void);   /* thread-local message of the last failure */

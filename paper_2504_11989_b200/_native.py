@@ -24,7 +24,7 @@ INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 SOURCES = ["kernels.cu", "direct.cu", "context.cpp", "capi.cpp"]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC", "-shared", "-ldl"]
 
 LZ_OK, LZ_EINVAL, LZ_EPOLE, LZ_ENONFINITE, LZ_ECUDA, LZ_ENCCL, LZ_ESHELLS, LZ_ELATTICE, LZ_ESINGULAR = range(9)
 NO_REDUCE, REG_ONLY, SINGULAR_ONLY = 1, 2, 4
@@ -89,6 +89,7 @@ SIGNATURES = {
     "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
     "lz_direct_sum3": (C.c_int, [C.c_int, C.c_int, _D, C.c_int64, C.c_int, _D, C.c_double, _D]),
     "lz_fp64_peak": (C.c_int, [C.c_int, _D, _D]),
+    "lz_allreduce_partials": (C.c_int, [_P, C.c_int64, _P, _P]),
     "lz_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "lz_strerror": (C.c_char_p, [C.c_int]),
     "lz_last_error": (C.c_char_p, []),

@@ -5,6 +5,7 @@
 // (kernels.cu) on the caller's stream.  No CPU compute path exists: every
 // compute entry point needs a CUDA device.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1256,6 +1257,33 @@ int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, cons
         double v;
         std::memcpy(&v, ar.hbuf, sizeof(double));
         *out = kind == 1 ? v / 6.0 : v;
+    });
+}
+
+int lz_allreduce_partials(double* partials, int64_t n, void* nccl_comm, void* stream) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && !partials)) throw Error{LZ_EINVAL, "bad partials buffer"};
+        if (!nccl_comm) throw Error{LZ_EINVAL, "null NCCL communicator"};
+        // ncclResult_t ncclAllReduce(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+        //                            ncclComm_t, cudaStream_t);  ncclDouble = 8, ncclSum = 0
+        using AllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+        using ErrFn = const char* (*)(int);
+        static AllReduceFn all_reduce = nullptr;
+        static ErrFn err_string = nullptr;
+        static std::once_flag once;
+        std::call_once(once, [] {
+            // prefer the NCCL already mapped into the process (it created the communicator)
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+            if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) return;
+            all_reduce = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
+            err_string = reinterpret_cast<ErrFn>(dlsym(h, "ncclGetErrorString"));
+        });
+        if (!all_reduce) throw Error{LZ_ENCCL, "NCCL (libnccl.so.2) is not available in this process"};
+        if (n == 0) return;
+        const int rc = all_reduce(partials, partials, size_t(n), 8, 0, nccl_comm, (cudaStream_t)stream);
+        if (rc != 0)
+            throw Error{LZ_ENCCL, std::string("ncclAllReduce: ") + (err_string ? err_string(rc) : std::to_string(rc))};
     });
 }
 

@@ -24,6 +24,34 @@ def shard_range(n_tiles: int, rank: int, world: int):
     return n_tiles * rank // world, n_tiles * (rank + 1) // world
 
 
+def nccl_comm_ptr(group=None, device=None) -> int:
+    """Raw ncclComm_t of a NCCL process group (0 if the group is not NCCL or not yet connected).
+    The communicator is created lazily by the first collective."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0
+    pg = group if group is not None else dist.group.WORLD
+    try:
+        if dist.get_backend(pg) != "nccl":
+            return 0
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        return int(pg._get_backend(dev)._comm_ptr())
+    except (AttributeError, RuntimeError):
+        return 0
+
+
+def allreduce_partials(partials: torch.Tensor, group=None, stream=None) -> None:
+    """Sum the slot-disjoint partials of every rank in place: through the C ABI
+    (lz_allreduce_partials: one ncclAllReduce on the library's stream order) when the group is
+    NCCL, else torch.distributed (gloo on CPU tests)."""
+    comm = nccl_comm_ptr(group, partials.device) if partials.is_cuda else 0
+    if comm:
+        from . import _native as N
+        st = stream if stream is not None else torch.cuda.current_stream(partials.device).cuda_stream
+        N.check(N.lib().lz_allreduce_partials(partials.data_ptr(), partials.numel(), comm, st), "all-reduce")
+    else:
+        dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+
+
 def _world(group=None):
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(group), dist.get_world_size(group)
@@ -55,7 +83,7 @@ class ShardedIntegral:
         self.plan.integrate_device(self.partials, self.n_u, self.n_v, self.grading,
                                    self.tile_lo, self.tile_hi, stream=stream)
         if self.world > 1:
-            dist.all_reduce(self.partials, op=dist.ReduceOp.SUM, group=self.group)
+            allreduce_partials(self.partials, self.group, stream)
         Plan.reduce_device(self.partials, self.n_tiles, self.ncomp, self.out, stream=stream)
         return self.out
 

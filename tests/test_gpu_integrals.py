@@ -116,6 +116,45 @@ def test_atm_scaling_homogeneity():
     assert abs(e2 * 1.3 ** 9 - e1) <= 1e-12 * abs(e1)
 
 
+def test_nccl_allreduce_through_cabi():
+    """lz_allreduce_partials on a one-rank NCCL group (the box has one GPU): the C-ABI all-reduce
+    is the identity for W = 1 and the sharded ATM sum through it matches the local one."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_11989_b200 import _native as N
+    from paper_2504_11989_b200.distributed import (ShardedIntegral, allreduce_partials,
+                                                   nccl_comm_ptr)
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        t = torch.arange(1000, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)  # connects the communicator
+        comm = nccl_comm_ptr()
+        assert comm != 0
+        x = torch.linspace(-1.0, 1.0, 4097, dtype=torch.float64, device="cuda")
+        y = x.clone()
+        allreduce_partials(y)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        st = torch.cuda.current_stream().cuda_stream
+        assert N.lib().lz_allreduce_partials(y.data_ptr(), y.numel(), None, st) == N.LZ_EINVAL
+        s = ShardedIntegral(atm_plan(named_lattice("fcc")), 32, 16, 3)
+        s.world = 2  # force the collective path (this rank still owns every tile: W = 1 sum)
+        out = s.run().cpu().numpy()
+        res = atm_integrals(named_lattice("fcc"), ATMGrid(32, 16, 3))
+        assert out[0] * 8 == res.zeta333
+    finally:
+        dist.destroy_process_group()
+
+
 def test_tile_sharding_bit_identical():
     """Slot-disjoint partials: any split of the tile range gives bit-identical sums."""
     import torch

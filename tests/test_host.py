@@ -1,6 +1,7 @@
 """Host-side logic of the drop-in (CPU only): C-ABI exports, lattice geometry, exponent
 classification, the native context/table builder vs the reference's point sets, configs,
 Duffy layout and the phase-scan arithmetic."""
+import ctypes as C
 import math
 import os
 import re
@@ -222,3 +223,10 @@ def test_host_only_plans():
     # ATM plans need nu and nu + 2
     h3 = C.c_void_p()
     assert N.lib().lz_plan_create_atm(c3.handle, c3.handle, C.byref(h3)) != 0
+
+
+def test_allreduce_partials_argument_errors():
+    """The C-ABI all-reduce validates its arguments before touching CUDA or NCCL."""
+    assert N.lib().lz_allreduce_partials(None, 0, None, None) == N.LZ_EINVAL
+    assert "communicator" in N.last_error()
+    assert N.lib().lz_allreduce_partials(None, 8, C.c_void_p(1), None) == N.LZ_EINVAL
