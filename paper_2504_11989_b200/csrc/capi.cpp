@@ -575,6 +575,8 @@ struct GridArrays {
     double* wu = nullptr;
     double* v = nullptr;
     double* wv = nullptr;
+    double* wpart = nullptr;        // warp partials of the tile kernel (scratch)
+    unsigned int* tcount = nullptr;  // per-tile arrival counters (zeroed once; kernels leave 0)
 };
 
 // Per-device scratch for the host-buffer entry points: one non-blocking stream,
@@ -728,6 +730,20 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
     ga.wu = dev + u.size();
     ga.v = dev + 2 * u.size();
     ga.wv = dev + 2 * u.size() + v.size();
+    {
+        lz::DevGrid tmp;
+        lz_grid full = *g;
+        full.tile_lo = full.tile_hi = 0;
+        fill_grid(d, &full, &tmp);
+        const size_t n_tiles = size_t((tmp.n_patch + 7) / 8);
+        const size_t wbytes = n_tiles * 8 * 2 * sizeof(double), cbytes = n_tiles * sizeof(unsigned int);
+        void* scratch = nullptr;
+        check_cuda(cudaMalloc(&scratch, wbytes + cbytes), "cudaMalloc");
+        allocs.push_back(scratch);
+        ga.wpart = static_cast<double*>(scratch);
+        ga.tcount = reinterpret_cast<unsigned int*>(static_cast<unsigned char*>(scratch) + wbytes);
+        check_cuda(cudaMemset(ga.tcount, 0, cbytes), "cudaMemset");
+    }
     return plan->grids.emplace(key, ga).first->second;
 }
 
@@ -1127,6 +1143,8 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
         dgd.wu = ga.wu;
         dgd.v = ga.v;
         dgd.wv = ga.wv;
+        dgd.wpart = ga.wpart;
+        dgd.tcount = ga.tcount;
         cudaStream_t st = (cudaStream_t)stream;
         if (pl->kind == 0)
             check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");

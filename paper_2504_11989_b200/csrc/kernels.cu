@@ -871,24 +871,25 @@ struct __align__(16) DirBlock {
 template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC, int UNR, bool CDIR>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
-    constexpr int kTilesPerCta = TPC;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
-    __shared__ double wsum[kTilesPerCta][kTileWarps][NCOMP];
     View V = stage<SMEM, CDIR>(P, smem);
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = warp_all / kTileWarps, warp = warp_all % kTileWarps;
+    constexpr int kWarpsPerCta = kTileWarps * TPC;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
-    for (int64_t base = g.tile_lo + int64_t(blockIdx.x) * kTilesPerCta; base < g.tile_hi;
-         base += int64_t(gridDim.x) * kTilesPerCta) {
-        const int64_t tile = base + sub;
-        const int64_t patch = tile * kTileWarps + warp;
+    // Warps are independent (no block barrier after staging): each takes 32-node patches of the
+    // shard's range in CTA-contiguous order, writes its warp partial, and the last of a tile's 8
+    // warps to finish sums the 8 warp partials in fixed order into the tile slot.
+    const int64_t p_lo = g.tile_lo * kTileWarps, p_hi = g.tile_hi * kTileWarps;
+    for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
+         patch += int64_t(gridDim.x) * kWarpsPerCta) {
+        const int64_t tile = patch / kTileWarps;
         double val[NCOMP];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
         double t[D], weight = 0.0, u = 0.0;
-        const bool ok = tile < g.tile_hi && patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
+        const bool ok = patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
         if (!ok) {  // padding lane: a harmless interior node with zero weight
 #pragma unroll
             for (int a = 0; a < D; ++a) t[a] = 1.0;
@@ -952,21 +953,30 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             }
         }
         // deterministic tile reduction: fixed xor tree per warp, fixed warp order
+        double wv[NCOMP];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
             double v = val[c];
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            if (lane == 0) wsum[sub][warp][c] = v;
+            wv[c] = v;
         }
-        __syncthreads();
-        if (threadIdx.x < NCOMP * kTilesPerCta) {
-            const int ts = threadIdx.x / NCOMP, c = threadIdx.x % NCOMP;
-            double s = 0.0;
-            for (int w = 0; w < kTileWarps; ++w) s += wsum[ts][w][c];
-            if (base + ts < g.tile_hi) partials[(base + ts) * NCOMP + c] = s;
+        if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) g.wpart[patch * NCOMP + c] = wv[c];
+            __threadfence();
+            const unsigned prev = atomicAdd(&g.tcount[tile], 1u);
+            if (prev == kTileWarps - 1) {  // last warp of the tile: fixed-order sum
+                __threadfence();
+#pragma unroll
+                for (int c = 0; c < NCOMP; ++c) {
+                    double s = 0.0;
+                    for (int w = 0; w < kTileWarps; ++w) s += __ldcg(&g.wpart[(tile * kTileWarps + w) * NCOMP + c]);
+                    partials[tile * NCOMP + c] = s;
+                }
+                g.tcount[tile] = 0u;  // ready for the next launch
+            }
         }
-        __syncthreads();
     }
 }
 

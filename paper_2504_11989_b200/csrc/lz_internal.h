@@ -117,6 +117,8 @@ struct DevGrid {
     const double* wv;  // angular weights
     int n_u, n_v, n_cell, pu, pv, npu, npv, nv2;
     int64_t tile_lo, tile_hi, n_patch;
+    double* wpart;             // [n_tiles * 8][ncomp] warp partials (scratch)
+    unsigned int* tcount;      // [n_tiles] arrival counters, zero between launches
 };
 
 
