@@ -544,6 +544,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.nbins = hp.tab.nbins;
     P.tab.nfunc = hp.tab.nfunc;
     P.tab.npieces = hp.tab.npieces;
+    P.tab.ncoef = int(hp.tab.coef.size());
     P.tab.x_lo = hp.tab.x_lo;
     P.tab.inv_hb = hp.tab.inv_hb;
     P.tab.x_hi = hp.tab.x_hi;

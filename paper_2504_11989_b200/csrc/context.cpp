@@ -356,12 +356,11 @@ struct Fn {
 // in [-1/2, 1/2] (c_j tau^j = (2^j c_j) delta^j: exact rescaling, same conditioning; the device
 // gets delta = (fs - 1/2) - floor(fs) without the extra 2 x - 1 step).
 // Chebyshev nodes, the cosine (DCT) matrix and the monomial coefficients of T_k, computed once.
-struct ChebConsts {
-    ld tau[kNC];
-    ld cosm[kNC][kNC];   // cos(pi k (i + 1/2) / N)
-    ld tk[kNC][kNC];     // T_k(tau) = sum_j tk[k][j] tau^j
+template <int N> struct ChebConsts {
+    ld tau[N];
+    ld cosm[N][N];   // cos(pi k (i + 1/2) / N)
+    ld tk[N][N];     // T_k(tau) = sum_j tk[k][j] tau^j
     ChebConsts() {
-        const int N = kNC;
         for (int i = 0; i < N; ++i) tau[i] = std::cos(kPiL * (i + 0.5L) / N);
         for (int k = 0; k < N; ++k)
             for (int i = 0; i < N; ++i) cosm[k][i] = std::cos(kPiL * k * (i + 0.5L) / N);
@@ -374,18 +373,17 @@ struct ChebConsts {
                 tk[k][j] = (j > 0 ? 2.0L * tk[k - 1][j - 1] : 0.0L) - tk[k - 2][j];
     }
 };
-const ChebConsts& cheb() {
-    static const ChebConsts c;
+template <int N> const ChebConsts<N>& cheb() {
+    static const ChebConsts<N> c;
     return c;
 }
 
-void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
-    const int N = kNC;
-    const ChebConsts& C = cheb();
-    ld fv[kNC];
+template <int N> void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
+    const ChebConsts<N>& C = cheb<N>();
+    ld fv[N];
     ld mid = 0.5L * (x0 + x1), half = 0.5L * (x1 - x0);
     for (int i = 0; i < N; ++i) fv[i] = f(mid + half * C.tau[i]);
-    ld ak[kNC];
+    ld ak[N];
     for (int k = 0; k < N; ++k) {
         ld s = 0.0L;
         for (int i = 0; i < N; ++i) s += fv[i] * C.cosm[k][i];
@@ -398,10 +396,9 @@ void fit_piece(const Fn& f, ld x0, ld x1, double* out) {
     }
 }
 
-ld eval_piece(const double* c, ld tau) {
-    // evaluate exactly as the device does (Estrin form, double)
-    return estrin(c, tau_powers(double(tau) * 0.5));
-}
+// evaluate exactly as the device does (Estrin form, double)
+ld eval_piece(const double* c, ld tau) { return estrin(c, tau_powers(double(tau) * 0.5)); }
+ld eval_piece_lo(const double* c, ld tau) { return estrin_lo(c, tau_powers(double(tau) * 0.5)); }
 
 }  // namespace
 
@@ -438,78 +435,105 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     out->dir.assign(nbins, 0);
     out->coef.clear();
     out->max_rel_err = 0.0;
-    // bins are independent: fit them on all host cores, then concatenate in order
+    // Bins are independent: fit them on all host cores, then concatenate in order.  A bin gets
+    // the cheap degree-kDegLo pieces when their error, weighted like the cutoff test (times
+    // |rfac pref| (1 + 4x)), stays below kLoBudget x cutoff everywhere in the bin -- far-out terms
+    // (most of the reciprocal ball: E_p decays like e^-x) need only absolute accuracy at the
+    // level of the terms the cutoff already drops.  Otherwise degree kDeg pieces are fitted to
+    // 6e-16 relative error.  Both are checked at 11 points per piece with the device's exact
+    // evaluation order.
     struct BinFit {
         int level = kDirectMarker;
+        int lo = 0;
         double err = 0.0;
-        std::vector<double> coefs;
+        std::vector<double> coefs;   // [sub][func][kNCP] fit arrays
     };
+    const ld lo_budget = kLoBudget * cutoff / std::max(std::fabs(ld(rfac_pref)), 1e-300L);
     std::vector<BinFit> fits(nbins);
     const int kMaxLevel = 8;
-    auto fit_bin = [&](int b) {
-        const ld b0 = ld(x_lo) + hb * b;
-        BinFit& bf = fits[b];
-        for (int level = 0; level <= kMaxLevel; ++level) {
-            const int nsub = 1 << level;
-            std::vector<double> coefs(size_t(nsub) * nfunc * kNCP, 0.0);
-            double worst_err = 0.0;
-            bool good = true;
-            for (int sidx = 0; sidx < nsub && good; ++sidx) {
-                ld x0 = b0 + hb * sidx / nsub, x1 = b0 + hb * (sidx + 1) / nsub;
-                for (int j = 0; j < nfunc && good; ++j) {
-                    double* cf = &coefs[(size_t(sidx) * nfunc + j) * kNCP];
-                    fit_piece(fns[j], x0, x1, cf);
-                    for (int tidx = 0; tidx <= 10; ++tidx) {
-                        ld tau = -1.0L + 2.0L * tidx / 10.0L;
-                        ld xx = 0.5L * (x0 + x1) + 0.5L * (x1 - x0) * tau;
-                        ld truth = fns[j](xx);
-                        ld approx = eval_piece(cf, tau);
+    auto try_fit = [&](ld b0, int level, bool lo, BinFit* bf) -> bool {
+        const int nsub = 1 << level;
+        std::vector<double> coefs(size_t(nsub) * nfunc * kNCP, 0.0);
+        double worst_err = 0.0;
+        for (int sidx = 0; sidx < nsub; ++sidx) {
+            ld x0 = b0 + hb * sidx / nsub, x1 = b0 + hb * (sidx + 1) / nsub;
+            for (int j = 0; j < nfunc; ++j) {
+                double* cf = &coefs[(size_t(sidx) * nfunc + j) * kNCP];
+                if (lo) fit_piece<kDegLo + 1>(fns[j], x0, x1, cf);
+                else fit_piece<kNC>(fns[j], x0, x1, cf);
+                for (int tidx = 0; tidx <= 10; ++tidx) {
+                    ld tau = -1.0L + 2.0L * tidx / 10.0L;
+                    ld xx = 0.5L * (x0 + x1) + 0.5L * (x1 - x0) * tau;
+                    ld truth = fns[j](xx);
+                    ld approx = lo ? eval_piece_lo(cf, tau) : eval_piece(cf, tau);
+                    if (lo) {
+                        if (std::fabs(approx - truth) * (1.0L + 4.0L * xx) > lo_budget) return false;
+                    } else {
                         double rel = double(std::fabs(approx - truth) / std::max(std::fabs(truth), 1e-300L));
                         worst_err = std::max(worst_err, rel);
-                        if (rel > 6e-16) good = false;
+                        if (rel > 6e-16) return false;
                     }
                 }
             }
-            if (good) {
-                bf.level = level;
-                bf.err = worst_err;
-                bf.coefs.swap(coefs);
-                return;
-            }
         }
+        bf->level = level;
+        bf->lo = lo ? 1 : 0;
+        bf->err = worst_err;
+        bf->coefs.swap(coefs);
+        return true;
+    };
+    const char* lo_env = std::getenv("LATSUM_TABLE_LO");
+    const bool use_lo = !(lo_env && std::atoi(lo_env) == 0);
+    auto fit_bin = [&](int b) {
+        const ld b0 = ld(x_lo) + hb * b;
+        BinFit& bf = fits[b];
+        if (use_lo)
+            for (int level = 0; level <= 1; ++level)
+                if (try_fit(b0, level, true, &bf)) return;
+        for (int level = 0; level <= kMaxLevel; ++level)
+            if (try_fit(b0, level, false, &bf)) return;
         bf.level = kDirectMarker;  // evaluate E_p directly in this bin
     };
     parallel_for(nbins, 1, [&](int64_t b) { fit_bin(int(b)); });
     // Direct (unfitted) bins must form a prefix: the kernel's conversion-free floor may step one
     // piece past a bin's last piece at an exact bin boundary, which is then the next bin's first
-    // piece evaluated at the same x -- valid only if that next bin has pieces.
+    // piece evaluated at the same x -- valid only if that next bin has pieces.  For the same
+    // reason a low-degree bin is never followed by a high-degree one (x is increasing, and the
+    // overshoot lands in the previous bin's last piece, whose stride must match).
     int last_direct = -1;
     for (int b = 0; b < nbins; ++b)
         if (fits[b].level == kDirectMarker) last_direct = b;
     for (int b = 0; b < last_direct; ++b) fits[b].level = kDirectMarker;
-    int npieces = 0;
+    size_t off = 0;
+    out->npieces = 0;
+    out->n_lo_bins = 0;
     for (int b = 0; b < nbins; ++b) {
         const BinFit& bf = fits[b];
         if (bf.level == kDirectMarker) {
             out->dir[b] = kDirectMarker;
             continue;
         }
-        out->max_rel_err = std::max(out->max_rel_err, bf.err);
-        out->dir[b] = (npieces << 4) | bf.level;
+        if (bf.lo) out->n_lo_bins += 1;
+        else out->max_rel_err = std::max(out->max_rel_err, bf.err);
+        // entry: element offset of the bin's first piece, low-degree flag, subdivision level
+        out->dir[b] = int((off << 5) | (size_t(bf.lo) << 4) | size_t(bf.level));
         // fit arrays [sub][func][kNCP] -> device layout [sub][piece_stride(nfunc)]
-        const int ps = piece_stride(nfunc);
+        const int ps = bf.lo ? piece_stride_lo(nfunc) : piece_stride(nfunc);
+        const int nc = bf.lo ? kDegLo : 8;  // leading coefficients per function
         for (int sidx = 0; sidx < (1 << bf.level); ++sidx) {
             const size_t base = out->coef.size();
             out->coef.resize(base + ps, 0.0);
             for (int j = 0; j < nfunc; ++j) {
                 const double* cf = &bf.coefs[(size_t(sidx) * nfunc + j) * kNCP];
-                for (int m = 0; m < 8; ++m) out->coef[base + j * 8 + m] = cf[m];
-                if (kDeg == 8) out->coef[base + nfunc * 8 + j] = cf[8];
+                for (int m = 0; m < nc; ++m) out->coef[base + j * nc + m] = cf[m];
+                if (bf.lo) out->coef[base + nfunc * nc + j] = cf[kDegLo];
+                else if (kDeg == 8) out->coef[base + nfunc * 8 + j] = cf[8];
             }
+            off += size_t(ps);
+            out->npieces += 1;
         }
-        npieces += 1 << bf.level;
     }
-    out->npieces = npieces;
+    if (off >= (size_t(1) << 26)) fail(1, "coefficient table too large");
 }
 
 void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t)>& body) {

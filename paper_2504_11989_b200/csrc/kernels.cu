@@ -65,7 +65,7 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     b += align16(sizeof(double) * P.n_direct);
     b += align16(sizeof(double) * P.n_rec * ((P.d + 1) & ~1));
     b += align16(sizeof(double) * P.n_rec);
-    b += align16(sizeof(double) * size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
+    b += align16(sizeof(double) * size_t(P.tab.ncoef));
     b += align16(sizeof(int) * P.tab.nbins);
     b += align16(sizeof(double) * size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
     return b;
@@ -119,7 +119,7 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         double* rn = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_rec);
         double* cf = reinterpret_cast<double*>(smem + off);
-        off += align16(sizeof(double) * size_t(P.tab.npieces) * piece_stride(P.tab.nfunc));
+        off += align16(sizeof(double) * size_t(P.tab.ncoef));
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
@@ -146,11 +146,12 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         mbar_wait(bar, 0);
         // directory relocated for the shared copy: the high word of 2^L in bits 20-30 and the
         // shared byte address of the bin's first piece in bits 0-19 (the 227 KB window fits)
+        // (bit 31: low-degree bin)
         const uint32_t cf_addr = uint32_t(__cvta_generic_to_shared(cf));
-        const uint32_t pbytes = uint32_t(sizeof(double) * piece_stride(P.tab.nfunc));
         for (int i = threadIdx.x; i < P.tab.nbins; i += blockDim.x) {
             const int e = td[i];
-            td[i] = int((uint32_t(1023 + (e & 15)) << 20) | (cf_addr + uint32_t(e >> 4) * pbytes));
+            td[i] = int((uint32_t((e >> 4) & 1) << 31) | (uint32_t(1023 + (e & 15)) << 20) |
+                        (cf_addr + uint32_t(e >> 5) * 8u));
         }
         (void)tc;
         __syncthreads();
@@ -284,29 +285,52 @@ constexpr double kMagic = 6755399441055744.0;
 template <int NF, bool SMEM>
 __device__ __forceinline__ void tab_piece(const View& V, double xb, double tb, int e, double (&f)[NF]) {
     constexpr int PS = piece_stride(NF);
+    constexpr int PSL = piece_stride_lo(NF);
     // 2^L from its exponent bits (no conversion); SMEM directory entries carry them pre-shifted
     const int hi = SMEM ? (e & 0x7ff00000) : ((1023 + (e & 15)) << 20);
+    const bool lo = SMEM ? (e < 0) : ((e >> 4) & 1);
     const double two_l = __hiloint2double(hi, 0);
     const double a = fma(xb - (tb - kMagic), two_l, -0.5);  // fs - 1/2
     const double ts = a + kMagic;
     const int sub = __double2loint(ts);
     const TauPowers tp = tau_powers(a - (ts - kMagic));
-    double2 c[PS / 2];
-    if constexpr (SMEM) {
-        const uint32_t addr = uint32_t(e & 0xfffff) + uint32_t(sub) * uint32_t(PS * 8);
+    if (lo) {
+        // degree-4 bin (terms already below the cutoff scale up to 1e-10 relative accuracy)
+        double2 c[PSL / 2];
+        if constexpr (SMEM) {
+            const uint32_t addr = uint32_t(e & 0xfffff) + uint32_t(sub) * uint32_t(PSL * 8);
 #pragma unroll
-        for (int m = 0; m < PS / 2; ++m) c[m] = lds_f64x2(addr + 16u * m);
+            for (int m = 0; m < PSL / 2; ++m) c[m] = lds_f64x2(addr + 16u * m);
+        } else {
+            const double2* g = reinterpret_cast<const double2*>(V.coef + size_t(e >> 5) + size_t(sub) * PSL);
+#pragma unroll
+            for (int m = 0; m < PSL / 2; ++m) c[m] = g[m];
+        }
+        const double* cd = reinterpret_cast<const double*>(c);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const double cc[5] = {cd[j * kDegLo + 0], cd[j * kDegLo + 1], cd[j * kDegLo + 2], cd[j * kDegLo + 3],
+                                  cd[NF * kDegLo + j]};
+            f[j] = estrin_lo(cc, tp);
+        }
     } else {
-        const double2* g = reinterpret_cast<const double2*>(V.coef + size_t((e >> 4) + sub) * PS);
+        double2 c[PS / 2];
+        if constexpr (SMEM) {
+            const uint32_t addr = uint32_t(e & 0xfffff) + uint32_t(sub) * uint32_t(PS * 8);
 #pragma unroll
-        for (int m = 0; m < PS / 2; ++m) c[m] = g[m];
-    }
-    const double* cd = reinterpret_cast<const double*>(c);
+            for (int m = 0; m < PS / 2; ++m) c[m] = lds_f64x2(addr + 16u * m);
+        } else {
+            const double2* g = reinterpret_cast<const double2*>(V.coef + size_t(e >> 5) + size_t(sub) * PS);
 #pragma unroll
-    for (int j = 0; j < NF; ++j) {
-        const double cc[9] = {cd[j * 8 + 0], cd[j * 8 + 1], cd[j * 8 + 2], cd[j * 8 + 3], cd[j * 8 + 4],
-                              cd[j * 8 + 5], cd[j * 8 + 6], cd[j * 8 + 7], kDeg == 8 ? cd[NF * 8 + j] : 0.0};
-        f[j] = estrin(cc, tp);
+            for (int m = 0; m < PS / 2; ++m) c[m] = g[m];
+        }
+        const double* cd = reinterpret_cast<const double*>(c);
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const double cc[9] = {cd[j * 8 + 0], cd[j * 8 + 1], cd[j * 8 + 2], cd[j * 8 + 3], cd[j * 8 + 4],
+                                  cd[j * 8 + 5], cd[j * 8 + 6], cd[j * 8 + 7], kDeg == 8 ? cd[NF * 8 + j] : 0.0};
+            f[j] = estrin(cc, tp);
+        }
     }
 }
 

@@ -29,6 +29,14 @@ __host__ __device__
 #endif
 constexpr int piece_stride(int nf) { return kDeg == 8 ? nf * 8 + ((nf + 1) & ~1) : nf * 8; }
 constexpr double kBinWidth = kDeg == 8 ? 0.25 : 0.125;  // directory bin width in x = c |y|^2
+// Low-degree pieces for bins where the terms are already small (see context.cpp build_table):
+// degree 4, layout c0..c3 of each function then c4 of every function (padded to even).
+constexpr int kDegLo = 4;
+constexpr double kLoBudget = 0.1;   // error budget of low-degree bins, in units of the cutoff
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int piece_stride_lo(int nf) { return nf * kDegLo + ((nf + 1) & ~1); }
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
 constexpr int kT0 = 64;             // max terms of the q = 0 power series
 
@@ -51,9 +59,9 @@ struct CtxConst {
 // Piecewise-polynomial table of up to 4 functions f_j(x) = scale_j E_{p_j}(x),
 // sharing one directory over x in [x_lo, x_hi).
 struct DevTable {
-    const int* dir;        // nbins entries: (first_piece << 4) | L ; L == 15 -> direct
+    const int* dir;        // nbins entries: (first coefficient offset << 5) | lo << 4 | L ; L == 15 -> direct
     const double* coef;    // [piece][piece_stride(nfunc)], monomials in delta in [-1/2, 1/2]
-    int nbins, nfunc, npieces, pad_;
+    int nbins, nfunc, npieces, ncoef;   // ncoef: doubles in coef (pieces have two strides)
     double x_lo, inv_hb, x_hi;
     double c, r_scale, x_off;  // x = c rho;  bin coordinate xb = rho * r_scale - x_off
     double r_off;              // x_lo / c:  xb = (rho - r_off) * r_scale (in-cell lookup)
@@ -144,7 +152,8 @@ struct HostTable {
     int nbins = 0, nfunc = 0, npieces = 0;
     double x_lo = 0, inv_hb = 0, x_hi = 0;
     double p[4] = {0, 0, 0, 0}, scale[4] = {0, 0, 0, 0};
-    double max_rel_err = 0;   // measured during the build
+    double max_rel_err = 0;   // measured during the build (degree-kDeg pieces)
+    int n_lo_bins = 0;        // bins with degree-kDegLo pieces
 };
 
 // Degree-kDeg polynomial in Estrin form: dependency depth 3-4 instead of 7-8, and the
@@ -177,6 +186,15 @@ inline double estrin(const double* c, const TauPowers& p) {
     const double e0 = fma(b1, p.t4, b0);
     if (kDeg == 8) return fma(c[8], p.t8, e0);
     return e0;
+}
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline double estrin_lo(const double* c, const TauPowers& p) {  // degree 4
+    const double a0 = fma(c[1], p.t1, c[0]);
+    const double a1 = fma(c[3], p.t1, c[2]);
+    const double b0 = fma(a1, p.t2, a0);
+    return fma(c[4], p.t4, b0);
 }
 
 // Errors raised by the host builder carry an lz status code.
