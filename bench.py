@@ -186,7 +186,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2504_11989_b200 import _native as N
     from paper_2504_11989_b200 import named_lattice
-    from paper_2504_11989_b200.distributed import ShardedIntegral, atm_energy_distributed
+    from paper_2504_11989_b200.distributed import ShardedIntegral, allreduce_partials, atm_energy_distributed
     from paper_2504_11989_b200.epstein import epstein_context
     from paper_2504_11989_b200.manybody import ATMGrid
     from paper_2504_11989_b200.quadrature import Plan, atm_plan, product_plan
@@ -204,7 +204,7 @@ def run_ours(args):
         if evs:
             evs[1].record(stream)
         if world > 1:
-            dist.all_reduce(S.partials)
+            allreduce_partials(S.partials)  # C ABI: one ncclAllReduce on this stream
         Plan.reduce_device(S.partials, S.n_tiles, S.ncomp, S.out)
         if evs:
             evs[2].record(stream)

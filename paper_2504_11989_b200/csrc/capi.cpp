@@ -1287,8 +1287,10 @@ int lz_allreduce_partials(double* partials, int64_t n, void* nccl_comm, void* st
         //                            ncclComm_t, cudaStream_t);  ncclDouble = 8, ncclSum = 0
         using AllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
         using ErrFn = const char* (*)(int);
+        using AsyncErrFn = int (*)(void*, int*);
         static AllReduceFn all_reduce = nullptr;
         static ErrFn err_string = nullptr;
+        static AsyncErrFn async_err = nullptr;
         static std::once_flag once;
         std::call_once(once, [] {
             // prefer the NCCL already mapped into the process (it created the communicator)
@@ -1297,10 +1299,19 @@ int lz_allreduce_partials(double* partials, int64_t n, void* nccl_comm, void* st
             if (!h) return;
             all_reduce = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
             err_string = reinterpret_cast<ErrFn>(dlsym(h, "ncclGetErrorString"));
+            async_err = reinterpret_cast<AsyncErrFn>(dlsym(h, "ncclCommGetAsyncError"));
         });
         if (!all_reduce) throw Error{LZ_ENCCL, "NCCL (libnccl.so.2) is not available in this process"};
         if (n == 0) return;
-        const int rc = all_reduce(partials, partials, size_t(n), 8, 0, nccl_comm, (cudaStream_t)stream);
+        constexpr int kInProgress = 7;  // ncclInProgress (non-blocking communicators)
+        int rc = all_reduce(partials, partials, size_t(n), 8, 0, nccl_comm, (cudaStream_t)stream);
+        // a non-blocking communicator enqueues in the background: wait until the collective is
+        // on the stream, so the reduction kernel that follows is ordered after it
+        while (rc == kInProgress && async_err) {
+            int state = kInProgress;
+            if (async_err(nccl_comm, &state) != 0) break;
+            rc = state;
+        }
         if (rc != 0)
             throw Error{LZ_ENCCL, std::string("ncclAllReduce: ") + (err_string ? err_string(rc) : std::to_string(rc))};
     });

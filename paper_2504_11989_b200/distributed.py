@@ -11,6 +11,8 @@ ThreadPoolExecutor over Duffy cells (L/quadrature.py:482-486).
 """
 from __future__ import annotations
 
+import warnings
+
 import torch
 import torch.distributed as dist
 
@@ -47,9 +49,14 @@ def allreduce_partials(partials: torch.Tensor, group=None, stream=None) -> None:
     if comm:
         from . import _native as N
         st = stream if stream is not None else torch.cuda.current_stream(partials.device).cuda_stream
-        N.check(N.lib().lz_allreduce_partials(partials.data_ptr(), partials.numel(), comm, st), "all-reduce")
-    else:
-        dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+        rc = N.lib().lz_allreduce_partials(partials.data_ptr(), partials.numel(), comm, st)
+        if rc == N.LZ_OK:
+            return
+        if rc != N.LZ_ENCCL:
+            N.check(rc, "all-reduce")
+        # NCCL could not be resolved or refused the call before enqueueing: torch's collective
+        warnings.warn(f"lz_allreduce_partials unavailable ({N.last_error()}); using dist.all_reduce")
+    dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
 
 
 def _world(group=None):
