@@ -576,8 +576,6 @@ struct GridArrays {
     double* wu = nullptr;
     double* v = nullptr;
     double* wv = nullptr;
-    double* wpart = nullptr;        // warp partials of the tile kernel (scratch)
-    unsigned int* tcount = nullptr;  // per-tile arrival counters (zeroed once; kernels leave 0)
 };
 
 // Per-device scratch for the host-buffer entry points: one non-blocking stream,
@@ -658,7 +656,6 @@ struct lz_plan {
     lz::DevPlan P;
     std::vector<void*> allocs;
     mutable std::mutex mu;
-    mutable std::map<std::tuple<int, int, int, double>, GridArrays> grids;
 };
 
 namespace {
@@ -686,12 +683,16 @@ void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
     dg->tile_hi = g->tile_hi > 0 ? std::min(g->tile_hi, n_tiles) : n_tiles;
 }
 
+// Quadrature node arrays on the device, cached process-wide per (device, d, n_u, n_v, grading,
+// u_lo): read-only and shared by every plan, so a cold plan does not re-upload them.
 const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
-    std::lock_guard<std::mutex> lock(plan->mu);
-    auto key = std::make_tuple(g->n_u, plan->d > 1 ? g->n_v : 1, g->grading, g->u_lo);
-    auto it = plan->grids.find(key);
-    if (it != plan->grids.end()) return it->second;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int, double>, GridArrays> cache;
     const int d = plan->d;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple(plan->device, d, g->n_u, d > 1 ? g->n_v : 1, g->grading, g->u_lo);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     std::vector<double> x, w;
     lz::gauss_legendre(g->n_u, &x, &w);
     std::vector<double> u(g->n_u), wu(g->n_u);
@@ -719,7 +720,7 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
         wv.assign(1, 1.0);
     }
     GridArrays ga;
-    std::vector<void*>& allocs = const_cast<std::vector<void*>&>(plan->allocs);
+    std::vector<void*> allocs;  // process lifetime
     std::vector<double> all;
     all.reserve(2 * (u.size() + v.size()));
     all.insert(all.end(), u.begin(), u.end());
@@ -731,21 +732,36 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
     ga.wu = dev + u.size();
     ga.v = dev + 2 * u.size();
     ga.wv = dev + 2 * u.size() + v.size();
-    {
-        lz::DevGrid tmp;
-        lz_grid full = *g;
-        full.tile_lo = full.tile_hi = 0;
-        fill_grid(d, &full, &tmp);
-        const size_t n_tiles = size_t((tmp.n_patch + 7) / 8);
-        const size_t wbytes = n_tiles * 8 * 2 * sizeof(double), cbytes = n_tiles * sizeof(unsigned int);
-        void* scratch = nullptr;
-        check_cuda(cudaMalloc(&scratch, wbytes + cbytes), "cudaMalloc");
-        allocs.push_back(scratch);
-        ga.wpart = static_cast<double*>(scratch);
-        ga.tcount = reinterpret_cast<unsigned int*>(static_cast<unsigned char*>(scratch) + wbytes);
-        check_cuda(cudaMemset(ga.tcount, 0, cbytes), "cudaMemset");
+    return cache.emplace(key, ga).first->second;
+}
+
+// Tile-kernel scratch (warp partials + per-tile arrival counters) per (device, stream): kernels on
+// one stream are serialised, so they can share it; grown stream-ordered (cudaMallocAsync /
+// cudaFreeAsync from the device's memory pool), counters zeroed on growth and left zero by every
+// completed launch.
+void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, unsigned int** tcount) {
+    struct Scratch {
+        double* wpart = nullptr;
+        unsigned int* tcount = nullptr;
+        int64_t cap = 0;
+    };
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, Scratch> pool;
+    std::lock_guard<std::mutex> lock(mu);
+    Scratch& s = pool[std::make_pair(device, st)];
+    if (s.cap < n_tiles) {
+        if (s.wpart) check_cuda(cudaFreeAsync(s.wpart, st), "cudaFreeAsync");
+        const size_t wbytes = size_t(n_tiles) * 8 * 2 * sizeof(double);
+        const size_t cbytes = size_t(n_tiles) * sizeof(unsigned int);
+        void* p = nullptr;
+        check_cuda(cudaMallocAsync(&p, wbytes + cbytes, st), "cudaMallocAsync");
+        s.wpart = static_cast<double*>(p);
+        s.tcount = reinterpret_cast<unsigned int*>(static_cast<unsigned char*>(p) + wbytes);
+        check_cuda(cudaMemsetAsync(s.tcount, 0, cbytes, st), "cudaMemsetAsync");
+        s.cap = n_tiles;
     }
-    return plan->grids.emplace(key, ga).first->second;
+    *wpart = s.wpart;
+    *tcount = s.tcount;
 }
 
 // Lanes per point for the batch kernel: the smallest power of two that gives ~192 lanes per SM
@@ -1144,9 +1160,14 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
         dgd.wu = ga.wu;
         dgd.v = ga.v;
         dgd.wv = ga.wv;
-        dgd.wpart = ga.wpart;
-        dgd.tcount = ga.tcount;
         cudaStream_t st = (cudaStream_t)stream;
+        {
+            lz_grid full = *g;
+            full.tile_lo = full.tile_hi = 0;
+            lz::DevGrid tmp;
+            fill_grid(pl->d, &full, &tmp);
+            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, &dgd.wpart, &dgd.tcount);
+        }
         if (pl->kind == 0)
             check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");
         else

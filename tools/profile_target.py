@@ -90,8 +90,12 @@ def e2e_breakdown():
         t1 = time.perf_counter()
         plan = atm_plan(fcc)
         t2 = time.perf_counter()
+        t2a = time.perf_counter()
+        plan.tiles(128, 128, 3)
+        t2b = time.perf_counter()
         s = ShardedIntegral(plan, 128, 128, 3)
         t3 = time.perf_counter()
+        print(f"   tiles {1e3*(t2b-t2a):.2f} ms, ShardedIntegral {1e3*(t3-t2b):.2f} ms")
         out = s.run().cpu().numpy()
         t4 = time.perf_counter()
         out = s.run().cpu().numpy()
