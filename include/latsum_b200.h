@@ -128,6 +128,19 @@ int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, doubl
 /* whole integral through host memory: out[ncomp] (value sums before the 2^d factor) */
 int lz_plan_integrate_host(const lz_plan* plan, const lz_grid* g, double* out);
 
+/* -- order-m derivatives at arbitrary k (the k != 0 generalisation of
+ * the reference's derivative tables L/epstein.py:347-415, same Hermite expansion and point-set
+ * rules): out[i * n_alpha + j] = d^alpha_j Z(k_i) for every multi-index |alpha| = order
+ * (1 <= order <= 4, d <= 3) in the order of lz_multi_indices (L/epstein.py:426-433, head
+ * ascending).  The polynomial-weighted zeta is M^alpha = sum'_z z^alpha |z|^-nu e^{-2 pi i k.z}
+ * = d^alpha Z / (-2 pi i)^order.  k is reduced into the cell; k in the reciprocal lattice sets
+ * status bit 1 (LZ_EPOLE from the host entry point).  lz_zeta_derivatives takes device pointers
+ * and is stream-ordered. */
+int lz_multi_indices(int d, int order, int* alphas, int64_t cap, int64_t* n);
+int lz_zeta_derivatives(const lz_ctx* ctx, int order, const double* k, int64_t n, double* out, int* status,
+                        void* stream);
+int lz_zeta_derivatives_host(const lz_ctx* ctx, int order, const double* k, int64_t n, double* out);
+
 /* -- Taylor table of Z_reg at k = 0: EpsteinContext.reg_derivatives (L/epstein.py:347-415).
  * Writes n multi-indices (alphas, n x d ints) with |alpha| even <= order and their values;
  * copies min(cap, n) entries, returns n through *n. */

@@ -500,6 +500,100 @@ int orc_hessian(int d, const double* a, double nu, const double* k, long n, doub
     return 0;
 }
 
+/* ---------------------------------------------------------------- order-m derivatives at k
+ * d^alpha Z(k), |alpha| = m >= 1, from the split differentiated term by term (the k != 0
+ * generalisation of L/epstein.py:376-414: direct sum weighted by z^alpha, reciprocal Hermite
+ * expansion with F^(p)(rho) = (-1)^p rho^{-s-p} Gamma(s+p, pi rho / t), q = 0 unsplit).
+ * Multi-indices in the order of L/epstein.py:426-433 (head ascending). */
+static int multi_rec(int d, int total, int* cur, int pos, int* out, int cnt) {
+    if (pos == d - 1) {
+        cur[pos] = total;
+        for (int a = 0; a < d; ++a) out[cnt * d + a] = cur[a];
+        return cnt + 1;
+    }
+    for (int h = 0; h <= total; ++h) {
+        cur[pos] = h;
+        cnt = multi_rec(d, total - h, cur, pos + 1, out, cnt);
+    }
+    return cnt;
+}
+
+int orc_multi_indices(int d, int order, int* out) {
+    int cur[MAXD];
+    return multi_rec(d, order, cur, 0, out, 0);
+}
+
+typedef struct {
+    const OCtx* c;
+    int order, na, nd, nr;
+    const int* alphas;
+    const R *dz, *dw, *rq;
+    const double* k;
+    double* out;
+} DArgs;
+
+static R fact_l(int n) { R f = 1.0L; for (int i = 2; i <= n; ++i) f *= i; return f; }
+
+static void deriv_body(long i, void* p) {
+    DArgs* A = (DArgs*)p;
+    const OCtx* c = A->c;
+    int d = c->d, m = A->order;
+    R k[MAXD];
+    for (int a = 0; a < d; ++a) k[a] = A->k[i * d + a];
+    R twopim = powl(2.0L * PI_L, (R)m);
+    for (int j = 0; j < A->na; ++j) {
+        const int* al = A->alphas + j * d;
+        R dsum = 0.0L, rsum = 0.0L;
+        for (int t = 0; t < A->nd; ++t) {
+            R ph = 0.0L, za = 1.0L;
+            for (int a = 0; a < d; ++a) {
+                ph += k[a] * A->dz[t * d + a];
+                for (int e = 0; e < al[a]; ++e) za *= A->dz[t * d + a];
+            }
+            dsum += A->dw[t] * za * cosl(2.0L * PI_L * ph + m * PI_L / 2.0L);
+        }
+        for (int t = -1; t < A->nr; ++t) {
+            R y[MAXD], r2 = 0.0L;
+            for (int a = 0; a < d; ++a) { y[a] = k[a] + (t >= 0 ? A->rq[t * d + a] : 0.0L); r2 += y[a] * y[a]; }
+            R x = PI_L * r2 / c->t;
+            /* Hermite terms: j_a <= alpha_a / 2 */
+            int jm[MAXD], cnt = 1;
+            for (int a = 0; a < d; ++a) { jm[a] = al[a] / 2; cnt *= jm[a] + 1; }
+            for (int q = 0; q < cnt; ++q) {
+                int rem = q, js = 0, jj[MAXD];
+                for (int a = 0; a < d; ++a) { jj[a] = rem % (jm[a] + 1); rem /= jm[a] + 1; js += jj[a]; }
+                R coef = 1.0L;
+                for (int a = 0; a < d; ++a) {
+                    coef *= fact_l(al[a]) / (fact_l(jj[a]) * fact_l(al[a] - 2 * jj[a]));
+                    for (int e = 0; e < al[a] - 2 * jj[a]; ++e) coef *= 2.0L * y[a];
+                }
+                int pp = m - js;
+                R fp = ((pp & 1) ? -1.0L : 1.0L) * powl(r2, -(c->s + pp)) * orc_upper_gamma_l(c->s + pp, x);
+                rsum += coef * fp;
+            }
+        }
+        A->out[i * A->na + j] = (double)(c->pref * (2.0L * twopim * dsum + c->rfac * rsum));
+    }
+}
+
+int orc_derivatives(int d, const double* a, double nu, int order, const double* k, long n, double* out) {
+    OCtx c;
+    int rc = octx_init(&c, d, a, nu, 0);
+    if (rc) { octx_free(&c); return rc; }
+    if (order < 1 || c.branch == 2) { octx_free(&c); return 1; }
+    R *dz = NULL, *dw = NULL, *rq = NULL;
+    int nd = enum_direct(&c, order, 1e-20L, &dz, &dw, NULL);
+    int nr = enum_recip(&c, c.s + order, 1e-20L, &rq);
+    if (nd < 0 || nr < 0) { free(dz); free(dw); free(rq); octx_free(&c); return 6; }
+    int alph[64 * MAXD];
+    int na = orc_multi_indices(d, order, alph);
+    DArgs A = {&c, order, na, nd, nr, alph, dz, dw, rq, k, out};
+    par_for(n, deriv_body, &A);
+    free(dz); free(dw); free(rq);
+    octx_free(&c);
+    return 0;
+}
+
 /* Gauss-Legendre on [-1,1] (Newton, long double), ascending */
 static void gl(int n, R* x, R* w) {
     for (int i = 0; i < n; ++i) {

@@ -35,6 +35,8 @@ def lib():
         D = C.POINTER(C.c_double)
         L.orc_zeta.argtypes = [C.c_int, D, C.c_double, D, C.c_long, D, C.c_int]
         L.orc_hessian.argtypes = [C.c_int, D, C.c_double, D, C.c_long, D]
+        L.orc_derivatives.argtypes = [C.c_int, D, C.c_double, C.c_int, D, C.c_long, D]
+        L.orc_multi_indices.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.orc_product_grid.argtypes = [C.c_int, D, D, C.c_int, C.c_int, C.c_int, C.c_int, C.c_long,
                                        C.c_long, D]
         L.orc_atm_grid.argtypes = [C.c_int, D, C.c_int, C.c_int, C.c_int, C.c_long, C.c_long, D]
@@ -79,6 +81,25 @@ def hessian(a, nu, k):
     k = np.ascontiguousarray(np.atleast_2d(np.asarray(k, dtype=np.float64)))
     out = np.empty((len(k), d, d))
     rc = lib().orc_hessian(d, _p(a), float(nu), _p(k), len(k), _p(out))
+    if rc:
+        raise RuntimeError(f"oracle error {rc}")
+    return out
+
+
+def multi_indices(d, order):
+    buf = (C.c_int * (64 * 4))()
+    n = lib().orc_multi_indices(d, order, buf)
+    return [tuple(buf[i * d:(i + 1) * d]) for i in range(n)]
+
+
+def derivatives(a, nu, order, k):
+    """All d^alpha Z(k), |alpha| = order, in multi_indices(d, order) order (long double)."""
+    a = _mat(a)
+    d = a.shape[0]
+    k = np.ascontiguousarray(np.atleast_2d(np.asarray(k, dtype=np.float64)))
+    na = len(multi_indices(d, order))
+    out = np.empty((len(k), na))
+    rc = lib().orc_derivatives(d, _p(a), float(nu), int(order), _p(k), len(k), _p(out))
     if rc:
         raise RuntimeError(f"oracle error {rc}")
     return out

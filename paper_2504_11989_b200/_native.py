@@ -21,7 +21,7 @@ LIB_DIR = os.path.join(_HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblatsum_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
-SOURCES = ["kernels.cu", "direct.cu", "context.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "direct.cu", "deriv.cu", "context.cpp", "capi.cpp"]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-ldl"]
@@ -84,6 +84,9 @@ SIGNATURES = {
     "lz_plan_integrate": (C.c_int, [_P, C.POINTER(Grid), _P, C.c_int, _P]),
     "lz_reduce_partials": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
     "lz_plan_integrate_host": (C.c_int, [_P, C.POINTER(Grid), _D]),
+    "lz_multi_indices": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int64, C.POINTER(C.c_int64)]),
+    "lz_zeta_derivatives": (C.c_int, [_P, C.c_int, _P, C.c_int64, _P, _P, _P]),
+    "lz_zeta_derivatives_host": (C.c_int, [_P, C.c_int, _D, C.c_int64, _D]),
     "lz_ctx_reg_derivatives": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
                                           C.POINTER(C.c_int64)]),
     "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
@@ -112,12 +115,32 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIB_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, *srcs, "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if verbose:
-        print(res.stdout + res.stderr)
+    # one nvcc per translation unit, in parallel, then one link (same flags as a single call)
+    from concurrent.futures import ThreadPoolExecutor
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-ldl")]
+    objs = [os.path.join(LIB_DIR, os.path.basename(src) + f".{os.getpid()}.o") for src in srcs]
+
+    def compile_one(pair):
+        src, obj = pair
+        cmd = [nvcc, *compile_flags, "-c", src, "-o", obj]
+        return cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    try:
+        with ThreadPoolExecutor(max_workers=len(srcs)) as pool:
+            results = list(pool.map(compile_one, zip(srcs, objs)))
+        for cmd, res in results:
+            if res.returncode != 0:
+                raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+            if verbose:
+                print(res.stdout + res.stderr)
+        cmd = [nvcc, *NVCC_FLAGS, *objs, "-o", tmp]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc link failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

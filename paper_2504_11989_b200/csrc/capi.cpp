@@ -33,6 +33,9 @@ cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, 
 cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                        cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st);
+cudaError_t launch_deriv(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st);
+int deriv_count(int d, int order);
+int deriv_nfunc(int order);
 cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cudaStream_t st);
 cudaError_t launch_direct(int d, int kind, int64_t L, int64_t npts, const double* A, const double* nus,
                           double* partials, int64_t nblocks, cudaStream_t st);
@@ -645,6 +648,9 @@ struct lz_ctx {
     HostPlan plain, hessp;
     lz::DevPlan dplain, dhess;
     std::vector<void*> allocs;
+    // order-m derivative plans (deriv.cu), built on first use
+    std::map<int, lz::DevDeriv> dderiv;
+    std::map<int, lz::HostTable> dtab;
 };
 
 struct lz_plan {
@@ -1058,6 +1064,180 @@ int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* ou
         check_cuda(cudaMemcpyAsync(A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st), "d2h");
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, ob);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Multi-indices |alpha| = order in the reference's order (L/epstein.py:426-433, head ascending);
+// the kernel's compile-time list (deriv.cu DerivSpec) enumerates the same way.
+std::vector<int> multi_indices(int d, int order) {
+    std::vector<int> out;
+    int total = 1;
+    for (int a = 0; a < d; ++a) total *= order + 1;
+    std::vector<int> cur(d);
+    for (int c = 0; c < total; ++c) {
+        int rem = c, sum = 0;
+        for (int a = d - 1; a >= 0; --a) {
+            cur[a] = rem % (order + 1);
+            rem /= order + 1;
+            sum += cur[a];
+        }
+        if (sum == order) out.insert(out.end(), cur.begin(), cur.end());
+    }
+    return out;
+}
+
+// Order-m derivative plan of a context: direct weights 2 (2 pi)^m w z^alpha, reciprocal points
+// sorted by |q|, tables of F^{(j)} = (-1)^j c^{s+j} E_{1-s-j}, j = ceil(m/2) .. m.
+const lz::DevDeriv& ensure_deriv(const lz_ctx* cc, int order) {
+    lz_ctx* c = const_cast<lz_ctx*>(cc);
+    std::lock_guard<std::mutex> lock(c->mu);
+    auto it = c->dderiv.find(order);
+    if (it != c->dderiv.end()) return it->second;
+    const lz::HostCtx& h = c->h;
+    const int d = h.d;
+    if (h.k.branch == lz::kTrivial) throw Error{LZ_EINVAL, "derivatives of a trivial-branch zeta are zero"};
+    std::vector<double> dir_n, rec_n;
+    lz::build_deriv_sets(h, order, &dir_n, &rec_n);
+    const std::vector<int> alphas = multi_indices(d, order);
+    const int na = int(alphas.size()) / d;
+    const size_t nd = dir_n.size() / d;
+    std::vector<double> W(nd * na);
+    const ld twopi_m = std::pow(2.0L * ld(lz::kPi), ld(order));
+    for (size_t i = 0; i < nd; ++i) {
+        ld z[lz::kMaxDim];
+        const ld w = direct_weight(h, &dir_n[i * d], z);
+        for (int j = 0; j < na; ++j) {
+            ld v = 2.0L * twopi_m * w;
+            for (int a = 0; a < d; ++a)
+                for (int e = 0; e < alphas[j * d + a]; ++e) v *= z[a];
+            W[i * na + j] = double(v);
+        }
+    }
+    const size_t nr = rec_n.size() / d;
+    std::vector<double> q(nr * d);
+    std::vector<ld> qn(nr);
+    for (size_t i = 0; i < nr; ++i) {
+        ld r2 = 0.0L;
+        for (int a = 0; a < d; ++a) {
+            ld v = 0.0L;
+            for (int b = 0; b < d; ++b) v += ld(h.B[a * d + b]) * rec_n[i * d + b];
+            q[i * d + a] = double(v);
+            r2 += v * v;
+        }
+        qn[i] = std::sqrt(r2);
+    }
+    std::vector<size_t> ord(nr);
+    for (size_t i = 0; i < nr; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return qn[a] < qn[b]; });
+    std::vector<double> rq(nr * d), rn(nr);
+    for (size_t i = 0; i < nr; ++i) {
+        for (int a = 0; a < d; ++a) rq[i * d + a] = q[ord[i] * d + a];
+        rn[i] = double(qn[ord[i]]);
+    }
+    const int j0 = (order + 1) / 2, nf = lz::deriv_nfunc(order);
+    double p[4], sc[4];
+    const ld cl = ld(lz::kPi) / ld(h.k.split);
+    for (int j = 0; j < nf; ++j) {
+        const int jj = j0 + j;
+        p[j] = 1.0 - h.k.s - jj;
+        sc[j] = double(((jj & 1) ? -1.0L : 1.0L) * std::pow(cl, ld(h.k.s) + jj));
+    }
+    lz::HostTable& tab = c->dtab[order];
+    const double rp = std::fabs(h.k.rfac * h.k.pref);
+    if (nr > 0) lz::build_table(p, sc, nf, double(cl), lz::table_x_lo(h), rp, &tab, std::max(1.0, order / 2.0));
+    else tab.nfunc = nf;
+    lz::DevDeriv P;
+    std::memset(&P, 0, sizeof(P));
+    P.d = d;
+    P.order = order;
+    P.n_dir = int(nd);
+    P.n_rec = int(nr);
+    std::memcpy(P.A, h.A, sizeof(P.A));
+    std::memcpy(P.B, h.B, sizeof(P.B));
+    P.pref = h.k.pref;
+    P.rfac = h.k.rfac;
+    P.r_cut = nr > 0 ? double(std::sqrt(ld(tab.x_hi) / cl) * (1.0L + 1e-9L)) : 0.0;
+    {
+        DeviceGuard dg(c->device);
+        P.dir_n = upload(dir_n, &c->allocs);
+        P.dir_w = upload(W, &c->allocs);
+        P.rec_q = upload(rq, &c->allocs);
+        P.rec_norm = upload(rn, &c->allocs);
+        P.tab.dir = upload(tab.dir, &c->allocs);
+        P.tab.coef = upload(tab.coef, &c->allocs);
+    }
+    P.tab.nbins = tab.nbins;
+    P.tab.nfunc = nf;
+    P.tab.npieces = tab.npieces;
+    P.tab.ncoef = int(tab.coef.size());
+    P.tab.x_lo = tab.x_lo;
+    P.tab.inv_hb = tab.inv_hb;
+    P.tab.x_hi = tab.x_hi;
+    P.tab.c = double(cl);
+    P.tab.r_scale = double(cl) * tab.inv_hb;
+    P.tab.x_off = tab.x_lo * tab.inv_hb;
+    P.tab.nbins_d = double(tab.nbins);
+    for (int j = 0; j < nf; ++j) {
+        P.tab.p[j] = p[j];
+        P.tab.scale[j] = sc[j];
+    }
+    return c->dderiv.emplace(order, P).first->second;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lz_multi_indices(int d, int order, int* alphas, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        if (d < 1 || d > 4 || order < 0) throw Error{LZ_EINVAL, "bad dimension or order"};
+        const std::vector<int> a = multi_indices(d, order);
+        *n = int64_t(a.size()) / d;
+        for (int64_t i = 0; i < std::min<int64_t>(cap, *n) * d; ++i) alphas[i] = a[size_t(i)];
+    });
+}
+
+int lz_zeta_derivatives(const lz_ctx* c, int order, const double* k, int64_t n, double* out, int* status,
+                        void* stream) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
+        if (order < 1 || order > 4 || c->h.d > 3) throw Error{LZ_EINVAL, "derivative order must be 1..4 (d <= 3)"};
+        const lz::DevDeriv& P = ensure_deriv(c, order);
+        DeviceGuard dg(c->device);
+        check_cuda(lz::launch_deriv(P, k, n, out, status, (cudaStream_t)stream), "derivative kernel");
+    });
+}
+
+int lz_zeta_derivatives_host(const lz_ctx* c, int order, const double* k, int64_t n, double* out) {
+    return guarded([&] {
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
+        if (order < 1 || order > 4 || c->h.d > 3) throw Error{LZ_EINVAL, "derivative order must be 1..4 (d <= 3)"};
+        for (int64_t i = 0; i < n * c->h.d; ++i)
+            if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
+        if (n == 0) return;
+        const lz::DevDeriv& P = ensure_deriv(c, order);
+        DeviceGuard dg(c->device);
+        const int d = c->h.d, na = lz::deriv_count(d, order);
+        Arena& A = arena(c->device);
+        std::lock_guard<std::mutex> lock(A.mu);
+        const size_t kb = sizeof(double) * size_t(n) * d, ob = sizeof(double) * size_t(n) * na;
+        A.ensure(al256(kb) + al256(ob) + 256, std::max(kb, ob) + 256);
+        double* dk = reinterpret_cast<double*>(A.dbuf);
+        double* dout = reinterpret_cast<double*>(A.dbuf + al256(kb));
+        int* dstat = reinterpret_cast<int*>(A.dbuf + al256(kb) + al256(ob));
+        check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
+        h2d(dk, k, kb, A.hbuf, A.st);
+        check_cuda(lz::launch_deriv(P, dk, n, dout, dstat, A.st), "derivative kernel");
+        check_cuda(cudaMemcpyAsync(A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st), "d2h");
+        int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
+        check_cuda(cudaMemcpyAsync(hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, A.st), "d2h");
+        check_cuda(cudaStreamSynchronize(A.st), "sync");
+        std::memcpy(out, A.hbuf, ob);
+        if (*hstat & 1) throw Error{LZ_EPOLE, "derivatives of Z are singular at k in the reciprocal lattice"};
     });
 }
 

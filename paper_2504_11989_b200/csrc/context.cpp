@@ -303,6 +303,12 @@ void build_hess_sets(HostCtx& h) {
     h.has_hess = 1;
 }
 
+void build_deriv_sets(const HostCtx& h, int order, std::vector<double>* dir_n, std::vector<double>* rec_n) {
+    std::vector<double> dz, dw, rq;
+    enumerate_direct(h, order, 1e-20, dir_n, &dz, &dw);
+    enumerate_reciprocal(h, h.k.s + order, 1e-20, rec_n, &rq);
+}
+
 // Rigorous lower bound of x = c |k + q|^2 over k in the BZ box and q != 0:
 // ||kappa + n||_inf >= 1/2 gives |B (kappa + n)|^2 >= sigma_min(B)^2 / 4.
 double table_x_lo(const HostCtx& h) {
@@ -403,7 +409,10 @@ ld eval_piece_lo(const double* c, ld tau) { return estrin_lo(c, tau_powers(doubl
 }  // namespace
 
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
-                 double rfac_pref, HostTable* out) {
+                 double rfac_pref, HostTable* out, double poly_pow) {
+    // weight of a term relative to the unit scale: (1 + 4x)^poly_pow covers the |y|^2 (Hessian)
+    // or |2y|^m (order-m derivative) factors multiplying the tabulated functions
+    auto wfac = [poly_pow](ld x) { return std::pow(1.0L + 4.0L * x, ld(poly_pow)); };
     (void)c;
     out->nfunc = nfunc;
     for (int j = 0; j < nfunc; ++j) {
@@ -423,7 +432,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     for (int b = 0; b < 1000; ++b) {
         ld x = ld(x_lo) + hb * b;
         ld worst = 0.0L;
-        for (const Fn& f : fns) worst = std::max(worst, std::fabs(f(x)) * (1.0L + 4.0L * x));
+        for (const Fn& f : fns) worst = std::max(worst, std::fabs(f(x)) * wfac(x));
         x_hi = x;
         if (worst * std::fabs(ld(rfac_pref)) < cutoff && x > 8.0L) break;
     }
@@ -467,7 +476,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
                     ld truth = fns[j](xx);
                     ld approx = lo ? eval_piece_lo(cf, tau) : eval_piece(cf, tau);
                     if (lo) {
-                        if (std::fabs(approx - truth) * (1.0L + 4.0L * xx) > lo_budget) return false;
+                        if (std::fabs(approx - truth) * wfac(xx) > lo_budget) return false;
                     } else {
                         double rel = double(std::fabs(approx - truth) / std::max(std::fabs(truth), 1e-300L));
                         worst_err = std::max(worst_err, rel);

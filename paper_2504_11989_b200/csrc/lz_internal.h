@@ -117,6 +117,19 @@ struct DevPlan {
     CtxConst hctx;         // constants of the Hessian context
 };
 
+// Derivative plan (deriv.cu): one context, derivatives of total order `order` (1..4) at arbitrary
+// k.  Plain global-memory arrays (read through L1).
+struct DevDeriv {
+    int d, order, n_dir, n_rec;
+    double A[16], B[16];
+    const double* dir_n;     // [n_dir][d] integer coordinates (half lattice)
+    const double* dir_w;     // [n_dir][n_alpha] 2 (2 pi)^m w z^alpha
+    const double* rec_q;     // [n_rec][d] sorted by |q|
+    const double* rec_norm;  // [n_rec]
+    double r_cut, pref, rfac;
+    DevTable tab;            // F^{(j)}, j = ceil(m/2) .. m
+};
+
 // Fixed Duffy grid description (device arrays + patch decomposition).
 struct DevGrid {
     const double* u;   // radial nodes in (0, 1/2)
@@ -207,7 +220,10 @@ struct Error {
 void build_context(int d, const double* a, double nu, double splitting, int deriv_order,
                    HostCtx* out);
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
-                 double rfac_pref, HostTable* out);
+                 double rfac_pref, HostTable* out, double poly_pow = 1.0);
+// Point sets of the order-`order` derivative tables (L/epstein.py:376-377): direct weights
+// widened by |z|^order, reciprocal Gamma order s + order, cutoff 1e-20.
+void build_deriv_sets(const HostCtx& h, int order, std::vector<double>* dir_n, std::vector<double>* rec_n);
 double table_x_lo(const HostCtx& h);
 void build_hess_sets(HostCtx& h);
 long double t0_coeff(const CtxConst& k, int n);   // rho-series coefficient of t0_reg

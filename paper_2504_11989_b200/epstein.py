@@ -240,6 +240,38 @@ class EpsteinContext:
         """M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k} = -Hess Z_nu(k) / (4 pi^2)."""
         return -self.zeta_hessian(k) / (4.0 * math.pi ** 2)
 
+    # -- order-m derivatives at arbitrary k (device kernel, deriv.cu)
+    def derivatives(self, k, order: int):
+        """All d^alpha Z_nu(k) with |alpha| = order (1..4, d <= 3): returns (alphas, values) with
+        alphas a list of d-tuples in the reference's order (L/epstein.py:426-433) and values of
+        shape (..., n_alpha).  k must avoid the reciprocal lattice (PoleError)."""
+        alphas = multi_indices(self.d, order)
+        kb, single, shape = _as_batch(k, self.d)
+        if self.branch == TRIVIAL:
+            out = np.zeros((len(kb), len(alphas)))
+        else:
+            N.require_cuda("Epstein zeta derivatives")
+            out = np.empty((len(kb), len(alphas)), dtype=np.float64)
+            if len(kb):
+                N.check(N.lib().lz_zeta_derivatives_host(self._h, int(order), N.dptr(kb), len(kb),
+                                                         N.dptr(out)), "zeta derivatives")
+        if single:
+            return alphas, out[0]
+        return alphas, out.reshape(shape + (len(alphas),))
+
+    def polynomial_weighted_general(self, k, alpha) -> np.ndarray:
+        """M^alpha(k) = sum'_z z^alpha |z|^-nu e^{-2 pi i z.k} = d^alpha Z(k) / (-2 pi i)^|alpha|
+        (complex; real for even |alpha|, imaginary for odd)."""
+        alpha = tuple(int(a) for a in alpha)
+        if len(alpha) != self.d or min(alpha) < 0:
+            raise ValueError("alpha must be a d-tuple of nonnegative integers")
+        m = sum(alpha)
+        if m == 0:
+            return self.zeta(k).astype(complex)
+        alphas, vals = self.derivatives(k, m)
+        j = alphas.index(alpha)
+        return vals[..., j] / (-2j * math.pi) ** m
+
     # -- derivatives of the regularized part at k = 0 (host tables, L/epstein.py:347-415)
     def reg_derivatives(self, order: int) -> "RegZetaTaylor":
         if order % 2 != 0:
@@ -314,6 +346,20 @@ def directional_taylor_coeff(taylor: RegZetaTaylor, w, k: int):
     return taylor.directional_coeff(w, k)
 
 
-def polynomial_weighted_zeta(lattice: Lattice, nu: float, k):
-    """M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k} (the ATM dot-product building block)."""
-    return epstein_context(lattice, nu).polynomial_weighted(k)
+def polynomial_weighted_zeta(lattice: Lattice, nu: float, k, alpha=None):
+    """M_ab(k) = sum' z_a z_b |z|^-nu e^{-2 pi i z.k} (the ATM dot-product building block), or
+    for a multi-index ``alpha`` the general M^alpha(k) = sum' z^alpha |z|^-nu e^{-2 pi i z.k}."""
+    if alpha is None:
+        return epstein_context(lattice, nu).polynomial_weighted(k)
+    return epstein_context(lattice, nu).polynomial_weighted_general(k, alpha)
+
+
+def multi_indices(d: int, order: int):
+    """All d-tuples of nonnegative integers summing to ``order`` (L/epstein.py:426-433 order),
+    as enumerated by the native library."""
+    import ctypes as C
+    n = C.c_int64(0)
+    N.check(N.lib().lz_multi_indices(int(d), int(order), None, 0, C.byref(n)), "multi indices")
+    buf = (C.c_int * (n.value * d))()
+    N.check(N.lib().lz_multi_indices(int(d), int(order), buf, n.value, C.byref(n)), "multi indices")
+    return [tuple(buf[i * d:(i + 1) * d]) for i in range(n.value)]

@@ -190,3 +190,46 @@ def test_four_dimensional_lattice(nu):
     Ho = O.hessian(lat.a, nu, k)
     sc = np.maximum(np.abs(Ho).max(axis=(1, 2), keepdims=True), 1.0)
     assert (np.abs(H - Ho) / sc).max() <= ZETA_TOL
+
+
+@pytest.mark.parametrize("name,nu", [("fcc", 3.0), ("fcc", 5.0), ("bcc", 6.5), ("square", 3.5),
+                                     ("hexagonal", 4.0), ("integer_1d", 2.5)])
+@pytest.mark.parametrize("order", [1, 2, 3, 4])
+def test_general_derivatives_vs_oracle(name, nu, order):
+    """d^alpha Z(k), |alpha| = 1..4, at random k in the cell vs the long-double oracle (the
+    polynomial-weighted zeta of SURVEY 8(f) item 2), scaled per point like the Hessian test."""
+    lat = named_lattice(name)
+    d = lat.d
+    kap = np.random.default_rng(order * 7 + d).uniform(-0.45, 0.45, size=(48, d))
+    k = kap @ lat.a_inv_t.T
+    ctx = EpsteinContext(lat, nu, device=0)
+    alphas, D = ctx.derivatives(k, order)
+    assert alphas == O.multi_indices(d, order)
+    Do = O.derivatives(lat.a, nu, order, k)
+    scale = np.maximum(np.abs(Do).max(axis=1, keepdims=True), 1.0)
+    assert (np.abs(D - Do) / scale).max() <= 1e-11
+    if order == 2 and d > 1:
+        H = ctx.zeta_hessian(k)
+        for j, a in enumerate(alphas):
+            i0, i1 = [i for i, v in enumerate(a) for _ in range(v)]
+            assert np.abs(D[:, j] - H[:, i0, i1]).max() <= 1e-11 * scale.max()
+
+
+def test_derivative_laplacian_identity_and_poly_weights():
+    """sum_a d_a d_a d_b Z_5 = -4 pi^2 d_b Z_3 (third order from the Laplacian identity), and the
+    general polynomial-weighted zeta reduces to M_ab for |alpha| = 2."""
+    fcc = named_lattice("fcc")
+    kap = np.random.default_rng(5).uniform(-0.45, 0.45, size=(64, 3))
+    k = kap @ fcc.a_inv_t.T
+    al3, D3 = EpsteinContext(fcc, 5.0, device=0).derivatives(k, 3)
+    al1, D1 = EpsteinContext(fcc, 3.0, device=0).derivatives(k, 1)
+    for b in range(3):
+        lap = sum(D3[:, al3.index(tuple(2 * (i == a) + (i == b) for i in range(3)))] for a in range(3))
+        ref = -4.0 * math.pi ** 2 * D1[:, al1.index(tuple(int(i == b) for i in range(3)))]
+        assert np.abs(lap - ref).max() <= 1e-11 * max(1.0, np.abs(ref).max())
+    M = polynomial_weighted_zeta(fcc, 5.0, k)
+    M01 = polynomial_weighted_zeta(fcc, 5.0, k, alpha=(1, 1, 0))
+    assert np.abs(M01.imag).max() == 0.0
+    assert np.abs(M01.real - M[:, 0, 1]).max() <= 1e-11 * max(1.0, np.abs(M).max())
+    with pytest.raises(PoleError):
+        EpsteinContext(fcc, 5.0, device=0).derivatives(np.zeros(3), 2)

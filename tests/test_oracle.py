@@ -78,3 +78,42 @@ def test_pole_raises():
     sq = named_lattice("square")
     with pytest.raises(ArithmeticError):
         O.zeta(sq.a, 2.0, np.zeros((1, 2)))
+
+
+def test_oracle_derivatives_identities():
+    """The oracle's order-m derivatives: m = 2 equals its Hessian, the Laplacian identity links
+    m = 3 of Z_5 to m = 1 of Z_3, and m = 1 matches central differences of its zeta."""
+    import math
+    a = np.array([[0.0, 0.5, 0.5], [0.5, 0.0, 0.5], [0.5, 0.5, 0.0]]) * math.sqrt(2.0)
+    k = np.array([[0.11, -0.07, 0.05]]) @ np.linalg.inv(a)
+    H = O.hessian(a, 5.0, k)[0]
+    al2 = O.multi_indices(3, 2)
+    D2 = O.derivatives(a, 5.0, 2, k)[0]
+    for j, al in enumerate(al2):
+        i0, i1 = [i for i, v in enumerate(al) for _ in range(v)]
+        assert abs(D2[j] - H[i0, i1]) <= 1e-12 * np.abs(H).max()
+    al3, al1 = O.multi_indices(3, 3), O.multi_indices(3, 1)
+    D3 = O.derivatives(a, 5.0, 3, k)[0]
+    D1 = O.derivatives(a, 3.0, 1, k)[0]
+    for b in range(3):
+        lap = sum(D3[al3.index(tuple(2 * (i == c) + (i == b) for i in range(3)))] for c in range(3))
+        ref = -4.0 * math.pi ** 2 * D1[al1.index(tuple(int(i == b) for i in range(3)))]
+        assert abs(lap - ref) <= 1e-12 * max(1.0, abs(ref))
+        e = np.zeros(3)
+        e[b] = 1e-5
+        fd = (O.zeta(a, 3.0, k + e) - O.zeta(a, 3.0, k - e))[0] / 2e-5
+        assert abs(fd - D1[al1.index(tuple(int(i == b) for i in range(3)))]) <= 1e-7 * max(1.0, abs(fd))
+
+
+def test_multi_index_order_matches_reference_rule():
+    """Head-ascending order of L/epstein.py:426-433, identical in the oracle and the library."""
+    from paper_2504_11989_b200.epstein import multi_indices
+
+    def ref(d, total):
+        if d == 1:
+            return [(total,)]
+        return [(h,) + r for h in range(total + 1) for r in ref(d - 1, total - h)]
+
+    for d in (1, 2, 3, 4):
+        for m in range(0, 5):
+            assert O.multi_indices(d, m) == ref(d, m) == multi_indices(d, m)
