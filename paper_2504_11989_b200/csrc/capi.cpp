@@ -557,6 +557,10 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.tab.xb_max = double(hp.tab.nbins) - 1.0 / 1048576.0;
     P.tab.r_off = hp.c > 0.0 ? double((long double)hp.tab.x_lo / (long double)hp.c) : 0.0;
     P.tab.nbins_d = double(hp.tab.nbins);
+    // radius of the first low-degree bin's left edge (x_switch = x_lo + lo_start h, rho = x / c)
+    P.tab.r_lo = (hp.tab.lo_start < hp.tab.nbins && hp.c > 0.0)
+                     ? double(std::sqrt((ld(hp.tab.x_lo) + ld(hp.tab.lo_start) / ld(hp.tab.inv_hb)) / ld(hp.c)))
+                     : 0.0;
     // branch-free lookup is opt-in (LATSUM_BRANCHFREE=1): measured slower on the fcc ATM grid,
     // where warps beyond the cutoff otherwise skip the polynomial entirely
     const char* bf = std::getenv("LATSUM_BRANCHFREE");

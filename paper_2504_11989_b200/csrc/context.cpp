@@ -504,11 +504,30 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
         bf.level = kDirectMarker;  // evaluate E_p directly in this bin
     };
     parallel_for(nbins, 1, [&](int64_t b) { fit_bin(int(b)); });
+    // Low-degree bins form a suffix [lo_start, nbins) (so the kernel can split its q loop by x
+    // without per-lane layout checks); low-degree fits before it are redone at degree kDeg.
+    int lo_start = nbins;
+    while (lo_start > 0 && fits[lo_start - 1].level != kDirectMarker && fits[lo_start - 1].lo) --lo_start;
+    {
+        std::vector<int> redo;
+        for (int b = 0; b < lo_start; ++b)
+            if (fits[b].lo) redo.push_back(b);
+        parallel_for(int64_t(redo.size()), 1, [&](int64_t i) {
+            const int b = redo[size_t(i)];
+            const ld b0 = ld(x_lo) + hb * b;
+            BinFit& bf = fits[b];
+            bf = BinFit();
+            for (int level = 0; level <= kMaxLevel; ++level)
+                if (try_fit(b0, level, false, &bf)) return;
+            bf.level = kDirectMarker;
+        });
+    }
+    out->lo_start = lo_start;
     // Direct (unfitted) bins must form a prefix: the kernel's conversion-free floor may step one
     // piece past a bin's last piece at an exact bin boundary, which is then the next bin's first
-    // piece evaluated at the same x -- valid only if that next bin has pieces.  For the same
-    // reason a low-degree bin is never followed by a high-degree one (x is increasing, and the
-    // overshoot lands in the previous bin's last piece, whose stride must match).
+    // piece evaluated at the same x (delta = -1/2) -- valid only if that next bin has pieces, and
+    // read in the previous bin's layout: the last high-degree bin is therefore followed by a
+    // guard piece, the first low-degree piece in the high-degree layout (exact: c5..c8 = 0).
     int last_direct = -1;
     for (int b = 0; b < nbins; ++b)
         if (fits[b].level == kDirectMarker) last_direct = b;
@@ -518,6 +537,16 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     out->n_lo_bins = 0;
     for (int b = 0; b < nbins; ++b) {
         const BinFit& bf = fits[b];
+        if (b == lo_start && b > 0 && fits[b - 1].level != kDirectMarker && !fits[b - 1].lo) {
+            const int ps = piece_stride(nfunc);
+            const size_t base = out->coef.size();
+            out->coef.resize(base + ps, 0.0);
+            for (int j = 0; j < nfunc; ++j) {
+                const double* cf = &bf.coefs[size_t(j) * kNCP];  // first sub-piece of bin b
+                for (int m = 0; m <= kDegLo; ++m) out->coef[base + j * 8 + m] = cf[m];
+            }
+            off += size_t(ps);
+        }
         if (bf.level == kDirectMarker) {
             out->dir[b] = kDirectMarker;
             continue;

@@ -282,13 +282,15 @@ constexpr double kMagic = 6755399441055744.0;
 // Piece lookup shared by both variants: bin b = floor(xb) from the directory, sub-piece
 // floor(fs) of fs = (xb - b) 2^L, and the local coordinate delta = (fs - 1/2) - floor(fs) in
 // [-1/2, 1/2] (coefficients are stored for delta, see context.cpp fit_piece).
-template <int NF, bool SMEM>
+// DEG: 0 = degree from the directory entry (per-lane branch), 1 = high degree only, 2 = low
+// degree only (the caller guarantees the whole warp is on that side of r_lo).
+template <int NF, bool SMEM, int DEG = 0>
 __device__ __forceinline__ void tab_piece(const View& V, double xb, double tb, int e, double (&f)[NF]) {
     constexpr int PS = piece_stride(NF);
     constexpr int PSL = piece_stride_lo(NF);
     // 2^L from its exponent bits (no conversion); SMEM directory entries carry them pre-shifted
     const int hi = SMEM ? (e & 0x7ff00000) : ((1023 + (e & 15)) << 20);
-    const bool lo = SMEM ? (e < 0) : ((e >> 4) & 1);
+    const bool lo = DEG == 2 ? true : DEG == 1 ? false : (SMEM ? (e < 0) : ((e >> 4) & 1));
     const double two_l = __hiloint2double(hi, 0);
     const double a = fma(xb - (tb - kMagic), two_l, -0.5);  // fs - 1/2
     const double ts = a + kMagic;
@@ -357,11 +359,11 @@ __device__ __forceinline__ void tab_eval_fast(const DevTable& T, const View& V, 
 // In-cell variant: k in the reduced cell guarantees xb >= 0 (x_lo = c lambda_min / 4, see
 // context.cpp table_x_lo), and a table without marker bins needs no direct branch; only lanes
 // past the cutoff branch out (warp-uniform for most q, which are sorted by |q|).
-template <int NF, bool SMEM>
+template <int NF, bool SMEM, int DEG = 0>
 __device__ __forceinline__ void tab_eval_cell(const View& V, double xb, double (&f)[NF]) {
     const double tb = (xb - 0.5) + kMagic;
     const int e = ld_s32<SMEM>(V.tdir, V.s_tdir, __double2loint(tb));
-    tab_piece<NF, SMEM>(V, xb, tb, e, f);
+    tab_piece<NF, SMEM, DEG>(V, xb, tb, e, f);
 }
 
 // Checked variant: arbitrary k (xb < 0 possible) and marker bins (E_p evaluated directly).
@@ -652,16 +654,18 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
         for (int a = 0; a < D; ++a) y[a] += k[a];
         double f[NF];
-        if constexpr (mode == 1 || mode == 3) {
+        if constexpr (mode == 1 || mode >= 3) {
             // in-cell: xb = (|k+q|^2 - x_lo / c) * r_scale.  mode 1: lanes past the cutoff skip
-            // the lookup and the accumulation; mode 3: every lane is inside (|q| + max|k| <= r_in),
-            // no branch, so consecutive terms interleave
+            // the lookup and the accumulation; modes 3-5: every lane is inside (|q| + max|k| <=
+            // r_in), no branch, so consecutive terms interleave; 4 / 5: the whole warp is below /
+            // above r_lo, so the piece degree is known at compile time
             double r = -P.tab.r_off;
 #pragma unroll
             for (int a = D - 1; a >= 0; --a) r = fma(y[a], y[a], r);
             const double xb = r * P.tab.r_scale;
-            if (mode == 3 || xb < P.tab.nbins_d) {
-                tab_eval_cell<NF, SMEM>(V, xb, f);
+            constexpr int DEG = mode == 4 ? 1 : mode == 5 ? 2 : 0;
+            if (mode >= 3 || xb < P.tab.nbins_d) {
+                tab_eval_cell<NF, SMEM, DEG>(V, xb, f);
                 accumulate(y, f);
             }
         } else {
@@ -678,7 +682,9 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 0>{});
     } else if (!P.tab.branchfree) {
-        // q with |q| <= r_in - max|k| are inside the table for every lane of the warp
+        // q with |q| <= r_in - max|k| are inside the table for every lane of the warp.  (Splitting
+        // further at r_lo +- max|k| into compile-time-degree regions, modes 4 / 5, measured no
+        // faster on the fcc ATM grid and slower on C1: the degree branch is warp-uniform.)
         const int n_in = min(n_eff, count_le(V.rec_norm, P.n_rec, P.r_in - kmag));
         int i = gl;
 #pragma unroll UNR

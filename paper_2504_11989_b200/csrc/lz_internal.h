@@ -67,6 +67,7 @@ struct DevTable {
     double r_off;              // x_lo / c:  xb = (rho - r_off) * r_scale (in-cell lookup)
     double xb_max;             // largest bin coordinate evaluated (nbins - 2^-20)
     double nbins_d;            // nbins as a double (no int->FP64 conversion in the hot loop)
+    double r_lo;               // |k+q| >= r_lo: low-degree bin; |k+q| < r_lo: high degree (0: no lo)
     int has_marker;            // 1 if some bin is evaluated directly (E_p; checked lookup path)
     int branchfree;            // opt-in (LATSUM_BRANCHFREE=1): select instead of the far branch
     double p[4], scale[4]; // for the direct fallback
@@ -167,6 +168,7 @@ struct HostTable {
     double p[4] = {0, 0, 0, 0}, scale[4] = {0, 0, 0, 0};
     double max_rel_err = 0;   // measured during the build (degree-kDeg pieces)
     int n_lo_bins = 0;        // bins with degree-kDegLo pieces
+    int lo_start = 0;         // first low-degree bin (low-degree bins form the suffix)
 };
 
 // Degree-kDeg polynomial in Estrin form: dependency depth 3-4 instead of 7-8, and the
