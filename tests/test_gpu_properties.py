@@ -75,3 +75,22 @@ def test_exponent_permutation_symmetry(lat, nus):
     for perm in ([nus[1], nus[2], nus[0]], nus[::-1]):
         w = integrate_product(lat, perm, cfg)[0]
         assert abs(w - v) <= 1e-12 * abs(v)
+
+
+@settings(max_examples=12, deadline=None, suppress_health_check=list(HealthCheck))
+@given(lat=lattices(), nu=st.floats(2.5, 8.0), order=st.integers(1, 4), seed=st.integers(0, 2 ** 31 - 1))
+def test_derivative_parity_and_periodicity(lat, nu, order, seed):
+    """d^alpha Z(-k) = (-1)^|alpha| d^alpha Z(k) and d^alpha Z(k + G) = d^alpha Z(k)."""
+    ctx = EpsteinContext(lat, nu, device=0)
+    if ctx.branch == "trivial":
+        return
+    rng = np.random.default_rng(seed)
+    k = rng.uniform(-0.45, 0.45, size=(8, lat.d)) @ lat.a_inv_t.T
+    k = k[np.linalg.norm(k, axis=1) > 0.05]
+    _, D = ctx.derivatives(k, order)
+    _, Dm = ctx.derivatives(-k, order)
+    scale = max(1.0, float(np.abs(D).max()))
+    assert np.abs(Dm - (-1) ** order * D).max() <= 1e-11 * scale
+    shift = rng.integers(-2, 3, size=lat.d) @ lat.a_inv_t.T
+    _, Ds = ctx.derivatives(k + shift, order)
+    assert np.abs(Ds - D).max() <= 1e-10 * scale
