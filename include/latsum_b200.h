@@ -69,7 +69,9 @@ int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out);
 int lz_ctx_destroy(lz_ctx* ctx);
 int lz_ctx_get_info(const lz_ctx* ctx, lz_ctx_info* out);
 /* Build (host) and upload (device) the evaluation tables now instead of on first use.
- * what: bit 1 = zeta tables, bit 2 = Hessian tables.  table_* info fields are zero until then. */
+ * what: bit 1 = zeta tables, bit 2 = Hessian tables, bit 4 = only the Hessian point sets (what a
+ * fused ATM plan needs; lets a caller enumerate them off the critical path).  table_* info
+ * fields are zero until then. */
 int lz_ctx_prepare(const lz_ctx* ctx, int what);
 /* which: 0 dir_pts (z = A n), 1 dir_w, 2 rec_pts, 3 hdir_pts, 4 hdir_w, 5 rec_pts_h, 6 dir_n (int coords)
  * copies min(cap, size) doubles; returns the full size through *size.                        */

@@ -927,6 +927,7 @@ int lz_ctx_prepare(const lz_ctx* c, int what) {
     return guarded([&] {
         if (what & 1) ensure_plain(c);
         if (what & 2) ensure_hess(c);
+        if (what & 4) ensure_hess_sets(c);
     });
 }
 

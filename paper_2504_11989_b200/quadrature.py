@@ -247,8 +247,13 @@ def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
         splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
     # the two contexts' host enumerations are independent native calls (GIL released): overlap them
     from concurrent.futures import ThreadPoolExecutor
+    def z5_with_sets():
+        z = epstein_context(lattice, 5.0, splitting)
+        N.check(N.lib().lz_ctx_prepare(z.handle, 4), "hessian point sets")  # off the critical path
+        return z
+
     with ThreadPoolExecutor(max_workers=2) as pool:
-        f5 = pool.submit(epstein_context, lattice, 5.0, splitting)
+        f5 = pool.submit(z5_with_sets)
         z3 = epstein_context(lattice, 3.0, splitting)
         z5 = f5.result()
     h = C.c_void_p()

@@ -102,6 +102,11 @@ def e2e_breakdown():
         t5 = time.perf_counter()
         print(f"rep {rep}: contexts {1e3*(t1-t0):.1f} ms, plan {1e3*(t2-t1):.1f} ms, "
               f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms, warm run+d2h {1e3*(t5-t4):.1f} ms")
+        epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
+        t6 = time.perf_counter()
+        atm_plan(fcc)
+        t7 = time.perf_counter()
+        print(f"   cold atm_plan (contexts in parallel + plan): {1e3*(t7-t6):.1f} ms")
 
 
 def c1_time():
