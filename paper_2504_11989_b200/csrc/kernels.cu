@@ -898,7 +898,7 @@ struct __align__(16) DirBlock {
     double w[kDirParam];
 };
 
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC, int UNR, bool CDIR>
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -906,7 +906,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     View V = stage<SMEM, CDIR>(P, smem);
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kWarpsPerCta = kTileWarps * TPC;
+    constexpr int kWarpsPerCta = WPC;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
     // Warps are independent (no block barrier after staging): each takes 32-node patches of the
     // shard's range in CTA-contiguous order, writes its warp partial, and the last of a tile's 8
@@ -1013,14 +1013,15 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
 template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int TPC = kTilesPerCta, int UNR = 2>
 __global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
     tile_kernel(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials) {
-    tile_body<D, NCTX, HESS, MODE, SMEM, TPC, UNR, false>(P, g, mult, partials, nullptr);
+    tile_body<D, NCTX, HESS, MODE, SMEM, kTileWarps * TPC, UNR, false>(P, g, mult, partials, nullptr);
 }
 
-template <int D, int NCTX, bool HESS, int MODE, int TPC = kTilesPerCta, int UNR = 2>
-__global__ void __launch_bounds__(32 * kTileWarps * TPC, 1)
+// WPC: warps per CTA (any count: warps take 32-node patches independently)
+template <int D, int NCTX, bool HESS, int MODE, int WPC = kTileWarps * kTilesPerCta, int UNR = 2>
+__global__ void __launch_bounds__(32 * WPC, 1)
     tile_kernel_c(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials,
                   const __grid_constant__ DirBlock B) {
-    tile_body<D, NCTX, HESS, MODE, true, TPC, UNR, true>(P, g, mult, partials, B.w);
+    tile_body<D, NCTX, HESS, MODE, true, WPC, UNR, true>(P, g, mult, partials, B.w);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -1213,25 +1214,36 @@ static cudaError_t launch_tile_s(const DevPlan& P, const DevGrid& g, int4 mult, 
     return cudaGetLastError();
 }
 
-template <int D, int NCTX, bool HESS, int MODE, int TPC, int UNR>
+template <int D, int NCTX, bool HESS, int MODE, int WPC, int UNR>
 static cudaError_t launch_tile_c(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
     static_assert(sizeof(DevPlan) + sizeof(DevGrid) + sizeof(int4) + sizeof(double*) + 16 + sizeof(DirBlock) <= 32764,
                   "kernel parameters exceed the 32 KB limit");
-    auto kern = tile_kernel_c<D, NCTX, HESS, MODE, TPC, UNR>;
-    const size_t sm = bytes - ((sizeof(double) * size_t(P.n_direct) + 15) & ~size_t(15));
+    auto kern = tile_kernel_c<D, NCTX, HESS, MODE, WPC, UNR>;
     cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
-    (void)sm;  // the direct region stays reserved (offsets unchanged) but is not staged
     thread_local DirBlock blk;  // host staging of the parameter copy (copied at launch)
     std::memcpy(blk.w, P.direct_host, sizeof(double) * size_t(P.n_direct));
-    const int threads = 32 * kTileWarps * TPC;
-    int64_t need = (g.tile_hi - g.tile_lo + TPC - 1) / TPC;
+    const int threads = 32 * WPC;
+    const int64_t patches = (g.tile_hi - g.tile_lo) * kTileWarps;
+    int64_t need = (patches + WPC - 1) / WPC;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, bytes, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
     kern<<<blocks, threads, bytes, st>>>(P, g, mult, partials, blk);
     return cudaGetLastError();
+}
+
+// Warps per CTA of the parameter-space ATM kernel (LATSUM_ATM_WPC, tuning sweeps; d = 3 only).
+// Measured on the fcc bench grid: 16 -> 16.6 ms (112 regs), 20 -> 14.0 (96), 24 -> 13.2 (80),
+// 28 -> 12.7 (72, some spills), 32 -> 15.0 (64, heavy spills).
+static int atm_wpc() {
+    static int w = -1;
+    if (w < 0) {
+        w = 28;
+        if (const char* e = std::getenv("LATSUM_ATM_WPC")) w = std::atoi(e);
+    }
+    return w;
 }
 
 // Parameter-space direct block for the ATM kernel: default on (measured 15.7 -> 14.4 ms on the
@@ -1269,8 +1281,18 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1) {
-        if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host)
-            return launch_tile_c<D, NCTX, HESS, MODE, kTilesPerCta, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+        if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host) {
+            if constexpr (D == 3) {
+                switch (atm_wpc()) {
+                    case 16: return launch_tile_c<D, NCTX, HESS, MODE, 16, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 20: return launch_tile_c<D, NCTX, HESS, MODE, 20, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 28: return launch_tile_c<D, NCTX, HESS, MODE, 28, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 32: return launch_tile_c<D, NCTX, HESS, MODE, 32, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    default: break;
+                }
+            }
+            return launch_tile_c<D, NCTX, HESS, MODE, 24, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+        }
     }
     if constexpr (MODE == 1 && D == 3) {
         if (smem) {
