@@ -1235,12 +1235,13 @@ static cudaError_t launch_tile_c(const DevPlan& P, const DevGrid& g, int4 mult, 
 }
 
 // Warps per CTA of the parameter-space ATM kernel (LATSUM_ATM_WPC, tuning sweeps; d = 3 only).
-// Measured on the fcc bench grid: 16 -> 16.6 ms (112 regs), 20 -> 14.0 (96), 24 -> 13.2 (80),
-// 28 -> 12.7 (72, some spills), 32 -> 15.0 (64, heavy spills).
+// Measured on the fcc bench grid (q-unroll 2): 16 -> 16.6 ms (112 regs), 20 -> 14.0 (96),
+// 24 -> 13.2 (80), 28 -> 12.7 (72, some spills), 32 -> 15.0 (64, heavy spills); 28 warps with
+// q-unroll 1 ("281", the default) -> 12.5; 32 with unroll 1 ("321") -> 15.1.
 static int atm_wpc() {
     static int w = -1;
     if (w < 0) {
-        w = 28;
+        w = 281;
         if (const char* e = std::getenv("LATSUM_ATM_WPC")) w = std::atoi(e);
     }
     return w;
@@ -1284,14 +1285,16 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
         if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host) {
             if constexpr (D == 3) {
                 switch (atm_wpc()) {
-                    case 16: return launch_tile_c<D, NCTX, HESS, MODE, 16, 2>(P, g, mult, partials, grid_blocks, st, bytes);
                     case 20: return launch_tile_c<D, NCTX, HESS, MODE, 20, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 24: return launch_tile_c<D, NCTX, HESS, MODE, 24, 2>(P, g, mult, partials, grid_blocks, st, bytes);
                     case 28: return launch_tile_c<D, NCTX, HESS, MODE, 28, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 281: return launch_tile_c<D, NCTX, HESS, MODE, 28, 1>(P, g, mult, partials, grid_blocks, st, bytes);
                     case 32: return launch_tile_c<D, NCTX, HESS, MODE, 32, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+                    case 321: return launch_tile_c<D, NCTX, HESS, MODE, 32, 1>(P, g, mult, partials, grid_blocks, st, bytes);
                     default: break;
                 }
             }
-            return launch_tile_c<D, NCTX, HESS, MODE, 24, 2>(P, g, mult, partials, grid_blocks, st, bytes);
+            return launch_tile_c<D, NCTX, HESS, MODE, 28, 1>(P, g, mult, partials, grid_blocks, st, bytes);
         }
     }
     if constexpr (MODE == 1 && D == 3) {
