@@ -280,7 +280,7 @@ def run_ours(args):
                         "from cold caches", "energy": res.energy},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
                      "frac": achieved / pk.value, "traffic": TRAFFIC_PER_LAUNCH,
-                     "kernel": "lz::tile_kernel<3,1,true,1> (fused ATM integrand)",
+                     "kernel": "lz::tile_kernel_c<3,1,true,1,28,1> (fused ATM integrand, direct block in parameter space)",
                      "kernel_ms": kern_ms, "flops_per_node": FLOPS_PER_NODE, "flops_source": FLOPS_SOURCE,
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
                                     "no FP64 entry)"},
