@@ -96,7 +96,7 @@ struct HostPlan {
     double e2[4] = {0, 0, 0, 0}, e3[4] = {0, 0, 0, 0};
     int n_t0 = 0;
     double t0_rho_max = -1.0;
-    std::vector<int> run_info;
+    std::vector<int> run_info;   // maximal runs of consecutive n_d (plan info only)
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;

@@ -12,6 +12,10 @@
 // Horner chains, coefficients in shared memory) instead of the reference's
 // per-term scipy gammaincc + recurrence (L/incgamma.py:78-94).
 //
+// Direct space is walked in 2D slabs (one sincos per slab, complex rotation per row,
+// Chebyshev cosine recurrence along rows); the plan is staged into shared memory by one TMA
+// bulk copy (the ATM kernel keeps its direct block in the kernel's parameter space instead).
+//
 // Kernels:
 //   batch_kernel   : Z or Hessian at a batch of k (C1), G lanes per point
 //   tile_kernel    : fixed Duffy grid (L/quadrature.py:136-177) generated on
@@ -19,8 +23,11 @@
 //                    L/quadrature.py:393-397) or the ATM integrand
 //                    [Z_3^3, tr M_5^3] (C3), reduced deterministically to one
 //                    partial per 256-node tile (slot-disjoint for multi-GPU)
+//   tile_kernel_c  : the ATM variant with the direct block in parameter space and
+//                    a free warps-per-CTA count (28 on B200)
 //   reduce_kernel  : fixed-order compensated sum of the tile partials
 //   fp64_probe     : DFMA-chain peak probe for the roofline denominator
+// (deriv.cu: order-m derivatives; direct.cu: brute-force direct sums.)
 #include <cuda_runtime.h>
 
 #include <cstdint>
