@@ -32,12 +32,12 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v18); used to turn the live kernel time into FLOP/s.
-FLOPS_PER_NODE = 10386.2
-FLOPS_SOURCE = "ncu r01 v18: 2.6138e+11 FP64 FLOPs per launch / 25,165,824 nodes"
-# ncu r01 v18 dram__bytes_read.sum + dram__bytes_write.sum (plan staging + the warp partials that
+# bench grid (profiles/r01_summary.md, v19); used to turn the live kernel time into FLOP/s.
+FLOPS_PER_NODE = 10119.3
+FLOPS_SOURCE = "ncu r01 v19: 2.5466e+11 FP64 FLOPs per launch / 25,165,824 nodes"
+# ncu r01 v19 dram__bytes_read.sum + dram__bytes_write.sum (plan staging + the warp partials that
 # leave L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
-TRAFFIC_PER_LAUNCH = 534_016 + 1_325_824
+TRAFFIC_PER_LAUNCH = 534_784 + 1_280_512
 
 
 def parse():
