@@ -88,6 +88,7 @@ void free_all(std::vector<void*>* allocs) {
 // Host-side description of a fused plan before upload.
 struct HostPlan {
     int d = 0, nctx = 0, hess = 0, nw = 0, alias_fp = 0;
+    int dir_plain = 0;  // plain-context channels in the direct weight rows (0 for trace-Z ATM plans)
     double c = 0.0, r_cut = 0.0, r_in = 0.0, alias_ratio = 0.0;
     std::vector<double> dir_n, rec_q, rec_norm, t0c;
     // direct space: [slab records][row records][weight rows] (see build_host_plan)
@@ -149,7 +150,12 @@ bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
 }
 
 // Build a fused plan from plain contexts (+ optionally one Hessian context).
-void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::HostCtx* hess, HostPlan* hp) {
+// trace_z (ATM plans): Z_nu = tr M_{nu+2} exactly (Sum_a z_a^2 |z|^{-nu-2} = |z|^{-nu}), so the
+// kernel takes Z_3 from the trace of the Hessian of Z_5 and the direct weight rows carry only the
+// three Hessian moment channels (nw = 3, loaded in pairs of points); the plain context still
+// supplies the shared table function (F of Z_3 = F' of Z_5 / alias_ratio) and its constants.
+void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::HostCtx* hess, HostPlan* hp,
+                     bool trace_z = false) {
     const lz::HostCtx* first = plain.empty() ? hess : plain[0];
     const int d = first->d;
     hp->d = d;
@@ -306,7 +312,9 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         }
     }
     const int nh = hess ? 3 : 0;
-    hp->nw = (hp->nctx + nh == 1) ? 1 : ((hp->nctx + nh + 1) & ~1);
+    if (trace_z && !hess) throw Error{LZ_EINVAL, "trace-Z plans need the Hessian context"};
+    hp->dir_plain = trace_z ? 0 : hp->nctx;
+    hp->nw = trace_z ? nh : ((hp->nctx + nh == 1) ? 1 : ((hp->nctx + nh + 1) & ~1));
     for (int a = 0; a < 4; ++a) hp->e2[a] = hp->e3[a] = 0.0;
     for (int a = 0; a < d; ++a) {
         hp->e3[a] = first->A[a * d + d - 1];
@@ -378,12 +386,13 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                     for (const auto& pt : r.pts) {
                         const size_t base = (row0 + size_t(pt.first - lo)) * hp->nw;
                         const std::vector<ld>& w = wmap.at(pack_key(d, &hp->dir_n[pt.second * d]));
-                        for (int c = 0; c < hp->nctx; ++c) wts_out[base + c] = double(w[c]);
+                        const int dp = hp->dir_plain;
+                        for (int c = 0; c < dp; ++c) wts_out[base + c] = double(w[c]);
                         if (hess) {
                             const ld wh = w[hp->nctx] * hscale, lp = ld(pt.first) - lc;
-                            wts_out[base + hp->nctx] = double(wh);
-                            wts_out[base + hp->nctx + 1] = double(wh * lp);
-                            wts_out[base + hp->nctx + 2] = double(wh * lp * lp);
+                            wts_out[base + dp] = double(wh);
+                            wts_out[base + dp + 1] = double(wh * lp);
+                            wts_out[base + dp + 2] = double(wh * lp * lp);
                         }
                     }
                 }
@@ -1305,7 +1314,7 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
         pl->kind = 1;
         if (std::fabs(z5->h.k.nu - z3->h.k.nu - 2.0) > 1e-12)
             throw Error{LZ_EINVAL, "ATM plan needs exponents nu and nu + 2 (Z_3 and the Hessian of Z_5)"};
-        build_host_plan({&z3->h}, &z5->h, &pl->hp);
+        build_host_plan({&z3->h}, &z5->h, &pl->hp, /*trace_z=*/true);
         if (!pl->hp.alias_fp) throw Error{LZ_EINVAL, "ATM plan: F' alias expected"};
         if (pl->device >= 0) {
             DeviceGuard dg(pl->device);

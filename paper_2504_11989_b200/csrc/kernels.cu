@@ -465,10 +465,15 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
     double h[HESS ? Sym<D>::n : 1];
 };
 
-template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true, bool CDIR = false>
+// TRZ (ATM plans built with trace_z): the direct weight rows carry no plain channel and out.z is
+// not formed -- the caller takes Z_{nu} = tr M_{nu+2} from the Hessian (context.cpp/capi.cpp
+// build_host_plan); the plain context's table function still feeds the Hessian's F' (ALIAS).
+template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true, bool CDIR = false,
+          bool TRZ = false>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out) {
+    static_assert(!TRZ || (HESS && ALIAS), "trace-Z needs the aliased Hessian plan");
     using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
@@ -482,7 +487,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     // sum w z_a z_b cos = zc_a X_b + e2_a Y_b + e3_a W_b, X = zc A0 + e2 A1 + e3 B0,
     // Y = zc A1 + e2 A2 + e3 B1, W = zc B0 + e2 B1 + e3 T.
     constexpr int NH = HESS ? 3 : 0;
-    constexpr int NWP = (NCTX + NH == 1) ? 1 : ((NCTX + NH + 1) & ~1);
+    constexpr int NDC = TRZ ? 0 : NCTX;  // plain channels in the direct weight rows
+    constexpr int NWP = TRZ ? NH : ((NCTX + NH == 1) ? 1 : ((NCTX + NH + 1) & ~1));
     constexpr int SR = 2 * D + 2;
     double dacc[NCTX > 0 ? NCTX : 1];
 #pragma unroll
@@ -534,11 +540,11 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                             for (int c = 0; c < NWP; ++c) wv[c] = ld_dir<SMEM, CDIR>(V, wp + c);
                         }
                     };
-                    auto accum = [&](const double (&wv)[NWP], double cs) {
+                    auto accum = [&](const double* wv, double cs) {
 #pragma unroll
-                        for (int c = 0; c < NCTX; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
+                        for (int c = 0; c < NDC; ++c) dacc[c] = fma(wv[c], cs, dacc[c]);
 #pragma unroll
-                        for (int m = 0; m < NH; ++m) S[m] = fma(wv[NCTX + m], cs, S[m]);
+                        for (int m = 0; m < NH; ++m) S[m] = fma(wv[NDC + m], cs, S[m]);
                     };
                     if (G == 1) {
                         double cs = pc;
@@ -558,11 +564,35 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                             cs = cnext;
                         };
                         // rows are short (~6 points): no unrolling beyond the pair
+                        if constexpr (NWP % 2 == 1 && NWP > 1) {
+                            // odd channel count (trace-Z rows, nw = 3): a pair of points is
+                            // 2 NWP doubles at an even offset, loaded as NWP 16-byte vectors
 #pragma unroll 1
-                        for (int l = 0; l < len; l += 2) {
-                            point(w);
-                            point(w + NWP);
-                            w += 2 * NWP;
+                            for (int l = 0; l < len; l += 2) {
+                                double wv[2 * NWP];
+#pragma unroll
+                                for (int c = 0; c < 2 * NWP; c += 2) {
+                                    const double2 v2 = ld_dir2<SMEM, CDIR>(V, w + c);
+                                    wv[c] = v2.x;
+                                    wv[c + 1] = v2.y;
+                                }
+                                accum(wv, cs);
+                                double cnext = fma(two_c3, cs, -cprev);
+                                cprev = cs;
+                                cs = cnext;
+                                accum(wv + NWP, cs);
+                                cnext = fma(two_c3, cs, -cprev);
+                                cprev = cs;
+                                cs = cnext;
+                                w += 2 * NWP;
+                            }
+                        } else {
+#pragma unroll 1
+                            for (int l = 0; l < len; l += 2) {
+                                point(w);
+                                point(w + NWP);
+                                w += 2 * NWP;
+                            }
                         }
                     } else {
                         // G lanes per node (small batches): the row's points are spread over the
@@ -730,7 +760,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     for (int j = 0; j < NF; ++j) f0[j] = 0.0;
     if (q0_table) tab_eval<NF, SMEM>(P.tab, V, rho, f0);
 #pragma unroll
-    for (int j = 0; j < NCTX; ++j) {
+    for (int j = 0; j < (TRZ ? 0 : NCTX); ++j) {
         const CtxConst& C = P.ctx[j];
         double zv;
         if (C.branch == kTrivial) {
@@ -945,7 +975,8 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
-            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM, CDIR>(P, V, kap, k, 0, 1, 0u, acc);
+            // MODE 1 plans are trace-Z plans (lz_plan_create_atm): Z_3 = tr M_5
+            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM, CDIR, MODE == 1>(P, V, kap, k, 0, 1, 0u, acc);
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll
@@ -962,7 +993,6 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 }
                 val[0] = ok ? weight * prod : 0.0;
             } else {
-                const double z = acc.z[0];
                 // M = -Hess / (4 pi^2); tr(M^3) over the symmetric matrix
                 double M[D][D];
                 constexpr double inv4pi2 = 1.0 / (4.0 * kPi * kPi);
@@ -985,7 +1015,10 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                         for (int e = 0; e < D; ++e) m2 = fma(M[a][e], M[e][b], m2);
                         tr3 = fma(m2, M[b][a], tr3);
                     }
-                val[0] = ok ? weight * (z * z * z) : 0.0;
+                double zt = 0.0;  // Z_3 = tr M_5
+#pragma unroll
+                for (int a = 0; a < D; ++a) zt += M[a][a];
+                val[0] = ok ? weight * (zt * zt * zt) : 0.0;
                 val[1] = ok ? weight * tr3 : 0.0;
             }
         }
@@ -1333,6 +1366,7 @@ cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, 
 
 cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks, cudaStream_t st) {
     int4 m = make_int4(0, 0, 0, 0);
+    if (P.nw != 3 || !P.alias_fp) return cudaErrorInvalidValue;  // trace-Z plan layout expected
     switch (P.d) {
         case 1: return launch_tile_t<1, 1, true, 1>(P, g, m, partials, grid_blocks, st);
         case 2: return launch_tile_t<2, 1, true, 1>(P, g, m, partials, grid_blocks, st);
