@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -98,6 +99,9 @@ struct HostPlan {
     int n_t0 = 0;
     double t0_rho_max = -1.0;
     std::vector<int> run_info;   // maximal runs of consecutive n_d (plan info only)
+    // line-factorised direct block (trace-Z ATM plans, d = 3; see build_line_block)
+    std::vector<unsigned char> line;
+    int line_K[3] = {0, 0, 0}, line_P[3] = {0, 0, 0}, line_slot_off[3] = {0, 0, 0}, line_meta_off[3] = {0, 0, 0};
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;
@@ -150,6 +154,99 @@ bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
 }
 
 // Build a fused plan from plain contexts (+ optionally one Hessian context).
+// Line-factorised direct block for the ATM kernel (d = 3).  The 32 lanes of a warp hold nodes
+// on one line of the Duffy grid: kappa = kappa_0 + x e_a with a = the cell's pyramid axis and x
+// varying per lane (kernels.cu line_direct).  Grouping the half lattice by planes n_a = m,
+//   sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m],  C_m = sum_{n_a = m} W_n e^{2 pi i kappa_0.n},
+// the C_m are warp-uniform: the warp computes them cooperatively (each lane a slice of one
+// plane), reduces them through shared memory and every lane finishes with one rotation per plane.
+// Per axis the half lattice is {n : (n_a, n_b, n_c) >lex 0} (b = a+1, c = a+2 mod 3), planes
+// m = 0..M get lane groups sized so that the slots per lane K = max_m ceil(s_m / L_m) is small.
+// Returns false (no line block) when the set does not fit the kernel's fixed limits.
+static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, std::vector<long double>>& wmap,
+                             const double* A, long double hscale, int hidx) {
+    const int d = 3;
+    const size_t np = hp->dir_n.size() / d;
+    if (np == 0 || np >= 65535) return false;
+    std::vector<double> W((np + 1) * 6, 0.0);
+    for (size_t i = 0; i < np; ++i) {
+        const double* n = &hp->dir_n[i * d];
+        long double z[3];
+        for (int a = 0; a < 3; ++a) {
+            z[a] = 0.0L;
+            for (int b = 0; b < 3; ++b) z[a] += (long double)A[a * 3 + b] * n[b];
+        }
+        const long double wh = wmap.at(pack_key(d, n))[hidx] * hscale;
+        int c = 0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = a; b < 3; ++b) W[i * 6 + c++] = double(wh * z[a] * z[b]);
+    }
+    std::vector<unsigned char> out;
+    auto put = [&](const void* p, size_t bytes) {
+        const size_t off = (out.size() + 15) & ~size_t(15);
+        out.resize(off + bytes, 0);
+        std::memcpy(out.data() + off, p, bytes);
+        return int(off);
+    };
+    put(W.data(), W.size() * sizeof(double));
+    for (int ax = 0; ax < 3; ++ax) {
+        const int b = (ax + 1) % 3, c = (ax + 2) % 3;
+        std::vector<std::vector<std::array<long, 3>>> planes;  // (nb, nc, index) per plane m
+        for (size_t i = 0; i < np; ++i) {
+            long n[3];
+            for (int a = 0; a < 3; ++a) n[a] = std::lround(hp->dir_n[i * d + a]);
+            const bool pos = n[ax] > 0 || (n[ax] == 0 && (n[b] > 0 || (n[b] == 0 && n[c] > 0)));
+            if (!pos)
+                for (int a = 0; a < 3; ++a) n[a] = -n[a];
+            if (n[b] < -16 || n[b] > 15 || n[c] < -16 || n[c] > 15) return false;
+            if (size_t(n[ax]) >= planes.size()) planes.resize(size_t(n[ax]) + 1);
+            planes[size_t(n[ax])].push_back({n[b], n[c], long(i)});
+        }
+        const int P = int(planes.size());
+        if (P > lz::kLinePlanes) return false;
+        std::vector<int> L(P, 0);
+        int used = 0;
+        for (int p = 0; p < P; ++p)
+            if (!planes[p].empty()) L[p] = 1, ++used;
+        if (used > 32) return false;
+        auto load = [&](int p) { return L[p] ? (long(planes[p].size()) + L[p] - 1) / L[p] : 0L; };
+        for (; used < 32; ++used) {
+            int best = 0;
+            for (int p = 1; p < P; ++p)
+                if (load(p) > load(best)) best = p;
+            ++L[best];
+        }
+        long K = 0;
+        for (int p = 0; p < P; ++p) K = std::max(K, load(p));
+        const uint32_t pad = uint32_t(np) | (16u << 16) | (16u << 24);
+        std::vector<uint32_t> slots(size_t(K) * 32, pad);
+        std::vector<uint8_t> glo(size_t(P) + 1, 0);
+        int lane = 0;
+        for (int p = 0; p < P; ++p) {
+            glo[p] = uint8_t(lane);
+            auto& pts = planes[p];
+            std::sort(pts.begin(), pts.end());
+            // plane p over lanes [lane, lane + L[p]): balanced contiguous chunks
+            const long sz = long(pts.size());
+            for (int j = 0; j < L[p]; ++j) {
+                const long lo = sz * j / L[p], hi = sz * (j + 1) / L[p];
+                for (long q = lo; q < hi; ++q)
+                    slots[size_t(q - lo) * 32 + lane + j] = uint32_t(pts[q][2]) | (uint32_t(pts[q][0] + 16) << 16) |
+                                                           (uint32_t(pts[q][1] + 16) << 24);
+            }
+            lane += L[p];
+        }
+        glo[P] = uint8_t(lane);
+        hp->line_K[ax] = int(K);
+        hp->line_P[ax] = P;
+        hp->line_slot_off[ax] = put(slots.data(), slots.size() * sizeof(uint32_t));
+        hp->line_meta_off[ax] = put(glo.data(), glo.size());
+    }
+    out.resize((out.size() + 15) & ~size_t(15), 0);
+    hp->line.swap(out);
+    return true;
+}
+
 // trace_z (ATM plans): Z_nu = tr M_{nu+2} exactly (Sum_a z_a^2 |z|^{-nu-2} = |z|^{-nu}), so the
 // kernel takes Z_3 from the trace of the Hessian of Z_5 and the direct weight rows carry only the
 // three Hessian moment channels (nw = 3, loaded in pairs of points); the plain context still
@@ -411,6 +508,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->direct.insert(hp->direct.end(), wts_out.begin(), wts_out.end());
         hp->n_wrows = int(wts_out.size() / hp->nw);
     }
+    hp->line.clear();
+    if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hp->nctx)) hp->line.clear();
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
     std::vector<double> q(nrec * d);
@@ -514,6 +613,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     std::vector<double> t0rows(size_t(hp.nctx + (hp.hess ? 2 : 0)) * lz::kT0, 0.0);
     std::copy(hp.t0c.begin(), hp.t0c.begin() + std::min(hp.t0c.size(), t0rows.size()), t0rows.begin());
     const size_t o_t0 = b.add(t0rows.data(), t0rows.size());
+    if (!hp.line.empty()) b.add(hp.line.data(), hp.line.size());  // last section (kernels.cu stage)
     b.host.resize((b.host.size() + 15) & ~size_t(15), 0);
     unsigned char* dev = nullptr;
     if (!b.host.empty()) {
@@ -541,6 +641,13 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.direct = reinterpret_cast<const double*>(at(o_dir, !hp.direct.empty()));
     P.direct_host = hp.direct.empty() ? nullptr : hp.direct.data();
     P.n_direct = int(hp.direct.size());
+    P.line_bytes = unsigned(hp.line.size());
+    for (int a = 0; a < 3; ++a) {
+        P.line_K[a] = hp.line_K[a];
+        P.line_P[a] = hp.line_P[a];
+        P.line_slot_off[a] = hp.line_slot_off[a];
+        P.line_meta_off[a] = hp.line_meta_off[a];
+    }
     P.n_slabs = hp.n_slabs;
     P.n_rows = hp.n_rows;
     P.rows_off = hp.rows_off;

@@ -57,6 +57,8 @@ struct View {
     // 32-bit shared-window addresses of the staged arrays (SMEM variant): the hot loops load
     // through ld.shared with these, so no generic->shared conversion is re-derived per access
     uint32_t s_dir, s_rec_q, s_coef, s_tdir;
+    uint32_t s_line;       // line-factorised direct block (0: none)
+    uint32_t s_end;        // first byte after the staged image (per-warp scratch follows)
     const double* dir;     // direct-space block (DevPlan::direct)
     const double* rec_q;
     const double* rec_norm;
@@ -75,6 +77,7 @@ __host__ size_t plan_smem_bytes(const DevPlan& P) {
     b += align16(sizeof(double) * size_t(P.tab.ncoef));
     b += align16(sizeof(int) * P.tab.nbins);
     b += align16(sizeof(double) * size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
+    b += align16(P.line_bytes);
     return b;
 }
 
@@ -105,10 +108,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
-template <bool SMEM, bool SKIP_DIR = false>
-__device__ inline View stage(const DevPlan& P, unsigned char* smem) {
+// SHIFT (with SKIP_DIR): the direct block gets no shared-memory space either -- the layout origin
+// is moved down by its size, so the image starts at the dynamic shared-memory base.
+template <bool SMEM, bool SKIP_DIR = false, bool SHIFT = false>
+__device__ inline View stage(const DevPlan& P, unsigned char* smem_base) {
+    static_assert(!SHIFT || SKIP_DIR, "SHIFT drops the (skipped) direct block");
     View v;
-    v.s_dir = v.s_rec_q = v.s_coef = v.s_tdir = 0;
+    v.s_dir = v.s_rec_q = v.s_coef = v.s_tdir = v.s_line = v.s_end = 0;
     if constexpr (!SMEM) {
         v.dir = P.direct;
         v.rec_q = P.rec_q;
@@ -118,6 +124,8 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         v.t0c = P.t0c;
         return v;
     } else {
+        const size_t skip = SKIP_DIR ? align16(sizeof(double) * P.n_direct) : 0;
+        unsigned char* smem = SHIFT ? smem_base - skip : smem_base;
         size_t off = 0;
         double* dd = reinterpret_cast<double*>(smem + off);
         off += align16(sizeof(double) * P.n_direct);
@@ -130,11 +138,13 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         int* td = reinterpret_cast<int*>(smem + off);
         off += align16(sizeof(int) * P.tab.nbins);
         double* tc = reinterpret_cast<double*>(smem + off);
+        off += align16(sizeof(double) * size_t(P.nctx + (P.hess ? 2 : 0)) * kT0);
+        unsigned char* ln = smem + off;
+        off += align16(P.line_bytes);
         // one TMA bulk copy of the plan image (minus the direct block when it travels in the
         // kernel parameters), then the directory is relocated in place
         __shared__ __align__(8) uint64_t bar_storage;
         const uint32_t bar = uint32_t(__cvta_generic_to_shared(&bar_storage));
-        const size_t skip = SKIP_DIR ? align16(sizeof(double) * P.n_direct) : 0;
         const uint32_t total = uint32_t(P.blob_bytes - skip);
         if (threadIdx.x == 0) {
             mbar_init(bar, 1);
@@ -166,6 +176,8 @@ __device__ inline View stage(const DevPlan& P, unsigned char* smem) {
         v.s_rec_q = uint32_t(__cvta_generic_to_shared(rq));
         v.s_coef = uint32_t(__cvta_generic_to_shared(cf));
         v.s_tdir = uint32_t(__cvta_generic_to_shared(td));
+        v.s_line = P.line_bytes ? uint32_t(__cvta_generic_to_shared(ln)) : 0u;
+        v.s_end = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t(off);
         v.dir = dd;
         v.rec_q = rq;
         v.rec_norm = rn;
@@ -192,6 +204,22 @@ __device__ __forceinline__ int lds_s32(uint32_t a) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f64x2(uint32_t a, double x, double y) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
 template <bool SMEM>
 __device__ __forceinline__ double ld_f64(const double* g, uint32_t s, int i) {
@@ -468,12 +496,15 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
 // TRZ (ATM plans built with trace_z): the direct weight rows carry no plain channel and out.z is
 // not formed -- the caller takes Z_{nu} = tr M_{nu+2} from the Hessian (context.cpp/capi.cpp
 // build_host_plan); the plain context's table function still feeds the Hessian's F' (ALIAS).
+// XDIR (line kernel, with TRZ): the direct-space Hessian channels arrive precomputed in hx
+// (line_direct) and the slab walk is skipped.
 template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true, bool CDIR = false,
-          bool TRZ = false>
+          bool TRZ = false, bool XDIR = false>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
-                                          NodeAcc<D, NCTX, HESS, ALIAS>& out) {
+                                          NodeAcc<D, NCTX, HESS, ALIAS>& out, const double* hx = nullptr) {
     static_assert(!TRZ || (HESS && ALIAS), "trace-Z needs the aliased Hessian plan");
+    static_assert(!XDIR || TRZ, "external direct block only for trace-Z plans");
     using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
@@ -495,8 +526,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     for (int c = 0; c < NCTX; ++c) dacc[c] = 0.0;
     double hh[NS > 0 ? NS : 1];
 #pragma unroll
-    for (int c = 0; c < NS; ++c) hh[c] = 0.0;
-    {
+    for (int c = 0; c < NS; ++c) hh[c] = XDIR ? hx[c] : 0.0;
+    if constexpr (!XDIR) {
         double s3, c3, s2 = 0.0, c2 = 1.0;
         sincos2pi(kap[D - 1], s3, c3);
         if constexpr (D >= 2) sincos2pi(kap[D - 2], s2, c2);
@@ -924,6 +955,101 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Line-factorised direct space of the ATM Hessian (capi.cpp build_line_block).  The warp's 32
+// nodes lie on one line kappa = kappa_0 + x e_ax (x = kappa_ax per lane, kappa_0 warp-uniform),
+// so with C_m = sum_{n in half lattice, n_ax = m} W_n e^{2 pi i kappa_0.n} (6 complex channels
+// W_n = hscale w(|z|) z_a z_b, warp-uniform):
+//   hh = sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m].
+// Phase 1: lane l sums its slots (points of one plane) with phases e^{2 pi i (kb nb + kc nc)}
+// from two per-warp tables; phase 2: fixed-order reduction of each plane over its lane group
+// in shared memory; phase 3: per lane, one complex rotation per plane.
+constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
+constexpr uint32_t kLineScrBytes = 12u * kLineScrStride * 8u + 32u;  // 3200 B per warp
+constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
+
+__device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint32_t scr, int ax,
+                                            const double (&kap)[3], double (&hh)[6]) {
+    const int lane = threadIdx.x & 31;
+    // kappa_b, kappa_c (b = ax+1, c = ax+2 mod 3) from lane 0: padding lanes carry dummy nodes
+    const double kb0 = ax == 0 ? kap[1] : ax == 1 ? kap[2] : kap[0];
+    const double kc0 = ax == 0 ? kap[2] : ax == 1 ? kap[0] : kap[1];
+    const double x = ax == 0 ? kap[0] : ax == 1 ? kap[1] : kap[2];
+    const double kb = __shfl_sync(0xffffffffu, kb0, 0), kc = __shfl_sync(0xffffffffu, kc0, 0);
+    {
+        double sn, cs;
+        sincos2pi(kb * double(lane - 16), sn, cs);
+        sts_f64x2(scr + 16u * lane, cs, sn);
+        sincos2pi(kc * double(lane - 16), sn, cs);
+        sts_f64x2(scr + 512u + 16u * lane, cs, sn);
+    }
+    __syncwarp();
+    double acc[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) acc[c] = 0.0;
+    const int K = P.line_K[ax];
+    const uint32_t sl = lb + uint32_t(P.line_slot_off[ax]) + 4u * lane;
+#pragma unroll 1
+    for (int q = 0; q < K; ++q) {
+        const uint32_t wd = lds_u32(sl + 128u * q);
+        const double2 eb = lds_f64x2(scr + ((wd >> 12) & 0x1f0u));
+        const double2 ec = lds_f64x2(scr + 512u + ((wd >> 20) & 0x1f0u));
+        const double cr = fma(eb.x, ec.x, -eb.y * ec.y), ci = fma(eb.x, ec.y, eb.y * ec.x);
+        const uint32_t wa = lb + 48u * (wd & 0xffffu);
+#pragma unroll
+        for (int c = 0; c < 6; c += 2) {
+            const double2 w = lds_f64x2(wa + 8u * c);
+            acc[2 * c] = fma(w.x, cr, acc[2 * c]);
+            acc[2 * c + 1] = fma(w.x, ci, acc[2 * c + 1]);
+            acc[2 * c + 2] = fma(w.y, cr, acc[2 * c + 2]);
+            acc[2 * c + 3] = fma(w.y, ci, acc[2 * c + 3]);
+        }
+    }
+    __syncwarp();  // tables read by every lane before the partials overwrite them
+#pragma unroll
+    for (int c = 0; c < 12; ++c) sts_f64(scr + 8u * (c * kLineScrStride + lane), acc[c]);
+    __syncwarp();
+    const int np = P.line_P[ax];
+    const uint32_t meta = lb + uint32_t(P.line_meta_off[ax]);
+    double res[kLineJobs];
+#pragma unroll
+    for (int r = 0; r < kLineJobs; ++r) {
+        const int j = lane + 32 * r;
+        double sum = 0.0;
+        if (j < 12 * np) {
+            const int p = j / 12, c = j - 12 * p;
+            const int lo = int(lds_u8(meta + p)), hi = int(lds_u8(meta + p + 1));
+            for (int l = lo; l < hi; ++l) sum += lds_f64(scr + 8u * (c * kLineScrStride + l));
+        }
+        res[r] = sum;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kLineJobs; ++r) {
+        const int j = lane + 32 * r;
+        if (j < 12 * np) sts_f64(scr + 8u * j, res[r]);  // C[p][c] at p * 12 + c
+    }
+    __syncwarp();
+    double sx, cx;
+    sincos2pi(x, sx, cx);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) hh[c] = lds_f64(scr + 16u * c);  // Re C_0 (half plane)
+    double cm = cx, sm = sx;  // e^{2 pi i x m}, complex rotation (error linear in m)
+#pragma unroll 1
+    for (int m = 1; m < np; ++m) {
+        const uint32_t cp = scr + 96u * m;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const double2 v = lds_f64x2(cp + 16u * c);
+            hh[c] = fma(v.x, cm, fma(-v.y, sm, hh[c]));
+        }
+        const double cn = fma(cm, cx, -sm * sx);
+        sm = fma(sm, cx, cm * sx);
+        cm = cn;
+    }
+    __syncwarp();  // C read by every lane before the next node's tables overwrite it
+}
+
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
 // One CTA = TPC tiles of 8 warps sharing ONE staged copy of the plan
@@ -935,14 +1061,17 @@ struct __align__(16) DirBlock {
     double w[kDirParam];
 };
 
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR>
+// LINE (ATM, d = 3): direct space by line_direct from the plan's line block (no slab block staged).
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR, bool LINE = false>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NCOMP = MODE == 0 ? 1 : 2;
-    View V = stage<SMEM, CDIR>(P, smem);
+    static_assert(!LINE || (D == 3 && MODE == 1 && SMEM && !CDIR), "line kernel: d = 3 ATM, shared memory");
+    View V = stage<SMEM, CDIR || LINE, LINE>(P, smem);
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t scr = V.s_end + kLineScrBytes * uint32_t(warp_all);  // LINE only
     constexpr int kWarpsPerCta = WPC;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
     // Warps are independent (no block barrier after staging): each takes 32-node patches of the
@@ -975,8 +1104,16 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 kap[a] = u * t[a];  // exact fractional coordinates A^T k
             }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
-            // MODE 1 plans are trace-Z plans (lz_plan_create_atm): Z_3 = tr M_5
-            eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM, CDIR, MODE == 1>(P, V, kap, k, 0, 1, 0u, acc);
+            if constexpr (LINE) {
+                // the warp's nodes share (u, v2, cell): the lane-varying coordinate is kappa_pyr
+                const int pyr = int((patch / (int64_t(g.npu) * g.npv * g.nv2)) % D);
+                double hx[6];
+                line_direct(P, V.s_line, scr, pyr, kap, hx);
+                eval_node<D, NCTX, HESS, true, UNR, true, false, true, true>(P, V, kap, k, 0, 1, 0u, acc, hx);
+            } else {
+                // MODE 1 plans are trace-Z plans (lz_plan_create_atm): Z_3 = tr M_5
+                eval_node<D, NCTX, HESS, MODE == 1, UNR, SMEM, CDIR, MODE == 1>(P, V, kap, k, 0, 1, 0u, acc);
+            }
             if constexpr (MODE == 0) {
                 double prod = 1.0;
 #pragma unroll
@@ -1062,6 +1199,14 @@ __global__ void __launch_bounds__(32 * WPC, 1)
     tile_kernel_c(DevPlan P, DevGrid g, int4 mult, double* __restrict__ partials,
                   const __grid_constant__ DirBlock B) {
     tile_body<D, NCTX, HESS, MODE, true, WPC, UNR, true>(P, g, mult, partials, B.w);
+}
+
+// ATM with the line-factorised direct block (plans with P.line_bytes > 0): WPC warps, each with
+// a kLineScrBytes shared scratch after the staged image.
+template <int WPC, int UNR>
+__global__ void __launch_bounds__(32 * WPC, 1)
+    tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials) {
+    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, nullptr);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -1315,12 +1460,54 @@ static int atm_shape() {
     return shape;
 }
 
+// Line-factorised ATM kernel (plans with a line block): default on, LATSUM_LINE=0 falls back to
+// the slab walk; LATSUM_LINE_WPC in {16, 20, 24, 28, 32} warps per CTA.
+static int line_mode() {
+    static int v = -1;
+    if (v < 0) {
+        v = 28;
+        if (const char* e = std::getenv("LATSUM_LINE")) v = std::atoi(e) == 0 ? 0 : v;
+        if (const char* e = std::getenv("LATSUM_LINE_WPC")) v = v ? std::atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int WPC, int UNR>
+static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
+                                 cudaStream_t st, size_t bytes) {
+    auto kern = tile_kernel_l<WPC, UNR>;
+    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + size_t(WPC) * kLineScrBytes;
+    if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
+    cudaError_t e = set_smem(kern, sm);
+    if (e != cudaSuccess) return e;
+    const int threads = 32 * WPC;
+    const int64_t patches = (g.tile_hi - g.tile_lo) * kTileWarps;
+    int64_t need = (patches + WPC - 1) / WPC;
+    int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
+    int blocks = int(need < cap ? need : cap);
+    if (blocks < 1) return cudaSuccess;
+    kern<<<blocks, threads, sm, st>>>(P, g, partials);
+    return cudaGetLastError();
+}
+
 template <int D, int NCTX, bool HESS, int MODE>
 static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st) {
     const size_t bytes = plan_smem_bytes(P);
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
+    if constexpr (MODE == 1 && D == 3) {
+        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 32u * kLineScrBytes + 2048;
+        if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin())) {
+            switch (line_mode()) {
+                case 16: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 20: return launch_tile_l<20, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 24: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 32: return launch_tile_l<32, 1>(P, g, partials, grid_blocks, st, bytes);
+                default: return launch_tile_l<28, 1>(P, g, partials, grid_blocks, st, bytes);
+            }
+        }
+    }
     if constexpr (MODE == 1) {
         if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host) {
             if constexpr (D == 3) {

@@ -15,6 +15,7 @@ enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
 
 constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
+constexpr int kLinePlanes = 16;  // planes per axis of the line-factorised ATM direct block
 // Degree of the piecewise polynomials (kDeg + 1 coefficients): 7 or 8.  Degree 7 on bins of
 // 0.125 in x saves two DFMA, one DMUL and one 16-byte load per function pair and term but needs
 // ~1.8x the pieces for the same 6e-16 bound; measured slower (fcc ATM 14.4 -> 20.8 ms, C1 2^20
@@ -116,6 +117,12 @@ struct DevPlan {
     DevTable tab;          // functions: nctx plain F_j, then (hess) F', F''
     CtxConst ctx[kMaxCtx];
     CtxConst hctx;         // constants of the Hessian context
+    // Line-factorised direct block (trace-Z ATM plans, d = 3; capi.cpp build_line_block): the
+    // last section of the staged image.  Hessian weight records [n + 1][6] (the last one zero),
+    // then per lattice axis `a` the lane slot words [line_K[a]][32] (point index | (n_b + 16) << 16
+    // | (n_c + 16) << 24) and the lane range of every plane n_a = m (uint8 glo[line_P[a] + 1]).
+    unsigned line_bytes;   // 0: no line block
+    int line_K[3], line_P[3], line_slot_off[3], line_meta_off[3];
 };
 
 // Derivative plan (deriv.cu): one context, derivatives of total order `order` (1..4) at arbitrary
