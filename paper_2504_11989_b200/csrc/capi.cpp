@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -102,6 +103,7 @@ struct HostPlan {
     // line-factorised direct block (trace-Z ATM plans, d = 3; see build_line_block)
     std::vector<unsigned char> line;
     int line_K[3] = {0, 0, 0}, line_P[3] = {0, 0, 0}, line_slot_off[3] = {0, 0, 0}, line_meta_off[3] = {0, 0, 0};
+    double line_sign = 1.0;
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;
@@ -158,17 +160,26 @@ bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
 // on one line of the Duffy grid: kappa = kappa_0 + x e_a with a = the cell's pyramid axis and x
 // varying per lane (kernels.cu line_direct).  Grouping the half lattice by planes n_a = m,
 //   sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m],  C_m = sum_{n_a = m} W_n e^{2 pi i kappa_0.n},
-// the C_m are warp-uniform: the warp computes them cooperatively (each lane a slice of one
-// plane), reduces them through shared memory and every lane finishes with one rotation per plane.
-// Per axis the half lattice is {n : (n_a, n_b, n_c) >lex 0} (b = a+1, c = a+2 mod 3), planes
-// m = 0..M get lane groups sized so that the slots per lane K = max_m ceil(s_m / L_m) is small.
+// the C_m are warp-uniform: the warp computes them cooperatively (each lane a contiguous slice of
+// one plane), reduces them through shared memory and every lane finishes with one rotation per
+// plane.  Per axis the half lattice is {n : (n_a, n_b, n_c) >lex 0} (b = a+1, c = a+2 mod 3);
+// planes m = 0..M get lane groups sized so that the slots per lane K = max_m ceil(s_m / L_m) is
+// small.  W_n = s v v^T with v = sqrt|hscale w| z (s = the common sign), stored in slot order
+// ([slot][lane], conflict-free shared loads) for each axis, with a step code per slot: the
+// phase moves from the lane's previous point by (0, +1) (code 0) or (+1, 1 - code) in (n_b, n_c).
 // Returns false (no line block) when the set does not fit the kernel's fixed limits.
 static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, std::vector<long double>>& wmap,
                              const double* A, long double hscale, int hidx) {
     const int d = 3;
+    const bool dbg = std::getenv("LATSUM_DEBUG_LINE") != nullptr;
+    auto fail = [&](const char* why) {
+        if (dbg) std::fprintf(stderr, "line block: %s\n", why);
+        return false;
+    };
     const size_t np = hp->dir_n.size() / d;
-    if (np == 0 || np >= 65535) return false;
-    std::vector<double> W((np + 1) * 6, 0.0);
+    if (np == 0) return fail("empty direct set");
+    std::vector<std::array<double, 3>> v(np);
+    int sign = 0;
     for (size_t i = 0; i < np; ++i) {
         const double* n = &hp->dir_n[i * d];
         long double z[3];
@@ -176,11 +187,14 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
             z[a] = 0.0L;
             for (int b = 0; b < 3; ++b) z[a] += (long double)A[a * 3 + b] * n[b];
         }
-        const long double wh = wmap.at(pack_key(d, n))[hidx] * hscale;
-        int c = 0;
-        for (int a = 0; a < 3; ++a)
-            for (int b = a; b < 3; ++b) W[i * 6 + c++] = double(wh * z[a] * z[b]);
+        const long double w = wmap.at(pack_key(d, n))[hidx] * hscale;
+        const int sg = w < 0 ? -1 : 1;
+        if (sign != 0 && sg != sign) return fail("mixed weight signs");
+        sign = sg;
+        const long double r = std::sqrt(std::fabs(w));
+        for (int a = 0; a < 3; ++a) v[i][a] = double(r * z[a]);
     }
+    hp->line_sign = double(sign);
     std::vector<unsigned char> out;
     auto put = [&](const void* p, size_t bytes) {
         const size_t off = (out.size() + 15) & ~size_t(15);
@@ -188,7 +202,6 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
         std::memcpy(out.data() + off, p, bytes);
         return int(off);
     };
-    put(W.data(), W.size() * sizeof(double));
     for (int ax = 0; ax < 3; ++ax) {
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
         std::vector<std::vector<std::array<long, 3>>> planes;  // (nb, nc, index) per plane m
@@ -198,17 +211,16 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
             const bool pos = n[ax] > 0 || (n[ax] == 0 && (n[b] > 0 || (n[b] == 0 && n[c] > 0)));
             if (!pos)
                 for (int a = 0; a < 3; ++a) n[a] = -n[a];
-            if (n[b] < -16 || n[b] > 15 || n[c] < -16 || n[c] > 15) return false;
             if (size_t(n[ax]) >= planes.size()) planes.resize(size_t(n[ax]) + 1);
             planes[size_t(n[ax])].push_back({n[b], n[c], long(i)});
         }
         const int P = int(planes.size());
-        if (P > lz::kLinePlanes) return false;
+        if (P > lz::kLinePlanes) return fail("too many planes");
         std::vector<int> L(P, 0);
         int used = 0;
         for (int p = 0; p < P; ++p)
             if (!planes[p].empty()) L[p] = 1, ++used;
-        if (used > 32) return false;
+        if (used > 32) return fail("more planes than lanes");
         auto load = [&](int p) { return L[p] ? (long(planes[p].size()) + L[p] - 1) / L[p] : 0L; };
         for (; used < 32; ++used) {
             int best = 0;
@@ -218,32 +230,59 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
         }
         long K = 0;
         for (int p = 0; p < P; ++p) K = std::max(K, load(p));
-        const uint32_t pad = uint32_t(np) | (16u << 16) | (16u << 24);
-        std::vector<uint32_t> slots(size_t(K) * 32, pad);
+        std::vector<double> v01(size_t(K) * 64, 0.0), v2(size_t(K) * 32, 0.0);
+        std::vector<uint8_t> code(size_t(K) * 32, 0);
+        std::vector<int32_t> init(32, 0);
         std::vector<uint8_t> glo(size_t(P) + 1, 0);
         int lane = 0;
         for (int p = 0; p < P; ++p) {
             glo[p] = uint8_t(lane);
             auto& pts = planes[p];
             std::sort(pts.begin(), pts.end());
-            // plane p over lanes [lane, lane + L[p]): balanced contiguous chunks
+            // plane p over lanes [lane, lane + L[p]): balanced contiguous chunks of the row-major
+            // (n_b, n_c) order, so consecutive slots of a lane are row neighbours or a row change
             const long sz = long(pts.size());
             for (int j = 0; j < L[p]; ++j) {
                 const long lo = sz * j / L[p], hi = sz * (j + 1) / L[p];
-                for (long q = lo; q < hi; ++q)
-                    slots[size_t(q - lo) * 32 + lane + j] = uint32_t(pts[q][2]) | (uint32_t(pts[q][0] + 16) << 16) |
-                                                           (uint32_t(pts[q][1] + 16) << 24);
+                const int ln = lane + j;
+                for (long q = lo; q < hi; ++q) {
+                    const size_t sl = size_t(q - lo) * 32 + ln;
+                    const auto& pt = pts[q];
+                    v01[2 * sl] = v[pt[2]][0];
+                    v01[2 * sl + 1] = v[pt[2]][1];
+                    v2[sl] = v[pt[2]][2];
+                    if (q == lo) {
+                        if (std::labs(pt[0]) > 32767 || std::labs(pt[1]) > 32767) return fail("coordinates");
+                        init[ln] = int32_t((uint32_t(uint16_t(int16_t(pt[0]))) << 16) | uint16_t(int16_t(pt[1])));
+                    } else {
+                        const long dnb = pt[0] - pts[q - 1][0], dnc = pt[1] - pts[q - 1][1];
+                        if (dnb == 0 && dnc == 1) {
+                            code[sl] = 0;
+                        } else if (dnb == 1 && dnc <= 0 && dnc >= -30) {
+                            code[sl] = uint8_t(1 - dnc);
+                        } else {
+                            return fail("row step out of range");
+                        }
+                    }
+                }
             }
             lane += L[p];
         }
         glo[P] = uint8_t(lane);
         hp->line_K[ax] = int(K);
         hp->line_P[ax] = P;
-        hp->line_slot_off[ax] = put(slots.data(), slots.size() * sizeof(uint32_t));
-        hp->line_meta_off[ax] = put(glo.data(), glo.size());
+        hp->line_slot_off[ax] = put(v01.data(), v01.size() * sizeof(double));
+        put(v2.data(), v2.size() * sizeof(double));        // at slot_off + 512 K
+        put(code.data(), code.size());                       // at slot_off + 768 K
+        hp->line_meta_off[ax] = put(init.data(), init.size() * sizeof(int32_t));
+        put(glo.data(), glo.size());                         // at meta_off + 128
     }
     out.resize((out.size() + 15) & ~size_t(15), 0);
     hp->line.swap(out);
+    if (dbg)
+        std::fprintf(stderr, "line block: %zu points, K = %d/%d/%d, planes = %d/%d/%d, %zu bytes\n", np,
+                     hp->line_K[0], hp->line_K[1], hp->line_K[2], hp->line_P[0], hp->line_P[1], hp->line_P[2],
+                     hp->line.size());
     return true;
 }
 
@@ -642,6 +681,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.direct_host = hp.direct.empty() ? nullptr : hp.direct.data();
     P.n_direct = int(hp.direct.size());
     P.line_bytes = unsigned(hp.line.size());
+    P.line_sign = hp.line_sign;
     for (int a = 0; a < 3; ++a) {
         P.line_K[a] = hp.line_K[a];
         P.line_P[a] = hp.line_P[a];

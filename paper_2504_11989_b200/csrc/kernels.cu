@@ -959,11 +959,12 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // Line-factorised direct space of the ATM Hessian (capi.cpp build_line_block).  The warp's 32
 // nodes lie on one line kappa = kappa_0 + x e_ax (x = kappa_ax per lane, kappa_0 warp-uniform),
 // so with C_m = sum_{n in half lattice, n_ax = m} W_n e^{2 pi i kappa_0.n} (6 complex channels
-// W_n = hscale w(|z|) z_a z_b, warp-uniform):
+// W_n = s v v^T, warp-uniform):
 //   hh = sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m].
-// Phase 1: lane l sums its slots (points of one plane) with phases e^{2 pi i (kb nb + kc nc)}
-// from two per-warp tables; phase 2: fixed-order reduction of each plane over its lane group
-// in shared memory; phase 3: per lane, one complex rotation per plane.
+// Phase 1: lane l sums its slots (a contiguous row-major slice of one plane) with the phase
+// carried by complex rotation from slot to slot (step factors from a per-warp table); phase 2:
+// fixed-order reduction of each plane over its lane group in shared memory; phase 3: per lane,
+// one complex rotation per plane.
 constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
 constexpr uint32_t kLineScrBytes = 12u * kLineScrStride * 8u + 32u;  // 3200 B per warp
 constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
@@ -976,41 +977,57 @@ __device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint3
     const double kc0 = ax == 0 ? kap[2] : ax == 1 ? kap[0] : kap[1];
     const double x = ax == 0 ? kap[0] : ax == 1 ? kap[1] : kap[2];
     const double kb = __shfl_sync(0xffffffffu, kb0, 0), kc = __shfl_sync(0xffffffffu, kc0, 0);
+    const int K = P.line_K[ax];
+    const uint32_t sl = lb + uint32_t(P.line_slot_off[ax]);
+    const uint32_t meta = lb + uint32_t(P.line_meta_off[ax]);
+    double pc, ps;  // e^{2 pi i kappa_0.n} at the lane's current point
     {
+        // step table: entry 0 = (0, +1), entry t >= 1 = (+1, 1 - t) in (n_b, n_c)
         double sn, cs;
-        sincos2pi(kb * double(lane - 16), sn, cs);
+        sincos2pi(lane == 0 ? kc : fma(kc, double(1 - lane), kb), sn, cs);
         sts_f64x2(scr + 16u * lane, cs, sn);
-        sincos2pi(kc * double(lane - 16), sn, cs);
-        sts_f64x2(scr + 512u + 16u * lane, cs, sn);
+        const int init = int(lds_u32(meta + 4u * lane));
+        sincos2pi(fma(kb, double(init >> 16), kc * double(int16_t(init & 0xffff))), ps, pc);
     }
     __syncwarp();
     double acc[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) acc[c] = 0.0;
-    const int K = P.line_K[ax];
-    const uint32_t sl = lb + uint32_t(P.line_slot_off[ax]) + 4u * lane;
+    const uint32_t a01 = sl + 16u * lane, a2 = sl + 512u * uint32_t(K) + 8u * lane,
+                   ac = sl + 768u * uint32_t(K) + uint32_t(lane);
 #pragma unroll 1
     for (int q = 0; q < K; ++q) {
-        const uint32_t wd = lds_u32(sl + 128u * q);
-        const double2 eb = lds_f64x2(scr + ((wd >> 12) & 0x1f0u));
-        const double2 ec = lds_f64x2(scr + 512u + ((wd >> 20) & 0x1f0u));
-        const double cr = fma(eb.x, ec.x, -eb.y * ec.y), ci = fma(eb.x, ec.y, eb.y * ec.x);
-        const uint32_t wa = lb + 48u * (wd & 0xffffu);
-#pragma unroll
-        for (int c = 0; c < 6; c += 2) {
-            const double2 w = lds_f64x2(wa + 8u * c);
-            acc[2 * c] = fma(w.x, cr, acc[2 * c]);
-            acc[2 * c + 1] = fma(w.x, ci, acc[2 * c + 1]);
-            acc[2 * c + 2] = fma(w.y, cr, acc[2 * c + 2]);
-            acc[2 * c + 3] = fma(w.y, ci, acc[2 * c + 3]);
+        const double2 v01 = lds_f64x2(a01 + 512u * q);
+        const double v[3] = {v01.x, v01.y, lds_f64(a2 + 256u * q)};
+        if (q > 0) {  // move the phase from the previous slot's point
+            const double2 st = lds_f64x2(scr + 16u * lds_u8(ac + 32u * q));
+            const double pcn = fma(pc, st.x, -ps * st.y);
+            ps = fma(pc, st.y, ps * st.x);
+            pc = pcn;
         }
+        double pr[3], pi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            pr[a] = v[a] * pc;
+            pi[a] = v[a] * ps;
+        }
+        int c = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = a; b < 3; ++b) {
+                acc[2 * c] = fma(pr[a], v[b], acc[2 * c]);
+                acc[2 * c + 1] = fma(pi[a], v[b], acc[2 * c + 1]);
+                ++c;
+            }
     }
-    __syncwarp();  // tables read by every lane before the partials overwrite them
+    __syncwarp();  // table read by every lane before the partials overwrite it
 #pragma unroll
     for (int c = 0; c < 12; ++c) sts_f64(scr + 8u * (c * kLineScrStride + lane), acc[c]);
     __syncwarp();
     const int np = P.line_P[ax];
-    const uint32_t meta = lb + uint32_t(P.line_meta_off[ax]);
+    const uint32_t glo = meta + 128u;
+    const double sgn = P.line_sign;
     double res[kLineJobs];
 #pragma unroll
     for (int r = 0; r < kLineJobs; ++r) {
@@ -1018,10 +1035,10 @@ __device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint3
         double sum = 0.0;
         if (j < 12 * np) {
             const int p = j / 12, c = j - 12 * p;
-            const int lo = int(lds_u8(meta + p)), hi = int(lds_u8(meta + p + 1));
+            const int lo = int(lds_u8(glo + p)), hi = int(lds_u8(glo + p + 1));
             for (int l = lo; l < hi; ++l) sum += lds_f64(scr + 8u * (c * kLineScrStride + l));
         }
-        res[r] = sum;
+        res[r] = sgn * sum;
     }
     __syncwarp();
 #pragma unroll
@@ -1040,8 +1057,8 @@ __device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint3
         const uint32_t cp = scr + 96u * m;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            const double2 v = lds_f64x2(cp + 16u * c);
-            hh[c] = fma(v.x, cm, fma(-v.y, sm, hh[c]));
+            const double2 w = lds_f64x2(cp + 16u * c);
+            hh[c] = fma(w.x, cm, fma(-w.y, sm, hh[c]));
         }
         const double cn = fma(cm, cx, -sm * sx);
         sm = fma(sm, cx, cm * sx);
@@ -1465,7 +1482,7 @@ static int atm_shape() {
 static int line_mode() {
     static int v = -1;
     if (v < 0) {
-        v = 28;
+        v = 24;
         if (const char* e = std::getenv("LATSUM_LINE")) v = std::atoi(e) == 0 ? 0 : v;
         if (const char* e = std::getenv("LATSUM_LINE_WPC")) v = v ? std::atoi(e) : 0;
     }
@@ -1497,14 +1514,15 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
-        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 32u * kLineScrBytes + 2048;
+        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + size_t(line_mode()) * kLineScrBytes + 1024;
         if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin())) {
             switch (line_mode()) {
                 case 16: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 20: return launch_tile_l<20, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 24: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 32: return launch_tile_l<32, 1>(P, g, partials, grid_blocks, st, bytes);
-                default: return launch_tile_l<28, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 28: return launch_tile_l<28, 1>(P, g, partials, grid_blocks, st, bytes);
+                default: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
             }
         }
     }

@@ -118,11 +118,13 @@ struct DevPlan {
     CtxConst ctx[kMaxCtx];
     CtxConst hctx;         // constants of the Hessian context
     // Line-factorised direct block (trace-Z ATM plans, d = 3; capi.cpp build_line_block): the
-    // last section of the staged image.  Hessian weight records [n + 1][6] (the last one zero),
-    // then per lattice axis `a` the lane slot words [line_K[a]][32] (point index | (n_b + 16) << 16
-    // | (n_c + 16) << 24) and the lane range of every plane n_a = m (uint8 glo[line_P[a] + 1]).
+    // last section of the staged image.  Per lattice axis a, at line_slot_off[a]: v0 v1 [K][32]
+    // (double2), v2 [K][32] (double), step codes [K][32] (uint8), K = line_K[a]; at
+    // line_meta_off[a]: each lane's first (n_b, n_c) as int16 pairs [32], then the lane range of
+    // every plane n_a = m (uint8 glo[line_P[a] + 1]).  Hessian channel weight = line_sign v v^T.
     unsigned line_bytes;   // 0: no line block
     int line_K[3], line_P[3], line_slot_off[3], line_meta_off[3];
+    double line_sign;
 };
 
 // Derivative plan (deriv.cu): one context, derivatives of total order `order` (1..4) at arbitrary
