@@ -969,14 +969,16 @@ constexpr int kLineScrStride = 33;                        // doubles per channel
 constexpr uint32_t kLineScrBytes = 12u * kLineScrStride * 8u + 32u;  // 3200 B per warp
 constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
 
-__device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint32_t scr, int ax,
-                                            const double (&kap)[3], double (&hh)[6]) {
+// Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
+// scratch as [m][12] doubles, valid until the next call.
+__device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint32_t scr, int ax,
+                                            const double (&kap)[3]) {
     const int lane = threadIdx.x & 31;
     // kappa_b, kappa_c (b = ax+1, c = ax+2 mod 3) from lane 0: padding lanes carry dummy nodes
     const double kb0 = ax == 0 ? kap[1] : ax == 1 ? kap[2] : kap[0];
     const double kc0 = ax == 0 ? kap[2] : ax == 1 ? kap[0] : kap[1];
-    const double x = ax == 0 ? kap[0] : ax == 1 ? kap[1] : kap[2];
     const double kb = __shfl_sync(0xffffffffu, kb0, 0), kc = __shfl_sync(0xffffffffu, kc0, 0);
+    __syncwarp();  // the previous line's C read by every lane before the tables overwrite it
     const int K = P.line_K[ax];
     const uint32_t sl = lb + uint32_t(P.line_slot_off[ax]);
     const uint32_t meta = lb + uint32_t(P.line_meta_off[ax]);
@@ -1047,6 +1049,13 @@ __device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint3
         if (j < 12 * np) sts_f64(scr + 8u * j, res[r]);  // C[p][c] at p * 12 + c
     }
     __syncwarp();
+}
+
+// Phase 3 for one node of the current line: hh = sum_m Re[e^{2 pi i x m} C_m], x = kappa_ax.
+__device__ __forceinline__ void line_node(const DevPlan& P, uint32_t scr, int ax, const double (&kap)[3],
+                                          double (&hh)[6]) {
+    const int np = P.line_P[ax];
+    const double x = ax == 0 ? kap[0] : ax == 1 ? kap[1] : kap[2];
     double sx, cx;
     sincos2pi(x, sx, cx);
 #pragma unroll
@@ -1064,7 +1073,6 @@ __device__ __forceinline__ void line_direct(const DevPlan& P, uint32_t lb, uint3
         sm = fma(sm, cx, cm * sx);
         cm = cn;
     }
-    __syncwarp();  // C read by every lane before the next node's tables overwrite it
 }
 
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
@@ -1078,7 +1086,9 @@ struct __align__(16) DirBlock {
     double w[kDirParam];
 };
 
-// LINE (ATM, d = 3): direct space by line_direct from the plan's line block (no slab block staged).
+// LINE (ATM, d = 3): direct space from the plan's line block (no slab block staged).  The warp
+// walks lines (cell, v2, u) instead of patches: the per-plane sums C_m depend only on the line,
+// so they are formed once (line_planes) and serve the line's npv patches of 32 v1 nodes each.
 template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR, bool LINE = false>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
@@ -1095,37 +1105,41 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     // shard's range in CTA-contiguous order, writes its warp partial, and the last of a tile's 8
     // warps to finish sums the 8 warp partials in fixed order into the tile slot.
     const int64_t p_lo = g.tile_lo * kTileWarps, p_hi = g.tile_hi * kTileWarps;
-    for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
-         patch += int64_t(gridDim.x) * kWarpsPerCta) {
-        const int64_t tile = patch / kTileWarps;
-        double val[NCOMP];
-#pragma unroll
-        for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
-        double t[D], weight = 0.0, u = 0.0;
+    // node coordinates of (patch, lane); padding lanes get a harmless interior node, weight 0
+    auto node = [&](int64_t patch, double (&k)[D], double (&kap)[D], double& weight) {
+        double t[D], u = 0.0;
+        weight = 0.0;
         const bool ok = patch < g.n_patch && node_of<D>(g, patch, lane, t, weight, u);
-        if (!ok) {  // padding lane: a harmless interior node with zero weight
+        if (!ok) {
 #pragma unroll
             for (int a = 0; a < D; ++a) t[a] = 1.0;
             u = 0.25;
             weight = 0.0;
         }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double sum = 0.0;
+#pragma unroll
+            for (int b = 0; b < D; ++b) sum = fma(P.B[a * D + b], t[b], sum);
+            k[a] = u * sum;     // k = u * w, w = A^{-T} t   (L/quadrature.py:143-152, 417)
+            kap[a] = u * t[a];  // exact fractional coordinates A^T k
+        }
+        return ok;
+    };
+    // one patch: evaluate every lane's node, reduce to the warp partial, commit the tile
+    auto run_patch = [&](int64_t patch, int ax) {
+        const int64_t tile = patch / kTileWarps;
+        double val[NCOMP];
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
+        double k[D], kap[D], weight;
         // every lane of the warp evaluates (the culling bound is a warp reduction)
+        const bool ok = node(patch, k, kap, weight);
         {
-            double k[D], kap[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                double s = 0.0;
-#pragma unroll
-                for (int b = 0; b < D; ++b) s = fma(P.B[a * D + b], t[b], s);
-                k[a] = u * s;       // k = u * w, w = A^{-T} t   (L/quadrature.py:143-152, 417)
-                kap[a] = u * t[a];  // exact fractional coordinates A^T k
-            }
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
             if constexpr (LINE) {
-                // the warp's nodes share (u, v2, cell): the lane-varying coordinate is kappa_pyr
-                const int pyr = int((patch / (int64_t(g.npu) * g.npv * g.nv2)) % D);
                 double hx[6];
-                line_direct(P, V.s_line, scr, pyr, kap, hx);
+                line_node(P, scr, ax, kap, hx);
                 eval_node<D, NCTX, HESS, true, UNR, true, false, true, true>(P, V, kap, k, 0, 1, 0u, acc, hx);
             } else {
                 // MODE 1 plans are trace-Z plans (lz_plan_create_atm): Z_3 = tr M_5
@@ -1194,13 +1208,39 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 __threadfence();
 #pragma unroll
                 for (int c = 0; c < NCOMP; ++c) {
-                    double s = 0.0;
-                    for (int w = 0; w < kTileWarps; ++w) s += __ldcg(&g.wpart[(tile * kTileWarps + w) * NCOMP + c]);
-                    partials[tile * NCOMP + c] = s;
+                    double sum = 0.0;
+                    for (int w = 0; w < kTileWarps; ++w) sum += __ldcg(&g.wpart[(tile * kTileWarps + w) * NCOMP + c]);
+                    partials[tile * NCOMP + c] = sum;
                 }
                 g.tcount[tile] = 0u;  // ready for the next launch
             }
         }
+    };
+    if constexpr (LINE) {
+        // patch = ((outer * npv) + pv) * npu + pu with outer = cell * nv2 + iv2; a line is
+        // (outer, pu).  Lines meeting [p_lo, p_hi) are walked; only in-range patches are run.
+        const int64_t per_outer = int64_t(g.npv) * g.npu;
+        const int64_t l_lo = (p_lo / per_outer) * g.npu, l_hi = ((p_hi - 1) / per_outer + 1) * g.npu;
+        for (int64_t line = l_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; line < l_hi;
+             line += int64_t(gridDim.x) * kWarpsPerCta) {
+            const int64_t outer = line / g.npu, pu = line - outer * g.npu;
+            const int64_t p0 = outer * per_outer + pu;  // pv = 0
+            if (p0 + int64_t(g.npv - 1) * g.npu < p_lo || p0 >= p_hi) continue;
+            const int ax = int((outer / g.nv2) % D);  // the cell's pyramid: lanes vary kappa_ax
+            {
+                double k[D], kap[D], weight;
+                node(p0, k, kap, weight);
+                line_planes(P, V.s_line, scr, ax, kap);
+            }
+            for (int pv = 0; pv < g.npv; ++pv) {
+                const int64_t patch = p0 + int64_t(pv) * g.npu;
+                if (patch >= p_lo && patch < p_hi) run_patch(patch, ax);
+            }
+        }
+    } else {
+        for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
+             patch += int64_t(gridDim.x) * kWarpsPerCta)
+            run_patch(patch, 0);
     }
 }
 
@@ -1482,7 +1522,7 @@ static int atm_shape() {
 static int line_mode() {
     static int v = -1;
     if (v < 0) {
-        v = 24;
+        v = 20;
         if (const char* e = std::getenv("LATSUM_LINE")) v = std::atoi(e) == 0 ? 0 : v;
         if (const char* e = std::getenv("LATSUM_LINE_WPC")) v = v ? std::atoi(e) : 0;
     }
@@ -1498,8 +1538,12 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
     const int threads = 32 * WPC;
-    const int64_t patches = (g.tile_hi - g.tile_lo) * kTileWarps;
-    int64_t need = (patches + WPC - 1) / WPC;
+    if (g.tile_hi <= g.tile_lo) return cudaSuccess;
+    // lines meeting the patch range (tile_body LINE walk)
+    const int64_t p_lo = g.tile_lo * kTileWarps, p_hi = g.tile_hi * kTileWarps;
+    const int64_t per_outer = int64_t(g.npv) * g.npu;
+    const int64_t lines = ((p_hi - 1) / per_outer + 1 - p_lo / per_outer) * g.npu;
+    int64_t need = (lines + WPC - 1) / WPC;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
@@ -1522,7 +1566,7 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
                 case 24: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 32: return launch_tile_l<32, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 28: return launch_tile_l<28, 1>(P, g, partials, grid_blocks, st, bytes);
-                default: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
+                default: return launch_tile_l<20, 1>(P, g, partials, grid_blocks, st, bytes);
             }
         }
     }
