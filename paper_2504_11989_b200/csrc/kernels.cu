@@ -1126,15 +1126,47 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         }
         return ok;
     };
-    // one patch: evaluate every lane's node, reduce to the warp partial, commit the tile
-    auto run_patch = [&](int64_t patch, int ax) {
+    // line kernel: node (cell, iv2, iu, iv1) without the patch decomposition (node_of, D = 3)
+    auto node_at = [&](int cell, int iv2, int iu, int iv1, double (&k)[D], double (&kap)[D], double& weight) {
+        const bool ok = cell < g.n_cell && iu < g.n_u && iv1 < g.n_v;
+        double t[D], u = 0.25;
+        weight = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) t[a] = 1.0;
+        if (ok) {
+            const int pyr = cell % D, sidx = cell / D;
+            double tt[D];
+            tt[0] = ((sidx >> (D - 2)) & 1) ? -2.0 * g.v[iv1] : 2.0 * g.v[iv1];
+            if constexpr (D >= 3) tt[1] = ((sidx >> (D - 3)) & 1) ? -2.0 * g.v[iv2] : 2.0 * g.v[iv2];
+            tt[D - 1] = 1.0;
+            weight = g.wu[iu] * g.wv[iv1] * (D >= 3 ? g.wv[iv2] : 1.0);
+            u = g.u[iu];
+            // np.roll(t, pyramid) (L/quadrature.py:151)
+#pragma unroll
+            for (int i = 0; i < D; ++i) t[i] = pyr == 0 ? tt[i] : pyr == 1 ? tt[(i + D - 1) % D] : tt[(i + D - 2) % D];
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double sum = 0.0;
+#pragma unroll
+            for (int b = 0; b < D; ++b) sum = fma(P.B[a * D + b], t[b], sum);
+            k[a] = u * sum;
+            kap[a] = u * t[a];
+        }
+        return ok;
+    };
+    // one patch: evaluate every lane's node, reduce to the warp partial, commit the tile.
+    // (LINE: the node is given as (cell, iv2, iu, iv1) in `where`; patch is the line numbering.)
+    auto run_patch = [&](int64_t patch, int ax, int4 where) {
         const int64_t tile = patch / kTileWarps;
         double val[NCOMP];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) val[c] = 0.0;
         double k[D], kap[D], weight;
         // every lane of the warp evaluates (the culling bound is a warp reduction)
-        const bool ok = node(patch, k, kap, weight);
+        bool ok;
+        if constexpr (LINE) ok = node_at(where.x, where.y, where.z, where.w, k, kap, weight);
+        else ok = node(patch, k, kap, weight);
         {
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
             if constexpr (LINE) {
@@ -1217,30 +1249,37 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         }
     };
     if constexpr (LINE) {
-        // patch = ((outer * npv) + pv) * npu + pu with outer = cell * nv2 + iv2; a line is
-        // (outer, pu).  Lines meeting [p_lo, p_hi) are walked; only in-range patches are run.
-        const int64_t per_outer = int64_t(g.npv) * g.npu;
-        const int64_t l_lo = (p_lo / per_outer) * g.npu, l_hi = ((p_hi - 1) / per_outer + 1) * g.npu;
-        for (int64_t line = l_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; line < l_hi;
-             line += int64_t(gridDim.x) * kWarpsPerCta) {
-            const int64_t outer = line / g.npu, pu = line - outer * g.npu;
-            const int64_t p0 = outer * per_outer + pu;  // pv = 0
-            if (p0 + int64_t(g.npv - 1) * g.npu < p_lo || p0 >= p_hi) continue;
-            const int ax = int((outer / g.nv2) % D);  // the cell's pyramid: lanes vary kappa_ax
+        // Line-pair numbering (this kernel's own patch order; tiles and partial slots follow it):
+        // the cells pyr + 3 s1 and pyr + 3 s1 + 6 (s0 = +-1) share kappa_0 on every line
+        // (u, v2) -- their lines are mirror images x -> -x -- so one C_m set serves both lines'
+        // npv patches: patch = lp * 2 npv + mirror * npv + pv, lp = (cp * nv2 + iv2) * n_u + iu,
+        // cp = pyr + 3 s1 in [0, n_cell / 2).  Requires pu = 1 (one radial node per warp).
+        const int npv = g.npv;
+        const int64_t per_lp = 2 * int64_t(npv);
+        const int64_t lp_lo = p_lo / per_lp, lp_hi = (p_hi - 1) / per_lp + 1;
+        for (int64_t lp = lp_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; lp < lp_hi;
+             lp += int64_t(gridDim.x) * kWarpsPerCta) {
+            const int iu = int(lp % g.n_u);
+            const int64_t r = lp / g.n_u;
+            const int iv2 = int(r % g.nv2), cp = int(r / g.nv2);
+            const int ax = cp % D;  // the cells' pyramid: lanes vary kappa_ax
+            const int64_t pfirst = lp * per_lp;
             {
                 double k[D], kap[D], weight;
-                node(p0, k, kap, weight);
+                node_at(cp, iv2, iu, lane, k, kap, weight);
                 line_planes(P, V.s_line, scr, ax, kap);
             }
-            for (int pv = 0; pv < g.npv; ++pv) {
-                const int64_t patch = p0 + int64_t(pv) * g.npu;
-                if (patch >= p_lo && patch < p_hi) run_patch(patch, ax);
-            }
+            for (int mirror = 0; mirror < 2; ++mirror)
+                for (int pv = 0; pv < npv; ++pv) {
+                    const int64_t patch = pfirst + mirror * npv + pv;
+                    if (patch >= p_lo && patch < p_hi)
+                        run_patch(patch, ax, make_int4(cp + mirror * (g.n_cell / 2), iv2, iu, pv * 32 + lane));
+                }
         }
     } else {
         for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
              patch += int64_t(gridDim.x) * kWarpsPerCta)
-            run_patch(patch, 0);
+            run_patch(patch, 0, make_int4(0, 0, 0, 0));
     }
 }
 
@@ -1539,10 +1578,10 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     if (e != cudaSuccess) return e;
     const int threads = 32 * WPC;
     if (g.tile_hi <= g.tile_lo) return cudaSuccess;
-    // lines meeting the patch range (tile_body LINE walk)
+    // line pairs meeting the patch range (tile_body LINE walk)
     const int64_t p_lo = g.tile_lo * kTileWarps, p_hi = g.tile_hi * kTileWarps;
-    const int64_t per_outer = int64_t(g.npv) * g.npu;
-    const int64_t lines = ((p_hi - 1) / per_outer + 1 - p_lo / per_outer) * g.npu;
+    const int64_t per_lp = 2 * int64_t(g.npv);
+    const int64_t lines = (p_hi - 1) / per_lp + 1 - p_lo / per_lp;
     int64_t need = (lines + WPC - 1) / WPC;
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
