@@ -164,9 +164,10 @@ bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
 // one plane), reduces them through shared memory and every lane finishes with one rotation per
 // plane.  Per axis the half lattice is {n : (n_a, n_b, n_c) >lex 0} (b = a+1, c = a+2 mod 3);
 // planes m = 0..M get lane groups sized so that the slots per lane K = max_m ceil(s_m / L_m) is
-// small.  W_n = s v v^T with v = sqrt|hscale w| z (s = the common sign), stored in slot order
-// ([slot][lane], conflict-free shared loads) for each axis, with a step code per slot: the
-// phase moves from the lane's previous point by (0, +1) (code 0) or (+1, 1 - code) in (n_b, n_c).
+// small.  W_n = s v v^T with v = sqrt|hscale w| z (s = the common sign), one shared array of v
+// (24-byte records, the last one zero); per axis each slot holds a point index (uint16) and a
+// step code: the phase moves from the lane's previous point by (0, +1) (code 0) or (+1, 1 - code)
+// in (n_b, n_c).
 // Returns false (no line block) when the set does not fit the kernel's fixed limits.
 static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, std::vector<long double>>& wmap,
                              const double* A, long double hscale, int hidx) {
@@ -178,6 +179,7 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
     };
     const size_t np = hp->dir_n.size() / d;
     if (np == 0) return fail("empty direct set");
+    if (np >= 65535) return fail("too many points");
     std::vector<std::array<double, 3>> v(np);
     int sign = 0;
     for (size_t i = 0; i < np; ++i) {
@@ -202,6 +204,12 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
         std::memcpy(out.data() + off, p, bytes);
         return int(off);
     };
+    {
+        std::vector<double> vv((np + 1) * 3, 0.0);
+        for (size_t i = 0; i < np; ++i)
+            for (int a = 0; a < 3; ++a) vv[i * 3 + a] = v[i][a];
+        put(vv.data(), vv.size() * sizeof(double));  // at 0
+    }
     for (int ax = 0; ax < 3; ++ax) {
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
         std::vector<std::vector<std::array<long, 3>>> planes;  // (nb, nc, index) per plane m
@@ -230,7 +238,7 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
         }
         long K = 0;
         for (int p = 0; p < P; ++p) K = std::max(K, load(p));
-        std::vector<double> v01(size_t(K) * 64, 0.0), v2(size_t(K) * 32, 0.0);
+        std::vector<uint16_t> idx(size_t(K) * 32, uint16_t(np));
         std::vector<uint8_t> code(size_t(K) * 32, 0);
         std::vector<int32_t> init(32, 0);
         std::vector<uint8_t> glo(size_t(P) + 1, 0);
@@ -248,9 +256,7 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
                 for (long q = lo; q < hi; ++q) {
                     const size_t sl = size_t(q - lo) * 32 + ln;
                     const auto& pt = pts[q];
-                    v01[2 * sl] = v[pt[2]][0];
-                    v01[2 * sl + 1] = v[pt[2]][1];
-                    v2[sl] = v[pt[2]][2];
+                    idx[sl] = uint16_t(pt[2]);
                     if (q == lo) {
                         if (std::labs(pt[0]) > 32767 || std::labs(pt[1]) > 32767) return fail("coordinates");
                         init[ln] = int32_t((uint32_t(uint16_t(int16_t(pt[0]))) << 16) | uint16_t(int16_t(pt[1])));
@@ -271,9 +277,8 @@ static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, st
         glo[P] = uint8_t(lane);
         hp->line_K[ax] = int(K);
         hp->line_P[ax] = P;
-        hp->line_slot_off[ax] = put(v01.data(), v01.size() * sizeof(double));
-        put(v2.data(), v2.size() * sizeof(double));        // at slot_off + 512 K
-        put(code.data(), code.size());                       // at slot_off + 768 K
+        hp->line_slot_off[ax] = put(idx.data(), idx.size() * sizeof(uint16_t));
+        put(code.data(), code.size());                       // at slot_off + 64 K (K * 64 is 16-aligned)
         hp->line_meta_off[ax] = put(init.data(), init.size() * sizeof(int32_t));
         put(glo.data(), glo.size());                         // at meta_off + 128
     }

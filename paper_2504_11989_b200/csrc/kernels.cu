@@ -210,6 +210,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -961,8 +966,9 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // so with C_m = sum_{n in half lattice, n_ax = m} W_n e^{2 pi i kappa_0.n} (6 complex channels
 // W_n = s v v^T, warp-uniform):
 //   hh = sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m].
-// Phase 1: lane l sums its slots (a contiguous row-major slice of one plane) with the phase
-// carried by complex rotation from slot to slot (step factors from a per-warp table); phase 2:
+// Phase 1: lane l sums its slots (a contiguous row-major slice of one plane, weights gathered by
+// point index) with the phase carried by complex rotation from slot to slot (step factors from a
+// per-warp table); phase 2:
 // fixed-order reduction of each plane over its lane group in shared memory; phase 3: per lane,
 // one complex rotation per plane.
 constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
@@ -995,12 +1001,11 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
     double acc[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) acc[c] = 0.0;
-    const uint32_t a01 = sl + 16u * lane, a2 = sl + 512u * uint32_t(K) + 8u * lane,
-                   ac = sl + 768u * uint32_t(K) + uint32_t(lane);
+    const uint32_t ai = sl + 2u * lane, ac = sl + 64u * uint32_t(K) + uint32_t(lane);
 #pragma unroll 1
     for (int q = 0; q < K; ++q) {
-        const double2 v01 = lds_f64x2(a01 + 512u * q);
-        const double v[3] = {v01.x, v01.y, lds_f64(a2 + 256u * q)};
+        const uint32_t va = lb + 24u * lds_u16(ai + 64u * q);
+        const double v[3] = {lds_f64(va), lds_f64(va + 8u), lds_f64(va + 16u)};
         if (q > 0) {  // move the phase from the previous slot's point
             const double2 st = lds_f64x2(scr + 16u * lds_u8(ac + 32u * q));
             const double pcn = fma(pc, st.x, -ps * st.y);

@@ -118,8 +118,9 @@ struct DevPlan {
     CtxConst ctx[kMaxCtx];
     CtxConst hctx;         // constants of the Hessian context
     // Line-factorised direct block (trace-Z ATM plans, d = 3; capi.cpp build_line_block): the
-    // last section of the staged image.  Per lattice axis a, at line_slot_off[a]: v0 v1 [K][32]
-    // (double2), v2 [K][32] (double), step codes [K][32] (uint8), K = line_K[a]; at
+    // last section of the staged image.  At 0: v [n + 1][3] doubles (the last record zero).  Per
+    // lattice axis a, at line_slot_off[a]: point indices [K][32] (uint16), then step codes [K][32]
+    // (uint8), K = line_K[a]; at
     // line_meta_off[a]: each lane's first (n_b, n_c) as int16 pairs [32], then the lane range of
     // every plane n_a = m (uint8 glo[line_P[a] + 1]).  Hessian channel weight = line_sign v v^T.
     unsigned line_bytes;   // 0: no line block
