@@ -1056,15 +1056,19 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
     __syncwarp();
 }
 
-// Phase 3 for one node of the current line: hh = sum_m Re[e^{2 pi i x m} C_m], x = kappa_ax.
-__device__ __forceinline__ void line_node(const DevPlan& P, uint32_t scr, int ax, const double (&kap)[3],
-                                          double (&hh)[6]) {
+// Phase 3 for the mirror pair of nodes +-x (x = kappa_ax) of the current line:
+//   hh(+-x) = A -+ B,  A = sum_m Re C_m cos 2 pi x m,  B = sum_m Im C_m sin 2 pi x m.
+__device__ __forceinline__ void line_node_pair(const DevPlan& P, uint32_t scr, int ax, double x, double (&hp)[6],
+                                               double (&hm)[6]) {
     const int np = P.line_P[ax];
-    const double x = ax == 0 ? kap[0] : ax == 1 ? kap[1] : kap[2];
     double sx, cx;
     sincos2pi(x, sx, cx);
+    double A[6], B[6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) hh[c] = lds_f64(scr + 16u * c);  // Re C_0 (half plane)
+    for (int c = 0; c < 6; ++c) {
+        A[c] = lds_f64(scr + 16u * c);  // Re C_0 (half plane)
+        B[c] = 0.0;
+    }
     double cm = cx, sm = sx;  // e^{2 pi i x m}, complex rotation (error linear in m)
 #pragma unroll 1
     for (int m = 1; m < np; ++m) {
@@ -1072,11 +1076,17 @@ __device__ __forceinline__ void line_node(const DevPlan& P, uint32_t scr, int ax
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
             const double2 w = lds_f64x2(cp + 16u * c);
-            hh[c] = fma(w.x, cm, fma(-w.y, sm, hh[c]));
+            A[c] = fma(w.x, cm, A[c]);
+            B[c] = fma(w.y, sm, B[c]);
         }
         const double cn = fma(cm, cx, -sm * sx);
         sm = fma(sm, cx, cm * sx);
         cm = cn;
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        hp[c] = A[c] - B[c];
+        hm[c] = A[c] + B[c];
     }
 }
 
@@ -1162,7 +1172,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     };
     // one patch: evaluate every lane's node, reduce to the warp partial, commit the tile.
     // (LINE: the node is given as (cell, iv2, iu, iv1) in `where`; patch is the line numbering.)
-    auto run_patch = [&](int64_t patch, int ax, int4 where) {
+    auto run_patch = [&](int64_t patch, int4 where, const double* hx) {
         const int64_t tile = patch / kTileWarps;
         double val[NCOMP];
 #pragma unroll
@@ -1175,8 +1185,6 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         {
             NodeAcc<D, NCTX, HESS, MODE == 1> acc;
             if constexpr (LINE) {
-                double hx[6];
-                line_node(P, scr, ax, kap, hx);
                 eval_node<D, NCTX, HESS, true, UNR, true, false, true, true>(P, V, kap, k, 0, 1, 0u, acc, hx);
             } else {
                 // MODE 1 plans are trace-Z plans (lz_plan_create_atm): Z_3 = tr M_5
@@ -1274,17 +1282,28 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 node_at(cp, iv2, iu, lane, k, kap, weight);
                 line_planes(P, V.s_line, scr, ax, kap);
             }
-            for (int mirror = 0; mirror < 2; ++mirror)
-                for (int pv = 0; pv < npv; ++pv) {
-                    const int64_t patch = pfirst + mirror * npv + pv;
-                    if (patch >= p_lo && patch < p_hi)
-                        run_patch(patch, ax, make_int4(cp + mirror * (g.n_cell / 2), iv2, iu, pv * 32 + lane));
-                }
+            const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles after C (<= 16 planes)
+            for (int pv = 0; pv < npv; ++pv) {
+                const int64_t patch = pfirst + pv;  // mirror 0; mirror 1 is patch + npv
+                const bool in0 = patch >= p_lo && patch < p_hi, in1 = patch + npv >= p_lo && patch + npv < p_hi;
+                if (!in0 && !in1) continue;
+                const int iv1 = pv * 32 + lane;
+                // x of the mirror-0 node (s0 = +1): kappa_ax = u * 2 v1; the mirror node has -x
+                const double x = iv1 < g.n_v ? 2.0 * g.u[iu < g.n_u ? iu : 0] * g.v[iv1] : 0.0;
+                double hp[6], hm[6];
+                line_node_pair(P, scr, ax, x, hp, hm);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
+                if (in0) run_patch(patch, make_int4(cp, iv2, iu, iv1), hp);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
+                if (in1) run_patch(patch + npv, make_int4(cp + g.n_cell / 2, iv2, iu, iv1), hm);
+            }
         }
     } else {
         for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
              patch += int64_t(gridDim.x) * kWarpsPerCta)
-            run_patch(patch, 0, make_int4(0, 0, 0, 0));
+            run_patch(patch, make_int4(0, 0, 0, 0), nullptr);
     }
 }
 
@@ -1562,13 +1581,23 @@ static int atm_shape() {
 }
 
 // Line-factorised ATM kernel (plans with a line block): default on, LATSUM_LINE=0 falls back to
-// the slab walk; LATSUM_LINE_WPC in {16, 20, 24, 28, 32} warps per CTA.
+// the slab walk; LATSUM_LINE_WPC in {16, 20, 24} warps per CTA.
 static int line_mode() {
     static int v = -1;
     if (v < 0) {
         v = 20;
         if (const char* e = std::getenv("LATSUM_LINE")) v = std::atoi(e) == 0 ? 0 : v;
         if (const char* e = std::getenv("LATSUM_LINE_WPC")) v = v ? std::atoi(e) : 0;
+    }
+    return v;
+}
+
+// q-unroll of the line kernel's reciprocal loop (LATSUM_LINE_UNR in {1, 2})
+static int line_unroll() {
+    static int v = -1;
+    if (v < 0) {
+        v = 1;
+        if (const char* e = std::getenv("LATSUM_LINE_UNR")) v = std::atoi(e) == 2 ? 2 : 1;
     }
     return v;
 }
@@ -1604,12 +1633,12 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if constexpr (MODE == 1 && D == 3) {
         const size_t need = bytes - align16(sizeof(double) * P.n_direct) + size_t(line_mode()) * kLineScrBytes + 1024;
         if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin())) {
-            switch (line_mode()) {
-                case 16: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
-                case 20: return launch_tile_l<20, 1>(P, g, partials, grid_blocks, st, bytes);
-                case 24: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
-                case 32: return launch_tile_l<32, 1>(P, g, partials, grid_blocks, st, bytes);
-                case 28: return launch_tile_l<28, 1>(P, g, partials, grid_blocks, st, bytes);
+            switch (line_mode() * 10 + line_unroll()) {
+                case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 162: return launch_tile_l<16, 2>(P, g, partials, grid_blocks, st, bytes);
+                case 202: return launch_tile_l<20, 2>(P, g, partials, grid_blocks, st, bytes);
+                case 241: return launch_tile_l<24, 1>(P, g, partials, grid_blocks, st, bytes);
+                case 242: return launch_tile_l<24, 2>(P, g, partials, grid_blocks, st, bytes);
                 default: return launch_tile_l<20, 1>(P, g, partials, grid_blocks, st, bytes);
             }
         }
