@@ -45,6 +45,7 @@ namespace lz {
 
 constexpr int kTileWarps = 8;
 constexpr int kTilesPerCta = 3;
+constexpr int kCntEntries = 256;  // line kernel: reciprocal count table (int32 entries)
 
 template <int D> struct Sym { static constexpr int n = D * (D + 1) / 2; };
 
@@ -59,6 +60,8 @@ struct View {
     uint32_t s_dir, s_rec_q, s_coef, s_tdir;
     uint32_t s_line;       // line-factorised direct block (0: none)
     uint32_t s_end;        // first byte after the staged image (per-warp scratch follows)
+    uint32_t s_cnt;        // line kernel: count table cnt[i] = #{q : |q| <= i h} (kCntEntries int32)
+    double cnt_inv_h;      // 1 / h
     const double* dir;     // direct-space block (DevPlan::direct)
     const double* rec_q;
     const double* rec_norm;
@@ -692,10 +695,25 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
     double kmag = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) kmag = fma(k[a], k[a], kmag);
-    kmag = sqrt(kmag);
+    int n_eff, n_in_line = 0;
+    if constexpr (XDIR) {
+        // line warp: |k|^2 is convex along the line, so its maximum is at an end lane (padding
+        // lanes repeat the last node); n_eff / n_in from the count table, rounded outwards /
+        // inwards (r_cut and r_in carry 1e-9 relative margins against rounding)
+        kmag = sqrt(fmax(__shfl_sync(0xffffffffu, kmag, 0), __shfl_sync(0xffffffffu, kmag, 31)));
+        constexpr double kM = 6755399441055744.0;
+        const double xe = fma(P.r_cut + kmag, V.cnt_inv_h, 0.5) + kM;  // floor + 1
+        const double xi = fma(P.r_in - kmag, V.cnt_inv_h, -0.5) + kM;  // floor (or one less)
+        const int ie = min(__double2loint(xe), kCntEntries - 1);
+        const int ii = max(min(__double2loint(xi), kCntEntries - 1), 0);
+        n_eff = int(lds_u32(V.s_cnt + 4u * ie));
+        n_in_line = P.r_in - kmag > 0.0 ? int(lds_u32(V.s_cnt + 4u * ii)) : 0;
+    } else {
+        kmag = sqrt(kmag);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
-    const int n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
+        for (int off = 16; off > 0; off >>= 1) kmag = fmax(kmag, __shfl_xor_sync(0xffffffffu, kmag, off));
+        n_eff = count_le(V.rec_norm, P.n_rec, P.r_cut + kmag);
+    }
     auto accumulate = [&](const double (&y)[(D + 1) & ~1], const double (&f)[NF]) {
 #pragma unroll
         for (int j = 0; j < NCTX; ++j) racc[j] += f[j];
@@ -758,7 +776,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         // q with |q| <= r_in - max|k| are inside the table for every lane of the warp.  (Splitting
         // further at r_lo +- max|k| into compile-time-degree regions, modes 4 / 5, measured no
         // faster on the fcc ATM grid and slower on C1: the degree branch is warp-uniform.)
-        const int n_in = min(n_eff, count_le(V.rec_norm, P.n_rec, P.r_in - kmag));
+        const int n_in = min(n_eff, XDIR ? n_in_line : count_le(V.rec_norm, P.n_rec, P.r_in - kmag));
         int i = gl;
 #pragma unroll UNR
         for (; i < n_in; i += G) term(i, std::integral_constant<int, 3>{});
@@ -1113,7 +1131,19 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     View V = stage<SMEM, CDIR || LINE, LINE>(P, smem);
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t scr = V.s_end + kLineScrBytes * uint32_t(warp_all);  // LINE only
+    // LINE: count table after the image, then the per-warp scratch
+    const uint32_t scr = V.s_end + 4u * kCntEntries + kLineScrBytes * uint32_t(warp_all);
+    if constexpr (LINE) {
+        V.s_cnt = V.s_end;
+        const double qmax = P.n_rec > 0 ? V.rec_norm[P.n_rec - 1] : 1.0;
+        const double h = (qmax > 0.0 ? qmax : 1.0) / double(kCntEntries - 2);
+        V.cnt_inv_h = 1.0 / h;
+        for (int i = threadIdx.x; i < kCntEntries; i += blockDim.x) {
+            const int c = count_le(V.rec_norm, P.n_rec, double(i) * h);
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(V.s_cnt + 4u * i), "r"(c) : "memory");
+        }
+        __syncthreads();
+    }
     constexpr int kWarpsPerCta = WPC;
     const int m[4] = {mult.x, mult.y, mult.z, mult.w};
     // Warps are independent (no block barrier after staging): each takes 32-node patches of the
@@ -1142,19 +1172,21 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         return ok;
     };
     // line kernel: node (cell, iv2, iu, iv1) without the patch decomposition (node_of, D = 3)
-    auto node_at = [&](int cell, int iv2, int iu, int iv1, double (&k)[D], double (&kap)[D], double& weight) {
-        const bool ok = cell < g.n_cell && iu < g.n_u && iv1 < g.n_v;
+    auto node_at = [&](int cell, int iv2, int iu, int iv1_in, double (&k)[D], double (&kap)[D], double& weight) {
+        // lanes past n_v repeat the line's last node (weight 0), so every lane lies on the line
+        const bool ok = cell < g.n_cell && iu < g.n_u && iv1_in < g.n_v;
+        const int iv1 = iv1_in < g.n_v ? iv1_in : g.n_v - 1;
         double t[D], u = 0.25;
         weight = 0.0;
 #pragma unroll
         for (int a = 0; a < D; ++a) t[a] = 1.0;
-        if (ok) {
+        if (cell < g.n_cell && iu < g.n_u) {
             const int pyr = cell % D, sidx = cell / D;
             double tt[D];
             tt[0] = ((sidx >> (D - 2)) & 1) ? -2.0 * g.v[iv1] : 2.0 * g.v[iv1];
             if constexpr (D >= 3) tt[1] = ((sidx >> (D - 3)) & 1) ? -2.0 * g.v[iv2] : 2.0 * g.v[iv2];
             tt[D - 1] = 1.0;
-            weight = g.wu[iu] * g.wv[iv1] * (D >= 3 ? g.wv[iv2] : 1.0);
+            weight = ok ? g.wu[iu] * g.wv[iv1] * (D >= 3 ? g.wv[iv2] : 1.0) : 0.0;
             u = g.u[iu];
             // np.roll(t, pyramid) (L/quadrature.py:151)
 #pragma unroll
@@ -1172,7 +1204,9 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     };
     // one patch: evaluate every lane's node, reduce to the warp partial, commit the tile.
     // (LINE: the node is given as (cell, iv2, iu, iv1) in `where`; patch is the line numbering.)
-    auto run_patch = [&](int64_t patch, int4 where, const double* hx) {
+    // tacc != nullptr (line kernel, tile owned by this warp): add the lane values to tacc instead of
+    // reducing and committing the patch
+    auto run_patch = [&](int64_t patch, int4 where, const double* hx, double* tacc) {
         const int64_t tile = patch / kTileWarps;
         double val[NCOMP];
 #pragma unroll
@@ -1235,6 +1269,11 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 val[1] = ok ? weight * tr3 : 0.0;
             }
         }
+        if (tacc) {
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) tacc[c] += val[c];
+            return;
+        }
         // deterministic tile reduction: fixed xor tree per warp, fixed warp order
         double wv[NCOMP];
 #pragma unroll
@@ -1283,27 +1322,43 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 line_planes(P, V.s_line, scr, ax, kap);
             }
             const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles after C (<= 16 planes)
+            // the line pair is exactly one tile and lies in the range: this warp owns the tile and
+            // sums it directly (per lane in fixed patch order, then one fixed xor tree)
+            const bool own = per_lp == kTileWarps && pfirst >= p_lo && pfirst + per_lp <= p_hi;
+            double tacc[NCOMP];
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) tacc[c] = 0.0;
             for (int pv = 0; pv < npv; ++pv) {
                 const int64_t patch = pfirst + pv;  // mirror 0; mirror 1 is patch + npv
                 const bool in0 = patch >= p_lo && patch < p_hi, in1 = patch + npv >= p_lo && patch + npv < p_hi;
                 if (!in0 && !in1) continue;
                 const int iv1 = pv * 32 + lane;
                 // x of the mirror-0 node (s0 = +1): kappa_ax = u * 2 v1; the mirror node has -x
-                const double x = iv1 < g.n_v ? 2.0 * g.u[iu < g.n_u ? iu : 0] * g.v[iv1] : 0.0;
+                const int iv1c = iv1 < g.n_v ? iv1 : g.n_v - 1;
+                const double x = 2.0 * g.u[iu < g.n_u ? iu : 0] * g.v[iv1c];
                 double hp[6], hm[6];
                 line_node_pair(P, scr, ax, x, hp, hm);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
-                if (in0) run_patch(patch, make_int4(cp, iv2, iu, iv1), hp);
+                if (in0) run_patch(patch, make_int4(cp, iv2, iu, iv1), hp, own ? tacc : nullptr);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
-                if (in1) run_patch(patch + npv, make_int4(cp + g.n_cell / 2, iv2, iu, iv1), hm);
+                if (in1) run_patch(patch + npv, make_int4(cp + g.n_cell / 2, iv2, iu, iv1), hm, own ? tacc : nullptr);
+            }
+            if (own) {
+#pragma unroll
+                for (int c = 0; c < NCOMP; ++c) {
+                    double v = tacc[c];
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    if (lane == 0) partials[(pfirst / kTileWarps) * NCOMP + c] = v;
+                }
             }
         }
     } else {
         for (int64_t patch = p_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; patch < p_hi;
              patch += int64_t(gridDim.x) * kWarpsPerCta)
-            run_patch(patch, make_int4(0, 0, 0, 0), nullptr);
+            run_patch(patch, make_int4(0, 0, 0, 0), nullptr, nullptr);
     }
 }
 
@@ -1606,7 +1661,7 @@ template <int WPC, int UNR>
 static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
     auto kern = tile_kernel_l<WPC, UNR>;
-    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + size_t(WPC) * kLineScrBytes;
+    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + size_t(WPC) * kLineScrBytes;
     if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
@@ -1631,7 +1686,7 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
-        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + size_t(line_mode()) * kLineScrBytes + 1024;
+        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + size_t(line_mode()) * kLineScrBytes + 1024;
         if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin())) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
