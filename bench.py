@@ -32,12 +32,13 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v19); used to turn the live kernel time into FLOP/s.
-FLOPS_PER_NODE = 10119.3
-FLOPS_SOURCE = "ncu r01 v19: 2.5466e+11 FP64 FLOPs per launch / 25,165,824 nodes"
-# ncu r01 v19 dram__bytes_read.sum + dram__bytes_write.sum (plan staging + the warp partials that
-# leave L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
-TRAFFIC_PER_LAUNCH = 534_784 + 1_280_512
+# bench grid (profiles/r01_summary.md, v25: line kernel, split 0.12); used to turn the live kernel
+# time into FLOP/s.  Re-measure whenever the kernel or the ATM split changes.
+FLOPS_PER_NODE = 1616.9
+FLOPS_SOURCE = "ncu r01 v25: 4.0691e+10 FP64 FLOPs per launch / 25,165,824 nodes"
+# ncu r01 v25 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
+# L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
+TRAFFIC_PER_LAUNCH = 221_184 + 0
 
 
 def parse():
@@ -282,7 +283,7 @@ def run_ours(args):
                         "from cold caches", "energy": res.energy},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
                      "frac": achieved / pk.value, "traffic": TRAFFIC_PER_LAUNCH,
-                     "kernel": "lz::tile_kernel_c<3,1,true,1,28,1> (fused ATM integrand, direct block in parameter space)",
+                     "kernel": "lz::tile_kernel_l<20,1> (fused ATM integrand, line-factorised direct space)",
                      "kernel_ms": kern_ms, "flops_per_node": FLOPS_PER_NODE, "flops_source": FLOPS_SOURCE,
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
                                     "no FP64 entry)"},
