@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -365,6 +366,15 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         table_job = std::async(std::launch::async, [&hp, p, sc, nf, c, x_lo_tab, rp] {
             lz::build_table(p, sc, nf, double(c), x_lo_tab, rp, &hp->tab);
         });
+    // LATSUM_TIMING=1: host phase times of the plan build on stderr (tuning aid)
+    const bool timing = std::getenv("LATSUM_TIMING") != nullptr;
+    auto tprev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  plan %-18s %.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tprev).count());
+        tprev = now;
+    };
     union_points(d, dsets, &hp->dir_n);
     std::vector<double> rec_n;
     union_points(d, rsets, &rec_n);
@@ -372,48 +382,60 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
     // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-18) times
     // the summed weights are dropped (|z|^2 factor covers the Hessian channels).
-    // weights of every context at every union point (long double), reused for the ball
-    // truncation and the kernel's weight channels
-    std::vector<const lz::HostCtx*> wctx(plain.begin(), plain.end());
+    // weights of the direct-channel contexts at every union point, reused for the ball truncation
+    // and the kernel's weight channels: the contexts' own weights (the reference's double-precision
+    // w_z, L/epstein.py:139) where the point is in that context's set, else the same formula.
+    // Trace-Z plans carry only the Hessian channel, so only its weights matter there.
+    std::vector<const lz::HostCtx*> wctx;
+    if (!trace_z) wctx.assign(plain.begin(), plain.end());
     if (hess) wctx.push_back(hess);
     std::unordered_map<uint64_t, std::vector<ld>> wmap;
     {
         ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
-        // keep/drop decisions in double precision (magnitudes only), final weights in long double
-        // for the kept points
-        std::vector<double> wabs(np * wctx.size()), mag(np, 0.0);
-        lz::parallel_for(int64_t(np), 128, [&](int64_t i) {
+        std::vector<std::unordered_map<uint64_t, double>> known(wctx.size());
+        for (size_t j = 0; j < wctx.size(); ++j) {
+            const bool h = wctx[j] == hess;
+            const std::vector<double>& nn = h ? hess->hdir_n : wctx[j]->dir_n;
+            const std::vector<double>& ww = h ? hess->hdir_w : wctx[j]->dir_w;
+            known[j].reserve(ww.size() * 2);
+            for (size_t i = 0; i < ww.size(); ++i) known[j].emplace(pack_key(d, &nn[i * d]), ww[i]);
+        }
+        std::vector<double> wv(np * wctx.size()), mag(np, 0.0);
+        lz::parallel_for(int64_t(np), 256, [&](int64_t i) {
             double r2 = 0.0;
             for (int a = 0; a < d; ++a) {
                 double za = 0.0;
                 for (int b = 0; b < d; ++b) za += first->A[a * d + b] * hp->dir_n[i * d + b];
                 r2 += za * za;
             }
+            const uint64_t key = pack_key(d, &hp->dir_n[i * d]);
             for (size_t j = 0; j < wctx.size(); ++j) {
-                const double nu = wctx[j]->k.nu;
-                const double w = std::fabs(lz::upper_gamma<double>(nu / 2.0, lz::kPi * wctx[j]->k.split * r2) *
-                                           std::pow(r2, -nu / 2.0));
-                wabs[i * wctx.size() + j] = w;
-                mag[i] = std::max(mag[i], w * std::max(1.0, r2));
+                const auto it = known[j].find(key);
+                double w;
+                if (it != known[j].end()) {
+                    w = it->second;
+                } else {
+                    const double nu = wctx[j]->k.nu;
+                    w = lz::upper_gamma<double>(nu / 2.0, lz::kPi * wctx[j]->k.split * r2) * std::pow(r2, -nu / 2.0);
+                }
+                wv[i * wctx.size() + j] = w;
+                mag[i] = std::max(mag[i], std::fabs(w) * std::max(1.0, r2));
             }
         });
         double total = 0.0;  // fixed summation order: independent of the thread count
-        for (double w : wabs) total += w;
+        for (double w : wv) total += std::fabs(w);
         std::vector<double> kept;
         for (size_t i = 0; i < np; ++i)
-            if (mag[i] > double(dcut) * total)
+            if (mag[i] > double(dcut) * total) {
                 kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
-        const size_t nk = kept.size() / d;
-        std::vector<std::vector<ld>> wall(nk, std::vector<ld>(wctx.size()));
-        lz::parallel_for(int64_t(nk), 32, [&](int64_t i) {
-            ld z[lz::kMaxDim];
-            for (size_t j = 0; j < wctx.size(); ++j) wall[i][j] = direct_weight(*wctx[j], &kept[i * d], z);
-        });
-        for (size_t i = 0; i < nk; ++i) wmap.emplace(pack_key(d, &kept[i * d]), std::move(wall[i]));
+                wmap.emplace(pack_key(d, &hp->dir_n[i * d]),
+                             std::vector<ld>(wv.begin() + i * wctx.size(), wv.begin() + (i + 1) * wctx.size()));
+            }
         hp->dir_n.swap(kept);
     }
+    lap("union+ball");
     // Direct points as 2D slabs: slab = fixed (n_1 .. n_{d-2}), rows along n_{d-1}, columns along
     // n_d.  The kernel evaluates one sincos per slab; row starts follow by a complex rotation
     // exp(2 pi i kappa_{d-1}) and points along a row by the Chebyshev cosine recurrence in
@@ -462,6 +484,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         if (d >= 2) hp->e2[a] = first->A[a * d + d - 2];
     }
     const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
+    const int hw = int(wctx.size()) - 1;  // the Hessian context's slot in the wmap rows
     {
         const size_t np = hp->dir_n.size() / d;
         const int ns = std::max(d - 2, 0);   // slab key length
@@ -530,7 +553,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                         const int dp = hp->dir_plain;
                         for (int c = 0; c < dp; ++c) wts_out[base + c] = double(w[c]);
                         if (hess) {
-                            const ld wh = w[hp->nctx] * hscale, lp = ld(pt.first) - lc;
+                            const ld wh = w[hw] * hscale, lp = ld(pt.first) - lc;
                             wts_out[base + dp] = double(wh);
                             wts_out[base + dp + 1] = double(wh * lp);
                             wts_out[base + dp + 2] = double(wh * lp * lp);
@@ -552,8 +575,10 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->direct.insert(hp->direct.end(), wts_out.begin(), wts_out.end());
         hp->n_wrows = int(wts_out.size() / hp->nw);
     }
+    lap("slab block");
     hp->line.clear();
-    if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hp->nctx)) hp->line.clear();
+    if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
+    lap("line block");
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
     std::vector<double> q(nrec * d);
@@ -577,6 +602,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         for (int a = 0; a < d; ++a) hp->rec_q[i * d + a] = q[order[i] * d + a];
         hp->rec_norm[i] = double(qn[order[i]]);
     }
+    lap("reciprocal sort");
     // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives)
     {
         const int rows = hp->nctx + (hess ? 2 : 0);
@@ -615,6 +641,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->n_t0 = std::min(need, lz::kT0);
         hp->t0_rho_max = ok ? double(rho_max) : -1.0;
     }
+    lap("q=0 series");
     if (!table_job.valid()) {
         hp->tab = lz::HostTable();
         hp->tab.nfunc = nf;
@@ -624,6 +651,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->r_cut = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L + 1e-9L));
         hp->r_in = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L - 1e-9L));
     }
+    lap("table wait");
 }
 
 // All device arrays of a plan in one allocation and one copy (16-byte aligned sections).

@@ -14,6 +14,10 @@
 //   BrillouinZone.corner_radius L/lattice.py:131-136
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <cmath>
 #include <cstdlib>
@@ -139,11 +143,15 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
     for (int r = 1; r <= kMaxShells; ++r) {
         std::vector<int> shell = integer_shell(d, r);
         const int cnt = int(shell.size()) / d;
-        std::vector<double> sn, sz, sw;
-        ld mag = 0.0L, wsum = 0.0L;
-        for (int i = 0; i < cnt; ++i) {
-            const int* n = &shell[i * d];
-            if (!lex_positive(n, d)) continue;
+        std::vector<int> idx;
+        for (int i = 0; i < cnt; ++i)
+            if (lex_positive(&shell[i * d], d)) idx.push_back(i);
+        const int m = int(idx.size());
+        std::vector<double> sn(size_t(m) * d), sz(size_t(m) * d), sw(m);
+        std::vector<ld> smag(m);
+        // per point in parallel (large shells), reduced below in the fixed point order
+        parallel_for(m, 128, [&](int64_t j) {
+            const int* n = &shell[idx[j] * d];
             ld z[kMaxDim], r2 = 0.0L;
             for (int a = 0; a < d; ++a) {
                 z[a] = 0.0L;
@@ -151,16 +159,20 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
                 r2 += z[a] * z[a];
             }
             // truncation decisions and the reported weights need double precision only (the
-            // reference computes them in double); plan weights are recomputed in long double
+            // reference computes them in double)
             const double xd = double(kPiL * t * r2), r2d = double(r2), nud = double(nu);
-            ld w = upper_gamma<double>(nud / 2.0, xd) * std::pow(r2d, -nud / 2.0);
-            mag = std::max(mag, std::fabs(w) * ld(std::pow(r2d, double(poly_order) / 2.0)));
-            wsum += std::fabs(w);
+            const double w = upper_gamma<double>(nud / 2.0, xd) * std::pow(r2d, -nud / 2.0);
+            smag[j] = std::fabs(ld(w)) * ld(std::pow(r2d, double(poly_order) / 2.0));
             for (int a = 0; a < d; ++a) {
-                sn.push_back(double(n[a]));
-                sz.push_back(double(z[a]));
+                sn[size_t(j) * d + a] = double(n[a]);
+                sz[size_t(j) * d + a] = double(z[a]);
             }
-            sw.push_back(double(w));
+            sw[j] = w;
+        });
+        ld mag = 0.0L, wsum = 0.0L;
+        for (int j = 0; j < m; ++j) {
+            mag = std::max(mag, smag[j]);
+            wsum += std::fabs(ld(sw[j]));
         }
         if (mag > ld(tol) * total) {
             pn->insert(pn->end(), sn.begin(), sn.end());
@@ -204,14 +216,15 @@ static void enumerate_reciprocal(const HostCtx& h, double gamma_order, double to
             if (rq[i] - kmax <= 0.05L) inf = true;
         }
         if (!inf) {
-            for (int i = 0; i < cnt; ++i) {
+            std::vector<ld> bnd(cnt);
+            parallel_for(cnt, 128, [&](int64_t i) {
                 ld r_low = rq[i] - kmax;
                 ld x_low = kPiL * r_low * r_low / t;
                 ld r_pow = (nu >= d) ? rq[i] + kmax : r_low;
-                ld bound = std::fabs(upper_gamma<double>(gamma_order, double(x_low))) *
-                           std::pow(double(r_pow), double(nu) - d);
-                mag = std::max(mag, bound);
-            }
+                bnd[i] = std::fabs(upper_gamma<double>(gamma_order, double(x_low))) *
+                         std::pow(double(r_pow), double(nu) - d);
+            });
+            for (int i = 0; i < cnt; ++i) mag = std::max(mag, ld(bnd[i]));
         }
         if (inf || mag > ld(tol) * total) {
             for (int i = 0; i < cnt; ++i)
@@ -579,19 +592,78 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     if (off >= (size_t(1) << 26)) fail(1, "coefficient table too large");
 }
 
+// Persistent worker pool (created on first use, never torn down: process exit ends the blocked
+// workers).  Several callers may have jobs queued at once (plan builds on different Python
+// threads, the table fit on its async thread); each caller also works on its own job, so nested
+// or concurrent calls always progress.
+namespace {
+struct PJob {
+    const std::function<void(int64_t)>* body;
+    int64_t n, grain;
+    std::atomic<int64_t> next{0}, done{0};
+};
+struct Pool {
+    std::mutex m;
+    std::condition_variable cv, cv_done;
+    std::deque<PJob*> q;
+    explicit Pool(unsigned workers) {
+        for (unsigned i = 0; i < workers; ++i) std::thread([this] { run(); }).detach();
+    }
+    void run() {
+        std::unique_lock<std::mutex> l(m);
+        for (;;) {
+            cv.wait(l, [this] { return !q.empty(); });
+            PJob* j = q.front();
+            const int64_t n = j->n, grain = j->grain;
+            const int64_t b = j->next.fetch_add(grain);
+            if (b >= n) {
+                q.pop_front();  // exhausted (its caller waits for the chunks still running)
+                continue;
+            }
+            l.unlock();
+            const int64_t e = std::min(n, b + grain);
+            for (int64_t i = b; i < e; ++i) (*j->body)(i);
+            const bool last = j->done.fetch_add(e - b) + (e - b) == n;
+            l.lock();
+            if (last) cv_done.notify_all();
+        }
+    }
+};
+Pool& pool(unsigned workers) {
+    static Pool* p = new Pool(workers);
+    return *p;
+}
+}  // namespace
+
 void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t)>& body) {
     grain = std::max<int64_t>(1, grain);
-    unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    if (n < 2 * grain || n < 8) nth = 1;
-    std::atomic<int64_t> next(0);
-    auto worker = [&]() {
-        for (int64_t b = next.fetch_add(grain); b < n; b = next.fetch_add(grain))
-            for (int64_t i = b; i < std::min(n, b + grain); ++i) body(i);
-    };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(worker);
-    worker();
-    for (auto& th : pool) th.join();
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n < 2 * grain || n < 8 || nth == 1) {
+        for (int64_t i = 0; i < n; ++i) body(i);
+        return;
+    }
+    Pool& P = pool(nth - 1);
+    PJob job;
+    job.body = &body;
+    job.n = n;
+    job.grain = grain;
+    {
+        std::lock_guard<std::mutex> l(P.m);
+        P.q.push_back(&job);
+    }
+    P.cv.notify_all();
+    for (int64_t b = job.next.fetch_add(grain); b < n; b = job.next.fetch_add(grain)) {
+        const int64_t e = std::min(n, b + grain);
+        for (int64_t i = b; i < e; ++i) body(i);
+        job.done.fetch_add(e - b);
+    }
+    std::unique_lock<std::mutex> l(P.m);
+    P.cv_done.wait(l, [&] { return job.done.load() == n; });
+    for (auto it = P.q.begin(); it != P.q.end(); ++it)
+        if (*it == &job) {
+            P.q.erase(it);
+            break;
+        }
 }
 
 // Gauss-Legendre nodes/weights on [-1, 1] by Newton iteration on P_n (long double).

@@ -84,7 +84,8 @@ def e2e_breakdown():
         epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        t = 0.45 * fcc.volume ** (-2.0 / 3.0)
+        from paper_2504_11989_b200.quadrature import ATM_SPLIT_SCALE
+        t = ATM_SPLIT_SCALE * fcc.volume ** (-2.0 / 3.0)
         z3 = epstein_context(fcc, 3.0, t)
         z5 = epstein_context(fcc, 5.0, t)
         t1 = time.perf_counter()
