@@ -1390,11 +1390,23 @@ __global__ void reduce_kernel(const double* __restrict__ partials, int64_t n_til
     __shared__ double ss[1024], cc[1024];
     for (int comp = 0; comp < ncomp; ++comp) {
         double s = 0.0, c = 0.0;
-        for (int64_t i = threadIdx.x; i < n_tiles; i += blockDim.x) {
-            const double x = partials[i * ncomp + comp];
-            const double t = s + x;
-            c += (fabs(s) >= fabs(x)) ? (s - t) + x : (x - t) + s;
-            s = t;
+        // the same per-thread sequence, with 8 loads in flight per round (one SM: latency-bound)
+        constexpr int kBatch = 8;
+        for (int64_t i0 = threadIdx.x; i0 < n_tiles; i0 += int64_t(blockDim.x) * kBatch) {
+            double xs[kBatch];
+#pragma unroll
+            for (int r = 0; r < kBatch; ++r) {
+                const int64_t i = i0 + int64_t(r) * blockDim.x;
+                xs[r] = i < n_tiles ? __ldg(&partials[i * ncomp + comp]) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < kBatch; ++r) {
+                if (i0 + int64_t(r) * blockDim.x >= n_tiles) break;
+                const double x = xs[r];
+                const double t = s + x;
+                c += (fabs(s) >= fabs(x)) ? (s - t) + x : (x - t) + s;
+                s = t;
+            }
         }
         ss[threadIdx.x] = s;
         cc[threadIdx.x] = c;
