@@ -475,6 +475,27 @@ __device__ __forceinline__ double series(const double* c, int n, double rho) {
     return acc;
 }
 
+// Two rows of the q = 0 series at once (the Hessian's F' and F''): independent Horner chains,
+// two coefficients per 16-byte load (rows are kT0-aligned and zero past n).
+template <bool SMEM>
+__device__ __forceinline__ void series2(const double* c0, const double* c1, int n, double rho, double& a0,
+                                        double& a1) {
+    a0 = 0.0;
+    a1 = 0.0;
+    uint32_t s0 = 0, s1 = 0;
+    if constexpr (SMEM) {
+        s0 = uint32_t(__cvta_generic_to_shared(c0));
+        s1 = uint32_t(__cvta_generic_to_shared(c1));
+    }
+#pragma unroll 1
+    for (int i = ((n + 1) & ~1) - 2; i >= 0; i -= 2) {
+        const double2 x = SMEM ? lds_f64x2(s0 + 8u * i) : *reinterpret_cast<const double2*>(c0 + i);
+        const double2 y = SMEM ? lds_f64x2(s1 + 8u * i) : *reinterpret_cast<const double2*>(c1 + i);
+        a0 = fma(fma(a0, rho, x.y), rho, x.x);
+        a1 = fma(fma(a1, rho, y.y), rho, y.x);
+    }
+}
+
 // Singular part shat(nu, k) (L/epstein.py:217-231).
 __device__ inline double singular(const CtxConst& C, double rho) {
     if (C.branch == kTrivial) return 0.0;
@@ -859,8 +880,10 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 s1 = -kk * C.s * p1;
                 s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
             }
-            fp = series(V.t0c + NCTX * kT0, P.n_t0, rho) + s1;
-            fpp = series(V.t0c + (NCTX + 1) * kT0, P.n_t0, rho) + s2;
+            double r1, r2;
+            series2<SMEM>(V.t0c + NCTX * kT0, V.t0c + (NCTX + 1) * kT0, P.n_t0, rho, r1, r2);
+            fp = r1 + s1;
+            fpp = r2 + s2;
         } else {
             const double x0 = C.c * rho;
             fp = -pow(C.c, C.s + 1.0) * expint_dev(-C.s, x0);
