@@ -155,28 +155,43 @@ def test_nccl_allreduce_through_cabi():
         dist.destroy_process_group()
 
 
-def test_tile_sharding_bit_identical():
+# (n_u, n_v): 16 -> a tile holds 4 line pairs (atomic tile protocol); 128 -> a line pair is one
+# tile, owned by its warp; 96 -> tiles cut line pairs (ranks share a pair's plane sums); 256 -> a
+# line pair spans two tiles
+@pytest.mark.parametrize("n_u,n_v", [(32, 16), (6, 128), (4, 96), (3, 256)])
+def test_tile_sharding_bit_identical(n_u, n_v):
     """Slot-disjoint partials: any split of the tile range gives bit-identical sums."""
     import torch
 
     from paper_2504_11989_b200.quadrature import Plan
     lat = named_lattice("fcc")
     plan = atm_plan(lat)
-    nn, nt = plan.tiles(32, 16, 3)
+    nn, nt = plan.tiles(n_u, n_v, 3)
     full = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
-    plan.integrate_device(full, 32, 16, 3)
+    plan.integrate_device(full, n_u, n_v, 3)
     for world in (2, 3, 8):
         parts = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
         for r in range(world):
             lo, hi = nt * r // world, nt * (r + 1) // world
             buf = torch.zeros(nt * 2, dtype=torch.float64, device="cuda")
-            plan.integrate_device(buf, 32, 16, 3, lo, hi)
+            plan.integrate_device(buf, n_u, n_v, 3, lo, hi)
             parts += buf  # exact: disjoint slots
         assert torch.equal(parts, full)
     o1 = torch.zeros(2, dtype=torch.float64, device="cuda")
     Plan.reduce_device(full, nt, 2, o1)
-    res = atm_integrals(lat, ATMGrid(32, 16, 3))
+    res = atm_integrals(lat, ATMGrid(n_u, n_v, 3))
     assert float(o1[0]) * 8 == res.zeta333
+
+
+@pytest.mark.parametrize("name", ["fcc", "bcc"])
+def test_atm_line_kernel_partial_patches_vs_oracle(name):
+    """n_v = 40: the second 32-node patch of every line has 24 padding lanes (they repeat the
+    line's last node with weight 0, keeping the warp on one line); against the oracle."""
+    lat = named_lattice(name)
+    res = atm_integrals(lat, ATMGrid(2, 40, 3))
+    s = O.atm_grid(lat.a, 2, 40, 3)
+    assert abs(res.zeta333 - 8 * s[0]) <= 1e-12 * abs(8 * s[0])
+    assert abs(res.dot_term - 8 * s[1]) <= 1e-12 * max(1.0, abs(8 * s[1]))
 
 
 @pytest.mark.parametrize("name", ["integer_1d", "square", "fcc", "bcc"])
