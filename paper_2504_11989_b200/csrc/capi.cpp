@@ -485,6 +485,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     }
     const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
     const int hw = int(wctx.size()) - 1;  // the Hessian context's slot in the wmap rows
+    // the slab block (built last, below, unless the line block replaces it)
+    auto build_slab = [&]() {
     {
         const size_t np = hp->dir_n.size() / d;
         const int ns = std::max(d - 2, 0);   // slab key length
@@ -575,7 +577,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->direct.insert(hp->direct.end(), wts_out.begin(), wts_out.end());
         hp->n_wrows = int(wts_out.size() / hp->nw);
     }
-    lap("slab block");
+    };
     hp->line.clear();
     if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
     lap("line block");
@@ -652,6 +654,21 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->r_in = double(std::sqrt(ld(hp->tab.x_hi) / c) * (1.0L - 1e-9L));
     }
     lap("table wait");
+    // The line kernel (kernels.cu tile_kernel_l) does not read the slab block: skip it when the
+    // line block exists, the kernel is not disabled (LATSUM_LINE=0) and its shared-memory image
+    // (everything but the slab block, the count table and 24 warp scratches) fits comfortably.
+    bool need_slab = hp->line.empty();
+    if (!need_slab) {
+        const char* e = std::getenv("LATSUM_LINE");
+        const size_t qs = size_t((d + 1) & ~1);
+        auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+        const size_t img = a16(8 * hp->rec_norm.size() * qs) + a16(8 * hp->rec_norm.size()) +
+                           a16(8 * hp->tab.coef.size()) + a16(4 * hp->tab.dir.size()) +
+                           a16(8 * size_t(hp->nctx + 2) * lz::kT0) + a16(hp->line.size());
+        need_slab = (e && std::atoi(e) == 0) || img + 1024 + 24 * 3200 + 8192 > 227 * 1024;
+    }
+    if (need_slab) build_slab();
+    lap("slab block");
 }
 
 // All device arrays of a plan in one allocation and one copy (16-byte aligned sections).

@@ -17,6 +17,7 @@
 #include <condition_variable>
 #include <deque>
 #include <functional>
+#include <future>
 #include <mutex>
 #include <thread>
 #include <cmath>
@@ -302,9 +303,14 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
         k.sing_coef = double(std::pow(kPiL, nul - ld(d) / 2.0L) * std::tgamma((ld(d) - nul) / 2.0L) /
                              std::tgamma(nul / 2.0L));
     }
+    h->want_hess = deriv_order >= 2 ? 1 : 0;
+    // the Hessian's widened sets (needed by every Hessian / ATM plan) are enumerated on a second
+    // thread while the plain sets are: context creation costs the longer of the two
+    std::future<void> hess;
+    if (h->want_hess) hess = std::async(std::launch::async, [h] { build_hess_sets(*h); });
     enumerate_direct(*h, 0, kTermCutoff, &h->dir_n, &h->dir_z, &h->dir_w);
     enumerate_reciprocal(*h, k.s, kTermCutoff, &h->rec_n, &h->rec_q);
-    h->want_hess = deriv_order >= 2 ? 1 : 0;  // Hessian sets are enumerated on first use
+    if (hess.valid()) hess.get();
 }
 
 void build_hess_sets(HostCtx& h) {

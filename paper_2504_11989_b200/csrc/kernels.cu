@@ -1733,6 +1733,8 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
             }
         }
     }
+    // plans whose slab block was skipped (capi.cpp build_host_plan) run only on the line kernel
+    if (MODE == 1 && P.line_bytes && P.n_direct == 0) return cudaErrorInvalidValue;
     if constexpr (MODE == 1) {
         if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host) {
             if constexpr (D == 3) {
