@@ -801,8 +801,57 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         int i = gl;
 #pragma unroll UNR
         for (; i < n_in; i += G) term(i, std::integral_constant<int, 3>{});
+        if constexpr (XDIR) {
+            // line warp: the lanes' k lie on the segment [k(lane 0), k(lane 31)], so a q whose
+            // distance from -q to the segment exceeds r_cut is zero for every lane.  Each lane
+            // tests one candidate, the survivors (ballot) are evaluated in order.
+            double k0[D], dv[D], dd = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                k0[a] = __shfl_sync(0xffffffffu, k[a], 0);
+                dv[a] = __shfl_sync(0xffffffffu, k[a], 31) - k0[a];
+                dd = fma(dv[a], dv[a], dd);
+            }
+            const double idd = dd > 0.0 ? 1.0 / dd : 0.0;
+            const double rc2 = P.r_cut * P.r_cut * (1.0 + 1e-12);
+            const int lane = threadIdx.x & 31;
+            for (int i0 = n_in; i0 < n_eff; i0 += 32) {
+                bool hit = false;
+                if (i0 + lane < n_eff) {
+                    constexpr int QS = (D + 1) & ~1;
+                    double w[QS];
+#pragma unroll
+                    for (int a = 0; a < QS; a += 2) {
+                        const double2 q2 = ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, (i0 + lane) * QS + a);
+                        w[a] = q2.x;
+                        w[a + 1] = q2.y;
+                    }
+                    double wd = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        w[a] += k0[a];
+                        wd = fma(w[a], dv[a], wd);
+                    }
+                    const double t = fmin(fmax(-wd * idd, 0.0), 1.0);
+                    double e2 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        const double e = fma(t, dv[a], w[a]);
+                        e2 = fma(e, e, e2);
+                    }
+                    hit = e2 <= rc2;
+                }
+                unsigned m = __ballot_sync(0xffffffffu, hit);
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    term(i0 + b, std::integral_constant<int, 1>{});
+                }
+            }
+        } else {
 #pragma unroll UNR
-        for (; i < n_eff; i += G) term(i, std::integral_constant<int, 1>{});
+            for (; i < n_eff; i += G) term(i, std::integral_constant<int, 1>{});
+        }
     } else {
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 2>{});
