@@ -94,6 +94,7 @@ struct HostPlan {
     int dir_plain = 0;  // plain-context channels in the direct weight rows (0 for trace-Z ATM plans)
     double c = 0.0, r_cut = 0.0, r_in = 0.0, alias_ratio = 0.0;
     std::vector<double> dir_n, rec_q, rec_norm, t0c;
+    std::vector<double> rq_pad;   // rec_q at the padded stride (d + 1) & ~1 (device image layout)
     // direct space: [slab records][row records][weight rows] (see build_host_plan)
     std::vector<double> direct;
     int n_slabs = 0, n_rows = 0, rows_off = 0, w_off = 0, n_wrows = 0;
@@ -604,6 +605,12 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         for (int a = 0; a < d; ++a) hp->rec_q[i * d + a] = q[order[i] * d + a];
         hp->rec_norm[i] = double(qn[order[i]]);
     }
+    {
+        const int qs = (d + 1) & ~1;
+        hp->rq_pad.assign(nrec * qs, 0.0);
+        for (size_t i = 0; i < nrec; ++i)
+            for (int a = 0; a < d; ++a) hp->rq_pad[i * qs + a] = hp->rec_q[i * d + a];
+    }
     lap("reciprocal sort");
     // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives)
     {
@@ -665,7 +672,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         const size_t img = a16(8 * hp->rec_norm.size() * qs) + a16(8 * hp->rec_norm.size()) +
                            a16(8 * hp->tab.coef.size()) + a16(4 * hp->tab.dir.size()) +
                            a16(8 * size_t(hp->nctx + 2) * lz::kT0) + a16(hp->line.size());
-        need_slab = (e && std::atoi(e) == 0) || img + 1024 + 24 * 3200 + 8192 > 227 * 1024;
+        need_slab = (e && std::atoi(e) == 0) || img + 1024 + 24 * 3200 + 8192 > 227 * 1024 ||
+                    hp->rec_norm.size() > 720;  // kernels.cu kLineQ
     }
     if (need_slab) build_slab();
     lap("slab block");
@@ -686,11 +694,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     lz::DevPlan P;
     std::memset(&P, 0, sizeof(P));
     // reciprocal vectors padded to an even stride (16-byte aligned double2 loads)
-    const int qs = (hp.d + 1) & ~1;
-    const size_t nrec = hp.rec_q.size() / hp.d;
-    std::vector<double> rq(nrec * qs, 0.0);
-    for (size_t i = 0; i < nrec; ++i)
-        for (int a = 0; a < hp.d; ++a) rq[i * qs + a] = hp.rec_q[i * hp.d + a];
+    const std::vector<double>& rq = hp.rq_pad;
     // section order and 16-byte alignment = the kernel's shared-memory image (stage<true>), so the
     // kernel stages the plan with one bulk copy
     Blob b;
@@ -730,6 +734,8 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.direct = reinterpret_cast<const double*>(at(o_dir, !hp.direct.empty()));
     P.direct_host = hp.direct.empty() ? nullptr : hp.direct.data();
     P.n_direct = int(hp.direct.size());
+    P.t0_host = hp.t0c.data();
+    P.rq_host = hp.rq_pad.data();
     P.line_bytes = unsigned(hp.line.size());
     P.line_sign = hp.line_sign;
     for (int a = 0; a < 3; ++a) {

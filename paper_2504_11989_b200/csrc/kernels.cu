@@ -62,6 +62,10 @@ struct View {
     uint32_t s_end;        // first byte after the staged image (per-warp scratch follows)
     uint32_t s_cnt;        // line kernel: count table cnt[i] = #{q : |q| <= i h} (kCntEntries int32)
     double cnt_inv_h;      // 1 / h
+    // line kernel: warp-uniform reads from the kernel's parameter space (LineParam): the
+    // reciprocal vectors (padded stride) and the Hessian's two q = 0 series rows
+    const double* p_rq;
+    const double* p_t0;
     const double* dir;     // direct-space block (DevPlan::direct)
     const double* rec_q;
     const double* rec_norm;
@@ -759,7 +763,9 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         double y[QS];
 #pragma unroll
         for (int a = 0; a < QS; a += 2) {
-            const double2 q2 = ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, i * QS + a);
+            // XDIR: i is warp-uniform, the parameter-space copy gives uniform constant loads
+            const double2 q2 = XDIR ? *reinterpret_cast<const double2*>(V.p_rq + i * QS + a)
+                                    : ld_f64x2<SMEM>(V.rec_q, V.s_rec_q, i * QS + a);
             y[a] = q2.x;
             y[a + 1] = q2.y;
         }
@@ -930,7 +936,8 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
             }
             double r1, r2;
-            series2<SMEM>(V.t0c + NCTX * kT0, V.t0c + (NCTX + 1) * kT0, P.n_t0, rho, r1, r2);
+            if constexpr (XDIR) series2<false>(V.p_t0, V.p_t0 + kT0, P.n_t0, rho, r1, r2);
+            else series2<SMEM>(V.t0c + NCTX * kT0, V.t0c + (NCTX + 1) * kT0, P.n_t0, rho, r1, r2);
             fp = r1 + s1;
             fpp = r2 + s2;
         } else {
@@ -1187,6 +1194,13 @@ __device__ __forceinline__ void line_node_pair(const DevPlan& P, uint32_t scr, i
 // Direct-space block passed by value in the kernel parameters (CDIR variant; 28 KB leaves room
 // for DevPlan and DevGrid within the 32764-byte parameter limit).
 constexpr int kDirParam = 3584;
+// line kernel parameter block: the Hessian's two q = 0 series rows and up to kLineQ reciprocal
+// vectors at the padded stride 4 (d = 3)
+constexpr int kLineQ = 720;
+struct __align__(16) LineParam {
+    double t0[2 * kT0];
+    double rq[kLineQ * 4];
+};
 struct __align__(16) DirBlock {
     double w[kDirParam];
 };
@@ -1206,6 +1220,8 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     // LINE: count table after the image, then the per-warp scratch
     const uint32_t scr = V.s_end + 4u * kCntEntries + kLineScrBytes * uint32_t(warp_all);
     if constexpr (LINE) {
+        V.p_t0 = cdir;                // LineParam::t0
+        V.p_rq = cdir + 2 * kT0;      // LineParam::rq
         V.s_cnt = V.s_end;
         const double qmax = P.n_rec > 0 ? V.rec_norm[P.n_rec - 1] : 1.0;
         const double h = (qmax > 0.0 ? qmax : 1.0) / double(kCntEntries - 2);
@@ -1449,11 +1465,12 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 }
 
 // ATM with the line-factorised direct block (plans with P.line_bytes > 0): WPC warps, each with
-// a kLineScrBytes shared scratch after the staged image.
+// a kLineScrBytes shared scratch after the staged image.  The warp-uniform reads of the
+// reciprocal loop and the q = 0 series come from the parameter block (constant cache, no LSU).
 template <int WPC, int UNR>
 __global__ void __launch_bounds__(32 * WPC, 1)
-    tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials) {
-    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, nullptr);
+    tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials, const __grid_constant__ LineParam LP) {
+    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, LP.t0);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -1749,6 +1766,12 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
+    static_assert(sizeof(DevPlan) + sizeof(DevGrid) + sizeof(double*) + 16 + sizeof(LineParam) <= 32764,
+                  "kernel parameters exceed the 32 KB limit");
+    if (P.n_rec > kLineQ || P.nctx != 1 || !P.t0_host || !P.rq_host) return cudaErrorInvalidValue;
+    thread_local LineParam lp;  // host staging of the parameter block (copied at launch)
+    std::memcpy(lp.t0, P.t0_host + size_t(P.nctx) * kT0, sizeof(double) * 2 * kT0);
+    std::memcpy(lp.rq, P.rq_host, sizeof(double) * 4 * size_t(P.n_rec));
     const int threads = 32 * WPC;
     if (g.tile_hi <= g.tile_lo) return cudaSuccess;
     // line pairs meeting the patch range (tile_body LINE walk)
@@ -1759,7 +1782,7 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
-    kern<<<blocks, threads, sm, st>>>(P, g, partials);
+    kern<<<blocks, threads, sm, st>>>(P, g, partials, lp);
     return cudaGetLastError();
 }
 
@@ -1771,7 +1794,8 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
         const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + size_t(line_mode()) * kLineScrBytes + 1024;
-        if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin())) {
+        if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin()) &&
+            P.n_rec <= kLineQ) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 162: return launch_tile_l<16, 2>(P, g, partials, grid_blocks, st, bytes);

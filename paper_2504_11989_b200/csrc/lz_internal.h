@@ -123,6 +123,8 @@ struct DevPlan {
     // (uint8), K = line_K[a]; at
     // line_meta_off[a]: each lane's first (n_b, n_c) as int16 pairs [32], then the lane range of
     // every plane n_a = m (uint8 glo[line_P[a] + 1]).  Hessian channel weight = line_sign v v^T.
+    const double* t0_host;  // host copy (plan-owned) of the q = 0 series rows [nctx + 2][kT0]
+    const double* rq_host;  // host copy (plan-owned) of rec_q at the padded stride (d + 1) & ~1
     unsigned line_bytes;   // 0: no line block
     int line_K[3], line_P[3], line_slot_off[3], line_meta_off[3];
     double line_sign;
