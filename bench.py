@@ -32,13 +32,13 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v25: line kernel, split 0.12); used to turn the live kernel
+# bench grid (profiles/r01_summary.md, v27: line kernel, split 0.12); used to turn the live kernel
 # time into FLOP/s.  Re-measure whenever the kernel or the ATM split changes.
-FLOPS_PER_NODE = 1616.9
-FLOPS_SOURCE = "ncu r01 v25: 4.0691e+10 FP64 FLOPs per launch / 25,165,824 nodes"
-# ncu r01 v25 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
+FLOPS_PER_NODE = 1566.3
+FLOPS_SOURCE = "ncu r01 v27: 3.9418e+10 FP64 FLOPs per launch / 25,165,824 nodes"
+# ncu r01 v27 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
 # L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
-TRAFFIC_PER_LAUNCH = 221_184 + 0
+TRAFFIC_PER_LAUNCH = 218_880 + 0
 
 
 def parse():
