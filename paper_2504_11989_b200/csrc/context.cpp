@@ -21,6 +21,7 @@
 #include <mutex>
 #include <thread>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -292,6 +293,11 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
     k.pref = double(1.0L / std::tgamma(nul / 2.0L));
     k.rfac = double(std::pow(kPiL, nul - ld(d) / 2.0L) / vol);
     k.bconst = double(-2.0L * std::pow(kPiL * t, nul / 2.0L) / nul);
+    {
+        const double q4 = 2.0 * (k.nu - double(d));
+        k.sing_q4 = (std::fabs(q4 - std::nearbyint(q4)) < 1e-12 && std::fabs(q4) <= 64.0) ? int(std::nearbyint(q4))
+                                                                                          : kNoQuarter;
+    }
     k.pi_over_t_pow_s = double(std::pow(kPiL / t, (ld(d) - nul) / 2.0L));
     if (k.branch == kLogCase) {
         int m = k.log_m;
@@ -556,6 +562,10 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     for (int b = 0; b < nbins; ++b)
         if (fits[b].level == kDirectMarker) last_direct = b;
     for (int b = 0; b < last_direct; ++b) fits[b].level = kDirectMarker;
+    if (std::getenv("LATSUM_DEBUG_TABLE"))
+        std::fprintf(stderr, "table: p0 %.3f nfunc %d x_lo %.4f x_hi %.3f bins %d direct-bins %d (up to x = %.3f)\n",
+                     p[0], nfunc, x_lo, double(out->x_hi), nbins, last_direct + (last_direct >= 0 ? 1 : 0),
+                     double(ld(x_lo) + hb * (last_direct + 1)));
     size_t off = 0;
     out->npieces = 0;
     out->n_lo_bins = 0;

@@ -500,6 +500,24 @@ __device__ __forceinline__ void series2(const double* c0, const double* c1, int 
     }
 }
 
+// rho^{n/4} by square roots and binary powering (correctly rounded sqrt, a few ulp overall; the
+// accurate pow costs ~10x more and ran once or twice per point of a zeta batch).
+__device__ __forceinline__ double pow_quarter(double rho, int n) {
+    const int a = n >> 2, b = n & 3;  // n = 4a + b, a = floor(n / 4)
+    double r = 1.0;
+    if (b) {
+        const double r2 = sqrt(rho);
+        r = (b & 2) ? r2 : 1.0;
+        if (b & 1) r *= sqrt(r2);
+    }
+    double p = 1.0, base = rho;
+    for (int m = a < 0 ? -a : a; m; m >>= 1) {
+        if (m & 1) p *= base;
+        base *= base;
+    }
+    return a < 0 ? r / p : r * p;
+}
+
 // Singular part shat(nu, k) (L/epstein.py:217-231).
 __device__ inline double singular(const CtxConst& C, double rho) {
     if (C.branch == kTrivial) return 0.0;
@@ -508,7 +526,7 @@ __device__ inline double singular(const CtxConst& C, double rho) {
         for (int i = 0; i < C.log_m; ++i) rm *= rho;
         return C.sing_coef * rm * log(kPi * rho);
     }
-    return C.sing_coef * pow(rho, 0.5 * (C.nu - double(C.d)));
+    return C.sing_coef * (C.sing_q4 != kNoQuarter ? pow_quarter(rho, C.sing_q4) : pow(rho, 0.5 * (C.nu - double(C.d))));
 }
 
 // ---------------------------------------------------------------------------
@@ -931,7 +949,7 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 s1 = kk * rm1 * (double(m) * L + 1.0);
                 s2 = kk * (rm1 / rho) * (double(m * (m - 1)) * L + double(2 * m - 1));
             } else {
-                const double p1 = pow(rho, -C.s - 1.0);
+                const double p1 = C.sing_q4 != kNoQuarter ? pow_quarter(rho, C.sing_q4 - 4) : pow(rho, -C.s - 1.0);
                 s1 = -kk * C.s * p1;
                 s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
             }

@@ -43,11 +43,15 @@ constexpr int kT0 = 64;             // max terms of the q = 0 power series
 
 // ---------------------------------------------------------------------------
 // Per-(lattice, nu) constants of the Crandall split (L/epstein.py:99-122, 202-259).
+constexpr int kNoQuarter = -1000000;  // CtxConst::sing_q4: exponent not a multiple of 1/4
 struct CtxConst {
     int branch;
     int log_m;
     int pole;            // |nu - d| < 1e-10: simple pole of the continuation at k in Lambda*
     int d;
+    int sing_q4;         // 2 (nu - d) when it is an integer (|k|^{nu-d} = rho^{sing_q4/4} by square
+                         // roots and products instead of pow), else kNoQuarter
+    int pad_q4;
     double nu, s;        // s = s_rec = (d - nu)/2
     double pref, rfac, bconst;
     double vol, inv_vol, split, c;   // c = pi / split
