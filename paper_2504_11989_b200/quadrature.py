@@ -26,7 +26,7 @@ from functools import lru_cache
 import numpy as np
 
 from . import _native as N
-from .epstein import TRIVIAL, epstein_context
+from .epstein import TRIVIAL, EpsteinContext, epstein_context
 from .errors import PoleError
 from .lattice import Lattice
 
@@ -254,7 +254,9 @@ def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
 
     with ThreadPoolExecutor(max_workers=2) as pool:
         f5 = pool.submit(z5_with_sets)
-        z3 = epstein_context(lattice, 3.0, splitting)
+        # Z_3 only lends the plan its constants and reciprocal set (the kernel takes Z_3 = tr M_5),
+        # so its own context skips the Hessian point sets; it is private to this (cached) plan
+        z3 = EpsteinContext(lattice, 3.0, splitting, deriv_order=0)
         z5 = f5.result()
     h = C.c_void_p()
     N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)), "atm plan")
