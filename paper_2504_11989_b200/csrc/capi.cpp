@@ -128,7 +128,11 @@ uint64_t pack_key(int d, const double* n) {
 
 void union_points(int d, const std::vector<const std::vector<double>*>& sets, std::vector<double>* out) {
     out->clear();
+    size_t total = 0;
+    for (const auto* s : sets) total += s->size() / d;
     std::unordered_set<uint64_t> seen;
+    seen.reserve(2 * total);
+    out->reserve(total * d);
     for (const auto* s : sets) {
         const size_t cnt = s->size() / d;
         for (size_t i = 0; i < cnt; ++i)
@@ -136,6 +140,18 @@ void union_points(int d, const std::vector<const std::vector<double>*>& sets, st
                 out->insert(out->end(), s->begin() + i * d, s->begin() + (i + 1) * d);
     }
 }
+
+// Weights of the kept direct points, one row of `nw` channels per point, found by packed key.
+struct WeightMap {
+    std::unordered_map<uint64_t, uint32_t> idx;
+    std::vector<long double> rows;
+    size_t nw = 0;
+    void add(uint64_t key, const double* w) {
+        idx.emplace(key, uint32_t(rows.size() / nw));
+        rows.insert(rows.end(), w, w + nw);
+    }
+    const long double* at(uint64_t key) const { return &rows[size_t(idx.at(key)) * nw]; }
+};
 
 // Direct-space weight w_z = Gamma(nu/2, pi t |z|^2) |z|^-nu (L/epstein.py:139), long double.
 ld direct_weight(const lz::HostCtx& h, const double* n, ld* z) {
@@ -171,7 +187,7 @@ bool rec_n_empty(const std::vector<const std::vector<double>*>& sets) {
 // step code: the phase moves from the lane's previous point by (0, +1) (code 0) or (+1, 1 - code)
 // in (n_b, n_c).
 // Returns false (no line block) when the set does not fit the kernel's fixed limits.
-static bool build_line_block(HostPlan* hp, const std::unordered_map<uint64_t, std::vector<long double>>& wmap,
+static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
                              const double* A, long double hscale, int hidx) {
     const int d = 3;
     const bool dbg = std::getenv("LATSUM_DEBUG_LINE") != nullptr;
@@ -311,7 +327,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         if (c->k.split != first->k.split) throw Error{LZ_EINVAL, "fused contexts must share the split"};
         if (std::memcmp(c->A, first->A, sizeof(c->A)) != 0)
             throw Error{LZ_EINVAL, "fused contexts must share the lattice"};
-        dsets.push_back(&c->dir_n);
+        if (!trace_z) dsets.push_back(&c->dir_n);  // trace-Z: the direct rows carry the Hessian only
         rsets.push_back(&c->rec_n);
     }
     if (hess) {
@@ -379,6 +395,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     union_points(d, dsets, &hp->dir_n);
     std::vector<double> rec_n;
     union_points(d, rsets, &rec_n);
+    lap("unions");
     // Ball truncation of the direct set: the reference appends whole max-norm shells
     // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
     // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-18) times
@@ -390,7 +407,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     std::vector<const lz::HostCtx*> wctx;
     if (!trace_z) wctx.assign(plain.begin(), plain.end());
     if (hess) wctx.push_back(hess);
-    std::unordered_map<uint64_t, std::vector<ld>> wmap;
+    WeightMap wmap;
+    wmap.nw = wctx.size();
     {
         ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
@@ -403,6 +421,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             known[j].reserve(ww.size() * 2);
             for (size_t i = 0; i < ww.size(); ++i) known[j].emplace(pack_key(d, &nn[i * d]), ww[i]);
         }
+        lap("known maps");
         std::vector<double> wv(np * wctx.size()), mag(np, 0.0);
         lz::parallel_for(int64_t(np), 256, [&](int64_t i) {
             double r2 = 0.0;
@@ -428,11 +447,11 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         double total = 0.0;  // fixed summation order: independent of the thread count
         for (double w : wv) total += std::fabs(w);
         std::vector<double> kept;
+        wmap.idx.reserve(2 * np);
         for (size_t i = 0; i < np; ++i)
             if (mag[i] > double(dcut) * total) {
                 kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
-                wmap.emplace(pack_key(d, &hp->dir_n[i * d]),
-                             std::vector<ld>(wv.begin() + i * wctx.size(), wv.begin() + (i + 1) * wctx.size()));
+                wmap.add(pack_key(d, &hp->dir_n[i * d]), &wv[i * wctx.size()]);
             }
         hp->dir_n.swap(kept);
     }
@@ -449,18 +468,16 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // slab folds carry the j' and zc parts.
     {
         const size_t np = hp->dir_n.size() / d;
-        std::vector<size_t> ord(np);
-        for (size_t i = 0; i < np; ++i) ord[i] = i;
-        auto key = [&](size_t i, int a) { return std::lround(hp->dir_n[i * d + a]); };
-        std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-            for (int j = 0; j < d; ++j)
-                if (key(a, j) != key(b, j)) return key(a, j) < key(b, j);
-            return false;
-        });
+        // lexicographic order = order of the packed keys (most significant field first; the
+        // points are distinct, so no ties)
+        std::vector<std::pair<uint64_t, uint32_t>> ord(np);
+        for (size_t i = 0; i < np; ++i) ord[i] = {pack_key(d, &hp->dir_n[i * d]), uint32_t(i)};
+        std::sort(ord.begin(), ord.end());
         std::vector<double> pts(np * d);
         for (size_t i = 0; i < np; ++i)
-            for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[ord[i] * d + a];
+            for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[size_t(ord[i].second) * d + a];
         hp->dir_n.swap(pts);
+        auto key = [&](size_t i, int a) { return std::lround(hp->dir_n[i * d + a]); };
         // maximal runs (for plan info only)
         hp->run_info.clear();
         for (size_t i = 0; i < np; ++i) {
@@ -552,7 +569,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                     wts_out.resize(wts_out.size() + size_t(lenp) * hp->nw, 0.0);
                     for (const auto& pt : r.pts) {
                         const size_t base = (row0 + size_t(pt.first - lo)) * hp->nw;
-                        const std::vector<ld>& w = wmap.at(pack_key(d, &hp->dir_n[pt.second * d]));
+                        const ld* w = wmap.at(pack_key(d, &hp->dir_n[pt.second * d]));
                         const int dp = hp->dir_plain;
                         for (int c = 0; c < dp; ++c) wts_out[base + c] = double(w[c]);
                         if (hess) {
@@ -579,6 +596,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->n_wrows = int(wts_out.size() / hp->nw);
     }
     };
+    lap("sort");
     hp->line.clear();
     if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
     lap("line block");
