@@ -290,3 +290,18 @@ def test_atm_energy_split_invariance(scale):
     if scale == 0.2:
         info = atm_plan(lat, t).info()
         assert info.n_dir * 4 > 3584  # direct block exceeds the 28 KB parameter block
+
+
+@pytest.mark.parametrize("seed", [3, 11])
+def test_atm_line_kernel_skewed_lattice_vs_oracle(seed):
+    """Line-factorised ATM kernel on a generic (skewed, anisotropic) 3D lattice: its line block
+    (plane grouping per pyramid axis, step codes, v = sqrt|w| z) against the long-double oracle."""
+    from paper_2504_11989_b200 import Lattice
+    rng = np.random.default_rng(seed)
+    a = (np.eye(3) + rng.uniform(-0.25, 0.25, (3, 3))) * rng.uniform(0.8, 1.3)
+    lat = Lattice(a)
+    res = atm_integrals(lat, ATMGrid(2, 8, 3))
+    s = O.atm_grid(lat.a, 2, 8, 3)
+    assert abs(res.zeta333 - 8 * s[0]) <= 1e-12 * abs(8 * s[0])
+    assert abs(res.dot_term - 8 * s[1]) <= 1e-12 * max(1.0, abs(8 * s[1]))
+    assert atm_plan(lat).info().n_dir > 0
