@@ -146,10 +146,6 @@ struct WeightMap {
     std::unordered_map<uint64_t, uint32_t> idx;
     std::vector<long double> rows;
     size_t nw = 0;
-    void add(uint64_t key, const double* w) {
-        idx.emplace(key, uint32_t(rows.size() / nw));
-        rows.insert(rows.end(), w, w + nw);
-    }
     const long double* at(uint64_t key) const { return &rows[size_t(idx.at(key)) * nw]; }
 };
 
@@ -400,9 +396,10 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // (L/epstein.py:134-149), i.e. a half cube whose corners carry weights many orders below
     // its 1e-18 term cutoff; points whose every channel is below `dcut` (default 1e-18) times
     // the summed weights are dropped (|z|^2 factor covers the Hessian channels).
-    // weights of the direct-channel contexts at every union point, reused for the ball truncation
-    // and the kernel's weight channels: the contexts' own weights (the reference's double-precision
-    // w_z, L/epstein.py:139) where the point is in that context's set, else the same formula.
+    // weights of the direct-channel contexts at every union point for the ball truncation: the
+    // contexts' own weights (the reference's double-precision w_z, L/epstein.py:139) where the
+    // point is in that context's set, else the same formula; the kept points' channel weights are
+    // then recomputed in long double.
     // Trace-Z plans carry only the Hessian channel, so only its weights matter there.
     std::vector<const lz::HostCtx*> wctx;
     if (!trace_z) wctx.assign(plain.begin(), plain.end());
@@ -447,12 +444,20 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         double total = 0.0;  // fixed summation order: independent of the thread count
         for (double w : wv) total += std::fabs(w);
         std::vector<double> kept;
-        wmap.idx.reserve(2 * np);
         for (size_t i = 0; i < np; ++i)
-            if (mag[i] > double(dcut) * total) {
+            if (mag[i] > double(dcut) * total)
                 kept.insert(kept.end(), hp->dir_n.begin() + i * d, hp->dir_n.begin() + (i + 1) * d);
-                wmap.add(pack_key(d, &hp->dir_n[i * d]), &wv[i * wctx.size()]);
-            }
+        // the kept points' weights in long double: the double-precision w_z are good to ~1e-15,
+        // which the cancellation between the regular and singular parts near the log-case
+        // exponents (nu -> d + 2m) can amplify past the 1e-12 parity bar
+        const size_t nk = kept.size() / d, nwc = wctx.size();
+        wmap.idx.reserve(2 * nk);
+        wmap.rows.assign(nk * nwc, 0.0L);
+        lz::parallel_for(int64_t(nk), 32, [&](int64_t i) {
+            ld z[lz::kMaxDim];
+            for (size_t j = 0; j < nwc; ++j) wmap.rows[size_t(i) * nwc + j] = direct_weight(*wctx[j], &kept[i * d], z);
+        });
+        for (size_t i = 0; i < nk; ++i) wmap.idx.emplace(pack_key(d, &kept[i * d]), uint32_t(i));
         hp->dir_n.swap(kept);
     }
     lap("union+ball");
