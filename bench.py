@@ -39,6 +39,8 @@ FLOPS_SOURCE = "ncu r01 v27: 3.9418e+10 FP64 FLOPs per launch / 25,165,824 nodes
 # ncu r01 v27 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
 # L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
 TRAFFIC_PER_LAUNCH = 218_880 + 0
+NCU_UTIL = {"fp64_pipe_active": 0.547, "issue_active": 0.560, "lsu_wavefronts": 0.641,
+            "warps_active": 0.310, "source": "ncu r01 v27 (--set full, one launch)"}
 
 
 def parse():
@@ -286,7 +288,11 @@ def run_ours(args):
                      "kernel": "lz::tile_kernel_l<20,1> (fused ATM integrand, line-factorised direct space)",
                      "kernel_ms": kern_ms, "flops_per_node": FLOPS_PER_NODE, "flops_source": FLOPS_SOURCE,
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
-                                    "no FP64 entry)"},
+                                    "no FP64 entry)",
+                     # utilisation counters of the same kernel from the ncu --set full capture
+                     # (profiles/r01_atm_v27_metrics.json): the FLOP fraction counts DADD/DMUL as one
+                     # FLOP although they occupy the FP64 pipe like a DFMA
+                     "ncu": NCU_UTIL},
         "gpu_launches": 2 * args.steps,
         "clocks": clk,
     }
