@@ -153,11 +153,13 @@ def lib():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        # LATSUM_LIB: load another build of the library (A/B timing of kernel variants)
+        path = os.environ.get("LATSUM_LIB") or LIB_PATH
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"latsum_b200 native library not found at {LIB_PATH}; run "
+                f"latsum_b200 native library not found at {path}; run "
                 "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res
