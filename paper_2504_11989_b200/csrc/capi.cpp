@@ -218,12 +218,13 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         std::memcpy(out.data() + off, p, bytes);
         return int(off);
     };
-    {
-        std::vector<double> vv((np + 1) * 3, 0.0);
-        for (size_t i = 0; i < np; ++i)
-            for (int a = 0; a < 3; ++a) vv[i * 3 + a] = v[i][a];
-        put(vv.data(), vv.size() * sizeof(double));  // at 0
-    }
+    struct AxisBlock {
+        std::vector<uint16_t> idx;
+        std::vector<uint8_t> code, glo;
+        std::vector<int32_t> init;
+        int K = 0, P = 0;
+    };
+    AxisBlock blk[3];
     for (int ax = 0; ax < 3; ++ax) {
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
         std::vector<std::vector<std::array<long, 3>>> planes;  // (nb, nc, index) per plane m
@@ -289,12 +290,94 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
             lane += L[p];
         }
         glo[P] = uint8_t(lane);
-        hp->line_K[ax] = int(K);
-        hp->line_P[ax] = P;
-        hp->line_slot_off[ax] = put(idx.data(), idx.size() * sizeof(uint16_t));
-        put(code.data(), code.size());                       // at slot_off + 64 K (K * 64 is 16-aligned)
-        hp->line_meta_off[ax] = put(init.data(), init.size() * sizeof(int32_t));
-        put(glo.data(), glo.size());                         // at meta_off + 128
+        blk[ax].idx.swap(idx);
+        blk[ax].code.swap(code);
+        blk[ax].glo.swap(glo);
+        blk[ax].init.swap(init);
+        blk[ax].K = int(K);
+        blk[ax].P = P;
+    }
+    // Bank-aware order of the v records: a 24-byte record at position pos starts in bank pair
+    // 6 pos mod 32, i.e. its bank depends on pos mod 16.  The 32 lanes of every (axis, slot)
+    // gather 32 records; residues pos mod 16 are chosen so that no residue occurs more than
+    // twice in any such group where possible (two wavefronts per 8-byte gather instead of ~5.6
+    // for an arbitrary order), then record i goes to pos = 16 k + residue(i).
+    std::vector<int> res(np, -1), perm(np, 0);
+    {
+        std::vector<std::array<int, 3>> groups(np, {-1, -1, -1});  // group id per axis
+        int ng = 0;
+        for (int ax = 0; ax < 3; ++ax) {
+            for (int q = 0; q < blk[ax].K; ++q, ++ng)
+                for (int l = 0; l < 32; ++l) {
+                    const int i = blk[ax].idx[size_t(q) * 32 + l];
+                    if (i < int(np)) groups[size_t(i)][ax] = ng;
+                }
+        }
+        const int cap = int((np + 15) / 16);
+        std::vector<std::array<int, 16>> cnt(static_cast<size_t>(ng));
+        for (auto& c16 : cnt) c16.fill(0);
+        std::array<int, 16> load;
+        load.fill(0);
+        auto cost = [&](size_t i, int r) {
+            int c = 0;
+            for (int ax = 0; ax < 3; ++ax) {
+                const int g = groups[i][ax];
+                if (g >= 0) c += std::max(0, cnt[size_t(g)][r] + 1 - 2);
+            }
+            return c;
+        };
+        auto place = [&](size_t i, int r, int sgn) {
+            for (int ax = 0; ax < 3; ++ax)
+                if (groups[i][ax] >= 0) cnt[size_t(groups[i][ax])][r] += sgn;
+            load[r] += sgn;
+        };
+        for (size_t i = 0; i < np; ++i) {
+            int best = -1, bc = 0;
+            for (int r = 0; r < 16; ++r) {
+                if (load[r] >= cap) continue;
+                const int c = cost(i, r);
+                if (best < 0 || c < bc || (c == bc && load[r] < load[best])) best = r, bc = c;
+            }
+            res[i] = best;
+            place(i, best, +1);
+        }
+        // one repair pass over the points that still sit in an over-full group
+        for (size_t i = 0; i < np; ++i) {
+            if (cost(i, res[i]) <= 0 && [&] {
+                    for (int ax = 0; ax < 3; ++ax)
+                        if (groups[i][ax] >= 0 && cnt[size_t(groups[i][ax])][res[i]] > 2) return false;
+                    return true;
+                }())
+                continue;
+            place(i, res[i], -1);
+            int best = res[i], bc = cost(i, res[i]);
+            for (int r = 0; r < 16 && bc > 0; ++r) {
+                if (r == res[i] || load[r] >= cap) continue;
+                const int c = cost(i, r);
+                if (c < bc) best = r, bc = c;
+            }
+            res[i] = best;
+            place(i, best, +1);
+        }
+        std::array<int, 16> next;
+        next.fill(0);
+        for (size_t i = 0; i < np; ++i) perm[i] = 16 * next[res[i]]++ + res[i];
+        const int nrec = 16 * cap + 1;  // the last record (a multiple of 16) is the zero padding
+        if (nrec >= 65535) return fail("too many points");
+        std::vector<double> vv(size_t(nrec) * 3, 0.0);
+        for (size_t i = 0; i < np; ++i)
+            for (int a = 0; a < 3; ++a) vv[size_t(perm[i]) * 3 + a] = v[i][a];
+        put(vv.data(), vv.size() * sizeof(double));  // at 0
+        for (int ax = 0; ax < 3; ++ax)
+            for (auto& ix : blk[ax].idx) ix = uint16_t(ix < np ? perm[ix] : nrec - 1);
+    }
+    for (int ax = 0; ax < 3; ++ax) {
+        hp->line_K[ax] = blk[ax].K;
+        hp->line_P[ax] = blk[ax].P;
+        hp->line_slot_off[ax] = put(blk[ax].idx.data(), blk[ax].idx.size() * sizeof(uint16_t));
+        put(blk[ax].code.data(), blk[ax].code.size());       // at slot_off + 64 K (K * 64 is 16-aligned)
+        hp->line_meta_off[ax] = put(blk[ax].init.data(), blk[ax].init.size() * sizeof(int32_t));
+        put(blk[ax].glo.data(), blk[ax].glo.size());          // at meta_off + 128
     }
     out.resize((out.size() + 15) & ~size_t(15), 0);
     hp->line.swap(out);

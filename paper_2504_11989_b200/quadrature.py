@@ -237,7 +237,7 @@ def product_plan(lattice: Lattice, nus_key: tuple, splitting: float | None = Non
 # (L/epstein.py:107).  The lattice sum is split-invariant; a smaller split moves work from the
 # reciprocal sum (table lookups, ~64 instructions per term) to the direct sum (phase rotations,
 # ~18 per point).  Measured on B200: see DESIGN.md section 3.2.
-ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "0.12"))
+ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "0.13"))
 
 
 @lru_cache(maxsize=64)
