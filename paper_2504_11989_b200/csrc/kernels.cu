@@ -13,8 +13,8 @@
 // per-term scipy gammaincc + recurrence (L/incgamma.py:78-94).
 //
 // Direct space is walked in 2D slabs (one sincos per slab, complex rotation per row,
-// Chebyshev cosine recurrence along rows); the plan is staged into shared memory by one TMA
-// bulk copy (the ATM kernel keeps its direct block in the kernel's parameter space instead).
+// Chebyshev cosine recurrence along rows) except in the line-factorised ATM kernel; the plan
+// is staged into shared memory by one TMA bulk copy.
 //
 // Kernels:
 //   batch_kernel   : Z or Hessian at a batch of k (C1), G lanes per point
@@ -23,8 +23,12 @@
 //                    L/quadrature.py:393-397) or the ATM integrand
 //                    [Z_3^3, tr M_5^3] (C3), reduced deterministically to one
 //                    partial per 256-node tile (slot-disjoint for multi-GPU)
-//   tile_kernel_c  : the ATM variant with the direct block in parameter space and
-//                    a free warps-per-CTA count (28 on B200)
+//   tile_kernel_l  : the ATM kernel (d = 3, default): line-factorised direct space --
+//                    a warp's 32 nodes lie on one line of the grid, so the direct sum
+//                    becomes warp-uniform plane sums C_m (formed once per line pair of
+//                    mirror cells, 8 patches) plus one rotation per plane and node
+//   tile_kernel_c  : the previous ATM variant (fallback, LATSUM_LINE=0) with the direct
+//                    block in parameter space and a free warps-per-CTA count
 //   reduce_kernel  : fixed-order compensated sum of the tile partials
 //   fp64_probe     : DFMA-chain peak probe for the roofline denominator
 // (deriv.cu: order-m derivatives; direct.cu: brute-force direct sums.)
