@@ -305,3 +305,16 @@ def test_atm_line_kernel_skewed_lattice_vs_oracle(seed):
     assert abs(res.zeta333 - 8 * s[0]) <= 1e-12 * abs(8 * s[0])
     assert abs(res.dot_term - 8 * s[1]) <= 1e-12 * max(1.0, abs(8 * s[1]))
     assert atm_plan(lat).info().n_dir > 0
+
+
+@pytest.mark.parametrize("u", [[[1, 1, 0], [0, 1, 0], [0, 0, 1]], [[1, 0, 0], [1, 1, 0], [-1, 0, 1]]])
+def test_atm_energy_basis_invariance(u):
+    """The ATM energy is a property of the lattice, not of its basis: fcc with a unimodular change
+    of basis (different line blocks, pyramid axes and reciprocal bookkeeping) gives the same sum
+    to the quadrature/rounding level (the Duffy cells follow the basis, so the grids differ)."""
+    from paper_2504_11989_b200 import Lattice
+    fcc = named_lattice("fcc")
+    other = Lattice(fcc.a @ np.array(u, dtype=float))
+    e0 = atm_cohesive_energy(fcc, grid=ATMGrid(64, 64, 3))
+    e1 = atm_cohesive_energy(other, grid=ATMGrid(64, 64, 3))
+    assert abs(e1 - e0) <= 1e-8 * abs(e0), (e0, e1)
