@@ -1114,7 +1114,9 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
         sincos2pi(lane == 0 ? kc : fma(kc, double(1 - lane), kb), sn, cs);
         sts_f64x2(scr + 16u * lane, cs, sn);
         const int init = int(lds_u32(meta + 4u * lane));
-        sincos2pi(fma(kb, double(init >> 16), kc * double(int16_t(init & 0xffff))), ps, pc);
+        // one (0, +1) step before the lane's first point: slot 0 carries step code 0, so every
+        // slot (the first included) applies its step without a branch
+        sincos2pi(fma(kb, double(init >> 16), kc * double(int16_t(init & 0xffff) - 1)), ps, pc);
     }
     __syncwarp();
     double acc[12];
@@ -1125,7 +1127,7 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
     for (int q = 0; q < K; ++q) {
         const uint32_t va = lb + 24u * lds_u16(ai + 64u * q);
         const double v[3] = {lds_f64(va), lds_f64(va + 8u), lds_f64(va + 16u)};
-        if (q > 0) {  // move the phase from the previous slot's point
+        {  // move the phase from the previous slot's point
             const double2 st = lds_f64x2(scr + 16u * lds_u8(ac + 32u * q));
             const double pcn = fma(pc, st.x, -ps * st.y);
             ps = fma(pc, st.y, ps * st.x);
