@@ -363,7 +363,7 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         next.fill(0);
         for (size_t i = 0; i < np; ++i) perm[i] = 16 * next[res[i]]++ + res[i];
         const int nrec = 16 * cap + 1;  // the last record (a multiple of 16) is the zero padding
-        if (nrec >= 65535) return fail("too many points");
+        if (size_t(nrec) * 24 >= 65536) return fail("too many points");
         std::vector<double> vv(size_t(nrec) * 3, 0.0);
         for (size_t i = 0; i < np; ++i)
             for (int a = 0; a < 3; ++a) vv[size_t(perm[i]) * 3 + a] = v[i][a];
@@ -374,8 +374,12 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
     for (int ax = 0; ax < 3; ++ax) {
         hp->line_K[ax] = blk[ax].K;
         hp->line_P[ax] = blk[ax].P;
-        hp->line_slot_off[ax] = put(blk[ax].idx.data(), blk[ax].idx.size() * sizeof(uint16_t));
-        put(blk[ax].code.data(), blk[ax].code.size());       // at slot_off + 64 K (K * 64 is 16-aligned)
+        // slot words: byte offset of the v record (bits 0-15) | byte offset of the step entry
+        // (16 code, bits 16-24)
+        std::vector<uint32_t> word(blk[ax].idx.size());
+        for (size_t i = 0; i < word.size(); ++i)
+            word[i] = uint32_t(blk[ax].idx[i]) * 24u | (uint32_t(blk[ax].code[i]) * 16u) << 16;
+        hp->line_slot_off[ax] = put(word.data(), word.size() * sizeof(uint32_t));
         hp->line_meta_off[ax] = put(blk[ax].init.data(), blk[ax].init.size() * sizeof(int32_t));
         put(blk[ax].glo.data(), blk[ax].glo.size());          // at meta_off + 128
     }

@@ -1122,13 +1122,14 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
     double acc[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) acc[c] = 0.0;
-    const uint32_t ai = sl + 2u * lane, ac = sl + 64u * uint32_t(K) + uint32_t(lane);
+    const uint32_t ai = sl + 4u * lane;
 #pragma unroll 1
     for (int q = 0; q < K; ++q) {
-        const uint32_t va = lb + 24u * lds_u16(ai + 64u * q);
+        const uint32_t wd = lds_u32(ai + 128u * q);  // v record and step entry byte offsets
+        const uint32_t va = lb + (wd & 0xffffu);
         const double v[3] = {lds_f64(va), lds_f64(va + 8u), lds_f64(va + 16u)};
         {  // move the phase from the previous slot's point
-            const double2 st = lds_f64x2(scr + 16u * lds_u8(ac + 32u * q));
+            const double2 st = lds_f64x2(scr + (wd >> 16));
             const double pcn = fma(pc, st.x, -ps * st.y);
             ps = fma(pc, st.y, ps * st.x);
             pc = pcn;

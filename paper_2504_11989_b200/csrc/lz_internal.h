@@ -123,8 +123,8 @@ struct DevPlan {
     CtxConst hctx;         // constants of the Hessian context
     // Line-factorised direct block (trace-Z ATM plans, d = 3; capi.cpp build_line_block): the
     // last section of the staged image.  At 0: v [n + 1][3] doubles (the last record zero).  Per
-    // lattice axis a, at line_slot_off[a]: point indices [K][32] (uint16), then step codes [K][32]
-    // (uint8), K = line_K[a]; at
+    // lattice axis a, at line_slot_off[a]: slot words [K][32] (uint32: byte offset of the v record
+    // | 16 x step code << 16), K = line_K[a]; at
     // line_meta_off[a]: each lane's first (n_b, n_c) as int16 pairs [32], then the lane range of
     // every plane n_a = m (uint8 glo[line_P[a] + 1]).  Hessian channel weight = line_sign v v^T.
     const double* t0_host;  // host copy (plan-owned) of the q = 0 series rows [nctx + 2][kT0]
