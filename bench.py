@@ -32,15 +32,15 @@ FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (te
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
 TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
 # FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v29: line kernel, split 0.13); used to turn the live kernel
+# bench grid (profiles/r01_summary.md, v30: line kernel, split 0.13); used to turn the live kernel
 # time into FLOP/s.  Re-measure whenever the kernel or the ATM split changes.
-FLOPS_PER_NODE = 1577.3
-FLOPS_SOURCE = "ncu r01 v29: 3.9693e+10 FP64 FLOPs per launch / 25,165,824 nodes"
-# ncu r01 v29 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
+FLOPS_PER_NODE = 1578.0
+FLOPS_SOURCE = "ncu r01 v30: 3.9712e+10 FP64 FLOPs per launch / 25,165,824 nodes"
+# ncu r01 v30 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
 # L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
-TRAFFIC_PER_LAUNCH = 214_016 + 0
-NCU_UTIL = {"fp64_pipe_active": 0.563, "issue_active": 0.575, "lsu_wavefronts": 0.618,
-            "warps_active": 0.309, "source": "ncu r01 v29 (--set full, one launch)"}
+TRAFFIC_PER_LAUNCH = 220416 + 0
+NCU_UTIL = {"fp64_pipe_active": 0.570, "issue_active": 0.576, "lsu_wavefronts": 0.623,
+            "warps_active": 0.309, "source": "ncu r01 v30 (--set full, one launch)"}
 
 
 def parse():
@@ -290,7 +290,7 @@ def run_ours(args):
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
                                     "no FP64 entry)",
                      # utilisation counters of the same kernel from the ncu --set full capture
-                     # (profiles/r01_atm_v29_metrics.json): the FLOP fraction counts DADD/DMUL as one
+                     # (profiles/r01_atm_v30_metrics.json): the FLOP fraction counts DADD/DMUL as one
                      # FLOP although they occupy the FP64 pipe like a DFMA
                      "ncu": NCU_UTIL},
         "gpu_launches": 2 * args.steps,
