@@ -745,7 +745,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                 big = std::max(big, std::fabs(v) * std::pow(rho_max, ld(n)));
             }
             int used = lz::kT0;
-            while (used > 1 && std::fabs(cf[used - 1]) * std::pow(rho_max, ld(used - 1)) <= 1e-22L * std::max(big, 1.0L))
+            while (used > 1 && std::fabs(cf[used - 1]) * std::pow(rho_max, ld(used - 1)) <= 1e-19L * std::max(big, 1.0L))
                 --used;
             if (used >= lz::kT0 - 2) ok = false;  // not converged within kT0 terms: disable
             need = std::max(need, used + 2);
