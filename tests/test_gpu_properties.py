@@ -11,7 +11,9 @@ from paper_2504_11989_b200.epstein import EpsteinContext
 from paper_2504_11989_b200.quadrature import QuadratureConfig, integrate_product
 
 pytestmark = pytest.mark.gpu
-SETTINGS = settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+# derandomize: the same examples on every run (reproducible round-end runs; widen by hand with
+# --hypothesis-seed when exploring)
+SETTINGS = settings(max_examples=25, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 
 
 @st.composite
@@ -66,7 +68,7 @@ def test_hessian_trace_identity_any_split(lat, t, seed):
     assert emetric(np.trace(M, axis1=1, axis2=2), z3).max() <= 1e-11 * max(1.0, float(np.abs(z3).max()))
 
 
-@settings(max_examples=6, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=6, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(lat=lattices((2,)), nus=st.lists(st.floats(2.3, 6.0), min_size=3, max_size=3))
 def test_exponent_permutation_symmetry(lat, nus):
     """zeta^(3) is invariant under cyclic shifts and reversal of the exponent vector."""
@@ -77,7 +79,7 @@ def test_exponent_permutation_symmetry(lat, nus):
         assert abs(w - v) <= 1e-12 * abs(v)
 
 
-@settings(max_examples=12, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=12, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
 @given(lat=lattices(), nu=st.floats(2.5, 8.0), order=st.integers(1, 4), seed=st.integers(0, 2 ** 31 - 1))
 def test_derivative_parity_and_periodicity(lat, nu, order, seed):
     """d^alpha Z(-k) = (-1)^|alpha| d^alpha Z(k) and d^alpha Z(k + G) = d^alpha Z(k)."""
