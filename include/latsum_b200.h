@@ -53,7 +53,9 @@ typedef struct {
     double a[16];        /* generator A, row-major d x d, columns = basis vectors */
     double nu;           /* exponent                                              */
     double splitting;    /* <= 0: default V^{-2/d} (L/epstein.py:107)             */
-    int deriv_order;     /* 0: zeta only; 2: also build the Hessian point sets    */
+    int deriv_order;     /* 0: zeta only; 2: also build the Hessian point sets;
+                            -1 / -2: plan-private contexts with only the reciprocal /
+                            only the Hessian sets (the ATM plan's Z_3 / Z_5)          */
 } lz_ctx_params;
 
 typedef struct {

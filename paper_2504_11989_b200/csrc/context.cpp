@@ -309,13 +309,15 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
         k.sing_coef = double(std::pow(kPiL, nul - ld(d) / 2.0L) * std::tgamma((ld(d) - nul) / 2.0L) /
                              std::tgamma(nul / 2.0L));
     }
-    h->want_hess = deriv_order >= 2 ? 1 : 0;
+    // deriv_order < 0: plan-private contexts (ATM plans) that need only part of the sets --
+    // -1: constants and the reciprocal set; -2: constants and the Hessian sets
+    h->want_hess = (deriv_order >= 2 || deriv_order == -2) ? 1 : 0;
     // the Hessian's widened sets (needed by every Hessian / ATM plan) are enumerated on a second
     // thread while the plain sets are: context creation costs the longer of the two
     std::future<void> hess;
     if (h->want_hess) hess = std::async(std::launch::async, [h] { build_hess_sets(*h); });
-    enumerate_direct(*h, 0, kTermCutoff, &h->dir_n, &h->dir_z, &h->dir_w);
-    enumerate_reciprocal(*h, k.s, kTermCutoff, &h->rec_n, &h->rec_q);
+    if (deriv_order >= 0) enumerate_direct(*h, 0, kTermCutoff, &h->dir_n, &h->dir_z, &h->dir_w);
+    if (deriv_order != -2) enumerate_reciprocal(*h, k.s, kTermCutoff, &h->rec_n, &h->rec_q);
     if (hess.valid()) hess.get();
 }
 

@@ -110,7 +110,9 @@ class EpsteinContext:
         self.dir_w = self._points(1)
         self.rec_pts = self._points(2).reshape(-1, d)
         self.rec_norm2 = np.einsum("ij,ij->i", self.rec_pts, self.rec_pts)
-        self.has_hessian = deriv_order >= 2  # Hessian point sets and tables are built on first use
+        # Hessian point sets and tables are built on first use; deriv_order < 0 marks the ATM
+        # plan's private contexts (-1: reciprocal set only, -2: Hessian sets only)
+        self.has_hessian = deriv_order >= 2 or deriv_order == -2
 
     def __del__(self):
         try:  # also reached at interpreter shutdown, when module globals may be gone

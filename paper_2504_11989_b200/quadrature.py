@@ -247,16 +247,12 @@ def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
         splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
     # the two contexts' host enumerations are independent native calls (GIL released): overlap them
     from concurrent.futures import ThreadPoolExecutor
-    def z5_with_sets():
-        z = epstein_context(lattice, 5.0, splitting)
-        N.check(N.lib().lz_ctx_prepare(z.handle, 4), "hessian point sets")  # off the critical path
-        return z
-
+    # Both contexts are private to this (cached) plan and enumerate only what it reads: Z_3 lends
+    # its constants and reciprocal set (the kernel takes Z_3 = tr M_5), Z_5 its constants and the
+    # Hessian's widened point sets
     with ThreadPoolExecutor(max_workers=2) as pool:
-        f5 = pool.submit(z5_with_sets)
-        # Z_3 only lends the plan its constants and reciprocal set (the kernel takes Z_3 = tr M_5),
-        # so its own context skips the Hessian point sets; it is private to this (cached) plan
-        z3 = EpsteinContext(lattice, 3.0, splitting, deriv_order=0)
+        f5 = pool.submit(EpsteinContext, lattice, 5.0, splitting, -2)
+        z3 = EpsteinContext(lattice, 3.0, splitting, deriv_order=-1)
         z5 = f5.result()
     h = C.c_void_p()
     N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)), "atm plan")
