@@ -73,41 +73,25 @@ def c1():
 
 
 def e2e_breakdown():
-    """Where the cold-cache time of atm_energy_distributed goes (host vs device)."""
-    import ctypes as C
-    from paper_2504_11989_b200 import _native as N
+    """Where the cold-cache time of atm_energy_distributed goes (host plan vs device)."""
     from paper_2504_11989_b200.distributed import ShardedIntegral
     from paper_2504_11989_b200.epstein import epstein_context
     from paper_2504_11989_b200.quadrature import atm_plan, product_plan
     fcc = named_lattice("fcc")
-    for rep in range(3):
+    for rep in range(4):
         epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        from paper_2504_11989_b200.quadrature import ATM_SPLIT_SCALE
-        t = ATM_SPLIT_SCALE * fcc.volume ** (-2.0 / 3.0)
-        z3 = epstein_context(fcc, 3.0, t)
-        z5 = epstein_context(fcc, 5.0, t)
+        plan = atm_plan(fcc)  # plan-private contexts (in parallel) + plan build + upload
         t1 = time.perf_counter()
-        plan = atm_plan(fcc)
-        t2 = time.perf_counter()
-        t2a = time.perf_counter()
-        plan.tiles(128, 128, 3)
-        t2b = time.perf_counter()
         s = ShardedIntegral(plan, 128, 128, 3)
+        t2 = time.perf_counter()
+        out = s.run().cpu().numpy()
         t3 = time.perf_counter()
-        print(f"   tiles {1e3*(t2b-t2a):.2f} ms, ShardedIntegral {1e3*(t3-t2b):.2f} ms")
         out = s.run().cpu().numpy()
         t4 = time.perf_counter()
-        out = s.run().cpu().numpy()
-        t5 = time.perf_counter()
-        print(f"rep {rep}: contexts {1e3*(t1-t0):.1f} ms, plan {1e3*(t2-t1):.1f} ms, "
-              f"buffers {1e3*(t3-t2):.1f} ms, run+d2h {1e3*(t4-t3):.1f} ms, warm run+d2h {1e3*(t5-t4):.1f} ms")
-        epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
-        t6 = time.perf_counter()
-        atm_plan(fcc)
-        t7 = time.perf_counter()
-        print(f"   cold atm_plan (contexts in parallel + plan): {1e3*(t7-t6):.1f} ms")
+        print(f"rep {rep}: cold atm_plan {1e3*(t1-t0):.2f} ms, ShardedIntegral {1e3*(t2-t1):.2f} ms, "
+              f"run+d2h {1e3*(t3-t2):.2f} ms, warm run+d2h {1e3*(t4-t3):.2f} ms")
 
 
 def c1_time():
