@@ -80,19 +80,31 @@ std::vector<int> integer_shell(int d, int r) {
         out.assign(d, 0);
         return out;
     }
+    // lexicographic order over [-r, r]^d (first coordinate most significant), max-norm r only:
+    // walk the prefixes; a prefix below r admits only the last coordinates -r and +r
     const int w = 2 * r + 1;
-    long total = 1;
-    for (int i = 0; i < d; ++i) total *= w;
+    long nprefix = 1;
+    for (int i = 0; i < d - 1; ++i) nprefix *= w;
     std::vector<int> n(d);
-    for (long idx = 0; idx < total; ++idx) {
+    for (long idx = 0; idx < nprefix; ++idx) {
         long rem = idx;
         int mx = 0;
-        for (int i = d - 1; i >= 0; --i) {
+        for (int i = d - 2; i >= 0; --i) {
             n[i] = int(rem % w) - r;
             rem /= w;
             mx = std::max(mx, std::abs(n[i]));
         }
-        if (mx == r) out.insert(out.end(), n.begin(), n.end());
+        if (mx == r) {
+            for (int last = -r; last <= r; ++last) {
+                n[d - 1] = last;
+                out.insert(out.end(), n.begin(), n.end());
+            }
+        } else {
+            n[d - 1] = -r;
+            out.insert(out.end(), n.begin(), n.end());
+            n[d - 1] = r;
+            out.insert(out.end(), n.begin(), n.end());
+        }
     }
     return out;
 }
@@ -132,8 +144,11 @@ static void classify(double nu, int d, CtxConst* k) {
     k->log_m = -1;
 }
 
+// r2_ball > 0 (plan-private Hessian sets): points with |z|^2 > r2_ball are skipped without their
+// Gamma function -- the shells' cube corners, whose terms lie below 1e-3 of the cutoff and which
+// the plan's ball truncation drops anyway.
 static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::vector<double>* pn,
-                             std::vector<double>* pz, std::vector<double>* pw) {
+                             std::vector<double>* pz, std::vector<double>* pw, double r2_ball = 0.0) {
     const int d = h.d;
     const ld nu = h.k.nu, t = h.k.split;
     pn->clear();
@@ -151,6 +166,7 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
         const int m = int(idx.size());
         std::vector<double> sn(size_t(m) * d), sz(size_t(m) * d), sw(m);
         std::vector<ld> smag(m);
+        std::vector<char> out(m, 0);
         // per point in parallel (large shells), reduced below in the fixed point order
         parallel_for(m, 128, [&](int64_t j) {
             const int* n = &shell[idx[j] * d];
@@ -159,6 +175,12 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
                 z[a] = 0.0L;
                 for (int b = 0; b < d; ++b) z[a] += ld(h.A[a * d + b]) * n[b];
                 r2 += z[a] * z[a];
+            }
+            if (r2_ball > 0.0 && double(r2) > r2_ball) {
+                out[j] = 1;
+                smag[j] = 0.0L;
+                sw[j] = 0.0;
+                return;
             }
             // truncation decisions and the reported weights need double precision only (the
             // reference computes them in double)
@@ -177,9 +199,12 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
             wsum += std::fabs(ld(sw[j]));
         }
         if (mag > ld(tol) * total) {
-            pn->insert(pn->end(), sn.begin(), sn.end());
-            pz->insert(pz->end(), sz.begin(), sz.end());
-            pw->insert(pw->end(), sw.begin(), sw.end());
+            for (int j = 0; j < m; ++j) {
+                if (out[j]) continue;
+                pn->insert(pn->end(), sn.begin() + size_t(j) * d, sn.begin() + size_t(j + 1) * d);
+                pz->insert(pz->end(), sz.begin() + size_t(j) * d, sz.begin() + size_t(j + 1) * d);
+                pw->push_back(sw[j]);
+            }
             total += wsum;
             below = 0;
         } else if (++below >= 2) {
@@ -312,6 +337,7 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
     // deriv_order < 0: plan-private contexts (ATM plans) that need only part of the sets --
     // -1: constants and the reciprocal set; -2: constants and the Hessian sets
     h->want_hess = (deriv_order >= 2 || deriv_order == -2) ? 1 : 0;
+    h->ball_sets = deriv_order == -2 ? 1 : 0;  // plan-private: skip the shells' far cube corners
     // the Hessian's widened sets (needed by every Hessian / ATM plan) are enumerated on a second
     // thread while the plain sets are: context creation costs the longer of the two
     std::future<void> hess;
@@ -325,7 +351,25 @@ void build_hess_sets(HostCtx& h) {
     if (h.has_hess || !h.want_hess || h.k.branch == kTrivial) return;
     // Hessian sets: the derivative-table enumerators of L/epstein.py:376-377
     // specialised to second order (z^alpha weight |z|^2, gamma order s + 2).
-    enumerate_direct(h, 2, kTermCutoff, &h.hdir_n, &h.hdir_z, &h.hdir_w);
+    double r2_ball = 0.0;
+    if (h.ball_sets) {
+        // radius where w |z|^2 (w = Gamma(nu/2, pi t r2) r2^-nu/2, decreasing) falls to 1e-3 of
+        // the term cutoff relative to a unit total (the plan's totals exceed one)
+        const double nu = h.k.nu, t = h.k.split, target = 1e-3 * kTermCutoff;
+        auto f = [&](double r2) {
+            return upper_gamma<double>(nu / 2.0, double(kPiL) * t * r2) * std::pow(r2, -nu / 2.0) * std::max(1.0, r2);
+        };
+        double lo = 1e-3, hi = 1e-3;
+        while (f(hi) > target && hi < 1e8) hi *= 2.0;
+        if (hi < 1e8) {
+            for (int it = 0; it < 60; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                (f(mid) > target ? lo : hi) = mid;
+            }
+            r2_ball = hi * (1.0 + 1e-9);
+        }
+    }
+    enumerate_direct(h, 2, kTermCutoff, &h.hdir_n, &h.hdir_z, &h.hdir_w, r2_ball);
     enumerate_reciprocal(h, h.k.s + 2.0, kTermCutoff, &h.hrec_n, &h.hrec_q);
     h.has_hess = 1;
 }

@@ -172,6 +172,7 @@ struct HostCtx {
     // widened sets for the Hessian (poly_order = 2, gamma order s + 2)
     int want_hess = 0;   // requested at creation (deriv_order >= 2)
     int has_hess = 0;    // sets enumerated
+    int ball_sets = 0;   // plan-private context: Hessian direct set cut to the ball that matters
     std::vector<double> hdir_n, hdir_z, hdir_w;
     std::vector<double> hrec_n, hrec_q;
 };
