@@ -128,6 +128,10 @@ uint64_t pack_key(int d, const double* n) {
 
 void union_points(int d, const std::vector<const std::vector<double>*>& sets, std::vector<double>* out) {
     out->clear();
+    if (sets.size() == 1) {  // one enumerated set: its points are distinct already
+        *out = *sets[0];
+        return;
+    }
     size_t total = 0;
     for (const auto* s : sets) total += s->size() / d;
     std::unordered_set<uint64_t> seen;
@@ -497,8 +501,14 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         ld dcut = 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
-        std::vector<std::unordered_map<uint64_t, double>> known(wctx.size());
-        for (size_t j = 0; j < wctx.size(); ++j) {
+        // one context whose own set is the union (trace-Z plans): its weights align by index
+        const std::vector<double>* aligned = nullptr;
+        if (wctx.size() == 1 && dsets.size() == 1) {
+            const bool h = wctx[0] == hess;
+            if (dsets[0] == (h ? &hess->hdir_n : &wctx[0]->dir_n)) aligned = h ? &hess->hdir_w : &wctx[0]->dir_w;
+        }
+        std::vector<std::unordered_map<uint64_t, double>> known(aligned ? 0 : wctx.size());
+        for (size_t j = 0; j < known.size(); ++j) {
             const bool h = wctx[j] == hess;
             const std::vector<double>& nn = h ? hess->hdir_n : wctx[j]->dir_n;
             const std::vector<double>& ww = h ? hess->hdir_w : wctx[j]->dir_w;
@@ -513,6 +523,12 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                 double za = 0.0;
                 for (int b = 0; b < d; ++b) za += first->A[a * d + b] * hp->dir_n[i * d + b];
                 r2 += za * za;
+            }
+            if (aligned) {
+                const double w = (*aligned)[size_t(i)];
+                wv[i] = w;
+                mag[i] = std::fabs(w) * std::max(1.0, r2);
+                return;
             }
             const uint64_t key = pack_key(d, &hp->dir_n[i * d]);
             for (size_t j = 0; j < wctx.size(); ++j) {
