@@ -1301,9 +1301,17 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             tt[D - 1] = 1.0;
             weight = ok ? g.wu[iu] * g.wv[iv1] * (D >= 3 ? g.wv[iv2] : 1.0) : 0.0;
             u = g.u[iu];
-            // np.roll(t, pyramid) (L/quadrature.py:151)
+            // np.roll(t, pyramid) (L/quadrature.py:151); pyr is warp-uniform: branch, not select
+            if (pyr == 0) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) t[i] = pyr == 0 ? tt[i] : pyr == 1 ? tt[(i + D - 1) % D] : tt[(i + D - 2) % D];
+                for (int i = 0; i < D; ++i) t[i] = tt[i];
+            } else if (pyr == 1) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) t[i] = tt[(i + D - 1) % D];
+            } else {
+#pragma unroll
+                for (int i = 0; i < D; ++i) t[i] = tt[(i + D - 2) % D];
+            }
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
