@@ -245,7 +245,8 @@ def run_ours(args):
 
     # ---- e2e through the public API (cold caches: host tables + H2D + kernel + D2H each call)
     e2e_ms = []
-    for _ in range(max(1, args.e2e_steps)):
+    # one untimed cold call first (first-call host paths, allocator), then the timed cold calls
+    for it in range(max(1, args.e2e_steps) + 1):
         epstein_context.cache_clear()
         atm_plan.cache_clear()
         product_plan.cache_clear()
@@ -254,7 +255,8 @@ def run_ours(args):
             dist.barrier()
         t0 = time.perf_counter()
         res = atm_energy_distributed(fcc, ATMGrid(*GRID))
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        if it > 0:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
     te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
