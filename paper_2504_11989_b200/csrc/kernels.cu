@@ -1507,9 +1507,57 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
-__global__ void reduce_kernel(const double* __restrict__ partials, int64_t n_tiles, int ncomp,
+__global__ void __launch_bounds__(1024) reduce_kernel(const double* __restrict__ partials, int64_t n_tiles, int ncomp,
                               double* __restrict__ out) {
     __shared__ double ss[1024], cc[1024];
+    if (ncomp == 2) {
+        // both components in one pass (16-byte loads), each in the per-component order below
+        __shared__ double ss1[1024], cc1[1024];
+        double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+        constexpr int kBatch = 8;
+        const double2* p2 = reinterpret_cast<const double2*>(partials);
+        for (int64_t i0 = threadIdx.x; i0 < n_tiles; i0 += int64_t(blockDim.x) * kBatch) {
+            double2 xs[kBatch];
+#pragma unroll
+            for (int r = 0; r < kBatch; ++r) {
+                const int64_t i = i0 + int64_t(r) * blockDim.x;
+                xs[r] = i < n_tiles ? __ldg(&p2[i]) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int r = 0; r < kBatch; ++r) {
+                if (i0 + int64_t(r) * blockDim.x >= n_tiles) break;
+                double t = s0 + xs[r].x;
+                c0 += (fabs(s0) >= fabs(xs[r].x)) ? (s0 - t) + xs[r].x : (xs[r].x - t) + s0;
+                s0 = t;
+                t = s1 + xs[r].y;
+                c1 += (fabs(s1) >= fabs(xs[r].y)) ? (s1 - t) + xs[r].y : (xs[r].y - t) + s1;
+                s1 = t;
+            }
+        }
+        ss[threadIdx.x] = s0;
+        cc[threadIdx.x] = c0;
+        ss1[threadIdx.x] = s1;
+        cc1[threadIdx.x] = c1;
+        __syncthreads();
+        for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+            if (threadIdx.x < h) {
+                double a = ss[threadIdx.x], b = ss[threadIdx.x + h], t = a + b;
+                double e = (fabs(a) >= fabs(b)) ? (a - t) + b : (b - t) + a;
+                ss[threadIdx.x] = t;
+                cc[threadIdx.x] += cc[threadIdx.x + h] + e;
+                a = ss1[threadIdx.x], b = ss1[threadIdx.x + h], t = a + b;
+                e = (fabs(a) >= fabs(b)) ? (a - t) + b : (b - t) + a;
+                ss1[threadIdx.x] = t;
+                cc1[threadIdx.x] += cc1[threadIdx.x + h] + e;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out[0] = ss[0] + cc[0];
+            out[1] = ss1[0] + cc1[0];
+        }
+        return;
+    }
     for (int comp = 0; comp < ncomp; ++comp) {
         double s = 0.0, c = 0.0;
         // the same per-thread sequence, with 8 loads in flight per round (one SM: latency-bound)
