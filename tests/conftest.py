@@ -26,6 +26,12 @@ def golden_integrals():
         return json.load(f)
 
 
+@pytest.fixture(scope="session")
+def golden_near_d():
+    with open(os.path.join(GOLDEN, "golden_near_d.json")) as f:
+        return json.load(f)
+
+
 def emetric(a, b):
     """Paper's per-point error E = min(E_abs, E_rel)."""
     import numpy as np

@@ -10,9 +10,14 @@ coexist with the new package) and writes small JSON fixtures next to itself:
 * ``golden_integrals.json`` slow items (minutes): the reference's adaptive
                             ``integrate_product`` for C4 and the fcc/bcc
                             three-body integrals behind the ATM energies.
+* ``golden_near_d.json``    ``--near-d``: the reference's whole-range adaptive
+                            ``integrate_product`` for exponents just above the
+                            dimension (slowly converging algebraic endpoint
+                            singularities) and ``integrate_bz_even`` on smooth
+                            even integrands.
 
 The GPU box has no ``/root/reference``; the fixtures travel instead.
-Usage:  python tests/golden/make_golden.py [--slow] [--threads N]
+Usage:  python tests/golden/make_golden.py [--slow | --near-d] [--threads N]
 """
 from __future__ import annotations
 
@@ -255,15 +260,62 @@ def slow(ref, threads):
     return out
 
 
+# products with every exponent above d whose integrand u^(d-1) prod Z(u w) carries a
+# non-analytic u^eta (eta = d-1 + min(nu)-d) or u^eta log u endpoint term
+NEAR_D = [("square", (2.05, 2.05, 2.05)), ("square", (2.2, 3.0, 3.0)), ("square", (2.5, 2.5)),
+          ("square", (2.01,)), ("square", (3.5, 4.0)), ("hexagonal", (2.1, 2.1, 2.1)),
+          ("integer_1d", (1.3, 2.0)), ("fcc", (3.3, 4.0, 4.0)), ("bcc", (3.5, 3.5))]
+
+
+def bz_even_cases(ref):
+    """Smooth even integrands for integrate_bz_even, as (lattice, label, callable)."""
+    out = []
+    for name in ("integer_1d", "square", "hexagonal", "fcc"):
+        lat = ref.named_lattice(name)
+        d = lat.d
+        z1 = lat.a[:, 0]
+        z2 = lat.a @ np.ones(d)
+        out.append((name, "one", lambda k: np.ones(len(k))))
+        out.append((name, "cos_a1", lambda k, z=z1: np.cos(2 * np.pi * k @ z)))
+        out.append((name, "cos_a1_sq", lambda k, z=z1: np.cos(2 * np.pi * k @ z) ** 2))
+        out.append((name, "gauss3", lambda k: np.exp(-3.0 * np.einsum("ij,ij->i", k, k))))
+        out.append((name, "mix", lambda k, z=z2: (1.0 + np.einsum("ij,ij->i", k, k)) ** -1.5
+                    * np.cos(2 * np.pi * k @ z)))
+    return out
+
+
+def near_d(ref, threads):
+    Q = ref.quadrature
+    out = {"generator": "tests/golden/make_golden.py --near-d", "threads": threads,
+           "cases": [], "bz_even": []}
+    for name, nus in NEAR_D:
+        lat = ref.named_lattice(name)
+        t = time.time()
+        v, e = Q.integrate_product(lat, nus, threads=threads)
+        rec = {"lattice": name, "nus": list(nus), "value": v, "err": e,
+               "seconds": time.time() - t}
+        print(rec, flush=True)
+        out["cases"].append(rec)
+    for name, label, f in bz_even_cases(ref):
+        lat = ref.named_lattice(name)
+        v = Q.integrate_bz_even(lat, f)
+        out["bz_even"].append({"lattice": name, "f": label, "value": v})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
+    ap.add_argument("--near-d", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     ref = load_reference()
     if args.slow:
         res = slow(ref, args.threads)
         path = os.path.join(HERE, "golden_integrals.json")
+    elif args.near_d:
+        res = near_d(ref, args.threads)
+        path = os.path.join(HERE, "golden_near_d.json")
     else:
         res = quick(ref)
         path = os.path.join(HERE, "golden.json")
