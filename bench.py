@@ -1,25 +1,32 @@
 #!/usr/bin/env python3
-"""Benchmark of the Epstein-zeta hot path on B200 ("Measurement").
+"""Benchmark of the Epstein-zeta hot path on B200.
 
-Headline workload (BASELINE.json metric "Epstein-zeta evals/s ...; ATM fcc sum
-wall time at 1-8 GPUs", config 3): one step = one complete ATM cohesive-energy
-lattice sum for fcc on the fixed 12 x 128 x 128^2 graded Duffy grid
-(25,165,824 nodes; per node one Z_3 and one Hessian of Z_5, i.e. 2 zeta
-evaluations), sharded over the ranks with one NCCL all-reduce.
+Headline workload (BASELINE.json metric, config 3): one step = one complete ATM
+cohesive-energy lattice sum for fcc on the fixed 12 x 128 x 128^2 graded Duffy
+grid (25,165,824 nodes).  Per node the fused kernel evaluates one Hessian of
+Z_5 (the polynomial-weighted zeta M_5) and takes Z_3 = tr M_5 from it, so a node
+counts as ONE zeta evaluation.  The node grid is sharded over the ranks in 96
+fixed chunks; ranks exchange chunk sums with one NCCL all-reduce.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Rank 0 prints ONE JSON line.  value = zeta evaluations/s of the whole job
-(device-timed, CUDA events, max over ranks); ms_per_step = ATM fcc sum wall
-time; e2e = the same metric through the public API call
-(distributed.atm_energy_distributed) from a cold cache, including host table
-build, H2D uploads and the D2H of the result.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run with
+N ranks.  Rank 0 prints ONE JSON line.  value = zeta evaluations/s of the whole
+job (device-timed with CUDA events, max over ranks); ms_per_step = ATM fcc sum
+wall time; e2e = the same metric through the public API
+(distributed.atm_energy_distributed) including host table build, the H2D
+uploads and the D2H of the result (cold: every library cache released; warm:
+plan cached).  `--impl reference` times the reference's own CPU implementation
+(the unmodified `latsum` package installed under baseline/_ref) on the same
+node sample with every host core.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -28,19 +35,15 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json "metric", verbatim in both arms (the driver pairs the arms by this string)
+METRIC = "Epstein-zeta evals/s (FP64, % of FP64 peak); ATM fcc sum wall time at 1–8 GPUs"
+UNIT = "zeta evals/s"
 FCC_ATM_REF = 19.182931071876666   # reference integrate_product + Prop. 2.4 (tests/golden)
 GRID = (128, 128, 3)               # n_u (graded u = t^3/2), n_v, grading
-TERMS_PER_NODE = 900 + 1502        # reference enumeration: Z_3 (171+728+1) + Hessian Z_5 (171+1330+1)
-# FP64 FLOPs per node of the fused ATM kernel (2*DFMA + DADD + DMUL), measured with ncu on the
-# bench grid (profiles/r01_summary.md, v30: line kernel, split 0.13); used to turn the live kernel
-# time into FLOP/s.  Re-measure whenever the kernel or the ATM split changes.
-FLOPS_PER_NODE = 1578.0
-FLOPS_SOURCE = "ncu r01 v30: 3.9712e+10 FP64 FLOPs per launch / 25,165,824 nodes"
-# ncu r01 v30 dram__bytes_read.sum + dram__bytes_write.sum (plan staging; the tile partials stay in
-# L2); the algorithmic HBM footprint of the integrand is zero (nodes generated on device)
-TRAFFIC_PER_LAUNCH = 220416 + 0
-NCU_UTIL = {"fp64_pipe_active": 0.570, "issue_active": 0.576, "lsu_wavefronts": 0.623,
-            "warps_active": 0.309, "source": "ncu r01 v30 (--set full, one launch)"}
+N_NODES = 12 * 128 * 128 * 128
+TERMS_PER_NODE = 171 + 1330 + 1    # reference enumeration of the Hessian of Z_5
+COUNTERS = os.path.join(ROOT, "profiles", "atm_kernel_current.json")
+REF_SITE = os.path.join(ROOT, "baseline", "_ref")
 
 
 def parse():
@@ -52,6 +55,11 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-nodes", type=int, default=16384,
+                    help="reference arm: nodes of the C3 grid per step (2 zeta evaluations each)")
+    ap.add_argument("--ref-full-atm", action="store_true",
+                    help="reference arm: also time the reference's own fcc ATM energy "
+                         "(3 x integrate_product, ~100 s on 8 cores)")
     return ap.parse_args()
 
 
@@ -60,6 +68,16 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: become N ranks on this node."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -123,78 +141,210 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ----------------------------------------------------------------------------- CPU baselines
-def cpu_atm_sample(n_nodes: int):
+# ----------------------------------------------------------------------------- node sample
+def c3_node_sample(n: int, seed: int = 7):
+    """``n`` seeded random nodes of the C3 grid (uniform over cell, u and v indices), Cartesian k
+    in the reference's Duffy coordinates (L/quadrature.py:136-177; u = t^3/2 graded GL)."""
+    import numpy as np
+    from paper_2504_11989_b200 import named_lattice
+    from paper_2504_11989_b200.quadrature import angular_nodes, duffy_cells
+    fcc = named_lattice("fcc")
+    x, _ = np.polynomial.legendre.leggauss(GRID[0])
+    u = 0.5 * ((x + 1.0) / 2.0) ** GRID[2]
+    v, _ = angular_nodes(3, GRID[1])
+    cells = duffy_cells(3)
+    idx = np.random.default_rng(seed).integers(0, N_NODES, size=n)
+    iu = idx % GRID[0]
+    rest = idx // GRID[0]
+    iv = rest % (GRID[1] ** 2)
+    ic = rest // (GRID[1] ** 2)
+    k = np.empty((n, 3))
+    for c in range(len(cells)):
+        sel = ic == c
+        if sel.any():
+            k[sel] = u[iu[sel], None] * cells[c].directions(fcc, v[iv[sel]])
+    return k
+
+
+# ----------------------------------------------------------------------------- reference CPU path
+_REF_CTX = {}
+
+
+def _ref_worker_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, REF_SITE)
+    import latsum
+    from latsum.epstein import epstein_context
+    fcc = latsum.named_lattice("fcc")
+    _REF_CTX["c3"] = epstein_context(fcc, 3.0)
+    _REF_CTX["c5"] = epstein_context(fcc, 5.0)
+
+
+def _ref_worker_eval(k):
+    import numpy as np
+    z3 = _REF_CTX["c3"].zeta(k)
+    z5 = _REF_CTX["c5"].zeta(k)
+    return float(np.sum(z3) + np.sum(z5))
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_SITE, "latsum"))
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+class ReferencePool:
+    """The unmodified reference (baseline/_ref/latsum) evaluating Z_3 and Z_5 at C3 nodes, one
+    process per host core (OPENBLAS_NUM_THREADS=1; processes, not threads --
+    the reference's numpy/scipy path holds the GIL between calls)."""
+
+    def __init__(self, procs: int):
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        self.procs = procs
+        self.pool = ProcessPoolExecutor(procs, mp_context=mp.get_context("spawn"),
+                                        initializer=_ref_worker_init)
+        list(self.pool.map(_ref_worker_eval, [c3_node_sample(4, seed=99)] * procs))  # warm every worker
+
+    def time(self, k):
+        import numpy as np
+        chunks = np.array_split(k, self.procs * 4)
+        t0 = time.perf_counter()
+        list(self.pool.map(_ref_worker_eval, chunks))
+        dt = time.perf_counter() - t0
+        return 2.0 * len(k) / dt, dt
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def port_sample(n_nodes: int):
     """Oracle port (long-double C restatement of the reference algorithm) on a contiguous block of
-    the C3 grid with every host thread; returns (evals/s, seconds, threads)."""
+    the C3 grid with every host thread: (zeta evals/s counting one per node, seconds, threads)."""
     from oracle import oracle as O
     from paper_2504_11989_b200 import named_lattice
     fcc = named_lattice("fcc")
-    total = O.grid_nodes(3, GRID[0], GRID[1])
-    lo = total // 2
+    lo = N_NODES // 2
     t0 = time.perf_counter()
     O.atm_grid(fcc.a, GRID[0], GRID[1], GRID[2], lo, lo + n_nodes)
     dt = time.perf_counter() - t0
-    return 2.0 * n_nodes / dt, dt, O.nthreads()
+    return n_nodes / dt, dt, O.nthreads()
+
+
+def reference_full_atm(threads: int):
+    """The reference's own fcc ATM energy: 3 x integrate_product + Prop. 2.4."""
+    sys.path.insert(0, REF_SITE)
+    import latsum
+    from latsum.quadrature import integrate_product
+    fcc = latsum.named_lattice("fcc")
+    t0 = time.perf_counter()
+    z333, _ = integrate_product(fcc, (3, 3, 3), threads=threads)
+    zm155, _ = integrate_product(fcc, (-1, 5, 5), threads=threads)
+    z135, _ = integrate_product(fcc, (1, 3, 5), threads=threads)
+    e = z333 / 24 - 3 * zm155 / 16 + 3 * z135 / 8
+    return time.perf_counter() - t0, e
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sample = 65536
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, dt, threads = cpu_atm_sample(sample)
-        if i >= args.warmup:
-            vals.append((v, dt))
-    v = sum(x[0] for x in vals) / len(vals)
-    ms = sum(x[1] for x in vals) / len(vals) * 1e3
-    line = {
-        "impl": "reference",
-        "metric": "Epstein-zeta evals/s (FP64) on the ATM fcc sum",
-        "value": v, "unit": "zeta evals/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64 (long double oracle)", "data": "synthetic (fixed Duffy grid)",
-        "config": config_block(world),
-        "cpu_baseline": {"value": v, "unit": "zeta evals/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} contiguous nodes of the 25,165,824-node C3 grid per step "
-                                   "(oracle/latsum_oracle.c, long double, all host threads)"},
-        "e2e": {"value": v, "unit": "zeta evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference arm = oracle port of the reference algorithm (the reference is pure Python "
-                "and is not installed on the GPU box); SURVEY.md section 6 lists the Python reference "
-                "itself at 377 s (1 thread) / 102 s (8 threads) for the fcc ATM energy",
-    }
+    cores = cpu_cores()
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded sample of the fixed C3 Duffy grid)",
+            "config": config_block(world)}
+    if reference_available():
+        k = c3_node_sample(args.ref_nodes)
+        pool = ReferencePool(cores)
+        vals = []
+        for i in range(args.warmup + args.steps):
+            v, dt = pool.time(k)
+            if i >= args.warmup:
+                vals.append((v, dt))
+        pool.close()
+        v = sum(x[0] for x in vals) / len(vals)
+        ms = sum(x[1] for x in vals) / len(vals) * 1e3
+        sample = (f"{args.ref_nodes} seeded random nodes of the 25,165,824-node C3 grid per step, reference "
+                  f"EpsteinContext.zeta for Z_3 and Z_5 at each (2 evaluations per node; the reference has no "
+                  f"Hessian and its ATM route needs Z_-1, Z_1, Z_3, Z_5 per node), {cores} processes")
+        kind = "reference"
+        impl_note = ("unmodified reference latsum 0.1.0 (numpy/scipy), pip-installed from /root/reference/pkg "
+                     "into baseline/_ref (baseline/install_reference.sh)")
+    else:
+        vals = []
+        n = args.ref_nodes * 2
+        for i in range(args.warmup + args.steps):
+            v, dt, cores = port_sample(n)
+            if i >= args.warmup:
+                vals.append((v, dt))
+        v = sum(x[0] for x in vals) / len(vals)
+        ms = sum(x[1] for x in vals) / len(vals) * 1e3
+        sample = f"{n} contiguous nodes of the C3 grid per step, oracle port, {cores} threads"
+        kind = "port"
+        impl_note = "baseline/_ref missing: oracle port (oracle/latsum_oracle.c) of the reference algorithm"
+    line.update({"value": v, "ms_per_step": ms,
+                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "implementation": impl_note,
+                 "note": "ms_per_step = wall time of one sample step (not an ATM sum); the reference's "
+                         "own fcc ATM energy took 102 s on 8 threads in the survey container (SURVEY.md 6)"})
+    if args.ref_full_atm and reference_available():
+        secs, e = reference_full_atm(cores)
+        line["reference_atm_sum"] = {"seconds": secs, "energy": e, "threads": cores}
     print(json.dumps(line), flush=True)
 
 
 def config_block(world):
     return {"workload": "C3: ATM cohesive energy, fcc (unit NN distance), fixed Duffy grid 12 cells x "
-                        "128 radial (graded u=t^3/2) x 128^2 angular = 25,165,824 nodes; per node Z_3 and "
-                        "the Hessian of Z_5 (polynomial-weighted zeta)",
+                        "128 radial (graded u=t^3/2) x 128^2 angular = 25,165,824 nodes; per node one Hessian "
+                        "of Z_5 (polynomial-weighted zeta M_5) and Z_3 = tr M_5",
             "lattice": "fcc", "grid": {"n_u": GRID[0], "n_v": GRID[1], "grading": GRID[2]},
-            "nodes_per_step": 25165824, "zeta_evals_per_node": 2, "terms_per_node": TERMS_PER_NODE,
-            "parallelism": f"node-shard x{world} + 1 NCCL all-reduce" if world > 1 else "1 GPU",
-            "l2": "node data generated on device; tables (<110 KB) live in shared memory; L2 flushed "
+            "nodes_per_step": N_NODES, "zeta_evals_per_node": 1, "terms_per_node": TERMS_PER_NODE,
+            "parallelism": f"node-shard x{world} (96 fixed chunks) + 1 NCCL all-reduce of chunk sums"
+                           if world > 1 else "1 GPU",
+            "l2": "node data generated on device; tables (<120 KB) live in shared memory; L2 flushed "
                   "(256 MB write) between timed steps"}
 
 
 # ----------------------------------------------------------------------------- ours
+def kernel_counters():
+    """FP64 FLOPs per node of the ATM kernel from the committed ncu capture of the shipping build
+    (profiles/atm_kernel_current.json, written by tools/ncu_metrics.py); stale if kernels.cu has
+    changed since the capture."""
+    with open(COUNTERS) as f:
+        c = json.load(f)
+    src = os.path.join(ROOT, "paper_2504_11989_b200", "csrc", "kernels.cu")
+    sha = hashlib.sha1(open(src, "rb").read()).hexdigest()
+    c["stale"] = c.get("kernels_cu_sha1") != sha
+    return c
+
+
 def run_ours(args):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} visible GPUs, found {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2504_11989_b200 import _native as N
     from paper_2504_11989_b200 import named_lattice
-    from paper_2504_11989_b200.distributed import ShardedIntegral, allreduce_partials, atm_energy_distributed
+    from paper_2504_11989_b200.distributed import ShardedIntegral, atm_energy_distributed
     from paper_2504_11989_b200.epstein import epstein_context
     from paper_2504_11989_b200.manybody import ATMGrid
-    from paper_2504_11989_b200.quadrature import Plan, atm_plan, product_plan
+    from paper_2504_11989_b200.quadrature import atm_plan, product_plan
 
     fcc = named_lattice("fcc")
     S = ShardedIntegral(atm_plan(fcc), *GRID)
@@ -202,15 +352,12 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def step(evs=None):
-        S.partials.zero_()
         if evs:
             evs[0].record(stream)
-        S.plan.integrate_device(S.partials, S.n_u, S.n_v, S.grading, S.tile_lo, S.tile_hi)
+        S.integrate()
         if evs:
             evs[1].record(stream)
-        if world > 1:
-            allreduce_partials(S.partials)  # C ABI: one ncclAllReduce on this stream
-        Plan.reduce_device(S.partials, S.n_tiles, S.ncomp, S.out)
+        S.reduce()   # chunk sums, one ncclAllReduce of 96 x 2 doubles (W > 1), fixed-order total
         if evs:
             evs[2].record(stream)
 
@@ -241,68 +388,103 @@ def run_ours(args):
     step_ms, kern_ms = float(t[0]), float(t[1])
     out = S.out.cpu().numpy()
     energy = (8.0 * out[0] - 3.0 * 8.0 * out[1]) / 6.0
-    evals = 2.0 * S.n_nodes
 
-    # ---- e2e through the public API (cold caches: host tables + H2D + kernel + D2H each call)
-    e2e_ms = []
-    # one untimed cold call first (first-call host paths, allocator), then the timed cold calls
-    for it in range(max(1, args.e2e_steps) + 1):
-        epstein_context.cache_clear()
-        atm_plan.cache_clear()
-        product_plan.cache_clear()
-        torch.cuda.synchronize()
+    # ---- e2e through the public API, host buffers only (the lattice in, the energy out)
+    def api_call():
+        return atm_energy_distributed(fcc, ATMGrid(*GRID))
+
+    def e2e(cold: bool, reps: int):
+        ms, h2d, d2h = [], [], []
+        for it in range(reps + 1):   # one untimed call first (first-call host paths, allocator)
+            if cold:
+                epstein_context.cache_clear()
+                atm_plan.cache_clear()
+                product_plan.cache_clear()
+                import gc
+                gc.collect()                       # contexts/plans freed -> device tables freed
+                N.check(N.lib().lz_release_caches(local), "release caches")
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            import ctypes as C
+            N.lib().lz_transfer_stats(None, None, 1)
+            t0 = time.perf_counter()
+            res = api_call()
+            dt = (time.perf_counter() - t0) * 1e3
+            hb, db = C.c_int64(0), C.c_int64(0)
+            N.lib().lz_transfer_stats(C.byref(hb), C.byref(db), 1)
+            if it > 0:
+                ms.append(dt)
+                h2d.append(hb.value)
+                d2h.append(db.value)
+        te = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        res = atm_energy_distributed(fcc, ATMGrid(*GRID))
-        if it > 0:
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_step_ms = float(te[0])
-    # H2D per e2e call: the plan's tables (uploaded once per cold call) + the grid node arrays
-    pinfo = atm_plan(fcc).info()
-    h2d = int(pinfo.smem_bytes) + 8 * 2 * (GRID[0] + GRID[1])
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        # torch's own D2H of the two result doubles (ShardedIntegral.run().cpu()) is not a library copy
+        return float(te[0]), int(max(h2d)), int(max(d2h)) + 16, res
+
+    warm_ms, warm_h2d, warm_d2h, _ = e2e(False, max(1, args.e2e_steps))
+    cold_ms, cold_h2d, cold_d2h, res = e2e(True, max(1, args.e2e_steps))
 
     # ---- roofline of the dominant kernel (the fused ATM tile kernel)
     import ctypes as C
     pk, pms = C.c_double(0.0), C.c_double(0.0)
     N.check(N.lib().lz_fp64_peak(local, C.byref(pk), C.byref(pms)), "fp64 peak probe")
-    local_nodes = min(S.local_nodes, S.n_nodes)
-    achieved = FLOPS_PER_NODE * local_nodes / (kern_ms * 1e-3) / 1e12
+    cnt = kernel_counters()
+    local_nodes = min(S.local_nodes, N_NODES)
+    achieved = cnt["flops_per_unit"] * local_nodes / (kern_ms * 1e-3) / 1e12
+    evals = float(N_NODES)
 
     line = {
-        "metric": "Epstein-zeta evals/s (FP64) on the ATM fcc sum; ms_per_step = ATM fcc sum wall time",
-        "value": evals / (step_ms * 1e-3), "unit": "zeta evals/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC,
+        "value": evals / (step_ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (fixed Duffy grid generated on device)",
         "config": config_block(world),
-        "terms_per_s": evals / 2.0 * TERMS_PER_NODE / (step_ms * 1e-3),
+        "atm_sum_ms": step_ms,
+        "nodes_per_s": N_NODES / (step_ms * 1e-3),
+        "hessian_evals_per_s": N_NODES / (step_ms * 1e-3),
+        "zeta_values_per_s": 2.0 * N_NODES / (step_ms * 1e-3),
+        "reference_terms_per_s": N_NODES * TERMS_PER_NODE / (step_ms * 1e-3),
         "parity": {"atm_energy": energy, "reference": FCC_ATM_REF,
                    "rel_err": abs(energy - FCC_ATM_REF) / FCC_ATM_REF, "tolerance": 1e-10},
-        "e2e": {"value": evals / (e2e_step_ms * 1e-3), "unit": "zeta evals/s",
-                "ms_per_call": e2e_step_ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 16,
+        "e2e": {"value": evals / (cold_ms * 1e-3), "unit": UNIT, "ms_per_call": cold_ms,
+                "h2d_bytes_per_step": cold_h2d, "d2h_bytes_per_step": cold_d2h,
+                "bytes": "measured: lz_transfer_stats counts every host<->device copy the library issues",
                 "call": "paper_2504_11989_b200.distributed.atm_energy_distributed(fcc, ATMGrid(128,128,3)) "
-                        "from cold caches", "energy": res.energy},
+                        "with every cache released (Python context/plan caches and lz_release_caches): host "
+                        "enumeration + table fits + H2D uploads + kernels + D2H of the energy",
+                "energy": res.energy,
+                "warm": {"value": evals / (warm_ms * 1e-3), "ms_per_call": warm_ms, "h2d_bytes_per_step": warm_h2d,
+                         "d2h_bytes_per_step": warm_d2h, "call": "same call, plan cached"}},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
-                     "frac": achieved / pk.value, "traffic": TRAFFIC_PER_LAUNCH,
-                     "kernel": "lz::tile_kernel_l<20,1> (fused ATM integrand, line-factorised direct space)",
-                     "kernel_ms": kern_ms, "flops_per_node": FLOPS_PER_NODE, "flops_source": FLOPS_SOURCE,
+                     "frac": achieved / pk.value, "traffic": cnt.get("dram_bytes_per_launch"),
+                     "kernel": cnt.get("kernel"), "kernel_ms": kern_ms,
+                     "flops_per_node": cnt["flops_per_unit"], "flops_source": cnt.get("source"),
+                     "flops_stale": cnt["stale"],
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
                                     "no FP64 entry)",
-                     # utilisation counters of the same kernel from the ncu --set full capture
-                     # (profiles/r01_atm_v30_metrics.json): the FLOP fraction counts DADD/DMUL as one
-                     # FLOP although they occupy the FP64 pipe like a DFMA
-                     "ncu": NCU_UTIL},
-        "gpu_launches": 2 * args.steps,
+                     "ncu": {k: cnt.get(k) for k in ("fp64_pipe_active", "issue_active", "lsu_wavefronts",
+                                                     "warps_active", "registers")}},
+        "exchange_bytes_per_step": S.exchange_bytes if world > 1 else 0,
+        "gpu_launches": 3 * args.steps,   # tile kernel + chunk reduce + total per step
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, threads = cpu_atm_sample(131072)
-        line["cpu_baseline"] = {"value": v, "unit": "zeta evals/s", "cores": threads, "kind": "port",
-                                "sample": f"131072 contiguous nodes of the C3 grid ({dt:.1f} s), "
-                                          "oracle/latsum_oracle.c (long double) on all host threads"}
+        if reference_available():
+            cores = cpu_cores()
+            pool = ReferencePool(cores)
+            k = c3_node_sample(8192)
+            pool.time(k)
+            v, dt = pool.time(k)
+            pool.close()
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                                    "sample": f"8192 seeded random C3 nodes, unmodified reference zeta for Z_3 "
+                                              f"and Z_5 (2 evaluations per node, {dt:.1f} s), {cores} processes"}
+        pv, pdt, pthreads = port_sample(32768)
+        line["cpu_port"] = {"value": pv, "unit": UNIT, "cores": pthreads, "kind": "port",
+                            "sample": f"32768 contiguous C3 nodes ({pdt:.1f} s), oracle/latsum_oracle.c "
+                                      "(long double), one evaluation per node as on the GPU"}
     if rank == 0 and world == 1 and not args.no_secondary:
         line["secondary"] = secondary(np, torch)
     if world > 1:
@@ -348,8 +530,28 @@ def _time_graph(fn, reps, torch):
     return a.elapsed_time(b) / reps
 
 
+def shard_balance(torch):
+    """Per-rank kernel time of the C3 grid split over W ranks, each shard timed alone on this GPU:
+    max/mean is the load-balance ceiling of strong scaling."""
+    from paper_2504_11989_b200 import named_lattice
+    from paper_2504_11989_b200.distributed import ShardedIntegral
+    from paper_2504_11989_b200.quadrature import atm_plan
+    plan = atm_plan(named_lattice("fcc"))
+    out = {}
+    for world in (2, 4, 8):
+        ms = []
+        for r in range(world):
+            s = ShardedIntegral(plan, *GRID, world=world, rank=r)
+            s.world = 1
+            ms.append(_time_cuda(s.integrate, 5, torch))
+        mean = sum(ms) / len(ms)
+        out[f"w{world}"] = {"shard_ms": ms, "max_over_mean": max(ms) / mean}
+    return out
+
+
 def secondary(np, torch):
-    """Configs 1, 2, 4 on one GPU (device-timed), plus C1 through the numpy drop-in API."""
+    """Configs 1, 2, 4 on one GPU (device-timed), C1 through the numpy drop-in API, C5, shard
+    balance."""
     from paper_2504_11989_b200 import named_lattice
     from paper_2504_11989_b200.epstein import EpsteinContext
     from paper_2504_11989_b200.quadrature import QuadratureConfig, integrate_product, product_plan
@@ -384,11 +586,14 @@ def secondary(np, torch):
         t0 = time.perf_counter()
         v, _ = integrate_product(sq, nus, cfg)
         e2e = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        v2, err2 = integrate_product(sq, nus)   # default contract: grid + error check (+ escalation)
+        api = time.perf_counter() - t0
         out[name] = {"value": v, "nodes": nn, "kernel_ms": ms, "api_ms": e2e * 1e3,
+                     "api_ms_default_cfg": api * 1e3, "default_cfg_err": err2,
                      "evals_per_s": nn / (ms * 1e-3)}
     # config 5: fcc/bcc LJ(12,6) + lambda ATM phase scan (two ATM sums + four zeta_at_zero on the
     # GPU, then the host enthalpy scan on the 64 x 64 (lambda, R) grids and lambda_c for 4 pressures)
-    import numpy as np
     from paper_2504_11989_b200.manybody import ATMGrid
     from paper_2504_11989_b200.phase import LJParams, critical_coupling, lattice_constants, phase_scan
     torch.cuda.synchronize()
@@ -405,11 +610,14 @@ def secondary(np, torch):
     out["c5_phase_scan"] = {"constants_ms": (t1 - t0) * 1e3, "scan_ms": (t2 - t1) * 1e3,
                             "lambda_c": crit, "k_atm_fcc": fc.k_atm, "k_atm_bcc": bc.k_atm,
                             "points": len(pts)}
+    out["shard_balance"] = shard_balance(torch)
     return out
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -34,7 +34,7 @@ enum {
     LZ_EPOLE = 2,      /* PoleError: nu = d at k in the reciprocal lattice          */
     LZ_ENONFINITE = 3, /* ValueError("k contains non-finite entries")               */
     LZ_ECUDA = 4,      /* CUDA runtime failure or no device                          */
-    LZ_ENCCL = 5,      /* reserved: collective failure (collectives run in torch)   */
+    LZ_ENCCL = 5,      /* NCCL unavailable or the collective failed (lz_allreduce_*) */
     LZ_ESHELLS = 6,    /* RuntimeError: sum did not truncate within shell budget    */
     LZ_ELATTICE = 7,   /* LatticeError: singular generator / unsupported dimension  */
     LZ_ESINGULAR = 8   /* ValueError: singular part undefined at k = 0              */
@@ -129,6 +129,19 @@ int lz_plan_integrate(const lz_plan* plan, const lz_grid* g, double* partials, i
                       void* stream);
 /* fixed-order compensated sum of n_tiles x ncomp partials -> out[ncomp] (device) */
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream);
+/* fixed chunks of tile partials, the multi-GPU exchange unit: for c in [chunk_lo, chunk_hi)
+ * chunk_out[c * ncomp + j] = fixed-order compensated sum of partials[t * ncomp + j] over tiles
+ * t in [c * chunk_tiles, min((c + 1) * chunk_tiles, n_tiles)); other slots are not touched.  A
+ * chunk sum depends only on the grid, so ranks that own whole chunks all-reduce
+ * n_chunks * ncomp doubles and lz_reduce_partials over the chunk vector
+ * gives the same bits for every world size.  Replaces the per-cell fsum of
+ * L/quadrature.py:487-490. */
+/* the library's chunking of an n_tiles grid: chunk_tiles = ceil(n_tiles / 96) tiles per chunk,
+ * n_chunks = ceil(n_tiles / chunk_tiles) <= 96 chunks (96 splits evenly over 1, 2, 3, 4, 6, 8, 12,
+ * 16, 24, 32, 48 ranks).  lz_plan_integrate_host reduces through the same chunks. */
+int lz_chunk_layout(int64_t n_tiles, int64_t* chunk_tiles, int64_t* n_chunks);
+int lz_reduce_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t chunk_tiles, int64_t chunk_lo,
+                     int64_t chunk_hi, double* chunk_out, void* stream);
 /* whole integral through host memory: out[ncomp] (value sums before the 2^d factor) */
 int lz_plan_integrate_host(const lz_plan* plan, const lz_grid* g, double* out);
 
@@ -162,6 +175,14 @@ int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, cons
 
 /* -- diagnostics */
 int lz_fp64_peak(int device, double* tflops_out, double* ms_out);  /* DFMA-chain probe on `device` */
+/* bytes the library itself copied host->device and device->host since the last reset (every
+ * cudaMemcpy* it issues: context / plan tables, grid node arrays, _host entry points' inputs and
+ * results).  reset != 0 zeroes the counters after reading. */
+int lz_transfer_stats(int64_t* h2d_bytes, int64_t* d2h_bytes, int reset);
+/* free the library's process-wide device caches (quadrature node arrays, host-entry arenas,
+ * tile scratch) so that the next call starts cold; contexts and plans the caller still holds
+ * are untouched.  Synchronises the device first.  device < 0: every device. */
+int lz_release_caches(int device);
 
 /* -- multi-GPU: sum the slot-disjoint tile partials of every rank in place (SURVEY.md 8(b)
  * lz_allreduce_partials; replaces the reference's per-cell thread pool reduction,

@@ -83,6 +83,10 @@ SIGNATURES = {
     "lz_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
     "lz_plan_integrate": (C.c_int, [_P, C.POINTER(Grid), _P, C.c_int, _P]),
     "lz_reduce_partials": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
+    "lz_reduce_chunks": (C.c_int, [_P, C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_int64, _P, _P]),
+    "lz_chunk_layout": (C.c_int, [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "lz_transfer_stats": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int]),
+    "lz_release_caches": (C.c_int, [C.c_int]),
     "lz_plan_integrate_host": (C.c_int, [_P, C.POINTER(Grid), _D]),
     "lz_multi_indices": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int64, C.POINTER(C.c_int64)]),
     "lz_zeta_derivatives": (C.c_int, [_P, C.c_int, _P, C.c_int64, _P, _P, _P]),

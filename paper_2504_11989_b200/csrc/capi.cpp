@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <array>
 #include <cmath>
@@ -36,6 +37,8 @@ cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, 
 cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                        cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st);
+cudaError_t launch_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t chunk, int64_t c_lo,
+                          int64_t c_hi, double* chunk_out, cudaStream_t st);
 cudaError_t launch_deriv(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st);
 int deriv_count(int d, int order);
 int deriv_nfunc(int order);
@@ -74,12 +77,27 @@ struct DeviceGuard {
     }
 };
 
+// bytes this library copied across PCIe (lz_transfer_stats): every host<->device copy below
+// goes through copy_h2d / copy_d2h
+std::atomic<int64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st, bool async = true) {
+    g_h2d_bytes += int64_t(bytes);
+    if (async) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    else check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "h2d");
+}
+
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    g_d2h_bytes += int64_t(bytes);
+    check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "d2h");
+}
+
 template <class T> T* upload(const std::vector<T>& v, std::vector<void*>* allocs) {
     if (v.empty()) return nullptr;
     void* p = nullptr;
     check_cuda(cudaMalloc(&p, v.size() * sizeof(T)), "cudaMalloc");
     allocs->push_back(p);
-    check_cuda(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy");
+    copy_h2d(p, v.data(), v.size() * sizeof(T), nullptr, false);
     return static_cast<T*>(p);
 }
 
@@ -838,7 +856,7 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     if (!b.host.empty()) {
         check_cuda(cudaMalloc(reinterpret_cast<void**>(&dev), b.host.size()), "cudaMalloc");
         allocs->push_back(dev);
-        check_cuda(cudaMemcpy(dev, b.host.data(), b.host.size(), cudaMemcpyHostToDevice), "cudaMemcpy");
+        copy_h2d(dev, b.host.data(), b.host.size(), nullptr, false);
     }
     auto at = [&](size_t off, bool nonempty) -> unsigned char* { return nonempty ? dev + off : nullptr; };
     P.blob = dev;
@@ -948,11 +966,12 @@ struct Arena {
     }
 };
 
+std::mutex g_arena_mu;
+std::map<int, Arena*> g_arenas;
+
 Arena& arena(int device) {
-    static std::mutex m;
-    static std::map<int, Arena*> arenas;
-    std::lock_guard<std::mutex> lock(m);
-    Arena*& a = arenas[device];
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    Arena*& a = g_arenas[device];
     if (!a) a = new Arena();
     return *a;
 }
@@ -972,10 +991,10 @@ size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 void h2d(void* dst, const void* src, size_t bytes, char* staging, cudaStream_t st) {
     if (bytes == 0) return;
     if (is_pinned(src)) {
-        check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
+        copy_h2d(dst, src, bytes, st);
     } else {
         std::memcpy(staging, src, bytes);
-        check_cuda(cudaMemcpyAsync(dst, staging, bytes, cudaMemcpyHostToDevice, st), "h2d");
+        copy_h2d(dst, staging, bytes, st);
     }
 }
 
@@ -1033,11 +1052,13 @@ void fill_grid(int d, const lz_grid* g, lz::DevGrid* dg) {
 
 // Quadrature node arrays on the device, cached process-wide per (device, d, n_u, n_v, grading,
 // u_lo): read-only and shared by every plan, so a cold plan does not re-upload them.
+std::mutex g_grid_mu;
+std::map<std::tuple<int, int, int, int, int, double>, GridArrays> g_grid_cache;
+
 const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, int, int, int, double>, GridArrays> cache;
+    auto& cache = g_grid_cache;
     const int d = plan->d;
-    std::lock_guard<std::mutex> lock(mu);
+    std::lock_guard<std::mutex> lock(g_grid_mu);
     auto key = std::make_tuple(plan->device, d, g->n_u, d > 1 ? g->n_v : 1, g->grading, g->u_lo);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
@@ -1087,15 +1108,17 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
 // one stream are serialised, so they can share it; grown stream-ordered (cudaMallocAsync /
 // cudaFreeAsync from the device's memory pool), counters zeroed on growth and left zero by every
 // completed launch.
+struct Scratch {
+    double* wpart = nullptr;
+    unsigned int* tcount = nullptr;
+    int64_t cap = 0;
+};
+std::mutex g_scratch_mu;
+std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
+
 void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, unsigned int** tcount) {
-    struct Scratch {
-        double* wpart = nullptr;
-        unsigned int* tcount = nullptr;
-        int64_t cap = 0;
-    };
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, Scratch> pool;
-    std::lock_guard<std::mutex> lock(mu);
+    auto& pool = g_scratch;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
     Scratch& s = pool[std::make_pair(device, st)];
     if (s.cap < n_tiles) {
         if (s.wpart) check_cuda(cudaFreeAsync(s.wpart, st), "cudaFreeAsync");
@@ -1399,10 +1422,9 @@ int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint3
         h2d(dk, k, kb, A.hbuf, A.st);
         check_cuda(lz::launch_batch(P, false, dk, n, dout, flags, auto_lanes(n), dstat, A.st), "zeta kernel");
         const bool pinned_out = is_pinned(out);
-        check_cuda(cudaMemcpyAsync(pinned_out ? (void*)out : (void*)A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st),
-                   "d2h");
+        copy_d2h(pinned_out ? (void*)out : (void*)A.hbuf, dout, ob, A.st);
         int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
-        check_cuda(cudaMemcpyAsync(hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, A.st), "d2h");
+        copy_d2h(hstat, dstat, sizeof(int), A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         if (!pinned_out) std::memcpy(out, A.hbuf, ob);
         if (*hstat & 1)
@@ -1438,7 +1460,7 @@ int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* ou
         double* dout = reinterpret_cast<double*>(A.dbuf + al256(kb));
         h2d(dk, k, kb, A.hbuf, A.st);
         check_cuda(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, A.st), "hessian kernel");
-        check_cuda(cudaMemcpyAsync(A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st), "d2h");
+        copy_d2h(A.hbuf, dout, ob, A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, ob);
     });
@@ -1609,9 +1631,9 @@ int lz_zeta_derivatives_host(const lz_ctx* c, int order, const double* k, int64_
         check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
         h2d(dk, k, kb, A.hbuf, A.st);
         check_cuda(lz::launch_deriv(P, dk, n, dout, dstat, A.st), "derivative kernel");
-        check_cuda(cudaMemcpyAsync(A.hbuf, dout, ob, cudaMemcpyDeviceToHost, A.st), "d2h");
+        copy_d2h(A.hbuf, dout, ob, A.st);
         int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
-        check_cuda(cudaMemcpyAsync(hstat, dstat, sizeof(int), cudaMemcpyDeviceToHost, A.st), "d2h");
+        copy_d2h(hstat, dstat, sizeof(int), A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, ob);
         if (*hstat & 1) throw Error{LZ_EPOLE, "derivatives of Z are singular at k in the reciprocal lattice"};
@@ -1777,6 +1799,88 @@ int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, doubl
     });
 }
 
+int lz_reduce_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t chunk_tiles, int64_t chunk_lo,
+                     int64_t chunk_hi, double* chunk_out, void* stream) {
+    return guarded([&] {
+        if (n_tiles < 0 || ncomp < 1 || chunk_tiles < 1 || chunk_lo < 0 || chunk_hi < chunk_lo ||
+            chunk_hi * chunk_tiles >= n_tiles + chunk_tiles)
+            throw Error{LZ_EINVAL, "chunk range outside the tile vector"};
+        if (chunk_hi == chunk_lo) return;
+        DeviceGuard dg(device_of(partials));
+        check_cuda(lz::launch_chunks(partials, n_tiles, ncomp, chunk_tiles, chunk_lo, chunk_hi, chunk_out,
+                                     (cudaStream_t)stream),
+                   "chunk kernel");
+    });
+}
+
+int lz_chunk_layout(int64_t n_tiles, int64_t* chunk_tiles, int64_t* n_chunks) {
+    constexpr int64_t kMaxChunks = 96;
+    const int64_t ct = std::max<int64_t>(1, (n_tiles + kMaxChunks - 1) / kMaxChunks);
+    if (chunk_tiles) *chunk_tiles = ct;
+    if (n_chunks) *n_chunks = n_tiles > 0 ? (n_tiles + ct - 1) / ct : 0;
+    return LZ_OK;
+}
+
+int lz_transfer_stats(int64_t* h2d_bytes, int64_t* d2h_bytes, int reset) {
+    if (h2d_bytes) *h2d_bytes = g_h2d_bytes.load();
+    if (d2h_bytes) *d2h_bytes = g_d2h_bytes.load();
+    if (reset) {
+        g_h2d_bytes = 0;
+        g_d2h_bytes = 0;
+    }
+    return LZ_OK;
+}
+
+int lz_release_caches(int device) {
+    return guarded([&] {
+        int old = -1;
+        check_cuda(cudaGetDevice(&old), "cudaGetDevice");
+        auto on = [&](int dev) { return device < 0 || dev == device; };
+        {
+            std::lock_guard<std::mutex> lock(g_grid_mu);
+            for (auto it = g_grid_cache.begin(); it != g_grid_cache.end();) {
+                if (on(std::get<0>(it->first))) {
+                    cudaSetDevice(std::get<0>(it->first));
+                    cudaDeviceSynchronize();
+                    cudaFree(const_cast<double*>(it->second.u));  // one allocation per entry
+                    it = g_grid_cache.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lock(g_scratch_mu);
+            for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+                if (on(it->first.first)) {
+                    cudaSetDevice(it->first.first);
+                    cudaDeviceSynchronize();
+                    if (it->second.wpart) cudaFree(it->second.wpart);
+                    it = g_scratch.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lock(g_arena_mu);
+            for (auto& kv : g_arenas) {
+                if (!on(kv.first) || !kv.second) continue;
+                Arena& a = *kv.second;
+                std::lock_guard<std::mutex> al(a.mu);
+                cudaSetDevice(kv.first);
+                cudaDeviceSynchronize();
+                if (a.dbuf) cudaFree(a.dbuf);
+                if (a.hbuf) cudaFreeHost(a.hbuf);
+                a.dbuf = a.hbuf = nullptr;
+                a.dcap = a.hcap = 0;
+            }
+        }
+        if (old >= 0) cudaSetDevice(old);
+        check_cuda(cudaGetLastError(), "release caches");
+    });
+}
+
 int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
     return guarded([&] {
         if (pl->device < 0) throw Error{LZ_ECUDA, "plan has no device tables (created from host-only contexts)"};
@@ -1785,19 +1889,26 @@ int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
         int rc = lz_grid_tiles(pl->d, g, &n_nodes, &n_tiles);
         if (rc != LZ_OK) throw Error{rc, g_last_error};
         const int ncomp = pl->kind == 0 ? 1 : 2;
+        // the same reduction as the sharded path (tiles -> fixed chunks -> total), so one-call and
+        // multi-rank results carry the same bits
+        int64_t chunk_tiles = 0, n_chunks = 0;
+        lz_chunk_layout(n_tiles, &chunk_tiles, &n_chunks);
         Arena& A = arena(pl->device);
         std::lock_guard<std::mutex> lock(A.mu);
         const size_t pb = sizeof(double) * size_t(n_tiles) * ncomp;
-        A.ensure(al256(pb) + 256, 256);
+        const size_t cb = sizeof(double) * size_t(n_chunks) * ncomp;
+        A.ensure(al256(pb) + al256(cb) + 256, 256);
         double* dp = reinterpret_cast<double*>(A.dbuf);
-        double* dout = reinterpret_cast<double*>(A.dbuf + al256(pb));
+        double* dc = reinterpret_cast<double*>(A.dbuf + al256(pb));
+        double* dout = reinterpret_cast<double*>(A.dbuf + al256(pb) + al256(cb));
         lz_grid gg = *g;
         gg.tile_lo = 0;
         gg.tile_hi = 0;
         rc = lz_plan_integrate(pl, &gg, dp, 0, A.st);
         if (rc != LZ_OK) throw Error{rc, g_last_error};
-        check_cuda(lz::launch_reduce(dp, n_tiles, ncomp, dout, A.st), "reduce");
-        check_cuda(cudaMemcpyAsync(A.hbuf, dout, sizeof(double) * ncomp, cudaMemcpyDeviceToHost, A.st), "d2h");
+        check_cuda(lz::launch_chunks(dp, n_tiles, ncomp, chunk_tiles, 0, n_chunks, dc, A.st), "chunk reduce");
+        check_cuda(lz::launch_reduce(dc, n_chunks, ncomp, dout, A.st), "reduce");
+        copy_d2h(A.hbuf, dout, sizeof(double) * ncomp, A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, sizeof(double) * ncomp);
     });
@@ -1845,11 +1956,11 @@ int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, cons
                                                  al256(sizeof(double) * size_t(nblocks)));
         double hA[16] = {0};
         for (int i = 0; i < d * d; ++i) hA[i] = a[i];
-        check_cuda(cudaMemcpyAsync(dA, hA, sizeof(hA), cudaMemcpyHostToDevice, ar.st), "h2d");
+        copy_h2d(dA, hA, sizeof(hA), ar.st);
         const double nz[3] = {nus ? nus[0] : 0.0, nus ? nus[1] : 0.0, nus ? nus[2] : 0.0};
         check_cuda(lz::launch_direct(d, kind, L, npts, dA, nz, dp, nblocks, ar.st), "direct kernel");
         check_cuda(lz::launch_reduce(dp, nblocks, 1, dout, ar.st), "reduce");
-        check_cuda(cudaMemcpyAsync(ar.hbuf, dout, sizeof(double), cudaMemcpyDeviceToHost, ar.st), "d2h");
+        copy_d2h(ar.hbuf, dout, sizeof(double), ar.st);
         check_cuda(cudaStreamSynchronize(ar.st), "sync");
         double v;
         std::memcpy(&v, ar.hbuf, sizeof(double));

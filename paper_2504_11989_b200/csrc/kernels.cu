@@ -1508,9 +1508,9 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
 __global__ void __launch_bounds__(1024) reduce_kernel(const double* __restrict__ partials, int64_t n_tiles, int ncomp,
-                              double* __restrict__ out) {
+                              double* __restrict__ out, bool vec2) {
     __shared__ double ss[1024], cc[1024];
-    if (ncomp == 2) {
+    if (vec2) {
         // both components in one pass (16-byte loads), each in the per-component order below
         __shared__ double ss1[1024], cc1[1024];
         double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
@@ -1592,6 +1592,41 @@ __global__ void __launch_bounds__(1024) reduce_kernel(const double* __restrict__
             __syncthreads();
         }
         if (threadIdx.x == 0) out[comp] = ss[0] + cc[0];
+        __syncthreads();
+    }
+}
+
+// Fixed chunks of tile partials (the multi-GPU exchange unit): block b sums tiles
+// [c chunk, min((c + 1) chunk, n_tiles)), c = c_lo + b, per component with a fixed-order
+// compensated (Neumaier) sum, and writes chunk_out[c ncomp + comp].  A chunk's sum depends only
+// on the grid, never on which rank computed it, so ranks owning whole chunks exchange
+// n_chunks x ncomp doubles instead of every tile partial and the result is bit-identical for
+// any world size.
+__global__ void __launch_bounds__(256) chunk_kernel(const double* __restrict__ partials, int64_t n_tiles, int ncomp,
+                                                    int64_t chunk, int64_t c_lo, double* __restrict__ chunk_out) {
+    __shared__ double ss[256], cc[256];
+    const int64_t c = c_lo + blockIdx.x;
+    const int64_t t0 = c * chunk, t1 = min(n_tiles, t0 + chunk);
+    for (int comp = 0; comp < ncomp; ++comp) {
+        double s = 0.0, e = 0.0;
+        for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+            const double x = __ldg(&partials[i * ncomp + comp]);
+            const double t = s + x;
+            e += (fabs(s) >= fabs(x)) ? (s - t) + x : (x - t) + s;
+            s = t;
+        }
+        ss[threadIdx.x] = s;
+        cc[threadIdx.x] = e;
+        __syncthreads();
+        for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+            if (threadIdx.x < h) {
+                const double a = ss[threadIdx.x], b = ss[threadIdx.x + h], t = a + b;
+                ss[threadIdx.x] = t;
+                cc[threadIdx.x] += cc[threadIdx.x + h] + ((fabs(a) >= fabs(b)) ? (a - t) + b : (b - t) + a);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) chunk_out[c * ncomp + comp] = ss[0] + cc[0];
         __syncthreads();
     }
 }
@@ -1944,7 +1979,17 @@ cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int
 }
 
 cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, double* out, cudaStream_t st) {
-    reduce_kernel<<<1, 1024, 0, st>>>(partials, n_tiles, ncomp, out);
+    // the two-component pass reads double2: only for 16-byte aligned buffers (the C ABI asks for
+    // 8-byte alignment); both paths add in the same per-component order
+    const bool vec2 = ncomp == 2 && (reinterpret_cast<uintptr_t>(partials) & 15) == 0;
+    reduce_kernel<<<1, 1024, 0, st>>>(partials, n_tiles, ncomp, out, vec2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t chunk, int64_t c_lo,
+                          int64_t c_hi, double* chunk_out, cudaStream_t st) {
+    if (c_hi <= c_lo) return cudaSuccess;
+    chunk_kernel<<<unsigned(c_hi - c_lo), 256, 0, st>>>(partials, n_tiles, ncomp, chunk, c_lo, chunk_out);
     return cudaGetLastError();
 }
 

@@ -1,17 +1,22 @@
 """Multi-GPU node sharding of the fused BZ integrals (one process per GPU).
 
 Every fixed Duffy grid is a flat list of 256-node tiles; each tile reduces
-deterministically to one partial per component, written to its own slot of a
-global partials vector.  Rank r of W computes the contiguous tile range
-[r T / W, (r+1) T / W) and leaves every other slot zero, so ONE all-reduce
-(sum, FP64) over NCCL/NVLink assembles the exact vector -- adding zeros is
-exact -- and the fixed-order compensated reduction that follows gives
-bit-identical results for any W.  This replaces the reference's
-ThreadPoolExecutor over Duffy cells (L/quadrature.py:482-486).
+deterministically to one partial per component.  The tiles are grouped into at
+most ``MAX_CHUNKS`` = 96 fixed chunks that depend only on the grid (C3: 96
+chunks of 1,024 tiles).  Rank r of W owns the contiguous chunk range
+[r C / W, (r+1) C / W): it runs the tile kernel on its tiles, reduces each of
+its chunks in a fixed order (``lz_reduce_chunks``) into its own slots of a
+C x ncomp vector, and ONE all-reduce (sum, FP64) over NCCL/NVLink assembles
+that vector exactly (every other slot is zero, and adding zeros is exact) --
+1.5 KB for C3 instead of the 1.5 MB of tile partials.  The fixed-order
+compensated reduction of the chunk vector then gives bit-identical results
+for any W.  This replaces the reference's ThreadPoolExecutor over Duffy cells
+and its fsum of their values (L/quadrature.py:482-490).
 """
 from __future__ import annotations
 
 import warnings
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -21,9 +26,37 @@ from .manybody import ATMGrid, ATMResult
 from .quadrature import Plan, atm_plan, product_plan
 
 
-def shard_range(n_tiles: int, rank: int, world: int):
-    """Contiguous tile range of one rank."""
-    return n_tiles * rank // world, n_tiles * (rank + 1) // world
+MAX_CHUNKS = 96  # divisible by 1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48: balanced ranks for those W
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous index range [lo, hi) of one rank out of ``n`` units."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+@dataclass(frozen=True)
+class ChunkLayout:
+    """Fixed grouping of ``n_tiles`` tile partials into chunks (a function of the grid only)."""
+
+    n_tiles: int
+    max_chunks: int = MAX_CHUNKS
+
+    @property
+    def chunk_tiles(self) -> int:
+        return max(1, -(-self.n_tiles // self.max_chunks))
+
+    @property
+    def n_chunks(self) -> int:
+        return -(-self.n_tiles // self.chunk_tiles) if self.n_tiles else 0
+
+    def chunks_of(self, rank: int, world: int):
+        """Chunk range [c_lo, c_hi) owned by ``rank``."""
+        return shard_range(self.n_chunks, rank, world)
+
+    def tiles_of(self, rank: int, world: int):
+        """Tile range [t_lo, t_hi) owned by ``rank`` (whole chunks)."""
+        c_lo, c_hi = self.chunks_of(rank, world)
+        return min(c_lo * self.chunk_tiles, self.n_tiles), min(c_hi * self.chunk_tiles, self.n_tiles)
 
 
 def nccl_comm_ptr(group=None, device=None) -> int:
@@ -44,7 +77,8 @@ def nccl_comm_ptr(group=None, device=None) -> int:
 def allreduce_partials(partials: torch.Tensor, group=None, stream=None) -> None:
     """Sum the slot-disjoint partials of every rank in place: through the C ABI
     (lz_allreduce_partials: one ncclAllReduce on the library's stream order) when the group is
-    NCCL, else torch.distributed (gloo on CPU tests)."""
+    NCCL, else torch.distributed on a host copy (gloo groups: CPU tests and the two-process
+    one-GPU test)."""
     comm = nccl_comm_ptr(group, partials.device) if partials.is_cuda else 0
     if comm:
         from . import _native as N
@@ -56,6 +90,11 @@ def allreduce_partials(partials: torch.Tensor, group=None, stream=None) -> None:
             N.check(rc, "all-reduce")
         # NCCL could not be resolved or refused the call before enqueueing: torch's collective
         warnings.warn(f"lz_allreduce_partials unavailable ({N.last_error()}); using dist.all_reduce")
+    if partials.is_cuda and dist.get_backend(group) != "nccl":
+        host = partials.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        partials.copy_(host)
+        return
     dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
 
 
@@ -68,31 +107,61 @@ def _world(group=None):
 class ShardedIntegral:
     """Reusable device buffers + plan for repeated sharded evaluation of one integral."""
 
-    def __init__(self, plan: Plan, n_u: int, n_v: int, grading: int, device=None, group=None):
+    def __init__(self, plan: Plan, n_u: int, n_v: int, grading: int, device=None, group=None,
+                 world=None, rank=None):
         self.plan = plan
         self.n_u, self.n_v, self.grading = n_u, n_v, grading
         self.group = group
-        self.rank, self.world = _world(group)
+        r, w = _world(group)
+        # rank/world overrides: time one rank's shard of a larger job on this process's GPU
+        self.rank = r if rank is None else rank
+        self.world = w if world is None else world
         self.n_nodes, self.n_tiles = plan.tiles(n_u, n_v, grading)
         self.ncomp = plan.ncomp
+        self.layout = ChunkLayout(self.n_tiles)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        self.partials = torch.zeros(self.n_tiles * self.ncomp, dtype=torch.float64, device=self.device)
+        # tile partials at their global slots (only this rank's range is written and read)
+        self.partials = torch.empty(self.n_tiles * self.ncomp, dtype=torch.float64, device=self.device)
+        self.chunks = torch.zeros(self.layout.n_chunks * self.ncomp, dtype=torch.float64, device=self.device)
         self.out = torch.zeros(self.ncomp, dtype=torch.float64, device=self.device)
-        self.tile_lo, self.tile_hi = shard_range(self.n_tiles, self.rank, self.world)
+        self.chunk_lo, self.chunk_hi = self.layout.chunks_of(self.rank, self.world)
+        self.tile_lo, self.tile_hi = self.layout.tiles_of(self.rank, self.world)
 
     @property
     def local_nodes(self) -> int:
         return (self.tile_hi - self.tile_lo) * 256
 
+    @property
+    def exchange_bytes(self) -> int:
+        return self.chunks.numel() * 8
+
+    def _stream(self, stream):
+        return stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+
+    def integrate(self, stream=None) -> None:
+        """Enqueue the tile kernel on this rank's tiles."""
+        if self.tile_hi > self.tile_lo:
+            self.plan.integrate_device(self.partials, self.n_u, self.n_v, self.grading,
+                                       self.tile_lo, self.tile_hi, stream=stream)
+
+    def reduce(self, stream=None) -> torch.Tensor:
+        """Chunk sums of this rank, the all-reduce of the chunk vector, the fixed-order total."""
+        from . import _native as N
+        st = self._stream(stream)
+        if self.world > 1:
+            self.chunks.zero_()
+        N.check(N.lib().lz_reduce_chunks(self.partials.data_ptr(), self.n_tiles, self.ncomp,
+                                         self.layout.chunk_tiles, self.chunk_lo, self.chunk_hi,
+                                         self.chunks.data_ptr(), st), "chunk reduce")
+        if self.world > 1:
+            allreduce_partials(self.chunks, self.group, stream)
+        Plan.reduce_device(self.chunks, self.layout.n_chunks, self.ncomp, self.out, stream=stream)
+        return self.out
+
     def run(self, stream=None) -> torch.Tensor:
         """Enqueue one evaluation; returns the device tensor of component sums (before 2^d)."""
-        self.partials.zero_()
-        self.plan.integrate_device(self.partials, self.n_u, self.n_v, self.grading,
-                                   self.tile_lo, self.tile_hi, stream=stream)
-        if self.world > 1:
-            allreduce_partials(self.partials, self.group, stream)
-        Plan.reduce_device(self.partials, self.n_tiles, self.ncomp, self.out, stream=stream)
-        return self.out
+        self.integrate(stream)
+        return self.reduce(stream)
 
 
 def atm_energy_distributed(lattice: Lattice, grid: ATMGrid | None = None, group=None) -> ATMResult:

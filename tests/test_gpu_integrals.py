@@ -5,7 +5,7 @@ import pytest
 from oracle import oracle as O
 from paper_2504_11989_b200 import named_lattice
 from paper_2504_11989_b200.manybody import ATMGrid, atm_cohesive_energy, atm_integrals, many_body_zeta
-from paper_2504_11989_b200.quadrature import QuadratureConfig, atm_plan, fixed_grid_integral, integrate_product
+from paper_2504_11989_b200.quadrature import Plan, QuadratureConfig, atm_plan, fixed_grid_integral, integrate_product
 
 pytestmark = pytest.mark.gpu
 SUM_TOL = 1e-10  # BASELINE north_star: <= 1e-10 relative on each lattice sum
@@ -160,10 +160,11 @@ def test_nccl_allreduce_through_cabi():
 # line pair spans two tiles
 @pytest.mark.parametrize("n_u,n_v", [(32, 16), (6, 128), (4, 96), (3, 256)])
 def test_tile_sharding_bit_identical(n_u, n_v):
-    """Slot-disjoint partials: any split of the tile range gives bit-identical sums."""
+    """Slot-disjoint partials: any split of the tile range gives bit-identical tile partials, and
+    the chunked reduction of every world size's shards gives the same bits as the one-call API."""
     import torch
 
-    from paper_2504_11989_b200.quadrature import Plan
+    from paper_2504_11989_b200.distributed import ShardedIntegral
     lat = named_lattice("fcc")
     plan = atm_plan(lat)
     nn, nt = plan.tiles(n_u, n_v, 3)
@@ -177,10 +178,24 @@ def test_tile_sharding_bit_identical(n_u, n_v):
             plan.integrate_device(buf, n_u, n_v, 3, lo, hi)
             parts += buf  # exact: disjoint slots
         assert torch.equal(parts, full)
-    o1 = torch.zeros(2, dtype=torch.float64, device="cuda")
-    Plan.reduce_device(full, nt, 2, o1)
     res = atm_integrals(lat, ATMGrid(n_u, n_v, 3))
-    assert float(o1[0]) * 8 == res.zeta333
+    for world in (1, 2, 3, 4, 8):
+        # each rank's chunks on this GPU in turn; the all-reduce of disjoint chunk slots is a sum
+        # with zeros, emulated exactly by adding the per-rank chunk vectors
+        chunks = None
+        for r in range(world):
+            s = ShardedIntegral(plan, n_u, n_v, 3, world=world, rank=r)
+            s.world = 1  # no collective: this process is every rank in turn
+            s.chunks.zero_()
+            s.integrate()
+            from paper_2504_11989_b200 import _native as N
+            N.check(N.lib().lz_reduce_chunks(s.partials.data_ptr(), s.n_tiles, 2, s.layout.chunk_tiles,
+                                             s.chunk_lo, s.chunk_hi, s.chunks.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+            chunks = s.chunks.clone() if chunks is None else chunks + s.chunks
+        o = torch.zeros(2, dtype=torch.float64, device="cuda")
+        Plan.reduce_device(chunks, s.layout.n_chunks, 2, o)
+        assert float(o[0]) * 8 == res.zeta333 and float(o[1]) * 8 == res.dot_term, world
 
 
 @pytest.mark.parametrize("name", ["fcc", "bcc"])

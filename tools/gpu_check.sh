@@ -1,0 +1,27 @@
+#!/usr/bin/env bash
+# One gpurun call: GPU tests, the bench line (both arms), the launch list and one ncu --set full
+# capture of the ATM kernel.  Usage (from the repo root, under gpurun):
+#   bash tools/gpu_check.sh TAG [skip-tests] [skip-ncu]
+TAG="${1:-run}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
+if [ "$2" != "skip-tests" ]; then
+  timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1
+  echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
+  echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
+fi
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
+echo "ref rc=$?" >> gpurun_out/${TAG}_ref.err
+if [ "$3" != "skip-ncu" ]; then
+  CMD="python bench.py --steps 2 --warmup 3 --no-secondary --no-cpu-baseline --e2e-steps 1"
+  timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
+  timeout 300 python tools/profile_target.py atm > gpurun_out/${TAG}_atm_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_kernel -c 1 \
+      -o gpurun_out/${TAG}_atm -f python tools/profile_target.py atm > gpurun_out/${TAG}_ncu_atm.log 2>&1
+fi
+echo done > gpurun_out/${TAG}_done
