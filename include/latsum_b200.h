@@ -148,8 +148,8 @@ int lz_plan_integrate_host(const lz_plan* plan, const lz_grid* g, double* out);
 /* -- order-m derivatives at arbitrary k (the k != 0 generalisation of
  * the reference's derivative tables L/epstein.py:347-415, same Hermite expansion and point-set
  * rules): out[i * n_alpha + j] = d^alpha_j Z(k_i) for every multi-index |alpha| = order
- * (1 <= order <= 4, d <= 3) in the order of lz_multi_indices (L/epstein.py:426-433, head
- * ascending).  The polynomial-weighted zeta is M^alpha = sum'_z z^alpha |z|^-nu e^{-2 pi i k.z}
+ * (1 <= order <= 12, any d <= 4: the reference's order and dimension limits, L/epstein.py:347-353,
+ * L/lattice.py:20) in the order of lz_multi_indices (L/epstein.py:426-433, head ascending).  The polynomial-weighted zeta is M^alpha = sum'_z z^alpha |z|^-nu e^{-2 pi i k.z}
  * = d^alpha Z / (-2 pi i)^order.  k is reduced into the cell; k in the reciprocal lattice sets
  * status bit 1 (LZ_EPOLE from the host entry point).  lz_zeta_derivatives takes device pointers
  * and is stream-ordered. */
@@ -162,6 +162,11 @@ int lz_zeta_derivatives_host(const lz_ctx* ctx, int order, const double* k, int6
  * Writes n multi-indices (alphas, n x d ints) with |alpha| even <= order and their values;
  * copies min(cap, n) entries, returns n through *n. */
 int lz_ctx_reg_derivatives(const lz_ctx* ctx, int order, int* alphas, double* vals, int64_t cap, int64_t* n);
+/* Same table computed on the context's device (deriv.cu moment kernel at k = 0, compensated sums;
+ * EpsteinContext.reg_derivatives uses this one; lz_ctx_reg_derivatives is the host long-double
+ * cross-check). */
+int lz_ctx_reg_derivatives_device(const lz_ctx* ctx, int order, int* alphas, double* vals, int64_t cap,
+                                  int64_t* n);
 
 /* -- host special function used by the tail algebra and tests: Gamma(s, x), x > 0 */
 double lz_upper_gamma(double s, double x);

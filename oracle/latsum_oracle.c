@@ -530,6 +530,7 @@ typedef struct {
     const R *dz, *dw, *rq;
     const double* k;
     double* out;
+    double* out_abs;  /* optional: sum of |terms| (the cancellation scale of each value) */
 } DArgs;
 
 static R fact_l(int n) { R f = 1.0L; for (int i = 2; i <= n; ++i) f *= i; return f; }
@@ -541,57 +542,86 @@ static void deriv_body(long i, void* p) {
     R k[MAXD];
     for (int a = 0; a < d; ++a) k[a] = A->k[i * d + a];
     R twopim = powl(2.0L * PI_L, (R)m);
+    /* per direct point: w cos(2 pi k.z + m pi / 2); per q (q = 0 first, unsplit): y and
+     * F^(pp)(|y|^2) = (-1)^pp |y|^{-2(s+pp)} Gamma(s + pp, pi |y|^2 / t), pp = 0..m -- evaluated
+     * once and shared by every multi-index */
+    R* dtr = (R*)malloc(sizeof(R) * (size_t)(A->nd > 0 ? A->nd : 1));
+    R* ys = (R*)malloc(sizeof(R) * (size_t)(A->nr + 1) * d);
+    R* fps = (R*)malloc(sizeof(R) * (size_t)(A->nr + 1) * (m + 1));
+    for (int t = 0; t < A->nd; ++t) {
+        R ph = 0.0L;
+        for (int a = 0; a < d; ++a) ph += k[a] * A->dz[t * d + a];
+        dtr[t] = A->dw[t] * cosl(2.0L * PI_L * ph + m * PI_L / 2.0L);
+    }
+    for (int t = -1; t < A->nr; ++t) {
+        R r2 = 0.0L;
+        R* y = ys + (size_t)(t + 1) * d;
+        for (int a = 0; a < d; ++a) { y[a] = k[a] + (t >= 0 ? A->rq[t * d + a] : 0.0L); r2 += y[a] * y[a]; }
+        R x = PI_L * r2 / c->t;
+        for (int pp = (m + 1) / 2; pp <= m; ++pp)
+            fps[(size_t)(t + 1) * (m + 1) + pp] =
+                ((pp & 1) ? -1.0L : 1.0L) * powl(r2, -(c->s + pp)) * orc_upper_gamma_l(c->s + pp, x);
+    }
     for (int j = 0; j < A->na; ++j) {
         const int* al = A->alphas + j * d;
-        R dsum = 0.0L, rsum = 0.0L;
+        R dsum = 0.0L, rsum = 0.0L, dabs = 0.0L, rabs = 0.0L;
         for (int t = 0; t < A->nd; ++t) {
-            R ph = 0.0L, za = 1.0L;
-            for (int a = 0; a < d; ++a) {
-                ph += k[a] * A->dz[t * d + a];
+            R za = 1.0L;
+            for (int a = 0; a < d; ++a)
                 for (int e = 0; e < al[a]; ++e) za *= A->dz[t * d + a];
-            }
-            dsum += A->dw[t] * za * cosl(2.0L * PI_L * ph + m * PI_L / 2.0L);
+            dsum += dtr[t] * za;
+            dabs += fabsl(dtr[t] * za);
         }
-        for (int t = -1; t < A->nr; ++t) {
-            R y[MAXD], r2 = 0.0L;
-            for (int a = 0; a < d; ++a) { y[a] = k[a] + (t >= 0 ? A->rq[t * d + a] : 0.0L); r2 += y[a] * y[a]; }
-            R x = PI_L * r2 / c->t;
-            /* Hermite terms: j_a <= alpha_a / 2 */
-            int jm[MAXD], cnt = 1;
-            for (int a = 0; a < d; ++a) { jm[a] = al[a] / 2; cnt *= jm[a] + 1; }
-            for (int q = 0; q < cnt; ++q) {
-                int rem = q, js = 0, jj[MAXD];
-                for (int a = 0; a < d; ++a) { jj[a] = rem % (jm[a] + 1); rem /= jm[a] + 1; js += jj[a]; }
-                R coef = 1.0L;
-                for (int a = 0; a < d; ++a) {
-                    coef *= fact_l(al[a]) / (fact_l(jj[a]) * fact_l(al[a] - 2 * jj[a]));
-                    for (int e = 0; e < al[a] - 2 * jj[a]; ++e) coef *= 2.0L * y[a];
-                }
-                int pp = m - js;
-                R fp = ((pp & 1) ? -1.0L : 1.0L) * powl(r2, -(c->s + pp)) * orc_upper_gamma_l(c->s + pp, x);
-                rsum += coef * fp;
+        /* Hermite terms: j_a <= alpha_a / 2 */
+        int jm[MAXD], cnt = 1;
+        for (int a = 0; a < d; ++a) { jm[a] = al[a] / 2; cnt *= jm[a] + 1; }
+        for (int q = 0; q < cnt; ++q) {
+            int rem = q, js = 0, jj[MAXD];
+            R cf = 1.0L;
+            for (int a = 0; a < d; ++a) {
+                jj[a] = rem % (jm[a] + 1); rem /= jm[a] + 1; js += jj[a];
+                cf *= fact_l(al[a]) / (fact_l(jj[a]) * fact_l(al[a] - 2 * jj[a]));
             }
+            int pp = m - js;
+            R part = 0.0L;
+            for (int t = 0; t <= A->nr; ++t) {
+                const R* y = ys + (size_t)t * d;
+                R v = fps[(size_t)t * (m + 1) + pp];
+                for (int a = 0; a < d; ++a)
+                    for (int e = 0; e < al[a] - 2 * jj[a]; ++e) v *= 2.0L * y[a];
+                part += v;
+                rabs += fabsl(cf * v);
+            }
+            rsum += cf * part;
         }
         A->out[i * A->na + j] = (double)(c->pref * (2.0L * twopim * dsum + c->rfac * rsum));
+        if (A->out_abs)
+            A->out_abs[i * A->na + j] = (double)(fabsl(c->pref) * (2.0L * twopim * dabs + fabsl(c->rfac) * rabs));
     }
+    free(dtr); free(ys); free(fps);
 }
 
-int orc_derivatives(int d, const double* a, double nu, int order, const double* k, long n, double* out) {
+int orc_derivatives_abs(int d, const double* a, double nu, int order, const double* k, long n, double* out,
+                        double* out_abs) {
     OCtx c;
     int rc = octx_init(&c, d, a, nu, 0);
     if (rc) { octx_free(&c); return rc; }
-    if (order < 1 || c.branch == 2) { octx_free(&c); return 1; }
+    if (order < 1 || order > 12 || c.branch == 2) { octx_free(&c); return 1; }
     R *dz = NULL, *dw = NULL, *rq = NULL;
     int nd = enum_direct(&c, order, 1e-20L, &dz, &dw, NULL);
     int nr = enum_recip(&c, c.s + order, 1e-20L, &rq);
     if (nd < 0 || nr < 0) { free(dz); free(dw); free(rq); octx_free(&c); return 6; }
-    int alph[64 * MAXD];
+    int* alph = (int*)malloc(sizeof(int) * 512 * MAXD);
     int na = orc_multi_indices(d, order, alph);
-    DArgs A = {&c, order, na, nd, nr, alph, dz, dw, rq, k, out};
+    DArgs A = {&c, order, na, nd, nr, alph, dz, dw, rq, k, out, out_abs};
     par_for(n, deriv_body, &A);
-    free(dz); free(dw); free(rq);
+    free(alph); free(dz); free(dw); free(rq);
     octx_free(&c);
     return 0;
+}
+
+int orc_derivatives(int d, const double* a, double nu, int order, const double* k, long n, double* out) {
+    return orc_derivatives_abs(d, a, nu, order, k, n, out, NULL);
 }
 
 /* Gauss-Legendre on [-1,1] (Newton, long double), ascending */

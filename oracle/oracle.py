@@ -36,6 +36,7 @@ def lib():
         L.orc_zeta.argtypes = [C.c_int, D, C.c_double, D, C.c_long, D, C.c_int]
         L.orc_hessian.argtypes = [C.c_int, D, C.c_double, D, C.c_long, D]
         L.orc_derivatives.argtypes = [C.c_int, D, C.c_double, C.c_int, D, C.c_long, D]
+        L.orc_derivatives_abs.argtypes = [C.c_int, D, C.c_double, C.c_int, D, C.c_long, D, D]
         L.orc_multi_indices.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.orc_product_grid.argtypes = [C.c_int, D, D, C.c_int, C.c_int, C.c_int, C.c_int, C.c_long,
                                        C.c_long, D]
@@ -87,22 +88,25 @@ def hessian(a, nu, k):
 
 
 def multi_indices(d, order):
-    buf = (C.c_int * (64 * 4))()
+    buf = (C.c_int * (512 * 4))()
     n = lib().orc_multi_indices(d, order, buf)
     return [tuple(buf[i * d:(i + 1) * d]) for i in range(n)]
 
 
-def derivatives(a, nu, order, k):
-    """All d^alpha Z(k), |alpha| = order, in multi_indices(d, order) order (long double)."""
+def derivatives(a, nu, order, k, with_abs=False):
+    """All d^alpha Z(k), |alpha| = order, in multi_indices(d, order) order (long double).
+    with_abs: also the sum of |terms| of each value (direct + Hermite reciprocal terms), the
+    cancellation scale that bounds the rounding error of any double-precision evaluation."""
     a = _mat(a)
     d = a.shape[0]
     k = np.ascontiguousarray(np.atleast_2d(np.asarray(k, dtype=np.float64)))
     na = len(multi_indices(d, order))
     out = np.empty((len(k), na))
-    rc = lib().orc_derivatives(d, _p(a), float(nu), int(order), _p(k), len(k), _p(out))
+    ab = np.empty((len(k), na))
+    rc = lib().orc_derivatives_abs(d, _p(a), float(nu), int(order), _p(k), len(k), _p(out), _p(ab))
     if rc:
         raise RuntimeError(f"oracle error {rc}")
-    return out
+    return (out, ab) if with_abs else out
 
 
 def product_grid(a, nus, n_u, n_v, grading=1, lo=0, hi=0):

@@ -93,6 +93,8 @@ SIGNATURES = {
     "lz_zeta_derivatives_host": (C.c_int, [_P, C.c_int, _D, C.c_int64, _D]),
     "lz_ctx_reg_derivatives": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
                                           C.POINTER(C.c_int64)]),
+    "lz_ctx_reg_derivatives_device": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _D, C.c_int64,
+                                                 C.POINTER(C.c_int64)]),
     "lz_upper_gamma": (C.c_double, [C.c_double, C.c_double]),
     "lz_direct_sum3": (C.c_int, [C.c_int, C.c_int, _D, C.c_int64, C.c_int, _D, C.c_double, _D]),
     "lz_fp64_peak": (C.c_int, [C.c_int, _D, _D]),

@@ -40,6 +40,7 @@ cudaError_t launch_reduce(const double* partials, int64_t n_tiles, int ncomp, do
 cudaError_t launch_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t chunk, int64_t c_lo,
                           int64_t c_hi, double* chunk_out, cudaStream_t st);
 cudaError_t launch_deriv(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st);
+cudaError_t launch_deriv_g(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st);
 int deriv_count(int d, int order);
 int deriv_nfunc(int order);
 cudaError_t launch_probe(double* scratch, int iters, int blocks, int threads, cudaStream_t st);
@@ -1012,6 +1013,9 @@ struct lz_ctx {
     // order-m derivative plans (deriv.cu), built on first use
     std::map<int, lz::DevDeriv> dderiv;
     std::map<int, lz::HostTable> dtab;
+    // moment-form plans keyed by (order, taylor, point-set order)
+    std::map<std::tuple<int, int, int>, lz::DevDeriv> dderiv_g;
+    std::map<std::tuple<int, int, int>, lz::HostTable> dtab_g;
 };
 
 struct lz_plan {
@@ -1587,6 +1591,208 @@ const lz::DevDeriv& ensure_deriv(const lz_ctx* cc, int order) {
     return c->dderiv.emplace(order, P).first->second;
 }
 
+
+// Moment-form plan (deriv.cu deriv_moment_kernel) of order m (0..12, d <= 4).  taylor = 0: d^alpha Z
+// at arbitrary k over the order-m point sets; taylor = 1: d^alpha Z_reg at k = 0 over the point
+// sets of order set_order (L/epstein.py:376-377, the table of reg_derivatives(set_order)), the
+// q = 0 term from the rho-series of t0_reg (L/epstein.py:403-413) and bconst (m = 0) in `add`.
+const lz::DevDeriv& ensure_deriv_g(const lz_ctx* cc, int order, int taylor, int set_order) {
+    lz_ctx* c = const_cast<lz_ctx*>(cc);
+    std::lock_guard<std::mutex> lock(c->mu);
+    const auto key = std::make_tuple(order, taylor, set_order);
+    auto it = c->dderiv_g.find(key);
+    if (it != c->dderiv_g.end()) return it->second;
+    const lz::HostCtx& h = c->h;
+    const int d = h.d, m = order;
+    if (h.k.branch == lz::kTrivial) throw Error{LZ_EINVAL, "derivatives of a trivial-branch zeta are zero"};
+    std::vector<double> dir_n, rec_n;
+    lz::build_deriv_sets(h, set_order, &dir_n, &rec_n);
+    const std::vector<int> alphas = multi_indices(d, m);
+    const int na = int(alphas.size()) / d;
+    const int j0 = (m + 1) / 2, nf = m - j0 + 1;
+    if (nf > lz::kMaxFunc - 1) throw Error{LZ_EINVAL, "derivative order too high"};
+    const int rs = nf + d * (m + 1);
+    if (rs > 255) throw Error{LZ_EINVAL, "derivative record too large"};
+    // direct set: Cartesian z and 2 (2 pi)^m w_z (long double, rounded once)
+    const size_t nd = dir_n.size() / d;
+    std::vector<double> dz(nd * d), dw0(nd);
+    const ld twopi_m = std::pow(2.0L * ld(lz::kPi), ld(m));
+    for (size_t i = 0; i < nd; ++i) {
+        ld z[lz::kMaxDim];
+        const ld w = direct_weight(h, &dir_n[i * d], z);
+        for (int a = 0; a < d; ++a) dz[i * d + a] = double(z[a]);
+        dw0[i] = double(2.0L * twopi_m * w);
+    }
+    // reciprocal set sorted by |q|
+    const size_t nr = rec_n.size() / d;
+    std::vector<double> q(nr * d);
+    std::vector<ld> qn(nr);
+    for (size_t i = 0; i < nr; ++i) {
+        ld r2 = 0.0L;
+        for (int a = 0; a < d; ++a) {
+            ld v = 0.0L;
+            for (int b = 0; b < d; ++b) v += ld(h.B[a * d + b]) * rec_n[i * d + b];
+            q[i * d + a] = double(v);
+            r2 += v * v;
+        }
+        qn[i] = std::sqrt(r2);
+    }
+    std::vector<size_t> ord(nr);
+    for (size_t i = 0; i < nr; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return qn[a] < qn[b]; });
+    std::vector<double> rq(nr * d), rn(nr);
+    for (size_t i = 0; i < nr; ++i) {
+        for (int a = 0; a < d; ++a) rq[i * d + a] = q[ord[i] * d + a];
+        rn[i] = double(qn[ord[i]]);
+    }
+    // tables of F^{(p)} = (-1)^p c^{s+p} E_{1-s-p}, p = j0 .. m
+    double p[lz::kMaxFunc] = {}, sc[lz::kMaxFunc] = {};
+    const ld cl = ld(lz::kPi) / ld(h.k.split);
+    for (int j = 0; j < nf; ++j) {
+        const int jj = j0 + j;
+        p[j] = 1.0 - h.k.s - jj;
+        sc[j] = double(((jj & 1) ? -1.0L : 1.0L) * std::pow(cl, ld(h.k.s) + jj));
+    }
+    lz::HostTable& tab = c->dtab_g[key];
+    const double rp = std::fabs(h.k.rfac * h.k.pref);
+    if (nr > 0) lz::build_table(p, sc, nf, double(cl), lz::table_x_lo(h), rp, &tab, std::max(1.0, m / 2.0));
+    else tab.nfunc = nf;
+    // moments: one direct moment per alpha, then R[p][e], |e| = 2p - m
+    auto code = [&](int fslot, const int* e) {
+        unsigned long long v = (unsigned long long)fslot;
+        for (int a = 0; a < d; ++a) v |= (unsigned long long)(nf + a * (m + 1) + e[a]) << (8 * (a + 1));
+        return v;
+    };
+    std::vector<unsigned long long> mom;
+    for (int ia = 0; ia < na; ++ia) mom.push_back(code(0, &alphas[ia * d]));
+    std::map<std::vector<int>, int> rmap;  // (p, e) -> reciprocal moment index
+    int n_rmom = 0;
+    for (int pp = j0; pp <= m; ++pp) {
+        const std::vector<int> es = multi_indices(d, 2 * pp - m);
+        for (size_t i = 0; i < es.size() / d; ++i) {
+            std::vector<int> key2 = {pp};
+            key2.insert(key2.end(), es.begin() + i * d, es.begin() + (i + 1) * d);
+            rmap[key2] = n_rmom++;
+            mom.push_back(code(pp - j0, &es[i * d]));
+        }
+    }
+    auto fact = [](int n) {
+        double f = 1.0;
+        for (int i = 2; i <= n; ++i) f *= i;
+        return f;
+    };
+    std::vector<int> hoff(na + 1, 0), hmom;
+    std::vector<double> hcoef, add;
+    for (int ia = 0; ia < na; ++ia) {
+        const int* al = &alphas[ia * d];
+        int jv[lz::kMaxDim] = {0, 0, 0, 0};
+        for (;;) {
+            int js = 0;
+            double cf = 1.0;
+            std::vector<int> key2(1);
+            for (int a = 0; a < d; ++a) {
+                js += jv[a];
+                cf *= fact(al[a]) / (fact(jv[a]) * fact(al[a] - 2 * jv[a]));
+                key2.push_back(al[a] - 2 * jv[a]);
+            }
+            key2[0] = m - js;
+            hmom.push_back(rmap.at(key2));
+            hcoef.push_back(cf);
+            int a = 0;
+            while (a < d) {
+                if (++jv[a] <= al[a] / 2) break;
+                jv[a] = 0;
+                ++a;
+            }
+            if (a == d) break;
+        }
+        hoff[ia + 1] = int(hmom.size());
+    }
+    if (taylor) {
+        add.assign(na, 0.0);
+        for (int ia = 0; ia < na; ++ia) {
+            const int* al = &alphas[ia * d];
+            ld v = (m == 0) ? ld(h.k.bconst) : 0.0L;
+            bool even = true;
+            for (int a = 0; a < d; ++a) even = even && (al[a] % 2 == 0);
+            if (even) {
+                const int nn = m / 2;
+                ld mult = ld(fact(nn)), fac = 1.0L;
+                for (int a = 0; a < d; ++a) {
+                    mult /= ld(fact(al[a] / 2));
+                    fac *= ld(fact(al[a]));
+                }
+                v += ld(h.k.rfac) * lz::t0_coeff(h.k, nn) * mult * fac;
+            }
+            add[ia] = double(v);
+        }
+    }
+    lz::DevDeriv P;
+    std::memset(&P, 0, sizeof(P));
+    P.d = d;
+    P.order = m;
+    P.n_dir = int(nd);
+    P.n_rec = int(nr);
+    std::memcpy(P.A, h.A, sizeof(P.A));
+    std::memcpy(P.B, h.B, sizeof(P.B));
+    P.pref = h.k.pref;
+    P.rfac = h.k.rfac;
+    P.r_cut = nr > 0 ? double(std::sqrt(ld(tab.x_hi) / cl) * (1.0L + 1e-9L)) : 0.0;
+    P.n_alpha = na;
+    P.n_dmom = na;
+    P.n_rmom = n_rmom;
+    P.nf = nf;
+    P.rs = rs;
+    P.taylor = taylor;
+    {
+        DeviceGuard dg(c->device);
+        P.dir_n = upload(dir_n, &c->allocs);
+        P.dir_z = upload(dz, &c->allocs);
+        P.dir_w0 = upload(dw0, &c->allocs);
+        P.rec_q = upload(rq, &c->allocs);
+        P.rec_norm = upload(rn, &c->allocs);
+        P.tab.dir = upload(tab.dir, &c->allocs);
+        P.tab.coef = upload(tab.coef, &c->allocs);
+        P.mom = upload(mom, &c->allocs);
+        P.hoff = upload(hoff, &c->allocs);
+        P.hmom = upload(hmom, &c->allocs);
+        P.hcoef = upload(hcoef, &c->allocs);
+        if (taylor) P.add = upload(add, &c->allocs);
+        std::vector<double> ws(size_t(lz::kDerivWsPoints) * (na + n_rmom) * 2, 0.0);
+        P.ws = const_cast<double*>(upload(ws, &c->allocs));
+    }
+    P.tab.nbins = tab.nbins;
+    P.tab.nfunc = nf;
+    P.tab.npieces = tab.npieces;
+    P.tab.ncoef = int(tab.coef.size());
+    P.tab.x_lo = tab.x_lo;
+    P.tab.inv_hb = tab.inv_hb;
+    P.tab.x_hi = tab.x_hi;
+    P.tab.c = double(cl);
+    P.tab.r_scale = double(cl) * tab.inv_hb;
+    P.tab.x_off = tab.x_lo * tab.inv_hb;
+    P.tab.nbins_d = double(tab.nbins);
+    for (int j = 0; j < nf; ++j) {
+        P.tab.p[j] = p[j];
+        P.tab.scale[j] = sc[j];
+    }
+    return c->dderiv_g.emplace(key, P).first->second;
+}
+
+// compile-time kernel (orders 1..4, d <= 3) unless LATSUM_DERIV_MOMENTS=1; the moment form otherwise
+bool deriv_use_fixed(int d, int order) {
+    static const int force = [] {
+        const char* e = std::getenv("LATSUM_DERIV_MOMENTS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return !force && order >= 1 && order <= 4 && d <= 3;
+}
+
+cudaError_t launch_derivatives(const lz_ctx* c, int order, const double* k, int64_t n, double* out, int* status,
+                               cudaStream_t st) {
+    if (deriv_use_fixed(c->h.d, order)) return lz::launch_deriv(ensure_deriv(c, order), k, n, out, status, st);
+    return lz::launch_deriv_g(ensure_deriv_g(c, order, 0, order), k, n, out, status, st);
+}
 }  // namespace
 
 extern "C" {
@@ -1604,21 +1810,19 @@ int lz_zeta_derivatives(const lz_ctx* c, int order, const double* k, int64_t n, 
                         void* stream) {
     return guarded([&] {
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
-        if (order < 1 || order > 4 || c->h.d > 3) throw Error{LZ_EINVAL, "derivative order must be 1..4 (d <= 3)"};
-        const lz::DevDeriv& P = ensure_deriv(c, order);
+        if (order < 1 || order > 12) throw Error{LZ_EINVAL, "derivative order must be 1..12"};
         DeviceGuard dg(c->device);
-        check_cuda(lz::launch_deriv(P, k, n, out, status, (cudaStream_t)stream), "derivative kernel");
+        check_cuda(launch_derivatives(c, order, k, n, out, status, (cudaStream_t)stream), "derivative kernel");
     });
 }
 
 int lz_zeta_derivatives_host(const lz_ctx* c, int order, const double* k, int64_t n, double* out) {
     return guarded([&] {
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
-        if (order < 1 || order > 4 || c->h.d > 3) throw Error{LZ_EINVAL, "derivative order must be 1..4 (d <= 3)"};
+        if (order < 1 || order > 12) throw Error{LZ_EINVAL, "derivative order must be 1..12"};
         for (int64_t i = 0; i < n * c->h.d; ++i)
             if (!std::isfinite(k[i])) throw Error{LZ_ENONFINITE, "k contains non-finite entries"};
         if (n == 0) return;
-        const lz::DevDeriv& P = ensure_deriv(c, order);
         DeviceGuard dg(c->device);
         const int d = c->h.d, na = lz::deriv_count(d, order);
         Arena& A = arena(c->device);
@@ -1630,7 +1834,7 @@ int lz_zeta_derivatives_host(const lz_ctx* c, int order, const double* k, int64_
         int* dstat = reinterpret_cast<int*>(A.dbuf + al256(kb) + al256(ob));
         check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
         h2d(dk, k, kb, A.hbuf, A.st);
-        check_cuda(lz::launch_deriv(P, dk, n, dout, dstat, A.st), "derivative kernel");
+        check_cuda(launch_derivatives(c, order, dk, n, dout, dstat, A.st), "derivative kernel");
         copy_d2h(A.hbuf, dout, ob, A.st);
         int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
         copy_d2h(hstat, dstat, sizeof(int), A.st);
@@ -1923,6 +2127,46 @@ int lz_ctx_reg_derivatives(const lz_ctx* c, int order, int* alphas, double* vals
         *n = int64_t(v.size());
         const int64_t m = std::min<int64_t>(cap, *n);
         if (alphas && m > 0) std::memcpy(alphas, al.data(), sizeof(int) * size_t(m) * c->h.d);
+        if (vals && m > 0) std::memcpy(vals, v.data(), sizeof(double) * size_t(m));
+    });
+}
+
+// Device Taylor tables (deriv.cu moment kernel in Taylor mode): every even total order <= order,
+// one single-point launch per order over the order-`order` point sets (L/epstein.py:376-377).
+int lz_ctx_reg_derivatives_device(const lz_ctx* c, int order, int* alphas, double* vals, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        if (order < 0 || order % 2 || order > 12) throw Error{LZ_EINVAL, "derivative order must be even and <= 12"};
+        if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
+        const int d = c->h.d;
+        std::vector<int> al;
+        for (int total = 0; total <= order; total += 2) {
+            const std::vector<int> a = multi_indices(d, total);
+            al.insert(al.end(), a.begin(), a.end());
+        }
+        const int64_t na = int64_t(al.size()) / d;
+        std::vector<double> v(size_t(na), 0.0);
+        if (c->h.k.branch == lz::kTrivial) {
+            v[0] = c->h.k.const_value;  // total order 0 comes first
+        } else {
+            DeviceGuard dg(c->device);
+            Arena& A = arena(c->device);
+            std::lock_guard<std::mutex> lock(A.mu);
+            const size_t ob = sizeof(double) * size_t(na);
+            A.ensure(al256(ob) + 256, ob + 256);
+            double* dout = reinterpret_cast<double*>(A.dbuf);
+            int64_t off = 0;
+            for (int total = 0; total <= order; total += 2) {
+                const lz::DevDeriv& P = ensure_deriv_g(c, total, 1, order);
+                check_cuda(lz::launch_deriv_g(P, nullptr, 1, dout + off, nullptr, A.st), "taylor kernel");
+                off += P.n_alpha;
+            }
+            copy_d2h(A.hbuf, dout, ob, A.st);
+            check_cuda(cudaStreamSynchronize(A.st), "sync");
+            std::memcpy(v.data(), A.hbuf, ob);
+        }
+        *n = na;
+        const int64_t m = std::min<int64_t>(cap, na);
+        if (alphas && m > 0) std::memcpy(alphas, al.data(), sizeof(int) * size_t(m) * d);
         if (vals && m > 0) std::memcpy(vals, v.data(), sizeof(double) * size_t(m));
     });
 }

@@ -18,6 +18,7 @@
 // in global memory (read through L1): this path serves the derivative API, not the bench grid.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "lz_internal.h"
@@ -266,6 +267,270 @@ cudaError_t launch_deriv_t(const DevDeriv& P, const double* k, int64_t n, double
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Any order m <= 12, d <= 4: moment form.  With y = k + q,
+//   d^alpha sum_q F(|y|^2) = sum_{j <= alpha/2} c(alpha, j) R[m - |j|][alpha - 2j],
+//   R[p][e] = sum_q F^{(p)}(|y|^2) prod_a (2 y_a)^{e_a}          (|e| = 2p - m),
+//   direct:  Dm[alpha] = sum_z W_z trig_m(2 pi k.z) z^alpha      (W_z = 2 (2 pi)^m w_z),
+// so the q loop accumulates sum_p binom(2p - m + d - 1, d - 1) moments instead of every Hermite
+// term of every alpha (d = 4, m = 12: 1036 + 455 moments against ~5,000 terms).  Items (direct
+// points, then reciprocal points sorted by |q| up to r_cut + |k|, then q = 0 unsplit) run in
+// chunks of kDgCh: each thread evaluates one item -- its trig factor or table functions, and
+// the power ladders of z or 2y -- into shared memory, then every thread adds the chunk to its
+// moments with compensated (Neumaier) sums (the Hermite expansion cancels at high order, the
+// reason the reference combines it with fsum, L/epstein.py:383-386).  Chunks are dealt
+// round-robin to gridDim.x splits; one split combines in the kernel, several through the plan's
+// workspace (deriv_combine_kernel, fixed split order).
+constexpr int kDgCh = 128;
+constexpr int kDgDirPT = 4;   // direct moments per thread: <= 512 (455 at d = 4, m = 12)
+constexpr int kDgRecPT = 9;   // reciprocal moments per thread: <= 1152 (1036 at d = 4, m = 12)
+
+__device__ __forceinline__ void neu_add(double& s, double& c, double v) {
+    const double t = s + v;
+    c += fabs(s) >= fabs(v) ? (s - t) + v : (v - t) + s;
+    s = t;
+}
+
+// F^{(J0 + j)}, j < nf, at rho (runtime nf)
+__device__ __forceinline__ void fderiv_rt(const DevDeriv& P, double rho, double* f) {
+    switch (P.nf) {
+#define LZ_FCASE(N)                     \
+    case N: {                           \
+        double g[N];                    \
+        fderiv<N>(P, rho, g);           \
+        for (int j = 0; j < N; ++j) f[j] = g[j]; \
+        break;                          \
+    }
+        LZ_FCASE(1) LZ_FCASE(2) LZ_FCASE(3) LZ_FCASE(4) LZ_FCASE(5) LZ_FCASE(6) LZ_FCASE(7)
+#undef LZ_FCASE
+        default: break;
+    }
+}
+
+// One point's moments (hi, lo pairs in msm) -> the n_alpha outputs.
+__device__ __forceinline__ void combine_point(const DevDeriv& P, const double* msm, double* orow) {
+    for (int ia = threadIdx.x; ia < P.n_alpha; ia += blockDim.x) {
+        double s = 0.0, c = 0.0;
+        neu_add(s, c, msm[2 * ia]);
+        neu_add(s, c, msm[2 * ia + 1]);
+        for (int t = __ldg(P.hoff + ia); t < __ldg(P.hoff + ia + 1); ++t) {
+            const int mi = P.n_dmom + __ldg(P.hmom + t);
+            const double cf = P.rfac * __ldg(P.hcoef + t);
+            neu_add(s, c, cf * msm[2 * mi]);
+            neu_add(s, c, cf * msm[2 * mi + 1]);
+        }
+        if (P.add) neu_add(s, c, __ldg(P.add + ia));
+        orow[ia] = P.pref * (s + c);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void chunk_moments(const double* sm, int rs, int cnt, unsigned long long code, double& s,
+                                              double& c) {
+    const int of = int(code & 0xff);
+    int op[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) op[a] = int((code >> (8 * (a + 1))) & 0xff);
+#pragma unroll 2
+    for (int it = 0; it < cnt; ++it) {
+        const double* r = sm + it * rs;
+        double v = r[of];
+#pragma unroll
+        for (int a = 0; a < D; ++a) v *= r[op[a]];
+        neu_add(s, c, v);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kDgCh) deriv_moment_kernel(DevDeriv P, const double* __restrict__ kin, int64_t n,
+                                                             double* __restrict__ out, int* status) {
+    extern __shared__ __align__(16) double dsm[];
+    const int m = P.order, nf = P.nf, rs = P.rs, tid = threadIdx.x;
+    const int nsplit = gridDim.x, split = blockIdx.x;
+    const int n_mom = P.n_dmom + P.n_rmom;
+    double* msm = dsm + kDgCh * rs;  // [n_mom][2] (combine)
+    for (int64_t pt = blockIdx.y; pt < n; pt += gridDim.y) {
+        double k[D], kap[D];
+        if (P.taylor) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) k[a] = kap[a] = 0.0;
+        } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) k[a] = kin[pt * D + a];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {  // reduce into the cell (L/lattice.py:107-112)
+                double s = 0.0;
+#pragma unroll
+                for (int b = 0; b < D; ++b) s = fma(P.A[b * D + a], k[b], s);
+                kap[a] = s - floor(s + 0.5);
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                double s = 0.0;
+#pragma unroll
+                for (int b = 0; b < D; ++b) s = fma(P.B[a * D + b], kap[b], s);
+                k[a] = s;
+            }
+        }
+        double rho0 = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) rho0 = fma(k[a], k[a], rho0);
+        const double kmag = sqrt(rho0);
+        // reciprocal items with |q| <= r_cut + |k| (binary search, q sorted by |q|)
+        int lo = 0, hi = P.n_rec;
+        const double rmax = P.r_cut + kmag;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(P.rec_norm + mid) <= rmax) lo = mid + 1;
+            else hi = mid;
+        }
+        const int n_rq = lo, n_ritems = n_rq + (P.taylor ? 0 : 1);
+        const int nd_ch = (P.n_dir + kDgCh - 1) / kDgCh, nr_ch = (n_ritems + kDgCh - 1) / kDgCh;
+        double ds[kDgDirPT], dc[kDgDirPT], rsum[kDgRecPT], rc[kDgRecPT];
+#pragma unroll
+        for (int r = 0; r < kDgDirPT; ++r) ds[r] = dc[r] = 0.0;
+#pragma unroll
+        for (int r = 0; r < kDgRecPT; ++r) rsum[r] = rc[r] = 0.0;
+        const int trig_case = m & 3;
+        for (int ch = split; ch < nd_ch + nr_ch; ch += nsplit) {
+            const bool dir = ch < nd_ch;
+            const int base = (dir ? ch : ch - nd_ch) * kDgCh;
+            const int cnt = min(kDgCh, (dir ? P.n_dir : n_ritems) - base);
+            const int i = base + tid;
+            double* rec = dsm + tid * rs;
+            __syncthreads();  // the previous chunk is consumed
+            if (tid < cnt) {
+                double x[D];
+                double f0 = 0.0;
+                if (dir) {
+                    double ph = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        ph = fma(kap[a], __ldg(P.dir_n + size_t(i) * D + a), ph);
+                        x[a] = __ldg(P.dir_z + size_t(i) * D + a);
+                    }
+                    double sn, cs;
+                    sincos2pi_d(ph, sn, cs);
+                    const double tr = trig_case == 0 ? cs : trig_case == 1 ? -sn : trig_case == 2 ? -cs : sn;
+                    f0 = __ldg(P.dir_w0 + i) * tr;
+                    rec[0] = f0;
+                } else {
+                    double rho = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        const double y = k[a] + (i < n_rq ? __ldg(P.rec_q + size_t(i) * D + a) : 0.0);
+                        x[a] = 2.0 * y;
+                        rho = fma(y, y, rho);
+                    }
+                    double f[kMaxFunc];
+                    if (i < n_rq) {
+                        fderiv_rt(P, rho, f);
+                    } else if (rho0 < 1e-28) {  // q = 0 at k in the reciprocal lattice: pole
+                        if (status && split == 0) atomicOr(status, 1);
+                        for (int j = 0; j < nf; ++j) f[j] = 0.0;
+                    } else {  // q = 0, unsplit F^{(p)} (carries the singular part)
+                        const double x0 = rho * P.tab.c;
+                        for (int j = 0; j < nf; ++j) f[j] = P.tab.scale[j] * expint<double>(P.tab.p[j], x0);
+                    }
+                    for (int j = 0; j < nf; ++j) rec[j] = f[j];
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a) {  // power ladder x_a^e, e = 0..m
+                    double pw = 1.0;
+                    double* pr = rec + nf + a * (m + 1);
+                    for (int e = 0; e <= m; ++e) {
+                        pr[e] = pw;
+                        pw *= x[a];
+                    }
+                }
+            }
+            __syncthreads();
+            if (dir) {
+#pragma unroll
+                for (int r = 0; r < kDgDirPT; ++r) {
+                    const int mi = tid + r * kDgCh;
+                    if (mi < P.n_dmom) chunk_moments<D>(dsm, rs, cnt, __ldg(P.mom + mi), ds[r], dc[r]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < kDgRecPT; ++r) {
+                    const int mi = tid + r * kDgCh;
+                    if (mi < P.n_rmom) chunk_moments<D>(dsm, rs, cnt, __ldg(P.mom + P.n_dmom + mi), rsum[r], rc[r]);
+                }
+            }
+        }
+        // partial moments -> shared (one split: combine here) or the plan's workspace
+        double* dst = nsplit == 1 ? msm : P.ws + (size_t(pt) * nsplit + split) * n_mom * 2;
+#pragma unroll
+        for (int r = 0; r < kDgDirPT; ++r) {
+            const int mi = tid + r * kDgCh;
+            if (mi < P.n_dmom) {
+                dst[2 * mi] = ds[r];
+                dst[2 * mi + 1] = dc[r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kDgRecPT; ++r) {
+            const int mi = tid + r * kDgCh;
+            if (mi < P.n_rmom) {
+                dst[2 * (P.n_dmom + mi)] = rsum[r];
+                dst[2 * (P.n_dmom + mi) + 1] = rc[r];
+            }
+        }
+        if (nsplit == 1) {
+            __syncthreads();
+            combine_point(P, msm, out + pt * P.n_alpha);
+            __syncthreads();
+        }
+    }
+}
+
+// Several splits per point (small batches): fixed-order sum over the splits, then the combine.
+__global__ void __launch_bounds__(kDgCh) deriv_combine_kernel(DevDeriv P, int64_t n, int nsplit, double* __restrict__ out) {
+    extern __shared__ __align__(16) double msm[];
+    const int n_mom = P.n_dmom + P.n_rmom;
+    for (int64_t pt = blockIdx.x; pt < n; pt += gridDim.x) {
+        for (int mi = threadIdx.x; mi < n_mom; mi += blockDim.x) {
+            double s = 0.0, c = 0.0;
+            for (int sp = 0; sp < nsplit; ++sp) {
+                const double* w = P.ws + ((size_t(pt) * nsplit + sp) * n_mom + mi) * 2;
+                neu_add(s, c, w[0]);
+                neu_add(s, c, w[1]);
+            }
+            msm[2 * mi] = s;
+            msm[2 * mi + 1] = c;
+        }
+        __syncthreads();
+        combine_point(P, msm, out + pt * P.n_alpha);
+        __syncthreads();
+    }
+}
+
+template <int D>
+cudaError_t launch_deriv_g_t(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int n_mom = P.n_dmom + P.n_rmom;
+    const size_t smem = sizeof(double) * (size_t(kDgCh) * P.rs + 2 * size_t(n_mom));
+    cudaError_t e = cudaFuncSetAttribute(deriv_moment_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    // splits: enough CTAs for two waves when the batch is small, never more than the chunks
+    const int64_t chunks = (P.n_dir + kDgCh - 1) / kDgCh + (P.n_rec + 1 + kDgCh - 1) / kDgCh;
+    int64_t nsplit = 1;
+    if (n < 2 * sms) nsplit = std::min<int64_t>(std::max<int64_t>(1, (2 * sms) / n), chunks);
+    if (nsplit > 1 && (!P.ws || n * nsplit > kDerivWsPoints)) nsplit = 1;
+    const int64_t gy = std::min<int64_t>(n, 65535);
+    deriv_moment_kernel<D><<<dim3(unsigned(nsplit), unsigned(gy)), kDgCh, smem, st>>>(P, k, n, out, status);
+    e = cudaGetLastError();
+    if (e != cudaSuccess || nsplit == 1) return e;
+    const size_t smem2 = sizeof(double) * 2 * size_t(n_mom);
+    e = cudaFuncSetAttribute(deriv_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+    if (e != cudaSuccess) return e;
+    deriv_combine_kernel<<<unsigned(std::min<int64_t>(n, 65535)), kDgCh, smem2, st>>>(P, n, int(nsplit), out);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int deriv_count(int d, int order) {  // binom(order + d - 1, d - 1)
@@ -285,6 +550,17 @@ cudaError_t launch_deriv(const DevDeriv& P, const double* k, int64_t n, double* 
     LZ_DCASE(3, 1) LZ_DCASE(3, 2) LZ_DCASE(3, 3) LZ_DCASE(3, 4)
 #undef LZ_DCASE
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_deriv_g(const DevDeriv& P, const double* k, int64_t n, double* out, int* status, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    switch (P.d) {
+        case 1: return launch_deriv_g_t<1>(P, k, n, out, status, st);
+        case 2: return launch_deriv_g_t<2>(P, k, n, out, status, st);
+        case 3: return launch_deriv_g_t<3>(P, k, n, out, status, st);
+        case 4: return launch_deriv_g_t<4>(P, k, n, out, status, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace lz

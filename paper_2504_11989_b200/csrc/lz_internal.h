@@ -40,6 +40,7 @@ __host__ __device__
 constexpr int piece_stride_lo(int nf) { return nf * kDegLo + ((nf + 1) & ~1); }
 constexpr int kDirectMarker = 15;   // directory L value meaning "evaluate E_p directly"
 constexpr int kT0 = 64;             // max terms of the q = 0 power series
+constexpr int kMaxFunc = 8;         // functions per table (order-12 derivatives need 7)
 
 // ---------------------------------------------------------------------------
 // Per-(lattice, nu) constants of the Crandall split (L/epstein.py:99-122, 202-259).
@@ -61,7 +62,7 @@ struct CtxConst {
     double const_value;  // trivial branch value
 };
 
-// Piecewise-polynomial table of up to 4 functions f_j(x) = scale_j E_{p_j}(x),
+// Piecewise-polynomial table of up to kMaxFunc functions f_j(x) = scale_j E_{p_j}(x),
 // sharing one directory over x in [x_lo, x_hi).
 struct DevTable {
     const int* dir;        // nbins entries: (first coefficient offset << 5) | lo << 4 | L ; L == 15 -> direct
@@ -75,7 +76,7 @@ struct DevTable {
     double r_lo;               // |k+q| >= r_lo: low-degree bin; |k+q| < r_lo: high degree (0: no lo)
     int has_marker;            // 1 if some bin is evaluated directly (E_p; checked lookup path)
     int branchfree;            // opt-in (LATSUM_BRANCHFREE=1): select instead of the far branch
-    double p[4], scale[4]; // for the direct fallback
+    double p[kMaxFunc], scale[kMaxFunc];  // for the direct fallback
 };
 
 // A device-resident evaluation plan: union point sets of one lattice plus the
@@ -134,18 +135,34 @@ struct DevPlan {
     double line_sign;
 };
 
-// Derivative plan (deriv.cu): one context, derivatives of total order `order` (1..4) at arbitrary
-// k.  Plain global-memory arrays (read through L1).
+// Derivative plan (deriv.cu): one context, derivatives of total order `order` (0..12) at
+// arbitrary k (or, in Taylor mode, of Z_reg at k = 0).  Plain global-memory arrays (read
+// through L1).
 struct DevDeriv {
     int d, order, n_dir, n_rec;
     double A[16], B[16];
     const double* dir_n;     // [n_dir][d] integer coordinates (half lattice)
-    const double* dir_w;     // [n_dir][n_alpha] 2 (2 pi)^m w z^alpha
+    const double* dir_w;     // [n_dir][n_alpha] 2 (2 pi)^m w z^alpha (compile-time kernel)
     const double* rec_q;     // [n_rec][d] sorted by |q|
     const double* rec_norm;  // [n_rec]
     double r_cut, pref, rfac;
     DevTable tab;            // F^{(j)}, j = ceil(m/2) .. m
+    // moment form (deriv.cu deriv_moment_kernel; any order <= 12, d <= 4)
+    const double* dir_z;     // [n_dir][d] Cartesian z
+    const double* dir_w0;    // [n_dir] 2 (2 pi)^m w_z
+    const unsigned long long* mom;  // packed offsets into an item record: byte 0 = function
+                                    // slot, byte 1 + a = power-ladder slot of axis a
+    int n_alpha, n_dmom, n_rmom, nf;  // moments: n_dmom direct (one per alpha), then n_rmom reciprocal
+    int rs;                  // doubles per item record: nf function slots + d (order + 1) powers
+    int taylor;              // 1: Z_reg at k = 0 (no q = 0 item; `add` carries bconst and the
+                             // q = 0 series term), 0: d^alpha Z at the given k (q = 0 unsplit)
+    const int* hoff;         // [n_alpha + 1] Hermite terms of each alpha ...
+    const int* hmom;         // ... their reciprocal moment index ...
+    const double* hcoef;     // ... and coefficient prod_a alpha_a! / (j_a! (alpha_a - 2 j_a)!)
+    const double* add;       // [n_alpha] added inside the pref bracket (Taylor mode), or null
+    double* ws;              // split partial moments [kDerivWsPoints][n_dmom + n_rmom][2]
 };
+constexpr int kDerivWsPoints = 296;  // (point, split) pairs of one split launch (2 x 148 SMs)
 
 // Fixed Duffy grid description (device arrays + patch decomposition).
 struct DevGrid {
@@ -182,7 +199,7 @@ struct HostTable {
     std::vector<double> coef;
     int nbins = 0, nfunc = 0, npieces = 0;
     double x_lo = 0, inv_hb = 0, x_hi = 0;
-    double p[4] = {0, 0, 0, 0}, scale[4] = {0, 0, 0, 0};
+    double p[kMaxFunc] = {}, scale[kMaxFunc] = {};
     double max_rel_err = 0;   // measured during the build (degree-kDeg pieces)
     int n_lo_bins = 0;        // bins with degree-kDegLo pieces
     int lo_start = 0;         // first low-degree bin (low-degree bins form the suffix)

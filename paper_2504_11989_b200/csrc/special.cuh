@@ -117,6 +117,7 @@ template <class T> LZ_HDI T expint_series_frac(T p, T x) {
 
 // E_p(x) for x > 0 and real p.  Branch structure:
 //   p integer <= 0 : E_0 = e^{-x}/x and the stable recurrence E_{p} = (e^{-x} - p E_{p+1}) / x
+//   p < 0 otherwise : E_{p + N} in (0, 1) and the same recurrence
 //   x > 1           : continued fraction
 //   p integer >= 1  : integer series
 //   p near integer  : continued fraction (the series cancels catastrophically;
@@ -134,6 +135,18 @@ template <class T> LZ_HDI T expint(T p, T x) {
             // E_{q-1} = (e^{-x} - (q-1) E_q) / x
             e = (emx - T(q - 1) * e) / x;
         }
+        return e;
+    }
+    if (p < T(0)) {
+        // non-integer p < 0: E_{p0}, p0 = p + N in (0, 1), then the same stable recurrence
+        // E_{q-1} = (e^{-x} + (1 - q) E_q) / x (all terms positive for q < 1).  The continued
+        // fraction alone loses up to 1e-5 relative near x = 1 at p = -11.
+        const int n = int(floor(-p)) + 1;
+        const T p0 = p + T(n);
+        T e = expint(p0, x);
+        const T emx = exp(-x);
+        T q = p0;
+        for (int i = 0; i < n; ++i, q -= T(1)) e = (emx + (T(1) - q) * e) / x;
         return e;
     }
     if (x > T(1)) return expint_cf(p, x, 100000);

@@ -303,16 +303,41 @@ def near_d(ref, threads):
     return out
 
 
+# the 4-dimensional test lattice of tests/test_gpu_zeta.py (L/lattice.py:20 allows d <= 4)
+LAT4 = [[1.0, 0.2, 0.0, 0.1], [0.0, 1.1, 0.3, 0.0], [0.0, 0.0, 0.9, 0.2], [0.1, 0.0, 0.0, 1.0]]
+
+
+def taylor_high(ref):
+    """Taylor tables of Z_reg at k = 0 up to the reference's maximum order 12 (L/epstein.py:347-353),
+    d = 2, 3 and 4, every branch (generic, log case)."""
+    E = sys.modules["latsum_ref.epstein"]
+    out = {"taylor": []}
+    cases = [("square", 3.5, 12), ("hexagonal", 4.0, 12), ("fcc", 3.0, 8), ("bcc", 5.0, 8),
+             ("fcc", 6.0, 12), ("lat4", 6.0, 6), ("lat4", 3.0, 4)]
+    for name, nu, order in cases:
+        lat = ref.Lattice(np.array(LAT4)) if name == "lat4" else ref.named_lattice(name)
+        t0 = time.time()
+        tab = E.reg_zeta_derivatives(lat, nu, order)
+        out["taylor"].append({"lattice": name, "nu": nu, "order": order, "seconds": time.time() - t0,
+                              "derivs": [[list(a), float(v)] for a, v in sorted(tab.derivs.items())]})
+        print(name, nu, order, "%.1f s" % (time.time() - t0), flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
     ap.add_argument("--near-d", action="store_true")
+    ap.add_argument("--taylor", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     ref = load_reference()
     if args.slow:
         res = slow(ref, args.threads)
         path = os.path.join(HERE, "golden_integrals.json")
+    elif args.taylor:
+        res = taylor_high(ref)
+        path = os.path.join(HERE, "golden_taylor.json")
     elif args.near_d:
         res = near_d(ref, args.threads)
         path = os.path.join(HERE, "golden_near_d.json")

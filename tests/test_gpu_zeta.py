@@ -233,3 +233,77 @@ def test_derivative_laplacian_identity_and_poly_weights():
     assert np.abs(M01.real - M[:, 0, 1]).max() <= 1e-11 * max(1.0, np.abs(M).max())
     with pytest.raises(PoleError):
         EpsteinContext(fcc, 5.0, device=0).derivatives(np.zeros(3), 2)
+
+
+# --------------------------------------------------------------------------------------------
+# Any order <= 12, any d <= 4: the moment form of the derivative kernel (deriv.cu)
+
+LAT4 = [[1.0, 0.2, 0.0, 0.1], [0.0, 1.1, 0.3, 0.0], [0.0, 0.0, 0.9, 0.2], [0.1, 0.0, 0.0, 1.0]]
+
+
+def _lat(name):
+    from paper_2504_11989_b200 import Lattice
+    return Lattice(np.array(LAT4)) if name == "lat4" else named_lattice(name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nu,order,npts", [
+    ("square", 3.5, 5, 32), ("square", 3.5, 8, 32), ("square", 4.0, 12, 24), ("hexagonal", 4.5, 10, 24),
+    ("integer_1d", 2.5, 12, 32), ("fcc", 5.0, 6, 16), ("fcc", 3.0, 8, 12), ("bcc", 6.5, 12, 8),
+    ("lat4", 6.0, 1, 16), ("lat4", 5.0, 2, 16), ("lat4", 6.5, 4, 12), ("lat4", 7.0, 6, 6)])
+def test_high_order_derivatives_vs_oracle(name, nu, order, npts):
+    """d^alpha Z(k) for orders 5..12 and d = 4 (the reference's limits, L/epstein.py:347-353 and
+    L/lattice.py:20) at random k in the cell vs the long-double oracle.
+
+    High-order Ewald derivatives cancel: the direct and reciprocal terms grow like
+    (2 pi m / e)^{m/2} while the value does not, so no double-precision evaluation (the reference's
+    fsum tables included) gets below eps x sum|terms|.  The bound is therefore 1e-12 of the point's
+    largest derivative plus 16 eps of the oracle's sum of |terms| for that value."""
+    lat = _lat(name)
+    d = lat.d
+    kap = np.random.default_rng(order * 11 + d).uniform(-0.45, 0.45, size=(npts, d))
+    k = kap @ lat.a_inv_t.T
+    alphas, D = EpsteinContext(lat, nu, device=0).derivatives(k, order)
+    assert alphas == O.multi_indices(d, order)
+    Do, Sabs = O.derivatives(lat.a, nu, order, k, with_abs=True)
+    scale = np.maximum(np.abs(Do).max(axis=1, keepdims=True), 1.0)
+    bound = ZETA_TOL * scale + 16 * np.finfo(float).eps * Sabs
+    assert (np.abs(D - Do) <= bound).all(), (np.abs(D - Do) / bound).max()
+
+
+@pytest.mark.gpu
+def test_high_order_laplacian_identity():
+    """sum_a d_a^2 d^beta Z_5 = -4 pi^2 d^beta Z_3 for every |beta| = 6 (order 8 of nu = 5 against
+    order 6 of nu = 3): ties the high orders together without the oracle."""
+    fcc = named_lattice("fcc")
+    k = np.random.default_rng(9).uniform(-0.4, 0.4, size=(24, 3)) @ fcc.a_inv_t.T
+    al8, D8 = EpsteinContext(fcc, 5.0, device=0).derivatives(k, 8)
+    al6, D6 = EpsteinContext(fcc, 3.0, device=0).derivatives(k, 6)
+    scale = max(1.0, np.abs(D8).max())
+    for j, beta in enumerate(al6):
+        lap = sum(D8[:, al8.index(tuple(beta[i] + 2 * (i == a) for i in range(3)))] for a in range(3))
+        assert np.abs(lap + 4.0 * math.pi ** 2 * D6[:, j]).max() <= 1e-12 * scale, beta
+
+
+@pytest.mark.gpu
+def test_device_taylor_tables_vs_reference_and_host(golden):
+    """EpsteinContext.reg_derivatives builds the k = 0 tables on the device (moment kernel in Taylor
+    mode): vs the reference's fsum tables (orders up to 12, d up to 4) at 1e-10 of each order's
+    scale, and vs the host long-double restatement."""
+    import json
+    import os
+    from test_host import taylor_scales
+    from paper_2504_11989_b200.taylor import build_reg_derivatives_host
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_taylor.json")) as f:
+        cases = list(golden["taylor"]) + json.load(f)["taylor"]
+    for t in cases:
+        ctx = EpsteinContext(_lat(t["lattice"]), t["nu"], device=0)
+        tab = ctx.reg_derivatives(t["order"])
+        host = build_reg_derivatives_host(ctx, t["order"])
+        sc = taylor_scales(t["derivs"])
+        assert len(tab.derivs) == len(t["derivs"])
+        for alpha, ref in t["derivs"]:
+            got = tab.derivs[tuple(alpha)]
+            s = sc[sum(alpha)]
+            assert abs(got - ref) <= 1e-10 * s, (t["lattice"], t["nu"], alpha, got, ref)
+            assert abs(got - host.derivs[tuple(alpha)]) <= 1e-12 * s, (t["lattice"], t["nu"], alpha)
