@@ -120,6 +120,11 @@ struct HostPlan {
     double e2[4] = {0, 0, 0, 0}, e3[4] = {0, 0, 0, 0};
     int n_t0 = 0;
     double t0_rho_max = -1.0;
+    // line kernel: the Hessian's q = 0 rows (t0_reg', t0_reg'') as degree-kDeg pieces on bins of
+    // kBinWidth in x = c rho over [0, c t0_rho_max] (piece_stride(2) doubles per bin)
+    std::vector<double> q0tab;
+    int q0_nb = 0;
+    double q0_inv_h = 0.0;
     std::vector<int> run_info;   // maximal runs of consecutive n_d (plan info only)
     // line-factorised direct block (trace-Z ATM plans, d = 3; see build_line_block)
     std::vector<unsigned char> line;
@@ -794,6 +799,39 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         }
         hp->n_t0 = std::min(need, lz::kT0);
         hp->t0_rho_max = ok ? double(rho_max) : -1.0;
+        // the Hessian rows as pieces (line kernel): series evaluated in long double at the
+        // Chebyshev nodes of each bin; kept only if every piece meets 1e-15 of the row's scale
+        hp->q0tab.clear();
+        hp->q0_nb = 0;
+        if (hess && ok) {
+            const int nb = int(std::ceil(double(c_l * rho_max / ld(lz::kBinWidth)) - 1e-12));
+            const int ps = lz::piece_stride(2);
+            std::vector<double> tab(size_t(nb) * ps, 0.0);
+            bool fit_ok = nb > 0;
+            for (int row = 0; row < 2 && fit_ok; ++row) {
+                const double* cf = &hp->t0c[size_t(hp->nctx + row) * lz::kT0];
+                auto g = [&](ld x) {
+                    const ld r = x / c_l;
+                    ld acc = 0.0L;
+                    for (int n = lz::kT0 - 1; n >= 0; --n) acc = acc * r + ld(cf[n]);
+                    return acc;
+                };
+                ld scale = 0.0L;
+                for (int i = 0; i <= 64 * nb; ++i) scale = std::max(scale, std::fabs(g(ld(lz::kBinWidth) * nb * i / (64.0L * nb))));
+                for (int b = 0; b < nb; ++b) {
+                    double pc[lz::kNC];
+                    const double err = lz::fit_piece_fn(g, ld(lz::kBinWidth) * b, ld(lz::kBinWidth) * (b + 1), pc);
+                    if (err > 1e-15 * double(scale)) fit_ok = false;
+                    for (int m = 0; m < 8; ++m) tab[size_t(b) * ps + row * 8 + m] = pc[m];
+                    tab[size_t(b) * ps + 16 + row] = pc[8];
+                }
+            }
+            if (fit_ok) {
+                hp->q0tab.swap(tab);
+                hp->q0_nb = nb;
+                hp->q0_inv_h = double(c_l / ld(lz::kBinWidth));
+            }
+        }
     }
     lap("q=0 series");
     if (!table_job.valid()) {
@@ -881,6 +919,14 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.n_direct = int(hp.direct.size());
     P.t0_host = hp.t0c.data();
     P.rq_host = hp.rq_pad.data();
+    P.q0_host = hp.q0tab.data();
+    P.q0_nb = hp.q0_nb;
+    P.q0_inv_h = hp.q0_inv_h;
+    if (hp.hess) {
+        const lz::CtxConst& k = hp.hctx;
+        P.h_kk = k.sing_coef * k.inv_vol / (k.pref * k.rfac);
+        P.h_cm = -4.0 * k.pref * k.rfac / (4.0 * lz::kPi * lz::kPi);
+    }
     P.line_bytes = unsigned(hp.line.size());
     P.line_sign = hp.line_sign;
     for (int a = 0; a < 3; ++a) {
@@ -1120,14 +1166,16 @@ struct Scratch {
 std::mutex g_scratch_mu;
 std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
 
-void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, unsigned int** tcount) {
+void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, unsigned int** tcount,
+                  unsigned int** work) {
     auto& pool = g_scratch;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     Scratch& s = pool[std::make_pair(device, st)];
     if (s.cap < n_tiles) {
         if (s.wpart) check_cuda(cudaFreeAsync(s.wpart, st), "cudaFreeAsync");
         const size_t wbytes = size_t(n_tiles) * 8 * 2 * sizeof(double);
-        const size_t cbytes = size_t(n_tiles) * sizeof(unsigned int);
+        // tile counters, then the line kernel's two work-queue counters
+        const size_t cbytes = (size_t(n_tiles) + 2) * sizeof(unsigned int);
         void* p = nullptr;
         check_cuda(cudaMallocAsync(&p, wbytes + cbytes, st), "cudaMallocAsync");
         s.wpart = static_cast<double*>(p);
@@ -1137,6 +1185,7 @@ void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, 
     }
     *wpart = s.wpart;
     *tcount = s.tcount;
+    *work = s.tcount + s.cap;
 }
 
 // Lanes per point for the batch kernel: the smallest power of two that gives ~192 lanes per SM
@@ -1949,7 +1998,7 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
             full.tile_lo = full.tile_hi = 0;
             lz::DevGrid tmp;
             fill_grid(pl->d, &full, &tmp);
-            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, &dgd.wpart, &dgd.tcount);
+            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, &dgd.wpart, &dgd.tcount, &dgd.work);
         }
         if (pl->kind == 0)
             check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");

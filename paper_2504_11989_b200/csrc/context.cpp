@@ -479,6 +479,31 @@ ld eval_piece_lo(const double* c, ld tau) { return estrin_lo(c, tau_powers(doubl
 
 }  // namespace
 
+double fit_piece_fn(const std::function<long double(long double)>& f, long double x0, long double x1, double* out) {
+    const ChebConsts<kNC>& C = cheb<kNC>();
+    ld fv[kNC];
+    const ld mid = 0.5L * (x0 + x1), half = 0.5L * (x1 - x0);
+    for (int i = 0; i < kNC; ++i) fv[i] = f(mid + half * C.tau[i]);
+    ld ak[kNC];
+    for (int k = 0; k < kNC; ++k) {
+        ld s = 0.0L;
+        for (int i = 0; i < kNC; ++i) s += fv[i] * C.cosm[k][i];
+        ak[k] = (k == 0 ? 1.0L : 2.0L) * s / kNC;
+    }
+    for (int j = 0; j < kNC; ++j) {
+        ld c = 0.0L;
+        for (int k = 0; k < kNC; ++k) c += ak[k] * C.tk[k][j];
+        out[j] = double(std::ldexp(c, j));
+    }
+    // worst absolute error at 21 points, evaluated in the device's order
+    double worst = 0.0;
+    for (int i = 0; i <= 20; ++i) {
+        const ld tau = -1.0L + 2.0L * i / 20.0L;
+        worst = std::max(worst, double(std::fabs(eval_piece(out, tau) - f(mid + half * tau))));
+    }
+    return worst;
+}
+
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
                  double rfac_pref, HostTable* out, double poly_pow) {
     // weight of a term relative to the unit scale: (1 + 4x)^poly_pow covers the |y|^2 (Hessian)

@@ -65,6 +65,7 @@ struct View {
     uint32_t s_line;       // line-factorised direct block (0: none)
     uint32_t s_end;        // first byte after the staged image (per-warp scratch follows)
     uint32_t s_cnt;        // line kernel: count table cnt[i] = #{q : |q| <= i h} (kCntEntries int32)
+    uint32_t s_q0;         // line kernel: the Hessian's q = 0 pieces (kQ0Max x piece_stride(2) doubles)
     double cnt_inv_h;      // 1 / h
     // line kernel: warp-uniform reads from the kernel's parameter space (LineParam): the
     // reciprocal vectors (padded stride) and the Hessian's two q = 0 series rows
@@ -320,6 +321,46 @@ __device__ __forceinline__ double cos2pi(double x) {
     return __hiloint2double(__double2hiint(q) ^ (__double2loint(t) << 31), __double2loint(q));
 }
 
+// 1/d for d > 0 normal: the FP64 reciprocal seed (MUFU.RCP64H) and two Newton steps (~1 ulp).
+__device__ __forceinline__ double fast_rcp(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// log(x) for x > 0 normal (a few ulp): x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(s), s = (m - 1) / (m + 1), |s| <= 0.1716: 2 s sum s^{2k} / (2k + 1), k <= 11,
+// coefficients from the constant bank.  About 30 instructions (the library log takes ~80 with
+// its special-case handling, which the q = 0 term never needs).
+__constant__ double kLogS[12] = {2.0, 2.0 / 3, 2.0 / 5, 2.0 / 7, 2.0 / 9, 2.0 / 11, 2.0 / 13, 2.0 / 15,
+                                 2.0 / 17, 2.0 / 19, 2.0 / 21, 2.0 / 23};
+__device__ __forceinline__ double fast_log(double x) {
+    constexpr double kLn2Hi = 6.93147180369123816490e-01, kLn2Lo = 1.90821492927058770002e-10;
+    int hi = __double2hiint(x);
+    int e = (hi >> 20) - 1023;
+    hi = (hi & 0x000fffff) | 0x3ff00000;
+    if (hi > 0x3ff6a09e) {  // m > sqrt(2): halve
+        hi -= 0x00100000;
+        e += 1;
+    }
+    const double m = __hiloint2double(hi, __double2loint(x));
+    const double f = m - 1.0;        // exact
+    const double u = 2.0 + f;        // m + 1, with its rounding error du (Fast2Sum)
+    const double du = f - (u - 2.0);
+    const double r = fast_rcp(u);
+    const double s0 = f * r;
+    const double s = fma(r, fma(-s0, du, fma(-s0, u, f)), s0);  // f / (u + du) to ~1 ulp
+    const double s2 = s * s;
+    double p = kLogS[11];
+#pragma unroll
+    for (int i = 10; i >= 0; --i) p = fma(p, s2, kLogS[i]);
+    const double ed = double(e);
+    return fma(ed, kLn2Hi, fma(ed, kLn2Lo, s * p));
+}
+
 // Out-of-line E_p for the rare direct paths, so the hot loop stays small.
 __device__ __noinline__ double expint_dev(double p, double x) { return expint<double>(p, x); }
 
@@ -328,6 +369,11 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 // floor(y) for 0 <= y < 2^31 without FP64<->int conversions: y - 1/2 + 1.5*2^52 rounds to the
 // integer in the low word.  At exact integers the tie may yield y - 1 with fractional part 1,
 // i.e. tau = +1 at the end of the previous piece -- equally valid.
+// Ticket order of the line kernel's work queue (A/B: -DLZ_LINE_ORDER=0 plain, 1 radial index
+// descending, 2 ascending)
+#ifndef LZ_LINE_ORDER
+#define LZ_LINE_ORDER 1
+#endif
 constexpr double kMagic = 6755399441055744.0;
 
 // Piece lookup shared by both variants: bin b = floor(xb) from the directory, sub-piece
@@ -747,7 +793,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         // line warp: |k|^2 is convex along the line, so its maximum is at an end lane (padding
         // lanes repeat the last node); n_eff / n_in from the count table, rounded outwards /
         // inwards (r_cut and r_in carry 1e-9 relative margins against rounding)
-        kmag = sqrt(fmax(__shfl_sync(0xffffffffu, kmag, 0), __shfl_sync(0xffffffffu, kmag, 31)));
+        // an upper bound is enough (a larger kmag only widens the culling): single-precision
+        // square root of the upward-rounded square, widened by one part in 1e6
+        {
+            const double k2 = fmax(__shfl_sync(0xffffffffu, kmag, 0), __shfl_sync(0xffffffffu, kmag, 31));
+            kmag = double(__fsqrt_ru(__double2float_ru(k2))) * (1.0 + 1e-6);
+        }
         constexpr double kM = 6755399441055744.0;
         const double xe = fma(P.r_cut + kmag, V.cnt_inv_h, 0.5) + kM;  // floor + 1
         const double xi = fma(P.r_in - kmag, V.cnt_inv_h, -0.5) + kM;  // floor (or one less)
@@ -942,9 +993,13 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             fp = ALIAS ? P.alias_ratio * f0[0] : f0[NCTX];
             fpp = f0[Acc::FPP];
         } else if (q0_series && rho > 0.0) {
-            const double kk = C.sing_coef * C.inv_vol / (C.pref * C.rfac);
+            const double kk = XDIR ? P.h_kk : C.sing_coef * C.inv_vol / (C.pref * C.rfac);
             double s1, s2;
-            if (C.branch == kLogCase) {
+            if (XDIR && C.branch == kLogCase && C.log_m == 1) {
+                // nu = d + 2 (the ATM Z_5): s1 = kk (log(pi rho) + 1), s2 = kk / rho
+                s1 = kk * (fast_log(kPi * rho) + 1.0);
+                s2 = kk * fast_rcp(rho);
+            } else if (C.branch == kLogCase) {
                 const int m = C.log_m;
                 double rm1 = 1.0;  // rho^{m-1}
                 if (m == 0) rm1 = 1.0 / rho;
@@ -958,8 +1013,26 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
             }
             double r1, r2;
-            if constexpr (XDIR) series2<false>(V.p_t0, V.p_t0 + kT0, P.n_t0, rho, r1, r2);
-            else series2<SMEM>(V.t0c + NCTX * kT0, V.t0c + (NCTX + 1) * kT0, P.n_t0, rho, r1, r2);
+            if constexpr (XDIR) {
+                // line kernel: t0_reg', t0_reg'' from the per-CTA pieces (degree kDeg on bins of
+                // kBinWidth in x = c rho) instead of the power series
+                const double xq = rho * P.q0_inv_h;
+                const double tb = (xq - 0.5) + kMagic;
+                const int b = min(__double2loint(tb), P.q0_nb - 1);
+                const TauPowers tp = tau_powers((xq - double(b)) - 0.5);
+                constexpr int PS = piece_stride(2);
+                const uint32_t a0 = V.s_q0 + uint32_t(b) * uint32_t(PS * 8);
+                double2 c[PS / 2];
+#pragma unroll
+                for (int m = 0; m < PS / 2; ++m) c[m] = lds_f64x2(a0 + 16u * m);
+                const double* cd = reinterpret_cast<const double*>(c);
+                const double c0[9] = {cd[0], cd[1], cd[2], cd[3], cd[4], cd[5], cd[6], cd[7], cd[16]};
+                const double c1[9] = {cd[8], cd[9], cd[10], cd[11], cd[12], cd[13], cd[14], cd[15], cd[17]};
+                r1 = estrin(c0, tp);
+                r2 = estrin(c1, tp);
+            } else {
+                series2<SMEM>(V.t0c + NCTX * kT0, V.t0c + (NCTX + 1) * kT0, P.n_t0, rho, r1, r2);
+            }
             fp = r1 + s1;
             fpp = r2 + s2;
         } else {
@@ -968,16 +1041,33 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             fpp = pow(C.c, C.s + 2.0) * expint_dev(-C.s - 1.0, x0);
         }
         const double G1 = (ALIAS ? P.alias_ratio * racc[0] : g1) + fp;
-        int c = 0;
+        if constexpr (XDIR) {
+            // line kernel: raw H' = Y + delta G1 / 2; the caller scales (M = h_cm H')
+            const double g2 = 0.5 * G1;
+            double fk[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a)
+            for (int a = 0; a < D; ++a) fk[a] = fpp * k[a];
+            int c = 0;
 #pragma unroll
-            for (int b = a; b < D; ++b) {
-                // yy = sum_z (-2 pi^2 / rfac) w z_a z_b cos + sum_{q != 0} y_a y_b F''
-                const double Y = fma(k[a] * k[b], fpp, yy[c]);
-                out.h[c] = C.pref * C.rfac * (4.0 * Y + (a == b ? 2.0 * G1 : 0.0));
-                ++c;
-            }
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = a; b < D; ++b) {
+                    const double Y = fma(fk[a], k[b], yy[c]);
+                    out.h[c] = a == b ? Y + g2 : Y;
+                    ++c;
+                }
+        } else {
+            int c = 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = a; b < D; ++b) {
+                    // yy = sum_z (-2 pi^2 / rfac) w z_a z_b cos + sum_{q != 0} y_a y_b F''
+                    const double Y = fma(k[a] * k[b], fpp, yy[c]);
+                    out.h[c] = C.pref * C.rfac * (4.0 * Y + (a == b ? 2.0 * G1 : 0.0));
+                    ++c;
+                }
+        }
     }
 }
 
@@ -1222,8 +1312,10 @@ constexpr int kDirParam = 3584;
 // line kernel parameter block: the Hessian's two q = 0 series rows and up to kLineQ reciprocal
 // vectors at the padded stride 4 (d = 3)
 constexpr int kLineQ = 720;
+constexpr int kQ0Max = 16;  // line kernel: Hessian q = 0 pieces (bins of kBinWidth in x = c rho)
+constexpr uint32_t kQ0Bytes = uint32_t(kQ0Max) * piece_stride(2) * 8u;
 struct __align__(16) LineParam {
-    double t0[2 * kT0];
+    double q0[kQ0Max * piece_stride(2)];
     double rq[kLineQ * 4];
 };
 struct __align__(16) DirBlock {
@@ -1242,12 +1334,13 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     View V = stage<SMEM, CDIR || LINE, LINE>(P, smem);
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // LINE: count table after the image, then the per-warp scratch
-    const uint32_t scr = V.s_end + 4u * kCntEntries + kLineScrBytes * uint32_t(warp_all);
+    // LINE: [count table][q = 0 pieces][per-warp scratch] after the image
+    const uint32_t scr = V.s_end + 4u * kCntEntries + (LINE ? kQ0Bytes : 0u) + kLineScrBytes * uint32_t(warp_all);
     if constexpr (LINE) {
-        V.p_t0 = cdir;                // LineParam::t0
-        V.p_rq = cdir + 2 * kT0;      // LineParam::rq
+        V.p_rq = cdir + kQ0Max * piece_stride(2);  // LineParam::rq
         V.s_cnt = V.s_end;
+        V.s_q0 = V.s_end + 4u * kCntEntries;
+        for (int i = threadIdx.x; i < P.q0_nb * piece_stride(2); i += blockDim.x) sts_f64(V.s_q0 + 8u * i, cdir[i]);
         const double qmax = P.n_rec > 0 ? V.rec_norm[P.n_rec - 1] : 1.0;
         const double h = (qmax > 0.0 ? qmax : 1.0) / double(kCntEntries - 2);
         V.cnt_inv_h = 1.0 / h;
@@ -1421,6 +1514,61 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             }
         }
     };
+    // Line walk: one node (k given, weight, direct-space Hessian channels hx) -> ATM integrand
+    // [Z_3^3, tr M_5^3] with M = h_cm H' (eval_node XDIR returns H' = Y + delta G1 / 2), Z_3 = tr M.
+    // tr(H'^3) of the symmetric matrix in closed form.  The value is added to tacc (warp owns the
+    // tile) or reduced and committed like run_patch.
+    auto run_node = [&](int64_t patch, const double (&k)[D], double weight, const double* hx, double* tacc) {
+      if constexpr (LINE) {
+        double val[NCOMP];
+        {
+            NodeAcc<D, NCTX, HESS, MODE == 1> acc;
+            eval_node<D, NCTX, HESS, true, UNR, true, false, true, true>(P, V, k, k, 0, 1, 0u, acc, hx);
+            if constexpr (D == 3 && NCOMP == 2) {
+                const double h00 = acc.h[0], h01 = acc.h[1], h02 = acc.h[2], h11 = acc.h[3], h12 = acc.h[4],
+                             h22 = acc.h[5];
+                const double tr = (h00 + h11) + h22;
+                const double d01 = h01 * h01, d02 = h02 * h02, d12 = h12 * h12;
+                const double cub = fma(h00 * h00, h00, fma(h11 * h11, h11, h22 * h22 * h22));
+                const double mix = fma(d01, h00 + h11, fma(d02, h00 + h22, d12 * (h11 + h22)));
+                const double tr3 = fma(3.0, mix, fma(6.0 * h01, h02 * h12, cub));
+                const double cm = P.h_cm, zt = cm * tr;
+                val[0] = weight * (zt * zt * zt);
+                val[1] = weight * ((cm * cm * cm) * tr3);
+            }
+        }
+        if (tacc) {
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) tacc[c] += val[c];
+            return;
+        }
+        const int64_t tile = patch / kTileWarps;
+        double wv[NCOMP];
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) {
+            double v = val[c];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            wv[c] = v;
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) g.wpart[patch * NCOMP + c] = wv[c];
+            __threadfence();
+            const unsigned prev = atomicAdd(&g.tcount[tile], 1u);
+            if (prev == kTileWarps - 1) {
+                __threadfence();
+#pragma unroll
+                for (int c = 0; c < NCOMP; ++c) {
+                    double sum = 0.0;
+                    for (int w = 0; w < kTileWarps; ++w) sum += __ldcg(&g.wpart[(tile * kTileWarps + w) * NCOMP + c]);
+                    partials[tile * NCOMP + c] = sum;
+                }
+                g.tcount[tile] = 0u;
+            }
+        }
+      }
+    };
     if constexpr (LINE) {
         // Line-pair numbering (this kernel's own patch order; tiles and partial slots follow it):
         // the cells pyr + 3 s1 and pyr + 3 s1 + 6 (s0 = +-1) share kappa_0 on every line
@@ -1430,18 +1578,52 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         const int npv = g.npv;
         const int64_t per_lp = 2 * int64_t(npv);
         const int64_t lp_lo = p_lo / per_lp, lp_hi = (p_hi - 1) / per_lp + 1;
-        for (int64_t lp = lp_lo + int64_t(blockIdx.x) * kWarpsPerCta + warp_all; lp < lp_hi;
-             lp += int64_t(gridDim.x) * kWarpsPerCta) {
+        // Dynamic work queue: a warp takes the next line pair from a global ticket counter.
+        // Tickets run in the order LZ_LINE_ORDER (1: radial index descending within whole
+        // (cp, iv2) blocks -- the costliest lines first, so the launch ends on the cheap ones);
+        // the partial slots are indexed by the line pair, so the result does not depend on which
+        // warp takes which ticket.  The last warp to leave resets the counters for the next launch.
+        const int64_t n_lp = lp_hi - lp_lo;
+        const bool by_radius = LZ_LINE_ORDER != 0 && lp_lo % g.n_u == 0 && n_lp % g.n_u == 0;
+        const int64_t n_outer = by_radius ? n_lp / g.n_u : 1;
+        auto grab = [&]() -> int64_t {
+            unsigned t = 0;
+            if (lane == 0) t = atomicAdd(g.work, 1u);
+            return int64_t(__shfl_sync(0xffffffffu, t, 0));
+        };
+        for (int64_t tk = grab(); tk < n_lp; tk = grab()) {
+            int64_t lp = lp_lo + tk;
+            if (by_radius) {
+                const int64_t rr = tk / n_outer, o = tk - rr * n_outer;
+                const int64_t ir = LZ_LINE_ORDER == 1 ? g.n_u - 1 - rr : rr;
+                lp = (lp_lo / g.n_u + o) * g.n_u + ir;
+            }
             const int iu = int(lp % g.n_u);
             const int64_t r = lp / g.n_u;
             const int iv2 = int(r % g.nv2), cp = int(r / g.nv2);
             const int ax = cp % D;  // the cells' pyramid: lanes vary kappa_ax
             const int64_t pfirst = lp * per_lp;
+            // the line pair's nodes: kappa = kappa0 +- x e_ax (x = 2 u v1, + for the s0 = +1 cell,
+            // - for its mirror), k = B kappa = k0 +- x B e_ax; kappa0 = u roll_ax(0, 2 s1 v2, 1)
+            // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
+            const double u = g.u[iu];
+            const double wline_u = g.wu[iu], wline_v2 = g.wv[iv2];
+            double kap0[D], k0[D], dk[D];
             {
-                double k[D], kap[D], weight;
-                node_at(cp, iv2, iu, lane, k, kap, weight);
-                line_planes(P, V.s_line, scr, ax, kap);
+                const double s1 = ((cp / D) & 1) ? -1.0 : 1.0;
+                const double kb = u * (2.0 * s1 * g.v[iv2]);
+#pragma unroll
+                for (int a = 0; a < D; ++a) kap0[a] = a == ax ? 0.0 : (a == (ax + 1) % D ? kb : u);
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int b = 0; b < D; ++b) sum = fma(P.B[a * D + b], kap0[b], sum);
+                    k0[a] = sum;
+                    dk[a] = ax == 0 ? P.B[a * D] : ax == 1 ? P.B[a * D + 1] : P.B[a * D + 2];
+                }
             }
+            line_planes(P, V.s_line, scr, ax, kap0);
             const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles after C (<= 16 planes)
             // the line pair is exactly one tile and lies in the range: this warp owns the tile and
             // sums it directly (per lane in fixed patch order, then one fixed xor tree)
@@ -1454,17 +1636,29 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 const bool in0 = patch >= p_lo && patch < p_hi, in1 = patch + npv >= p_lo && patch + npv < p_hi;
                 if (!in0 && !in1) continue;
                 const int iv1 = pv * 32 + lane;
-                // x of the mirror-0 node (s0 = +1): kappa_ax = u * 2 v1; the mirror node has -x
+                // lanes past n_v repeat the line's last node with weight 0 (every lane stays on
+                // the line, which the culling bound needs)
                 const int iv1c = iv1 < g.n_v ? iv1 : g.n_v - 1;
-                const double x = 2.0 * g.u[iu < g.n_u ? iu : 0] * g.v[iv1c];
+                const double x = 2.0 * u * g.v[iv1c];
+                const double weight = iv1 < g.n_v ? (wline_u * g.wv[iv1c]) * wline_v2 : 0.0;
                 double hp[6], hm[6];
                 line_node_pair(P, scr, ax, x, hp, hm);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
-                if (in0) run_patch(patch, make_int4(cp, iv2, iu, iv1), hp, own ? tacc : nullptr);
+                if (in0) {
+                    double k[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) k[a] = fma(x, dk[a], k0[a]);
+                    run_node(patch, k, weight, hp, own ? tacc : nullptr);
+                }
 #pragma unroll
                 for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
-                if (in1) run_patch(patch + npv, make_int4(cp + g.n_cell / 2, iv2, iu, iv1), hm, own ? tacc : nullptr);
+                if (in1) {
+                    double k[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) k[a] = fma(-x, dk[a], k0[a]);
+                    run_node(patch + npv, k, weight, hm, own ? tacc : nullptr);
+                }
             }
             if (own) {
 #pragma unroll
@@ -1474,6 +1668,13 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
                     if (lane == 0) partials[(pfirst / kTileWarps) * NCOMP + c] = v;
                 }
+            }
+        }
+        if (lane == 0) {
+            const unsigned done = atomicAdd(g.work + 1, 1u);
+            if (done == gridDim.x * unsigned(kWarpsPerCta) - 1u) {  // every warp has left the queue
+                g.work[0] = 0u;
+                g.work[1] = 0u;
             }
         }
     } else {
@@ -1503,7 +1704,7 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 template <int WPC, int UNR>
 __global__ void __launch_bounds__(32 * WPC, 1)
     tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials, const __grid_constant__ LineParam LP) {
-    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, LP.t0);
+    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, LP.q0);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -1878,15 +2079,16 @@ template <int WPC, int UNR>
 static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
     auto kern = tile_kernel_l<WPC, UNR>;
-    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + size_t(WPC) * kLineScrBytes;
+    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes + size_t(WPC) * kLineScrBytes;
     if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
     static_assert(sizeof(DevPlan) + sizeof(DevGrid) + sizeof(double*) + 16 + sizeof(LineParam) <= 32764,
                   "kernel parameters exceed the 32 KB limit");
-    if (P.n_rec > kLineQ || P.nctx != 1 || !P.t0_host || !P.rq_host) return cudaErrorInvalidValue;
+    if (P.n_rec > kLineQ || P.nctx != 1 || !P.q0_host || P.q0_nb < 1 || P.q0_nb > kQ0Max || !P.rq_host)
+        return cudaErrorInvalidValue;
     thread_local LineParam lp;  // host staging of the parameter block (copied at launch)
-    std::memcpy(lp.t0, P.t0_host + size_t(P.nctx) * kT0, sizeof(double) * 2 * kT0);
+    std::memcpy(lp.q0, P.q0_host, sizeof(double) * piece_stride(2) * size_t(P.q0_nb));
     std::memcpy(lp.rq, P.rq_host, sizeof(double) * 4 * size_t(P.n_rec));
     const int threads = 32 * WPC;
     if (g.tile_hi <= g.tile_lo) return cudaSuccess;
@@ -1909,9 +2111,10 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
-        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + size_t(line_mode()) * kLineScrBytes + 1024;
+        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
+                            size_t(line_mode()) * kLineScrBytes + 1024;
         if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin()) &&
-            P.n_rec <= kLineQ) {
+            P.n_rec <= kLineQ && P.q0_nb >= 1 && P.q0_nb <= kQ0Max) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 162: return launch_tile_l<16, 2>(P, g, partials, grid_blocks, st, bytes);

@@ -128,6 +128,11 @@ struct DevPlan {
     // | 16 x step code << 16), K = line_K[a]; at
     // line_meta_off[a]: each lane's first (n_b, n_c) as int16 pairs [32], then the lane range of
     // every plane n_a = m (uint8 glo[line_P[a] + 1]).  Hessian channel weight = line_sign v v^T.
+    const double* q0_host;  // host copy (plan-owned) of the Hessian q = 0 pieces [q0_nb][piece_stride(2)]
+    int q0_nb, pad5_;       // (line kernel; 0: no pieces, the line kernel is not used)
+    double q0_inv_h;        // bins per unit rho (c / kBinWidth)
+    double h_kk;            // Hessian context: sing_coef inv_vol / (pref rfac)
+    double h_cm;            // Hessian context: -4 pref rfac / (4 pi^2) (M = h_cm (Y + delta G1 / 2))
     const double* t0_host;  // host copy (plan-owned) of the q = 0 series rows [nctx + 2][kT0]
     const double* rq_host;  // host copy (plan-owned) of rec_q at the padded stride (d + 1) & ~1
     unsigned line_bytes;   // 0: no line block
@@ -174,6 +179,7 @@ struct DevGrid {
     int64_t tile_lo, tile_hi, n_patch;
     double* wpart;             // [n_tiles * 8][ncomp] warp partials (scratch)
     unsigned int* tcount;      // [n_tiles] arrival counters, zero between launches
+    unsigned int* work;        // [2] line kernel work queue: next ticket, warps done (zero between launches)
 };
 
 
@@ -261,6 +267,9 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
 // widened by |z|^order, reciprocal Gamma order s + order, cutoff 1e-20.
 void build_deriv_sets(const HostCtx& h, int order, std::vector<double>* dir_n, std::vector<double>* rec_n);
 double table_x_lo(const HostCtx& h);
+// Degree-kDeg Chebyshev interpolant of f on [x0, x1] as monomials in delta in [-1/2, 1/2] (the
+// device's piece layout); returns the worst absolute error at 21 points (device evaluation order).
+double fit_piece_fn(const std::function<long double(long double)>& f, long double x0, long double x1, double* out);
 void build_hess_sets(HostCtx& h);
 long double t0_coeff(const CtxConst& k, int n);   // rho-series coefficient of t0_reg
 void build_reg_derivatives(const HostCtx& h, int order, std::vector<int>* alphas, std::vector<double>* vals);
