@@ -1181,7 +1181,9 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // fixed-order reduction of each plane over its lane group in shared memory; phase 3: per lane,
 // one complex rotation per plane.
 constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
-constexpr uint32_t kLineScrBytes = 12u * kLineScrStride * 8u + 32u;  // 3200 B per warp
+// per-warp scratch: phase-1 partials [12][33] / C_m [planes][12] from 0, the mirror node's state
+// [10][32] doubles from 1536 (H channels, k, weight), the line pair's constants (9 doubles) from 4096
+constexpr uint32_t kLineScrBytes = 4096u + 80u;
 constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
@@ -1606,25 +1608,33 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             // the line pair's nodes: kappa = kappa0 +- x e_ax (x = 2 u v1, + for the s0 = +1 cell,
             // - for its mirror), k = B kappa = k0 +- x B e_ax; kappa0 = u roll_ax(0, 2 s1 v2, 1)
             // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
-            const double u = g.u[iu];
-            const double wline_u = g.wu[iu], wline_v2 = g.wv[iv2];
-            double kap0[D], k0[D], dk[D];
+            // line-pair constants kept in the warp's scratch (broadcast reloads per pv instead of
+            // registers live across the node evaluations)
+            const uint32_t lsave = scr + 4096u;
             {
+                const double u = g.u[iu];
                 const double s1 = ((cp / D) & 1) ? -1.0 : 1.0;
                 const double kb = u * (2.0 * s1 * g.v[iv2]);
+                double kap0[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a) kap0[a] = a == ax ? 0.0 : (a == (ax + 1) % D ? kb : u);
+                __syncwarp();
+                if (lane == 0) {
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    double sum = 0.0;
+                    for (int a = 0; a < D; ++a) {
+                        double sum = 0.0;
 #pragma unroll
-                    for (int b = 0; b < D; ++b) sum = fma(P.B[a * D + b], kap0[b], sum);
-                    k0[a] = sum;
-                    dk[a] = ax == 0 ? P.B[a * D] : ax == 1 ? P.B[a * D + 1] : P.B[a * D + 2];
+                        for (int b = 0; b < D; ++b) sum = fma(P.B[a * D + b], kap0[b], sum);
+                        sts_f64(lsave + 8u * a, sum);  // k0
+                        sts_f64(lsave + 24u + 8u * a, ax == 0 ? P.B[a * D] : ax == 1 ? P.B[a * D + 1] : P.B[a * D + 2]);
+                    }
+                    sts_f64(lsave + 48u, u);
+                    sts_f64(lsave + 56u, g.wu[iu]);
+                    sts_f64(lsave + 64u, g.wv[iv2]);
                 }
+                line_planes(P, V.s_line, scr, ax, kap0);  // (its first __syncwarp orders the stores)
             }
-            line_planes(P, V.s_line, scr, ax, kap0);
-            const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles after C (<= 16 planes)
+            const uint32_t hsave = scr + 1536u + 8u * lane;  // [10][32] doubles
             // the line pair is exactly one tile and lies in the range: this warp owns the tile and
             // sums it directly (per lane in fixed patch order, then one fixed xor tree)
             const bool own = per_lp == kTileWarps && pfirst >= p_lo && pfirst + per_lp <= p_hi;
@@ -1639,25 +1649,32 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 // lanes past n_v repeat the line's last node with weight 0 (every lane stays on
                 // the line, which the culling bound needs)
                 const int iv1c = iv1 < g.n_v ? iv1 : g.n_v - 1;
-                const double x = 2.0 * u * g.v[iv1c];
-                const double weight = iv1 < g.n_v ? (wline_u * g.wv[iv1c]) * wline_v2 : 0.0;
-                double hp[6], hm[6];
-                line_node_pair(P, scr, ax, x, hp, hm);
+                const double x = 2.0 * lds_f64(lsave + 48u) * g.v[iv1c];
+                const double weight =
+                    iv1 < g.n_v ? (lds_f64(lsave + 56u) * g.wv[iv1c]) * lds_f64(lsave + 64u) : 0.0;
+                double hp[6];
+                {
+                    double hm[6];
+                    line_node_pair(P, scr, ax, x, hp, hm);
 #pragma unroll
-                for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
-                if (in0) {
-                    double k[D];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) k[a] = fma(x, dk[a], k0[a]);
-                    run_node(patch, k, weight, hp, own ? tacc : nullptr);
+                    for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
                 }
+                double k[D];
 #pragma unroll
-                for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
+                for (int a = 0; a < D; ++a) {
+                    const double k0a = lds_f64(lsave + 8u * a), dka = lds_f64(lsave + 24u + 8u * a);
+                    k[a] = fma(x, dka, k0a);
+                    sts_f64(hsave + 256u * (6 + a), fma(-x, dka, k0a));  // the mirror node
+                }
+                sts_f64(hsave + 256u * 9, weight);
+                if (in0) run_node(patch, k, weight, hp, own ? tacc : nullptr);
                 if (in1) {
-                    double k[D];
+                    double hm[6], km[D];
 #pragma unroll
-                    for (int a = 0; a < D; ++a) k[a] = fma(-x, dk[a], k0[a]);
-                    run_node(patch + npv, k, weight, hm, own ? tacc : nullptr);
+                    for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
+#pragma unroll
+                    for (int a = 0; a < D; ++a) km[a] = lds_f64(hsave + 256u * (6 + a));
+                    run_node(patch + npv, km, lds_f64(hsave + 256u * 9), hm, own ? tacc : nullptr);
                 }
             }
             if (own) {
