@@ -281,6 +281,11 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         }
         long K = 0;
         for (int p = 0; p < P; ++p) K = std::max(K, load(p));
+        if (dbg) {
+            std::fprintf(stderr, "line block axis %d: %zu points, K %ld, planes:", ax, np, K);
+            for (int p = 0; p < P; ++p) std::fprintf(stderr, " %zu/%d", planes[p].size(), L[p]);
+            std::fprintf(stderr, "\n");
+        }
         std::vector<uint16_t> idx(size_t(K) * 32, uint16_t(np));
         std::vector<uint8_t> code(size_t(K) * 32, 0);
         std::vector<int32_t> init(32, 0);

@@ -1181,9 +1181,9 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // fixed-order reduction of each plane over its lane group in shared memory; phase 3: per lane,
 // one complex rotation per plane.
 constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
-// per-warp scratch: phase-1 partials [12][33] / C_m [planes][12] from 0, the mirror node's state
-// [10][32] doubles from 1536 (H channels, k, weight), the line pair's constants (9 doubles) from 4096
-constexpr uint32_t kLineScrBytes = 4096u + 80u;
+// per-warp scratch: the step table [32] (phase 1) / C_m [planes][12] from 0, the mirror node's
+// direct-space channels [6][32] doubles from 1536, the line pair's constants (9 doubles) from 3072
+constexpr uint32_t kLineScrBytes = 3072u + 80u;
 constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
@@ -1242,30 +1242,39 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
                 ++c;
             }
     }
-    __syncwarp();  // table read by every lane before the partials overwrite it
-#pragma unroll
-    for (int c = 0; c < 12; ++c) sts_f64(scr + 8u * (c * kLineScrStride + lane), acc[c]);
-    __syncwarp();
+    // plane sums: segmented tree reduction over each plane's lane group [glo[p], glo[p + 1])
+    // (contiguous lanes; fixed order, so the sum does not depend on scheduling); the group's
+    // first lane writes C_m.  Empty planes get zeros.
     const int np = P.line_P[ax];
     const uint32_t glo = meta + 128u;
-    const double sgn = P.line_sign;
-    double res[kLineJobs];
-#pragma unroll
-    for (int r = 0; r < kLineJobs; ++r) {
-        const int j = lane + 32 * r;
-        double sum = 0.0;
-        if (j < 12 * np) {
-            const int p = j / 12, c = j - 12 * p;
-            const int lo = int(lds_u8(glo + p)), hi = int(lds_u8(glo + p + 1));
-            for (int l = lo; l < hi; ++l) sum += lds_f64(scr + 8u * (c * kLineScrStride + l));
+    int g0 = 0, gs = 1, pl = 0, maxg = 1;
+    for (int p = 0; p < np; ++p) {
+        const int lo = int(lds_u8(glo + p)), hi = int(lds_u8(glo + p + 1));
+        maxg = max(maxg, hi - lo);
+        if (lane >= lo && lane < hi) {
+            g0 = lo;
+            gs = hi - lo;
+            pl = p;
         }
-        res[r] = sgn * sum;
     }
-    __syncwarp();
+    const int gl = lane - g0;
+    for (int st = 1; st < maxg; st <<= 1) {
+        const bool take = (gl & (2 * st - 1)) == 0 && gl + st < gs;
 #pragma unroll
-    for (int r = 0; r < kLineJobs; ++r) {
-        const int j = lane + 32 * r;
-        if (j < 12 * np) sts_f64(scr + 8u * j, res[r]);  // C[p][c] at p * 12 + c
+        for (int c = 0; c < 12; ++c) {
+            const double o = __shfl_down_sync(0xffffffffu, acc[c], st);
+            if (take) acc[c] += o;
+        }
+    }
+    __syncwarp();  // the step table is read by every lane before C overwrites it
+    const double sgn = P.line_sign;
+    if (gl == 0) {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) sts_f64(scr + 8u * (pl * 12 + c), sgn * acc[c]);
+    }
+    if (lane < np && lds_u8(glo + lane) == lds_u8(glo + lane + 1)) {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) sts_f64(scr + 8u * (lane * 12 + c), 0.0);
     }
     __syncwarp();
 }
@@ -1610,7 +1619,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
             // line-pair constants kept in the warp's scratch (broadcast reloads per pv instead of
             // registers live across the node evaluations)
-            const uint32_t lsave = scr + 4096u;
+            const uint32_t lsave = scr + 3072u;
             {
                 const double u = g.u[iu];
                 const double s1 = ((cp / D) & 1) ? -1.0 : 1.0;
@@ -1634,7 +1643,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 }
                 line_planes(P, V.s_line, scr, ax, kap0);  // (its first __syncwarp orders the stores)
             }
-            const uint32_t hsave = scr + 1536u + 8u * lane;  // [10][32] doubles
+            const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles
             // the line pair is exactly one tile and lies in the range: this warp owns the tile and
             // sums it directly (per lane in fixed patch order, then one fixed xor tree)
             const bool own = per_lp == kTileWarps && pfirst >= p_lo && pfirst + per_lp <= p_hi;
@@ -1659,22 +1668,23 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
 #pragma unroll
                     for (int c = 0; c < 6; ++c) sts_f64(hsave + 256u * c, hm[c]);
                 }
-                double k[D];
+                if (in0) {
+                    double k[D];
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    const double k0a = lds_f64(lsave + 8u * a), dka = lds_f64(lsave + 24u + 8u * a);
-                    k[a] = fma(x, dka, k0a);
-                    sts_f64(hsave + 256u * (6 + a), fma(-x, dka, k0a));  // the mirror node
+                    for (int a = 0; a < D; ++a) k[a] = fma(x, lds_f64(lsave + 24u + 8u * a), lds_f64(lsave + 8u * a));
+                    run_node(patch, k, weight, hp, own ? tacc : nullptr);
                 }
-                sts_f64(hsave + 256u * 9, weight);
-                if (in0) run_node(patch, k, weight, hp, own ? tacc : nullptr);
                 if (in1) {
+                    // the mirror node (s0 = -1): same weight, k = k0 - x dk (x and the weight re-derived)
+                    const double xm = 2.0 * lds_f64(lsave + 48u) * g.v[iv1c];
+                    const double wm =
+                        iv1 < g.n_v ? (lds_f64(lsave + 56u) * g.wv[iv1c]) * lds_f64(lsave + 64u) : 0.0;
                     double hm[6], km[D];
 #pragma unroll
                     for (int c = 0; c < 6; ++c) hm[c] = lds_f64(hsave + 256u * c);
 #pragma unroll
-                    for (int a = 0; a < D; ++a) km[a] = lds_f64(hsave + 256u * (6 + a));
-                    run_node(patch + npv, km, lds_f64(hsave + 256u * 9), hm, own ? tacc : nullptr);
+                    for (int a = 0; a < D; ++a) km[a] = fma(-xm, lds_f64(lsave + 24u + 8u * a), lds_f64(lsave + 8u * a));
+                    run_node(patch + npv, km, wm, hm, own ? tacc : nullptr);
                 }
             }
             if (own) {
