@@ -369,6 +369,13 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 // floor(y) for 0 <= y < 2^31 without FP64<->int conversions: y - 1/2 + 1.5*2^52 rounds to the
 // integer in the low word.  At exact integers the tie may yield y - 1 with fractional part 1,
 // i.e. tau = +1 at the end of the previous piece -- equally valid.
+#ifndef LZ_KMAG_RSQ
+#define LZ_KMAG_RSQ 1
+#endif
+#ifndef LZ_P1_UNROLL
+#define LZ_P1_UNROLL 1
+#endif
+constexpr int kP1Unroll = LZ_P1_UNROLL;  // phase-1 slots per loop iteration
 // Ticket order of the line kernel's work queue (A/B: -DLZ_LINE_ORDER=0 plain, 1 radial index
 // descending, 2 ascending)
 #ifndef LZ_LINE_ORDER
@@ -797,7 +804,14 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         // square root of the upward-rounded square, widened by one part in 1e6
         {
             const double k2 = fmax(__shfl_sync(0xffffffffu, kmag, 0), __shfl_sync(0xffffffffu, kmag, 31));
+#if LZ_KMAG_RSQ
+            // approximate reciprocal square root (~2^-20 relative), widened by 1e-5: k2 rsq(k2) >= |k|
+            double rs;
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(fmax(k2, 1e-300)));
+            kmag = k2 * rs * (1.0 + 1e-5);
+#else
             kmag = double(__fsqrt_ru(__double2float_ru(k2))) * (1.0 + 1e-6);
+#endif
         }
         constexpr double kM = 6755399441055744.0;
         const double xe = fma(P.r_cut + kmag, V.cnt_inv_h, 0.5) + kM;  // floor + 1
@@ -1215,7 +1229,7 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
 #pragma unroll
     for (int c = 0; c < 12; ++c) acc[c] = 0.0;
     const uint32_t ai = sl + 4u * lane;
-#pragma unroll 1
+#pragma unroll kP1Unroll
     for (int q = 0; q < K; ++q) {
         const uint32_t wd = lds_u32(ai + 128u * q);  // v record and step entry byte offsets
         const uint32_t va = lb + (wd & 0xffffu);

@@ -211,6 +211,9 @@ struct HostTable {
     int lo_start = 0;         // first low-degree bin (low-degree bins form the suffix)
 };
 
+#ifndef LZ_LO_HORNER
+#define LZ_LO_HORNER 1
+#endif
 // Degree-kDeg polynomial in Estrin form: dependency depth 3-4 instead of 7-8, and the
 // powers tau^2, tau^4 (, tau^8) are shared by every function of a table row.
 // Host (table build check) and device evaluate with the same operation order.
@@ -246,10 +249,15 @@ inline double estrin(const double* c, const TauPowers& p) {
 __host__ __device__
 #endif
 inline double estrin_lo(const double* c, const TauPowers& p) {  // degree 4
+#if LZ_LO_HORNER
+    // Horner: no tau powers (2 DMUL fewer per table term; the degree-4 bins carry most terms)
+    return fma(fma(fma(fma(c[4], p.t1, c[3]), p.t1, c[2]), p.t1, c[1]), p.t1, c[0]);
+#else
     const double a0 = fma(c[1], p.t1, c[0]);
     const double a1 = fma(c[3], p.t1, c[2]);
     const double b0 = fma(a1, p.t2, a0);
     return fma(c[4], p.t4, b0);
+#endif
 }
 
 // Errors raised by the host builder carry an lz status code.
