@@ -320,10 +320,17 @@ def kernel_counters():
     changed since the capture."""
     with open(COUNTERS) as f:
         c = json.load(f)
-    src = os.path.join(ROOT, "paper_2504_11989_b200", "csrc", "kernels.cu")
-    sha = hashlib.sha1(open(src, "rb").read()).hexdigest()
-    c["stale"] = c.get("kernels_cu_sha1") != sha
+    c["stale"] = c.get("csrc_sha1") != csrc_sha1()
     return c
+
+
+def csrc_sha1():
+    """sha1 over the sources that shape the ATM kernel's instruction stream (kernel, shared
+    device headers, host plan builder); tools/ncu_metrics.py records the same digest."""
+    h = hashlib.sha1()
+    for name in ("kernels.cu", "lz_internal.h", "special.cuh", "capi.cpp", "context.cpp"):
+        h.update(open(os.path.join(ROOT, "paper_2504_11989_b200", "csrc", name), "rb").read())
+    return h.hexdigest()
 
 
 def run_ours(args):

@@ -52,7 +52,9 @@ def main(rep, units, out, kernel=None):
     fl = 2 * f('smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed') + \
         f('smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed') + \
         f('smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed')
-    sha = hashlib.sha1(open(os.path.join(ROOT, "paper_2504_11989_b200", "csrc", "kernels.cu"), "rb").read())
+    sha = hashlib.sha1()
+    for name in ("kernels.cu", "lz_internal.h", "special.cuh", "capi.cpp", "context.cpp"):
+        sha.update(open(os.path.join(ROOT, "paper_2504_11989_b200", "csrc", name), "rb").read())
     res = {"kernel": d.get("Kernel Name"), "source": f"ncu --set full capture {os.path.basename(rep)}",
            "seconds": secs, "fp64_flops_per_launch": fl, "units_per_launch": float(units),
            "flops_per_unit": fl / float(units), "tflops": fl / secs / 1e12,
@@ -62,7 +64,7 @@ def main(rep, units, out, kernel=None):
            "lsu_wavefronts": val('l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed') / 100,
            "warps_active": val('sm__warps_active.avg.pct_of_peak_sustained_active') / 100,
            "registers": int(val('launch__registers_per_thread')),
-           "kernels_cu_sha1": sha.hexdigest(),
+           "csrc_sha1": sha.hexdigest(),
            "raw": {k: d.get(k) for k in KEYS}}
     for k, v in res.items():
         print(k, v)
