@@ -127,6 +127,10 @@ typedef struct {
 int lz_plan_get_info(const lz_plan* plan, lz_plan_info* out);
 int lz_plan_integrate(const lz_plan* plan, const lz_grid* g, double* partials, int grid_blocks,
                       void* stream);
+/* product plan at arbitrary k (device pointers, stream-ordered): out[i] = prod_j Z_j(k_i)^{m_j},
+ * k reduced into the cell; k in the reciprocal lattice of a pole context sets status bit 1.
+ * Replaces _product_on_batch (L/quadrature.py:393-397) for the adaptive radial quadrature. */
+int lz_plan_product_at(const lz_plan* plan, const double* k, int64_t n, double* out, int* status, void* stream);
 /* fixed-order compensated sum of n_tiles x ncomp partials -> out[ncomp] (device) */
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream);
 /* fixed chunks of tile partials, the multi-GPU exchange unit: for c in [chunk_lo, chunk_hi)

@@ -81,6 +81,7 @@ SIGNATURES = {
     "lz_plan_create_atm": (C.c_int, [_P, _P, C.POINTER(_P)]),
     "lz_plan_destroy": (C.c_int, [_P]),
     "lz_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
+    "lz_plan_product_at": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P]),
     "lz_plan_integrate": (C.c_int, [_P, C.POINTER(Grid), _P, C.c_int, _P]),
     "lz_reduce_partials": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P]),
     "lz_reduce_chunks": (C.c_int, [_P, C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_int64, _P, _P]),

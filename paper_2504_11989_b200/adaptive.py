@@ -114,25 +114,25 @@ class _CellState:
 
 class _DeviceProfile:
     """f(u, w) = const * u^(d-1) prod_j Z_j(u w)^{m_j} - subtracted monomials, with the zeta
-    products of a whole refinement round evaluated in one GPU batch."""
+    products of a whole refinement round evaluated in one GPU batch: one fused product kernel
+    per group of <= 4 distinct exponents (lz_plan_product_at), contexts at cfg.splitting."""
 
-    def __init__(self, lattice, groups, const):
-        from .epstein import epstein_context
+    def __init__(self, lattice, groups, const, splitting=None):
+        from .quadrature import product_plan
         self.d = lattice.d
         self.const = const
-        self.ctxs = [(epstein_context(lattice, nu), m) for nu, m in groups]
+        self.plans = [product_plan(lattice, tuple(groups[i:i + 4]), splitting) for i in range(0, len(groups), 4)]
 
     def __call__(self, blocks, subs):
         import torch
         d = self.d
         k = np.concatenate([(u[:, None, None] * w[None, :, :]).reshape(-1, d) for u, w in blocks])
-        kt = torch.tensor(k, dtype=torch.float64, device="cuda")
+        kt = torch.from_numpy(k).pin_memory().to("cuda", non_blocking=True)
         prod = None
-        for ctx, m in self.ctxs:
-            z, _ = ctx.zeta_device(kt)
-            zm = z if m == 1 else z ** m
-            prod = zm if prod is None else prod * zm
-        vals = (prod * self.const).cpu().numpy()
+        for plan in self.plans:
+            z = plan.product_at(kt)
+            prod = z if prod is None else prod * z
+        vals = prod.cpu().numpy() * self.const
         out, off = [], 0
         for (u, w), sub in zip(blocks, subs):
             n = len(u) * len(w)
@@ -181,7 +181,7 @@ def integrate_product_adaptive(lattice, contexts, cfg):
                 sub.append((eta, m, c * const))
             subtract.append(sub)
     states = [_CellState(lo, 0.5) for _ in dirs]
-    profile = _DeviceProfile(lattice, groups, const)
+    profile = _DeviceProfile(lattice, groups, const, cfg.splitting)
     while True:
         active = [ci for ci, s in enumerate(states) if s.pending is not None]
         if not active:

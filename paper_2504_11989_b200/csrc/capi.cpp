@@ -30,6 +30,8 @@
 #include "special.cuh"
 
 namespace lz {
+cudaError_t launch_product_at(const DevPlan& P, int4 mult, const double* k, int64_t n, double* out, int G,
+                              int* status, cudaStream_t st);
 cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n, double* out, uint32_t flags,
                          int G, int* status, cudaStream_t st);
 cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, double* partials,
@@ -2009,6 +2011,16 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
             check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");
         else
             check_cuda(lz::launch_atm(pl->P, dgd, partials, grid_blocks, st), "atm kernel");
+    });
+}
+
+int lz_plan_product_at(const lz_plan* pl, const double* k, int64_t n, double* out, int* status, void* stream) {
+    return guarded([&] {
+        if (pl->kind != 0) throw Error{LZ_EINVAL, "lz_plan_product_at needs a product plan"};
+        DeviceGuard dg(pl->device);
+        const int4 m = make_int4(pl->mult[0], pl->mult[1], pl->mult[2], pl->mult[3]);
+        check_cuda(lz::launch_product_at(pl->P, m, k, n, out, auto_lanes(n), status, (cudaStream_t)stream),
+                   "product kernel");
     });
 }
 

@@ -1088,10 +1088,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 // ---------------------------------------------------------------------------
 // Batch kernel: G lanes per point, persistent grid-stride over points.
 // flags: 1 = NO_REDUCE, 2 = REG_ONLY, 4 = SINGULAR_ONLY.  status bit 1 = pole.
-template <int D, int NCTX, bool HESS, bool SMEM>
+// PROD: out[pt] = prod_j Z_j(k)^{m_j} over the plan's contexts (product plans; the adaptive
+// radial quadrature's integrand, L/quadrature.py:393-397), one kernel for every factor.
+template <int D, int NCTX, bool HESS, bool SMEM, bool PROD = false>
 __global__ void __launch_bounds__(256) batch_kernel(DevPlan P, const double* __restrict__ kin, int64_t n,
                                                     double* __restrict__ out, uint32_t flags, int G,
-                                                    int* status) {
+                                                    int* status, int4 mult = int4{0, 0, 0, 0}) {
     extern __shared__ __align__(16) unsigned char smem[];
     const View V = stage<SMEM>(P, smem);
     const int64_t nslots = ((n * G + 31) / 32) * 32;
@@ -1126,7 +1128,29 @@ __global__ void __launch_bounds__(256) batch_kernel(DevPlan P, const double* __r
         NodeAcc<D, NCTX, HESS> acc;
         eval_node<D, NCTX, HESS, false, 2, SMEM>(P, V, kap, k, gl, G, flags, acc);
         if (valid && gl == 0) {
-            if constexpr (NCTX > 0) {
+            if constexpr (PROD) {
+                const int m[4] = {mult.x, mult.y, mult.z, mult.w};
+                double prod = 1.0;
+#pragma unroll
+                for (int j = 0; j < NCTX; ++j) {
+                    double base = acc.z[j], r = 1.0;  // z^m by binary powering
+                    for (int e = m[j]; e; e >>= 1) {
+                        if (e & 1) r *= base;
+                        base *= base;
+                    }
+                    prod *= r;
+                }
+                out[pt] = prod;
+                if (!(flags & 1u) && status) {
+                    bool pole = false;
+#pragma unroll
+                    for (int j = 0; j < NCTX; ++j) pole = pole || P.ctx[j].pole;
+                    double rho = 0.0;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) rho = fma(k[a], k[a], rho);
+                    if (pole && rho < 1e-28) atomicOr(status, 1);
+                }
+            } else if constexpr (NCTX > 0) {
                 out[pt] = acc.z[0];
                 if (!(flags & 1u) && P.ctx[0].pole && status) {
                     double rho = 0.0;
@@ -1980,7 +2004,7 @@ static cudaError_t launch_batch_s(const DevPlan& P, const double* k, int64_t n, 
     int64_t cap = blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) blocks = 1;
-    kern<<<blocks, threads, sm, st>>>(P, k, n, out, flags, G, status);
+    kern<<<blocks, threads, sm, st>>>(P, k, n, out, flags, G, status, int4{0, 0, 0, 0});
     return cudaGetLastError();
 }
 
@@ -1992,6 +2016,36 @@ static cudaError_t launch_batch_t(const DevPlan& P, const double* k, int64_t n, 
     if (bytes + 2048 <= size_t(smem_optin()))
         return launch_batch_s<D, NCTX, HESS, true>(P, k, n, out, flags, G, status, st, bytes);
     return launch_batch_s<D, NCTX, HESS, false>(P, k, n, out, flags, G, status, st, bytes);
+}
+
+template <int D, int NCTX>
+static cudaError_t launch_product_at_t(const DevPlan& P, int4 mult, const double* k, int64_t n, double* out, int G,
+                                      int* status, cudaStream_t st) {
+    const size_t bytes = plan_smem_bytes(P);
+    if (P.blob_bytes != bytes || bytes + 2048 > size_t(smem_optin())) return cudaErrorInvalidValue;
+    auto kern = batch_kernel<D, NCTX, false, true, true>;
+    cudaError_t e = set_smem(kern, bytes);
+    if (e != cudaSuccess) return e;
+    const int threads = 256;
+    int64_t need = (n * G + threads - 1) / threads;
+    int64_t cap = blocks_for(kern, bytes, threads);
+    int blocks = int(need < cap ? need : cap);
+    if (blocks < 1) blocks = 1;
+    kern<<<blocks, threads, bytes, st>>>(P, k, n, out, 0u, G, status, mult);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_product_at(const DevPlan& P, int4 mult, const double* k, int64_t n, double* out, int G,
+                              int* status, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+#define LZ_PCASE(DD, NC) \
+    if (P.d == DD && P.nctx == NC) return launch_product_at_t<DD, NC>(P, mult, k, n, out, G, status, st);
+    LZ_PCASE(1, 1) LZ_PCASE(1, 2) LZ_PCASE(1, 3) LZ_PCASE(1, 4)
+    LZ_PCASE(2, 1) LZ_PCASE(2, 2) LZ_PCASE(2, 3) LZ_PCASE(2, 4)
+    LZ_PCASE(3, 1) LZ_PCASE(3, 2) LZ_PCASE(3, 3) LZ_PCASE(3, 4)
+    LZ_PCASE(4, 1) LZ_PCASE(4, 2) LZ_PCASE(4, 3) LZ_PCASE(4, 4)
+#undef LZ_PCASE
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n, double* out, uint32_t flags,

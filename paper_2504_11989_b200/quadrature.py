@@ -232,6 +232,17 @@ class Plan:
         N.check(N.lib().lz_plan_integrate(self._h, C.byref(g), partials.data_ptr(), grid_blocks, st),
                 "integral")
 
+    def product_at(self, k):
+        """prod_j Z_j(k)^{m_j} at a CUDA tensor of k points (n, d) -> CUDA tensor (n,) (product
+        plans; one fused kernel for every factor)."""
+        import torch
+        k = k.contiguous()
+        out = torch.empty(k.shape[0], dtype=torch.float64, device=k.device)
+        st = torch.cuda.current_stream(k.device).cuda_stream
+        N.check(N.lib().lz_plan_product_at(self._h, k.data_ptr(), k.shape[0], out.data_ptr(), None, st),
+                "product at k")
+        return out
+
     @staticmethod
     def reduce_device(partials, n_tiles: int, ncomp: int, out, stream=None):
         import torch

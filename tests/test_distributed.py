@@ -37,10 +37,24 @@ def _run(worker, world, *args, timeout=300):
     procs = [ctx.Process(target=worker, args=(r, world, port, q, *args)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=timeout) for _ in procs)
+    # collect results, failing fast when a worker dies (its peer would otherwise wait in the
+    # rendezvous or a collective until the timeout)
+    import queue
+    import time
+    res, deadline = [], time.monotonic() + timeout
+    while len(res) < len(procs):
+        try:
+            res.append(q.get(timeout=2.0))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or time.monotonic() > deadline:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                raise RuntimeError(f"distributed worker failed (exit codes {dead})" if dead else "timeout")
     for p in procs:
         p.join(timeout=60)
-    return res
+    return sorted(res)
 
 
 def _init(rank, world, port):

@@ -4,6 +4,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_2504_11989_b200 import named_lattice
+from paper_2504_11989_b200.epstein import EpsteinContext
 from paper_2504_11989_b200.manybody import ATMGrid, atm_cohesive_energy, atm_integrals, many_body_zeta
 from paper_2504_11989_b200.quadrature import Plan, QuadratureConfig, atm_plan, fixed_grid_integral, integrate_product
 
@@ -363,3 +364,20 @@ def test_near_d_escalation_to_adaptive(golden_near_d):
     # method="grid" is the literal grid: no escalation, and its estimate shows the gap
     vg, eg = integrate_product(lat, rec["nus"], QuadratureConfig(grid_u=64, grid_v=64, method="grid"))
     assert abs(vg - rec["value"]) > 1e-6 * abs(rec["value"]) and eg > 1e-6 * abs(vg)
+
+
+@pytest.mark.gpu
+def test_product_at_matches_zeta_products():
+    """lz_plan_product_at (one fused kernel for prod_j Z_j^{m_j} at arbitrary k, the adaptive
+    path's integrand) against the single-context zeta kernels on the same points."""
+    import torch
+    from paper_2504_11989_b200.quadrature import product_plan
+    for name, groups in [("fcc", ((3.0, 1), (5.0, 2))), ("square", ((3.5, 3),)),
+                         ("bcc", ((-1.0, 1), (5.0, 1), (1.0, 1), (3.0, 2)))]:
+        lat = named_lattice(name)
+        k = np.random.default_rng(4).uniform(-0.5, 0.5, size=(2000, lat.d)) @ lat.a_inv_t.T
+        got = product_plan(lat, groups).product_at(torch.tensor(k, device="cuda")).cpu().numpy()
+        ref = np.ones(len(k))
+        for nu, m in groups:
+            ref = ref * EpsteinContext(lat, nu, device=0).zeta(k) ** m
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), name

@@ -72,6 +72,27 @@ def c1():
     print("c1 ok", float(z.sum()))
 
 
+def adaptive_fcc():
+    """The reference's own route to the fcc ATM energy (Prop. 2.4: three meromorphically continued
+    integrals through integrate_product, method="adaptive" = the reference's GK15/G7 refinement with
+    every round's zeta products on the GPU), timed; the survey's reference timing is 102 s on 8
+    threads (377 s on 1)."""
+    from paper_2504_11989_b200.quadrature import integrate_product
+    fcc = named_lattice("fcc")
+    cfg = QuadratureConfig(method="adaptive")
+    integrate_product(named_lattice("square"), (3, 3, 3), cfg)  # warm-up (contexts, kernels)
+    out = {}
+    t_all = time.perf_counter()
+    for nus in ((3, 3, 3), (-1, 5, 5), (1, 3, 5)):
+        t0 = time.perf_counter()
+        v, err = integrate_product(fcc, nus, cfg)
+        out[nus] = v
+        print(f"fcc {nus}: {v!r} +- {err:.2e}  {time.perf_counter() - t0:.3f} s", flush=True)
+    e = out[(3, 3, 3)] / 24 - 3 * out[(-1, 5, 5)] / 16 + 3 * out[(1, 3, 5)] / 8
+    print(f"E_ATM (Prop. 2.4, adaptive) {e!r}  rel err vs reference {abs(e - 19.182931071876666) / 19.182931071876666:.2e}"
+          f"  total {time.perf_counter() - t_all:.3f} s (reference: 102 s on 8 threads, 377 s on 1)")
+
+
 def e2e_breakdown():
     """Where the cold-cache time of atm_energy_distributed goes (host plan vs device)."""
     from paper_2504_11989_b200.distributed import ShardedIntegral
@@ -173,4 +194,4 @@ def e2e():
 
 if __name__ == "__main__":
     {"atm": atm, "c1": c1, "c1_time": c1_time, "e2e": e2e,
-     "e2e_breakdown": e2e_breakdown, "atm_sweep": atm_sweep, "c1_small": c1_small}[sys.argv[1]]()
+     "e2e_breakdown": e2e_breakdown, "atm_sweep": atm_sweep, "c1_small": c1_small, "adaptive_fcc": adaptive_fcc}[sys.argv[1]]()
