@@ -618,6 +618,34 @@ def secondary(np, torch):
                             "lambda_c": crit, "k_atm_fcc": fc.k_atm, "k_atm_bcc": bc.k_atm,
                             "points": len(pts)}
     out["shard_balance"] = shard_balance(torch)
+    # the reference's own route to the fcc ATM energy (Prop. 2.4: three continued integrals with
+    # its adaptive GK15/G7 refinement, method="adaptive", every round's zeta products on the GPU)
+    fcc = named_lattice("fcc")
+    acfg = QuadratureConfig(method="adaptive")
+    integrate_product(fcc, (3, 3, 3), acfg)   # contexts and plans built outside the timing
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    zs = [integrate_product(fcc, nus, acfg)[0] for nus in ((3, 3, 3), (-1, 5, 5), (1, 3, 5))]
+    t_ad = time.perf_counter() - t0
+    e_ad = zs[0] / 24 - 3 * zs[1] / 16 + 3 * zs[2] / 8
+    out["c3_prop24_adaptive"] = {"seconds": t_ad, "energy": e_ad,
+                                 "rel_err_vs_reference": abs(e_ad - 19.182931071876666) / 19.182931071876666,
+                                 "reference_seconds": {"threads_8": 102.0, "threads_1": 377.0,
+                                                       "source": "SURVEY.md section 6 (reference run in the survey container)"}}
+    # order-m derivatives at arbitrary k (moment kernel) and the device Taylor table at k = 0
+    k3 = torch.tensor(np.random.default_rng(2).uniform(-0.45, 0.45, size=(1 << 14, 3)) @ fcc.a_inv_t.T,
+                      device="cuda")
+    c5 = EpsteinContext(fcc, 5.0, device=torch.cuda.current_device())
+    der = {}
+    for m in (4, 8, 12):
+        c5.derivatives_device(k3, m)
+        ms = _time_cuda(lambda: c5.derivatives_device(k3, m), 5, torch)
+        der[f"order_{m}"] = {"points": int(k3.shape[0]), "ms": ms, "points_per_s": k3.shape[0] / (ms * 1e-3)}
+    c3 = EpsteinContext(fcc, 3.0, device=torch.cuda.current_device())
+    t0 = time.perf_counter()
+    c3.reg_derivatives(8)
+    der["taylor_table_order8_ms"] = (time.perf_counter() - t0) * 1e3
+    out["fcc_nu5_derivatives"] = der
     return out
 
 

@@ -261,6 +261,19 @@ class EpsteinContext:
             return alphas, out[0]
         return alphas, out.reshape(shape + (len(alphas),))
 
+    def derivatives_device(self, k, order: int, out=None):
+        """All d^alpha Z_nu(k), |alpha| = order, for a CUDA tensor of k points (n, d): returns the
+        CUDA tensor (n, n_alpha) (stream-ordered, no host copies; pole points are not checked)."""
+        import torch
+        n = k.shape[0]
+        na = len(multi_indices(self.d, order))
+        if out is None:
+            out = torch.empty((n, na), dtype=torch.float64, device=k.device)
+        st = torch.cuda.current_stream(k.device).cuda_stream
+        N.check(N.lib().lz_zeta_derivatives(self._h, int(order), k.contiguous().data_ptr(), n, out.data_ptr(),
+                                            None, st), "zeta derivatives")
+        return out
+
     def polynomial_weighted_general(self, k, alpha) -> np.ndarray:
         """M^alpha(k) = sum'_z z^alpha |z|^-nu e^{-2 pi i z.k} = d^alpha Z(k) / (-2 pi i)^|alpha|
         (complex; real for even |alpha|, imaginary for odd)."""
