@@ -30,6 +30,7 @@
 #include "special.cuh"
 
 namespace lz {
+bool atm_needs_wpart(const DevPlan& P, const DevGrid& g);
 cudaError_t launch_product_at(const DevPlan& P, int4 mult, const double* k, int64_t n, double* out, int G,
                               int* status, cudaStream_t st);
 cudaError_t launch_batch(const DevPlan& P, bool hess, const double* k, int64_t n, double* out, uint32_t flags,
@@ -824,7 +825,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                     return acc;
                 };
                 ld scale = 0.0L;
-                for (int i = 0; i <= 64 * nb; ++i) scale = std::max(scale, std::fabs(g(ld(lz::kBinWidth) * nb * i / (64.0L * nb))));
+                for (int i = 0; i <= 8 * nb; ++i) scale = std::max(scale, std::fabs(g(ld(lz::kBinWidth) * i / 8.0L)));
                 for (int b = 0; b < nb; ++b) {
                     double pc[lz::kNC];
                     const double err = lz::fit_piece_fn(g, ld(lz::kBinWidth) * b, ld(lz::kBinWidth) * (b + 1), pc);
@@ -1166,31 +1167,50 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
 // cudaFreeAsync from the device's memory pool), counters zeroed on growth and left zero by every
 // completed launch.
 struct Scratch {
-    double* wpart = nullptr;
-    unsigned int* tcount = nullptr;
-    int64_t cap = 0;
+    double* wpart = nullptr;        // [cap_w * 8][2] warp partials (only launches that need them)
+    unsigned int* tcount = nullptr; // [cap + 2]: tile counters, then the work-queue counters
+    int64_t cap = 0, cap_w = 0;
 };
 std::mutex g_scratch_mu;
 std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
 
-void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, double** wpart, unsigned int** tcount,
-                  unsigned int** work) {
+// The device's default memory pool keeps freed memory (release threshold: unlimited), so a
+// scratch re-allocation after lz_release_caches does not map new pages at every cold call.
+void keep_pool(int device) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done.insert(device).second) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
+void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, bool need_wpart, double** wpart,
+                  unsigned int** tcount, unsigned int** work) {
+    keep_pool(device);
     auto& pool = g_scratch;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
     Scratch& s = pool[std::make_pair(device, st)];
     if (s.cap < n_tiles) {
-        if (s.wpart) check_cuda(cudaFreeAsync(s.wpart, st), "cudaFreeAsync");
-        const size_t wbytes = size_t(n_tiles) * 8 * 2 * sizeof(double);
-        // tile counters, then the line kernel's two work-queue counters
+        if (s.tcount) check_cuda(cudaFreeAsync(s.tcount, st), "cudaFreeAsync");
         const size_t cbytes = (size_t(n_tiles) + 2) * sizeof(unsigned int);
         void* p = nullptr;
-        check_cuda(cudaMallocAsync(&p, wbytes + cbytes, st), "cudaMallocAsync");
-        s.wpart = static_cast<double*>(p);
-        s.tcount = reinterpret_cast<unsigned int*>(static_cast<unsigned char*>(p) + wbytes);
+        check_cuda(cudaMallocAsync(&p, cbytes, st), "cudaMallocAsync");
+        s.tcount = static_cast<unsigned int*>(p);
         check_cuda(cudaMemsetAsync(s.tcount, 0, cbytes, st), "cudaMemsetAsync");
         s.cap = n_tiles;
     }
-    *wpart = s.wpart;
+    if (need_wpart && s.cap_w < n_tiles) {
+        if (s.wpart) check_cuda(cudaFreeAsync(s.wpart, st), "cudaFreeAsync");
+        void* p = nullptr;
+        check_cuda(cudaMallocAsync(&p, size_t(n_tiles) * 8 * 2 * sizeof(double), st), "cudaMallocAsync");
+        s.wpart = static_cast<double*>(p);
+        s.cap_w = n_tiles;
+    }
+    *wpart = need_wpart ? s.wpart : nullptr;
     *tcount = s.tcount;
     *work = s.tcount + s.cap;
 }
@@ -2005,7 +2025,8 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
             full.tile_lo = full.tile_hi = 0;
             lz::DevGrid tmp;
             fill_grid(pl->d, &full, &tmp);
-            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, &dgd.wpart, &dgd.tcount, &dgd.work);
+            const bool need_wpart = pl->kind != 1 || lz::atm_needs_wpart(pl->P, dgd);
+            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, need_wpart, &dgd.wpart, &dgd.tcount, &dgd.work);
         }
         if (pl->kind == 0)
             check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");
@@ -2126,6 +2147,7 @@ int lz_release_caches(int device) {
                     cudaSetDevice(it->first.first);
                     cudaDeviceSynchronize();
                     if (it->second.wpart) cudaFree(it->second.wpart);
+                    if (it->second.tcount) cudaFree(it->second.tcount);
                     it = g_scratch.erase(it);
                 } else {
                     ++it;

@@ -2199,6 +2199,15 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     return cudaGetLastError();
 }
 
+// The ATM launch takes the line kernel for this plan and grid (launch_tile_t, d = 3)
+static bool line_eligible(const DevPlan& P, const DevGrid& g) {
+    if (P.d != 3 || !P.line_bytes || !line_mode() || g.pu != 1 || g.pv != 32) return false;
+    const size_t bytes = plan_smem_bytes(P);
+    const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
+                        size_t(line_mode()) * kLineScrBytes + 1024;
+    return need <= size_t(smem_optin()) && P.n_rec <= kLineQ && P.q0_nb >= 1 && P.q0_nb <= kQ0Max;
+}
+
 template <int D, int NCTX, bool HESS, int MODE>
 static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st) {
@@ -2206,10 +2215,7 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
-        const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
-                            size_t(line_mode()) * kLineScrBytes + 1024;
-        if (P.line_bytes && line_mode() && g.pu == 1 && g.pv == 32 && need <= size_t(smem_optin()) &&
-            P.n_rec <= kLineQ && P.q0_nb >= 1 && P.q0_nb <= kQ0Max) {
+        if (line_eligible(P, g)) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
                 case 162: return launch_tile_l<16, 2>(P, g, partials, grid_blocks, st, bytes);
@@ -2263,6 +2269,13 @@ cudaError_t launch_product(const DevPlan& P, const DevGrid& g, const int* mult, 
     LZ_CASE(3, 1) LZ_CASE(3, 2) LZ_CASE(3, 3) LZ_CASE(3, 4)
 #undef LZ_CASE
     return cudaErrorInvalidValue;
+}
+
+// Whether an ATM launch of this plan on this grid needs the warp-partial scratch (DevGrid.wpart):
+// not when the line kernel runs with whole line pairs per tile (2 npv == kTileWarps), which it
+// owns and sums directly.
+bool atm_needs_wpart(const DevPlan& P, const DevGrid& g) {
+    return !(line_eligible(P, g) && 2 * g.npv == kTileWarps);
 }
 
 cudaError_t launch_atm(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks, cudaStream_t st) {

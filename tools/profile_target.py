@@ -99,8 +99,12 @@ def e2e_breakdown():
     from paper_2504_11989_b200.epstein import epstein_context
     from paper_2504_11989_b200.quadrature import atm_plan, product_plan
     fcc = named_lattice("fcc")
+    import gc
+    from paper_2504_11989_b200 import _native as N
     for rep in range(4):
         epstein_context.cache_clear(); atm_plan.cache_clear(); product_plan.cache_clear()
+        gc.collect()
+        N.check(N.lib().lz_release_caches(0), "release caches")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         plan = atm_plan(fcc)  # plan-private contexts (in parallel) + plan build + upload
