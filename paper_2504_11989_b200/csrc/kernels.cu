@@ -688,8 +688,15 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                     if (G == 1) {
                         double cs = pc;
                         double cprev = fma(pc, c3, ps * s3);  // cos(phi - th)
+                        // skip steps of the recurrence, two per iteration in place (no register
+                        // moves), then the odd one
+                        int t = skip;
 #pragma unroll 1
-                        for (int t = 0; t < skip; ++t) {
+                        for (; t >= 2; t -= 2) {
+                            cprev = fma(two_c3, cs, -cprev);
+                            cs = fma(two_c3, cprev, -cs);
+                        }
+                        if (t) {
                             const double cn = fma(two_c3, cs, -cprev);
                             cprev = cs;
                             cs = cn;
@@ -724,6 +731,19 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                                 cprev = cs;
                                 cs = cnext;
                                 w += 2 * NWP;
+                            }
+                        } else if constexpr (NWP == 1) {
+                            // one context, one channel: a row's weights pair up in 16-byte loads
+                            // (rows start at even element offsets, even lengths) and the
+                            // recurrence advances in place: 2 points per 1 LDS.128 + 4 DFMA
+#pragma unroll 1
+                            for (int l = 0; l < len; l += 2) {
+                                const double2 w2 = ld_dir2<SMEM, CDIR>(V, w);
+                                dacc[0] = fma(w2.x, cs, dacc[0]);
+                                cprev = fma(two_c3, cs, -cprev);
+                                dacc[0] = fma(w2.y, cprev, dacc[0]);
+                                cs = fma(two_c3, cprev, -cs);
+                                w += 2;
                             }
                         } else {
 #pragma unroll 1
