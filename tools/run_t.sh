@@ -1,3 +1,8 @@
 mkdir -p gpurun_out
-LATSUM_LIB=paper_2504_11989_b200/_lib_ab/c1a.so timeout 900 python -m pytest tests/test_gpu_zeta.py tests/test_gpu_properties.py -q -m gpu -x > gpurun_out/c1a_pytest.log 2>&1; echo rc=$? >> gpurun_out/c1a_pytest.log
-for r in 1 2; do for v in c1base c1a; do echo "== $v" >> gpurun_out/c1ab.log; LATSUM_LIB=paper_2504_11989_b200/_lib_ab/$v.so timeout 300 python tools/profile_target.py c1_time >> gpurun_out/c1ab.log 2>&1; done; done
+for v in prev head; do
+  if [ $v = head ]; then lib=""; else lib=paper_2504_11989_b200/_lib_ab/$v.so; fi
+  LATSUM_LIB=$lib timeout 300 python tools/profile_target.py atm > /dev/null 2>&1
+  LATSUM_LIB=$lib timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_kernel -c 1 -o /tmp/seg_$v -f python tools/profile_target.py atm > gpurun_out/seg_$v.log 2>&1
+  ncu -i /tmp/seg_$v.ncu-rep --page raw --csv > gpurun_out/seg_${v}_raw.csv 2>/dev/null
+  ncu -i /tmp/seg_$v.ncu-rep --page source --csv --print-source sass > gpurun_out/seg_${v}_sass.csv 2>/dev/null
+done
