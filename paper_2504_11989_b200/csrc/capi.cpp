@@ -141,6 +141,23 @@ struct HostPlan {
 
 using ld = long double;
 
+// LATSUM_TIMING=1: host phase times on stderr (tuning aid for the cold end-to-end path)
+struct PhaseTimer {
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    bool on;
+    explicit PhaseTimer(const char* w) : what(w), t0(std::chrono::steady_clock::now()), on(enabled()) {}
+    static bool enabled() {
+        static const bool e = std::getenv("LATSUM_TIMING") != nullptr;
+        return e;
+    }
+    ~PhaseTimer() {
+        if (on)
+            std::fprintf(stderr, "  %-22s %.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 // Union of integer point sets (keeps the order of the first, appends the rest).
 // lattice coordinates packed into one 64-bit key (16 bits per axis, d <= 4)
 uint64_t pack_key(int d, const double* n) {
@@ -1380,7 +1397,10 @@ int lz_ctx_create(const lz_ctx_params* p, int device, lz_ctx** out) {
     *out = nullptr;
     lz_ctx* c = new lz_ctx();
     int rc = guarded([&] {
-        lz::build_context(p->d, p->a, p->nu, p->splitting, p->deriv_order, &c->h);
+        {
+            PhaseTimer pt("ctx build_context");
+            lz::build_context(p->d, p->a, p->nu, p->splitting, p->deriv_order, &c->h);
+        }
         c->device = device;
         if (device >= 0) {
             int n = 0;
@@ -1979,9 +1999,13 @@ int lz_plan_create_atm(const lz_ctx* z3, const lz_ctx* z5, lz_plan** out) {
         pl->kind = 1;
         if (std::fabs(z5->h.k.nu - z3->h.k.nu - 2.0) > 1e-12)
             throw Error{LZ_EINVAL, "ATM plan needs exponents nu and nu + 2 (Z_3 and the Hessian of Z_5)"};
-        build_host_plan({&z3->h}, &z5->h, &pl->hp, /*trace_z=*/true);
+        {
+            PhaseTimer pt("atm build_host_plan");
+            build_host_plan({&z3->h}, &z5->h, &pl->hp, /*trace_z=*/true);
+        }
         if (!pl->hp.alias_fp) throw Error{LZ_EINVAL, "ATM plan: F' alias expected"};
         if (pl->device >= 0) {
+            PhaseTimer pt("atm upload_plan");
             DeviceGuard dg(pl->device);
             pl->P = upload_plan(pl->hp, &pl->allocs);
         }
@@ -2014,6 +2038,7 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
         DeviceGuard dg(pl->device);
         lz::DevGrid dgd;
         fill_grid(pl->d, g, &dgd);
+        PhaseTimer pt_ga("integrate grid+scratch");
         const GridArrays& ga = grid_arrays(pl, g);
         dgd.u = ga.u;
         dgd.wu = ga.wu;

@@ -757,34 +757,50 @@ void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t)>& 
 void gauss_legendre(int n, std::vector<double>* xs, std::vector<double>* ws) {
     xs->assign(n, 0.0);
     ws->assign(n, 0.0);
-    for (int i = 0; i < n; ++i) {
+    // Bonnet recurrence P_k = a_k x P_{k-1} - b_k P_{k-2} with a_k = (2k-1)/k, b_k = (k-1)/k
+    // precomputed (no division per step); the nodes are symmetric, so only the upper half is
+    // iterated (Newton from the Tricomi guess), x_{n-1-i} = -x_i
+    std::vector<ld> ak(size_t(n) + 1, 0.0L), bk(size_t(n) + 1, 0.0L);
+    for (int k = 2; k <= n; ++k) {
+        ak[size_t(k)] = (2.0L * k - 1.0L) / k;
+        bk[size_t(k)] = (k - 1.0L) / k;
+    }
+    auto legendre = [&](ld x, ld* pn, ld* pn1) {
+        ld p0 = 1.0L, p1 = x;
+        for (int k = 2; k <= n; ++k) {
+            const ld p2 = ak[size_t(k)] * x * p1 - bk[size_t(k)] * p0;
+            p0 = p1;
+            p1 = p2;
+        }
+        if (n == 1) {
+            p1 = x;
+            p0 = 1.0L;
+        }
+        *pn = p1;
+        *pn1 = p0;
+    };
+    for (int i = 0; i < (n + 1) / 2; ++i) {
         ld x = std::cos(kPiL * (i + 0.75L) / (n + 0.5L));
-        ld dp = 0.0L;
+        ld p1 = 0.0L, p0 = 0.0L, dp = 0.0L;
         for (int it = 0; it < 100; ++it) {
-            ld p0 = 1.0L, p1 = x;
-            for (int k = 2; k <= n; ++k) {
-                ld p2 = ((2.0L * k - 1.0L) * x * p1 - (k - 1.0L) * p0) / k;
-                p0 = p1;
-                p1 = p2;
-            }
-            if (n == 1) { p1 = x; p0 = 1.0L; }
+            legendre(x, &p1, &p0);
             dp = n * (x * p1 - p0) / (x * x - 1.0L);
-            ld dx = p1 / dp;
+            const ld dx = p1 / dp;
             x -= dx;
             // relative test: an absolute one never triggers near +-1 in long double
             if (std::fabs(dx) <= 4e-19L * std::fabs(x) || it > 20) break;
         }
-        ld p0 = 1.0L, p1 = x;
-        for (int k = 2; k <= n; ++k) {
-            ld p2 = ((2.0L * k - 1.0L) * x * p1 - (k - 1.0L) * p0) / k;
-            p0 = p1;
-            p1 = p2;
-        }
-        if (n == 1) { p1 = x; p0 = 1.0L; }
+        if (2 * i + 1 == n) x = 0.0L;  // the middle node of an odd rule
+        legendre(x, &p1, &p0);
         dp = n * (x * p1 - p0) / (x * x - 1.0L);
+        const double w = double(2.0L / ((1.0L - x * x) * dp * dp));
         // ascending order (numpy leggauss order)
         (*xs)[n - 1 - i] = double(x);
-        (*ws)[n - 1 - i] = double(2.0L / ((1.0L - x * x) * dp * dp));
+        (*ws)[n - 1 - i] = w;
+        if (2 * i + 1 != n) {
+            (*xs)[i] = -double(x);
+            (*ws)[i] = w;
+        }
     }
 }
 

@@ -105,11 +105,6 @@ class EpsteinContext:
         self.rfac = info.rfac
         self.bconst = info.bconst
         self.kmax = info.kmax
-        self._bz = lattice.brillouin_zone()
-        self.dir_pts = self._points(0).reshape(-1, d)
-        self.dir_w = self._points(1)
-        self.rec_pts = self._points(2).reshape(-1, d)
-        self.rec_norm2 = np.einsum("ij,ij->i", self.rec_pts, self.rec_pts)
         # Hessian point sets and tables are built on first use; deriv_order < 0 marks the ATM
         # plan's private contexts (-1: reciprocal set only, -2: Hessian sets only)
         self.has_hessian = deriv_order >= 2 or deriv_order == -2
@@ -129,6 +124,31 @@ class EpsteinContext:
         info = N.CtxInfo()
         N.lib().lz_ctx_get_info(self._h, C.byref(info))
         return info
+
+    # the reference's point-set attributes (L/epstein.py:126-198), fetched from the native
+    # context on first access (plan-private contexts never need them)
+    @property
+    def dir_pts(self) -> np.ndarray:
+        return self._cached("_dir_pts", lambda: self._points(0).reshape(-1, self.d))
+
+    @property
+    def dir_w(self) -> np.ndarray:
+        return self._cached("_dir_w", lambda: self._points(1))
+
+    @property
+    def rec_pts(self) -> np.ndarray:
+        return self._cached("_rec_pts", lambda: self._points(2).reshape(-1, self.d))
+
+    @property
+    def rec_norm2(self) -> np.ndarray:
+        return self._cached("_rec_norm2", lambda: np.einsum("ij,ij->i", self.rec_pts, self.rec_pts))
+
+    def _cached(self, name, make):
+        v = self.__dict__.get(name)
+        if v is None:
+            v = make()
+            self.__dict__[name] = v
+        return v
 
     def _points(self, which):
         n = C.c_int64(0)

@@ -107,6 +107,16 @@ def e2e_breakdown():
         N.check(N.lib().lz_release_caches(0), "release caches")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        if os.environ.get("SPLIT_PLAN"):
+            from paper_2504_11989_b200.epstein import EpsteinContext as EC
+            from paper_2504_11989_b200.quadrature import ATM_SPLIT_SCALE
+            sp = ATM_SPLIT_SCALE * fcc.volume ** (-2.0 / 3)
+            ta = time.perf_counter()
+            z5 = EC(fcc, 5.0, sp, -2)
+            tb = time.perf_counter()
+            z3 = EC(fcc, 3.0, sp, deriv_order=-1)
+            tc = time.perf_counter()
+            print(f"  ctx z5 {1e3*(tb-ta):.2f} ms, ctx z3 {1e3*(tc-tb):.2f} ms (serial)")
         plan = atm_plan(fcc)  # plan-private contexts (in parallel) + plan build + upload
         t1 = time.perf_counter()
         s = ShardedIntegral(plan, 128, 128, 3)
