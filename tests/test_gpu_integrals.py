@@ -381,3 +381,52 @@ def test_product_at_matches_zeta_products():
         for nu, m in groups:
             ref = ref * EpsteinContext(lat, nu, device=0).zeta(k) ** m
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), name
+
+
+@pytest.mark.gpu
+def test_product_at_edge_cases():
+    """Empty batches, pole detection at k in the reciprocal lattice (nu = d), and the ATM plan
+    rejected by lz_plan_product_at."""
+    import ctypes as C
+    import torch
+    from paper_2504_11989_b200 import _native as N
+    from paper_2504_11989_b200.quadrature import product_plan
+    sq = named_lattice("square")
+    plan = product_plan(sq, ((3.0, 2),))
+    assert plan.product_at(torch.zeros((0, 2), dtype=torch.float64, device="cuda")).numel() == 0
+    pole = product_plan(sq, ((2.0, 1), (3.0, 1)))   # nu = d: pole at k in the reciprocal lattice
+    k = torch.tensor([[0.1, 0.2], [1.0, 0.0]], dtype=torch.float64, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().lz_plan_product_at(pole.handle, k.data_ptr(), 2, out.data_ptr(), st.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream), "product at")
+    torch.cuda.synchronize()
+    assert int(st.item()) & 1
+    with pytest.raises(ValueError):
+        atm_plan(named_lattice("fcc")).product_at(k[:, :1].repeat(1, 3).contiguous())
+
+
+@pytest.mark.gpu
+def test_derivatives_device_matches_host_path():
+    """EpsteinContext.derivatives_device (device pointers, stream-ordered) equals the host-buffer
+    entry point bit for bit, for the compile-time (order 3) and moment (order 7, d = 4) kernels."""
+    import torch
+    from paper_2504_11989_b200 import Lattice
+    lat4 = Lattice(np.array([[1.0, 0.2, 0.0, 0.1], [0.0, 1.1, 0.3, 0.0], [0.0, 0.0, 0.9, 0.2],
+                             [0.1, 0.0, 0.0, 1.0]]))
+    for lat, nu, m in ((named_lattice("fcc"), 5.0, 3), (lat4, 6.0, 7)):
+        k = np.random.default_rng(5).uniform(-0.4, 0.4, size=(300, lat.d)) @ lat.a_inv_t.T
+        ctx = EpsteinContext(lat, nu, device=0)
+        _, host = ctx.derivatives(k, m)
+        dev = ctx.derivatives_device(torch.tensor(k, device="cuda"), m).cpu().numpy()
+        assert np.array_equal(host, dev)
+        assert ctx.derivatives_device(torch.zeros((0, lat.d), dtype=torch.float64, device="cuda"), m).shape[0] == 0
+
+
+@pytest.mark.gpu
+def test_device_taylor_table_trivial_branch():
+    """Trivial branch (nu in -2N0): Z_reg is the constant Z(nu, 0) (L/epstein.py:371-375)."""
+    ctx = EpsteinContext(named_lattice("square"), -2.0, device=0)
+    tab = ctx.reg_derivatives(6)
+    assert tab.derivs[(0, 0)] == ctx.const_value
+    assert all(v == 0.0 for a, v in tab.derivs.items() if sum(a) > 0)
