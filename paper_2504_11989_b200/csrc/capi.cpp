@@ -242,6 +242,7 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
     const size_t np = hp->dir_n.size() / d;
     if (np == 0) return fail("empty direct set");
     if (np >= 65535) return fail("too many points");
+    const auto t_line0 = std::chrono::steady_clock::now();
     std::vector<std::array<double, 3>> v(np);
     int sign = 0;
     for (size_t i = 0; i < np; ++i) {
@@ -266,6 +267,7 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         std::memcpy(out.data() + off, p, bytes);
         return int(off);
     };
+    const auto t_line1 = std::chrono::steady_clock::now();
     struct AxisBlock {
         std::vector<uint16_t> idx;
         std::vector<uint8_t> code, glo;
@@ -273,7 +275,8 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         int K = 0, P = 0;
     };
     AxisBlock blk[3];
-    for (int ax = 0; ax < 3; ++ax) {
+    const char* why[3] = {nullptr, nullptr, nullptr};
+    auto axis_job = [&](int ax) {
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
         std::vector<std::vector<std::array<long, 3>>> planes;  // (nb, nc, index) per plane m
         for (size_t i = 0; i < np; ++i) {
@@ -286,12 +289,12 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
             planes[size_t(n[ax])].push_back({n[b], n[c], long(i)});
         }
         const int P = int(planes.size());
-        if (P > lz::kLinePlanes) return fail("too many planes");
+        if (P > lz::kLinePlanes) { why[ax] = "too many planes"; return; }
         std::vector<int> L(P, 0);
         int used = 0;
         for (int p = 0; p < P; ++p)
             if (!planes[p].empty()) L[p] = 1, ++used;
-        if (used > 32) return fail("more planes than lanes");
+        if (used > 32) { why[ax] = "more planes than lanes"; return; }
         auto load = [&](int p) { return L[p] ? (long(planes[p].size()) + L[p] - 1) / L[p] : 0L; };
         for (; used < 32; ++used) {
             int best = 0;
@@ -326,7 +329,7 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
                     const auto& pt = pts[q];
                     idx[sl] = uint16_t(pt[2]);
                     if (q == lo) {
-                        if (std::labs(pt[0]) > 32767 || std::labs(pt[1]) > 32767) return fail("coordinates");
+                        if (std::labs(pt[0]) > 32767 || std::labs(pt[1]) > 32767) { why[ax] = "coordinates"; return; }
                         init[ln] = int32_t((uint32_t(uint16_t(int16_t(pt[0]))) << 16) | uint16_t(int16_t(pt[1])));
                     } else {
                         const long dnb = pt[0] - pts[q - 1][0], dnc = pt[1] - pts[q - 1][1];
@@ -335,7 +338,7 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
                         } else if (dnb == 1 && dnc <= 0 && dnc >= -30) {
                             code[sl] = uint8_t(1 - dnc);
                         } else {
-                            return fail("row step out of range");
+                            { why[ax] = "row step out of range"; return; }
                         }
                     }
                 }
@@ -349,7 +352,12 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         blk[ax].init.swap(init);
         blk[ax].K = int(K);
         blk[ax].P = P;
+        };
+    for (int ax = 0; ax < 3; ++ax) {
+        axis_job(ax);
+        if (why[ax]) return fail(why[ax]);
     }
+    const auto t_line2 = std::chrono::steady_clock::now();
     // Bank-aware order of the v records: a 24-byte record at position pos starts in bank pair
     // 6 pos mod 32, i.e. its bank depends on pos mod 16.  The 32 lanes of every (axis, slot)
     // gather 32 records; residues pos mod 16 are chosen so that no residue occurs more than
@@ -438,6 +446,12 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
     }
     out.resize((out.size() + 15) & ~size_t(15), 0);
     hp->line.swap(out);
+    if (PhaseTimer::enabled()) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "  line: records %.3f ms, lane slots %.3f ms, bank order + image %.3f ms\n",
+                     ms(t_line0, t_line1), ms(t_line1, t_line2), ms(t_line2, t3));
+    }
     if (dbg)
         std::fprintf(stderr, "line block: %zu points, K = %d/%d/%d, planes = %d/%d/%d, %zu bytes\n", np,
                      hp->line_K[0], hp->line_K[1], hp->line_K[2], hp->line_P[0], hp->line_P[1], hp->line_P[2],
@@ -519,6 +533,79 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         table_job = std::async(std::launch::async, [&hp, p, sc, nf, c, x_lo_tab, rp] {
             lz::build_table(p, sc, nf, double(c), x_lo_tab, rp, &hp->tab);
         });
+    // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives) and the line kernel's
+    // pieces of the Hessian rows: they depend only on the contexts' constants, so they are
+    // prepared on a helper thread while the point sets are merged
+    std::future<void> q0_job = std::async(std::launch::async, [&]     {
+        const int rows = hp->nctx + (hess ? 2 : 0);
+        hp->t0c.assign(size_t(std::max(rows, 1)) * lz::kT0, 0.0);
+        std::vector<ld> a(lz::kT0 + 2);
+        // series region: x = c rho <= max(2, x_lo) (and never beyond the BZ box); outside it
+        // the kernel uses the tables, so the alternating series never cancels by more than e^2
+        const ld c_l = ld(lz::kPi) / ld(first->k.split);
+        const ld x_ser = std::max(2.0L, ld(lz::table_x_lo(*first)) * 1.0001L);
+        ld rho_max = std::min(ld(first->kmax) * ld(first->kmax) * (1.0L + 1e-9L), x_ser / c_l);
+        int need = 0;
+        bool ok = true;
+        auto fill = [&](const lz::CtxConst& k, int row, int deriv) {
+            for (int n = 0; n < lz::kT0 + 2; ++n) a[n] = lz::t0_coeff(k, n);
+            ld big = 0.0L;
+            std::vector<ld> cf(lz::kT0);
+            for (int n = 0; n < lz::kT0; ++n) {
+                ld v = a[n + deriv];
+                for (int j = 1; j <= deriv; ++j) v *= ld(n + j);
+                cf[n] = v;
+                big = std::max(big, std::fabs(v) * std::pow(rho_max, ld(n)));
+            }
+            int used = lz::kT0;
+            while (used > 1 && std::fabs(cf[used - 1]) * std::pow(rho_max, ld(used - 1)) <= 1e-19L * std::max(big, 1.0L))
+                --used;
+            if (used >= lz::kT0 - 2) ok = false;  // not converged within kT0 terms: disable
+            need = std::max(need, used + 2);
+            for (int n = 0; n < lz::kT0; ++n) hp->t0c[size_t(row) * lz::kT0 + n] = double(cf[n]);
+        };
+        for (int j = 0; j < hp->nctx; ++j)
+            if (plain[j]->k.branch != lz::kTrivial) fill(plain[j]->k, j, 0);
+        if (hess) {
+            fill(hess->k, hp->nctx, 1);
+            fill(hess->k, hp->nctx + 1, 2);
+        }
+        hp->n_t0 = std::min(need, lz::kT0);
+        hp->t0_rho_max = ok ? double(rho_max) : -1.0;
+        // the Hessian rows as pieces (line kernel): series evaluated in long double at the
+        // Chebyshev nodes of each bin; kept only if every piece meets 1e-15 of the row's scale
+        hp->q0tab.clear();
+        hp->q0_nb = 0;
+        if (hess && ok) {
+            const int nb = int(std::ceil(double(c_l * rho_max / ld(lz::kBinWidth)) - 1e-12));
+            const int ps = lz::piece_stride(2);
+            std::vector<double> tab(size_t(nb) * ps, 0.0);
+            bool fit_ok = nb > 0;
+            for (int row = 0; row < 2 && fit_ok; ++row) {
+                const double* cf = &hp->t0c[size_t(hp->nctx + row) * lz::kT0];
+                auto g = [&](ld x) {
+                    const ld r = x / c_l;
+                    ld acc = 0.0L;
+                    for (int n = lz::kT0 - 1; n >= 0; --n) acc = acc * r + ld(cf[n]);
+                    return acc;
+                };
+                ld scale = 0.0L;
+                for (int i = 0; i <= 8 * nb; ++i) scale = std::max(scale, std::fabs(g(ld(lz::kBinWidth) * i / 8.0L)));
+                for (int b = 0; b < nb; ++b) {
+                    double pc[lz::kNC];
+                    const double err = lz::fit_piece_fn(g, ld(lz::kBinWidth) * b, ld(lz::kBinWidth) * (b + 1), pc);
+                    if (err > 1e-15 * double(scale)) fit_ok = false;
+                    for (int m = 0; m < 8; ++m) tab[size_t(b) * ps + row * 8 + m] = pc[m];
+                    tab[size_t(b) * ps + 16 + row] = pc[8];
+                }
+            }
+            if (fit_ok) {
+                hp->q0tab.swap(tab);
+                hp->q0_nb = nb;
+                hp->q0_inv_h = double(c_l / ld(lz::kBinWidth));
+            }
+        }
+    });
     // LATSUM_TIMING=1: host phase times of the plan build on stderr (tuning aid)
     const bool timing = std::getenv("LATSUM_TIMING") != nullptr;
     auto tprev = std::chrono::steady_clock::now();
@@ -787,77 +874,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             for (int a = 0; a < d; ++a) hp->rq_pad[i * qs + a] = hp->rec_q[i * d + a];
     }
     lap("reciprocal sort");
-    // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives)
-    {
-        const int rows = hp->nctx + (hess ? 2 : 0);
-        hp->t0c.assign(size_t(std::max(rows, 1)) * lz::kT0, 0.0);
-        std::vector<ld> a(lz::kT0 + 2);
-        // series region: x = c rho <= max(2, x_lo) (and never beyond the BZ box); outside it
-        // the kernel uses the tables, so the alternating series never cancels by more than e^2
-        const ld c_l = ld(lz::kPi) / ld(first->k.split);
-        const ld x_ser = std::max(2.0L, ld(lz::table_x_lo(*first)) * 1.0001L);
-        ld rho_max = std::min(ld(first->kmax) * ld(first->kmax) * (1.0L + 1e-9L), x_ser / c_l);
-        int need = 0;
-        bool ok = true;
-        auto fill = [&](const lz::CtxConst& k, int row, int deriv) {
-            for (int n = 0; n < lz::kT0 + 2; ++n) a[n] = lz::t0_coeff(k, n);
-            ld big = 0.0L;
-            std::vector<ld> cf(lz::kT0);
-            for (int n = 0; n < lz::kT0; ++n) {
-                ld v = a[n + deriv];
-                for (int j = 1; j <= deriv; ++j) v *= ld(n + j);
-                cf[n] = v;
-                big = std::max(big, std::fabs(v) * std::pow(rho_max, ld(n)));
-            }
-            int used = lz::kT0;
-            while (used > 1 && std::fabs(cf[used - 1]) * std::pow(rho_max, ld(used - 1)) <= 1e-19L * std::max(big, 1.0L))
-                --used;
-            if (used >= lz::kT0 - 2) ok = false;  // not converged within kT0 terms: disable
-            need = std::max(need, used + 2);
-            for (int n = 0; n < lz::kT0; ++n) hp->t0c[size_t(row) * lz::kT0 + n] = double(cf[n]);
-        };
-        for (int j = 0; j < hp->nctx; ++j)
-            if (plain[j]->k.branch != lz::kTrivial) fill(plain[j]->k, j, 0);
-        if (hess) {
-            fill(hess->k, hp->nctx, 1);
-            fill(hess->k, hp->nctx + 1, 2);
-        }
-        hp->n_t0 = std::min(need, lz::kT0);
-        hp->t0_rho_max = ok ? double(rho_max) : -1.0;
-        // the Hessian rows as pieces (line kernel): series evaluated in long double at the
-        // Chebyshev nodes of each bin; kept only if every piece meets 1e-15 of the row's scale
-        hp->q0tab.clear();
-        hp->q0_nb = 0;
-        if (hess && ok) {
-            const int nb = int(std::ceil(double(c_l * rho_max / ld(lz::kBinWidth)) - 1e-12));
-            const int ps = lz::piece_stride(2);
-            std::vector<double> tab(size_t(nb) * ps, 0.0);
-            bool fit_ok = nb > 0;
-            for (int row = 0; row < 2 && fit_ok; ++row) {
-                const double* cf = &hp->t0c[size_t(hp->nctx + row) * lz::kT0];
-                auto g = [&](ld x) {
-                    const ld r = x / c_l;
-                    ld acc = 0.0L;
-                    for (int n = lz::kT0 - 1; n >= 0; --n) acc = acc * r + ld(cf[n]);
-                    return acc;
-                };
-                ld scale = 0.0L;
-                for (int i = 0; i <= 8 * nb; ++i) scale = std::max(scale, std::fabs(g(ld(lz::kBinWidth) * i / 8.0L)));
-                for (int b = 0; b < nb; ++b) {
-                    double pc[lz::kNC];
-                    const double err = lz::fit_piece_fn(g, ld(lz::kBinWidth) * b, ld(lz::kBinWidth) * (b + 1), pc);
-                    if (err > 1e-15 * double(scale)) fit_ok = false;
-                    for (int m = 0; m < 8; ++m) tab[size_t(b) * ps + row * 8 + m] = pc[m];
-                    tab[size_t(b) * ps + 16 + row] = pc[8];
-                }
-            }
-            if (fit_ok) {
-                hp->q0tab.swap(tab);
-                hp->q0_nb = nb;
-                hp->q0_inv_h = double(c_l / ld(lz::kBinWidth));
-            }
-        }
-    }
+    q0_job.get();  // q = 0 series and pieces (started with the table fit)
     lap("q=0 series");
     if (!table_job.valid()) {
         hp->tab = lz::HostTable();
