@@ -269,20 +269,30 @@ def product_plan(lattice: Lattice, nus_key: tuple, splitting: float | None = Non
 ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "0.13"))
 
 
+_HELPER = None
+
+
+def _helper():
+    global _HELPER
+    if _HELPER is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _HELPER = ThreadPoolExecutor(max_workers=1, thread_name_prefix="latsum-plan")
+    return _HELPER
+
+
 @lru_cache(maxsize=64)
 def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
     """Plan for the ATM integrand [Z_3^3, tr(M_5^3)], M_5 = polynomial-weighted zeta at nu = 5."""
     if splitting is None and ATM_SPLIT_SCALE != 1.0:
         splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
     # the two contexts' host enumerations are independent native calls (GIL released): overlap them
-    from concurrent.futures import ThreadPoolExecutor
+    # (one helper thread, kept for the process)
     # Both contexts are private to this (cached) plan and enumerate only what it reads: Z_3 lends
     # its constants and reciprocal set (the kernel takes Z_3 = tr M_5), Z_5 its constants and the
     # Hessian's widened point sets
-    with ThreadPoolExecutor(max_workers=2) as pool:
-        f5 = pool.submit(EpsteinContext, lattice, 5.0, splitting, -2)
-        z3 = EpsteinContext(lattice, 3.0, splitting, deriv_order=-1)
-        z5 = f5.result()
+    f5 = _helper().submit(EpsteinContext, lattice, 5.0, splitting, -2)
+    z3 = EpsteinContext(lattice, 3.0, splitting, deriv_order=-1)
+    z5 = f5.result()
     h = C.c_void_p()
     N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)), "atm plan")
     return Plan(h, lattice.d, 2, (z3, z5))
