@@ -804,7 +804,10 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                 if (ri < rows.size() && rows[ri].j == j) {
                     const Row& r = rows[ri++];
                     const long lo = r.pts.front().first, hi = r.pts.back().first;
-                    const long len = hi - lo + 1, lenp = len + (len & 1), skip = lo - l0;
+                    // rows padded to even length (16-byte pairs of points), to a multiple of 4
+                    // for one-channel plans (the kernel's plain-zeta row loop takes 4 points per step)
+                    const long len = hi - lo + 1, skip = lo - l0;
+                    const long lenp = hp->nw == 1 ? (len + 3) & ~3L : len + (len & 1);
                     if (lenp > 65535 || skip > 65535) throw Error{LZ_EINVAL, "direct row too long"};
                     const size_t row0 = wts_out.size() / hp->nw;
                     if (row0 > size_t(INT32_MAX)) throw Error{LZ_EINVAL, "direct set too large"};

@@ -733,18 +733,31 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                                 w += 2 * NWP;
                             }
                         } else if constexpr (NWP == 1) {
-                            // one context, one channel: a row's weights pair up in 16-byte loads
-                            // (rows start at even element offsets, even lengths) and the
-                            // recurrence advances in place: 2 points per 1 LDS.128 + 4 DFMA
+                            // one context, one channel: rows are padded to a multiple of 4 points
+                            // (zero weights; capi.cpp build_host_plan).  Even and odd points run
+                            // as two independent recurrences with step 2 theta
+                            // (cos(a + 2 th) = 2 cos 2th cos a - cos(a - 2 th)) into two
+                            // accumulators, so the latency chain per point halves; 16-byte weight
+                            // pairs, registers advanced in place
+                            const double two_c6 = fma(4.0 * c3, c3, -2.0);  // 2 cos 2 theta
+                            double e = cs, o = fma(two_c3, cs, -cprev);     // cos(phi + 0 th), (+1 th)
+                            double ep = fma(two_c3, cprev, -cs), op = cprev;  // (-2 th), (-1 th)
+                            double acc_o = 0.0;
 #pragma unroll 1
-                            for (int l = 0; l < len; l += 2) {
-                                const double2 w2 = ld_dir2<SMEM, CDIR>(V, w);
-                                dacc[0] = fma(w2.x, cs, dacc[0]);
-                                cprev = fma(two_c3, cs, -cprev);
-                                dacc[0] = fma(w2.y, cprev, dacc[0]);
-                                cs = fma(two_c3, cprev, -cs);
-                                w += 2;
+                            for (int l = 0; l < len; l += 4) {
+                                const double2 wa = ld_dir2<SMEM, CDIR>(V, w);
+                                const double2 wb = ld_dir2<SMEM, CDIR>(V, w + 2);
+                                dacc[0] = fma(wa.x, e, dacc[0]);
+                                acc_o = fma(wa.y, o, acc_o);
+                                ep = fma(two_c6, e, -ep);  // + 2 th
+                                op = fma(two_c6, o, -op);  // + 3 th
+                                dacc[0] = fma(wb.x, ep, dacc[0]);
+                                acc_o = fma(wb.y, op, acc_o);
+                                e = fma(two_c6, ep, -e);   // + 4 th
+                                o = fma(two_c6, op, -o);   // + 5 th
+                                w += 4;
                             }
+                            dacc[0] += acc_o;
                         } else {
 #pragma unroll 1
                             for (int l = 0; l < len; l += 2) {
