@@ -67,10 +67,9 @@ struct View {
     uint32_t s_cnt;        // line kernel: count table cnt[i] = #{q : |q| <= i h} (kCntEntries int32)
     uint32_t s_q0;         // line kernel: the Hessian's q = 0 pieces (kQ0Max x piece_stride(2) doubles)
     double cnt_inv_h;      // 1 / h
-    // line kernel: warp-uniform reads from the kernel's parameter space (LineParam): the
-    // reciprocal vectors (padded stride) and the Hessian's two q = 0 series rows
+    // line kernel: warp-uniform reads of the reciprocal vectors (padded stride) from the kernel's
+    // parameter space (LineParam)
     const double* p_rq;
-    const double* p_t0;
     const double* dir;     // direct-space block (DevPlan::direct)
     const double* rec_q;
     const double* rec_norm;
@@ -1248,14 +1247,11 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 //   hh = sum_n W_n cos 2 pi kappa.n = sum_m Re[e^{2 pi i x m} C_m].
 // Phase 1: lane l sums its slots (a contiguous row-major slice of one plane, weights gathered by
 // point index) with the phase carried by complex rotation from slot to slot (step factors from a
-// per-warp table); phase 2:
-// fixed-order reduction of each plane over its lane group in shared memory; phase 3: per lane,
-// one complex rotation per plane.
-constexpr int kLineScrStride = 33;                        // doubles per channel row (bank skew)
+// per-warp table); phase 2: fixed-order segmented shuffle reduction of each plane over its lane
+// group; phase 3: per lane, one complex rotation per plane.
 // per-warp scratch: the step table [32] (phase 1) / C_m [planes][12] from 0, the mirror node's
 // direct-space channels [6][32] doubles from 1536, the line pair's constants (9 doubles) from 3072
 constexpr uint32_t kLineScrBytes = 3072u + 80u;
-constexpr int kLineJobs = (12 * kLinePlanes + 31) / 32;   // reduction jobs per lane
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
 // scratch as [m][12] doubles, valid until the next call.
