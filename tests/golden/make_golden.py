@@ -324,17 +324,47 @@ def taylor_high(ref):
     return out
 
 
+# lattices without the catalog's symmetry for the ATM goldens (line kernel on a generic cell)
+TRICLINIC = [[1.0, 0.15, 0.25], [0.0, 1.1, 0.3], [0.05, 0.0, 0.95]]
+OBLIQUE = [[1.0, 0.35], [0.0, 0.9]]
+
+
+def atm_generic(ref, threads):
+    """ATM energies (Prop. 2.4: the three continued integrals of the reference's own adaptive
+    route) on the hexagonal lattice and on lattices without symmetry (triclinic 3D, oblique 2D)."""
+    Q = ref.quadrature
+    out = {"generator": "tests/golden/make_golden.py --atm-generic", "threads": threads}
+    for name, lat in (("hexagonal", ref.named_lattice("hexagonal")),
+                      ("oblique", ref.Lattice(np.array(OBLIQUE))),
+                      ("triclinic", ref.Lattice(np.array(TRICLINIC)))):
+        rec = {}
+        for key, nus in (("z333", (3, 3, 3)), ("zm155", (-1, 5, 5)), ("z135", (1, 3, 5))):
+            t = time.time()
+            v, e = Q.integrate_product(lat, nus, threads=threads)
+            rec[key] = v
+            rec[key + "_err"] = e
+            rec[key + "_seconds"] = time.time() - t
+            print(name, key, v, e, time.time() - t, flush=True)
+        rec["atm"] = rec["z333"] / 24 - 3 * rec["zm155"] / 16 + 3 * rec["z135"] / 8
+        out[name] = rec
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true")
     ap.add_argument("--near-d", action="store_true")
     ap.add_argument("--taylor", action="store_true")
+    ap.add_argument("--atm-generic", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     ref = load_reference()
     if args.slow:
         res = slow(ref, args.threads)
         path = os.path.join(HERE, "golden_integrals.json")
+    elif args.atm_generic:
+        res = atm_generic(ref, args.threads)
+        path = os.path.join(HERE, "golden_atm_generic.json")
     elif args.taylor:
         res = taylor_high(ref)
         path = os.path.join(HERE, "golden_taylor.json")

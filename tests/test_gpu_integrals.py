@@ -430,3 +430,29 @@ def test_device_taylor_table_trivial_branch():
     tab = ctx.reg_derivatives(6)
     assert tab.derivs[(0, 0)] == ctx.const_value
     assert all(v == 0.0 for a, v in tab.derivs.items() if sum(a) > 0)
+
+
+def _golden_atm_generic():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_atm_generic.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["hexagonal", "oblique", "triclinic"])
+def test_atm_generic_lattices(name):
+    """The fused ATM kernels (d = 2 tile kernel, d = 3 line kernel) on lattices without the
+    catalog's symmetry, and the Prop. 2.4 adaptive route, against the reference's own Prop. 2.4
+    energies (tests/golden/make_golden.py --atm-generic)."""
+    from paper_2504_11989_b200 import Lattice
+    g = _golden_atm_generic()[name]
+    mats = {"oblique": [[1.0, 0.35], [0.0, 0.9]],
+            "triclinic": [[1.0, 0.15, 0.25], [0.0, 1.1, 0.3], [0.05, 0.0, 0.95]]}
+    lat = named_lattice(name) if name == "hexagonal" else Lattice(np.array(mats[name]))
+    res = atm_integrals(lat, ATMGrid(128, 128, 3))
+    assert abs(res.energy - g["atm"]) <= 1e-10 * abs(g["atm"]), (res.energy, g["atm"])
+    cfg = QuadratureConfig(method="adaptive")
+    for key, nus in (("z333", (3, 3, 3)), ("zm155", (-1, 5, 5)), ("z135", (1, 3, 5))):
+        v, _ = integrate_product(lat, nus, cfg)
+        assert abs(v - g[key]) <= max(1e-12 * abs(g[key]), 2 * g[key + "_err"]), (key, v, g[key])
