@@ -1874,8 +1874,6 @@ const lz::DevDeriv& ensure_deriv_g(const lz_ctx* cc, int order, int taylor, int 
         P.hmom = upload(hmom, &c->allocs);
         P.hcoef = upload(hcoef, &c->allocs);
         if (taylor) P.add = upload(add, &c->allocs);
-        std::vector<double> ws(size_t(lz::kDerivWsPoints) * (na + n_rmom) * 2, 0.0);
-        P.ws = const_cast<double*>(upload(ws, &c->allocs));
     }
     P.tab.nbins = tab.nbins;
     P.tab.nfunc = nf;

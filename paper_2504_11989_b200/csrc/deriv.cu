@@ -519,16 +519,31 @@ cudaError_t launch_deriv_g_t(const DevDeriv& P, const double* k, int64_t n, doub
     const int64_t chunks = (P.n_dir + kDgCh - 1) / kDgCh + (P.n_rec + 1 + kDgCh - 1) / kDgCh;
     int64_t nsplit = 1;
     if (n < 2 * sms) nsplit = std::min<int64_t>(std::max<int64_t>(1, (2 * sms) / n), chunks);
-    if (nsplit > 1 && (!P.ws || n * nsplit > kDerivWsPoints)) nsplit = 1;
+    if (n * nsplit > kDerivWsPoints) nsplit = 1;
+    // split partial moments: a stream-ordered workspace per launch (concurrent launches of one plan
+    // on different streams stay independent)
+    DevDeriv Q = P;
+    Q.ws = nullptr;
+    if (nsplit > 1) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&Q.ws), sizeof(double) * 2 * size_t(n_mom) * size_t(n * nsplit), st);
+        if (e != cudaSuccess) return e;
+    }
     const int64_t gy = std::min<int64_t>(n, 65535);
-    deriv_moment_kernel<D><<<dim3(unsigned(nsplit), unsigned(gy)), kDgCh, smem, st>>>(P, k, n, out, status);
+    deriv_moment_kernel<D><<<dim3(unsigned(nsplit), unsigned(gy)), kDgCh, smem, st>>>(Q, k, n, out, status);
     e = cudaGetLastError();
-    if (e != cudaSuccess || nsplit == 1) return e;
-    const size_t smem2 = sizeof(double) * 2 * size_t(n_mom);
-    e = cudaFuncSetAttribute(deriv_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
-    if (e != cudaSuccess) return e;
-    deriv_combine_kernel<<<unsigned(std::min<int64_t>(n, 65535)), kDgCh, smem2, st>>>(P, n, int(nsplit), out);
-    return cudaGetLastError();
+    if (e == cudaSuccess && nsplit > 1) {
+        const size_t smem2 = sizeof(double) * 2 * size_t(n_mom);
+        e = cudaFuncSetAttribute(deriv_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        if (e == cudaSuccess) {
+            deriv_combine_kernel<<<unsigned(std::min<int64_t>(n, 65535)), kDgCh, smem2, st>>>(Q, n, int(nsplit), out);
+            e = cudaGetLastError();
+        }
+    }
+    if (Q.ws) {
+        const cudaError_t f = cudaFreeAsync(Q.ws, st);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
 }
 
 }  // namespace

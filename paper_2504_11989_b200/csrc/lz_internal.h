@@ -165,9 +165,9 @@ struct DevDeriv {
     const int* hmom;         // ... their reciprocal moment index ...
     const double* hcoef;     // ... and coefficient prod_a alpha_a! / (j_a! (alpha_a - 2 j_a)!)
     const double* add;       // [n_alpha] added inside the pref bracket (Taylor mode), or null
-    double* ws;              // split partial moments [kDerivWsPoints][n_dmom + n_rmom][2]
+    double* ws;              // split partial moments [points x splits][n_dmom + n_rmom][2] (per launch)
 };
-constexpr int kDerivWsPoints = 296;  // (point, split) pairs of one split launch (2 x 148 SMs)
+constexpr int kDerivWsPoints = 296;  // most (point, split) pairs of one split launch (2 x 148 SMs)
 
 // Fixed Duffy grid description (device arrays + patch decomposition).
 struct DevGrid {
