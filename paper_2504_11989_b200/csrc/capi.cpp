@@ -68,6 +68,17 @@ void check_cuda(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error{LZ_ECUDA, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
+// Kernel launches: the launch status, and with LATSUM_SYNC_DEBUG=1 the completion of the launch
+// on its stream (a fault is then reported by the launch that caused it, not by a later sync).
+void check_launch(cudaError_t e, const char* what, cudaStream_t st) {
+    check_cuda(e, what);
+    static const bool dbg = std::getenv("LATSUM_SYNC_DEBUG") != nullptr;
+    if (dbg) {
+        const cudaError_t f = cudaStreamSynchronize(st);
+        if (f != cudaSuccess) throw Error{LZ_ECUDA, std::string("after ") + what + ": " + cudaGetErrorString(f)};
+    }
+}
+
 struct DeviceGuard {
     int old = -1;
     explicit DeviceGuard(int dev) {
@@ -1518,8 +1529,7 @@ int lz_zeta(const lz_ctx* c, const double* k, int64_t n, double* out, uint32_t f
         DeviceGuard dg(c->device);
         int G = lanes > 0 ? lanes : auto_lanes(n);
         if (G & (G - 1) || G > 32) throw Error{LZ_EINVAL, "lanes_per_point must be a power of two <= 32"};
-        check_cuda(lz::launch_batch(P, false, k, n, out, flags, G, status, (cudaStream_t)stream),
-                   "zeta kernel launch");
+        check_launch(lz::launch_batch(P, false, k, n, out, flags, G, status, (cudaStream_t)stream), "zeta kernel launch", (cudaStream_t)stream);
     });
 }
 
@@ -1540,7 +1550,7 @@ int lz_zeta_host(const lz_ctx* c, const double* k, int64_t n, double* out, uint3
         int* dstat = reinterpret_cast<int*>(A.dbuf + al256(kb) + al256(ob));
         check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
         h2d(dk, k, kb, A.hbuf, A.st);
-        check_cuda(lz::launch_batch(P, false, dk, n, dout, flags, auto_lanes(n), dstat, A.st), "zeta kernel");
+        check_launch(lz::launch_batch(P, false, dk, n, dout, flags, auto_lanes(n), dstat, A.st), "zeta kernel", A.st);
         const bool pinned_out = is_pinned(out);
         copy_d2h(pinned_out ? (void*)out : (void*)A.hbuf, dout, ob, A.st);
         int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
@@ -1558,8 +1568,7 @@ int lz_zeta_hessian(const lz_ctx* c, const double* k, int64_t n, double* out, in
         ensure_hess(c);
         DeviceGuard dg(c->device);
         int G = lanes > 0 ? lanes : auto_lanes(n);
-        check_cuda(lz::launch_batch(c->dhess, true, k, n, out, 1u, G, nullptr, (cudaStream_t)stream),
-                   "hessian kernel launch");
+        check_launch(lz::launch_batch(c->dhess, true, k, n, out, 1u, G, nullptr, (cudaStream_t)stream), "hessian kernel launch", (cudaStream_t)stream);
     });
 }
 
@@ -1579,7 +1588,7 @@ int lz_zeta_hessian_host(const lz_ctx* c, const double* k, int64_t n, double* ou
         double* dk = reinterpret_cast<double*>(A.dbuf);
         double* dout = reinterpret_cast<double*>(A.dbuf + al256(kb));
         h2d(dk, k, kb, A.hbuf, A.st);
-        check_cuda(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, A.st), "hessian kernel");
+        check_launch(lz::launch_batch(c->dhess, true, dk, n, dout, 1u, auto_lanes(n), nullptr, A.st), "hessian kernel", A.st);
         copy_d2h(A.hbuf, dout, ob, A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, ob);
@@ -1926,7 +1935,7 @@ int lz_zeta_derivatives(const lz_ctx* c, int order, const double* k, int64_t n, 
         if (c->device < 0) throw Error{LZ_ECUDA, "context has no device tables"};
         if (order < 1 || order > 12) throw Error{LZ_EINVAL, "derivative order must be 1..12"};
         DeviceGuard dg(c->device);
-        check_cuda(launch_derivatives(c, order, k, n, out, status, (cudaStream_t)stream), "derivative kernel");
+        check_launch(launch_derivatives(c, order, k, n, out, status, (cudaStream_t)stream), "derivative kernel", (cudaStream_t)stream);
     });
 }
 
@@ -1948,7 +1957,7 @@ int lz_zeta_derivatives_host(const lz_ctx* c, int order, const double* k, int64_
         int* dstat = reinterpret_cast<int*>(A.dbuf + al256(kb) + al256(ob));
         check_cuda(cudaMemsetAsync(dstat, 0, sizeof(int), A.st), "memset");
         h2d(dk, k, kb, A.hbuf, A.st);
-        check_cuda(launch_derivatives(c, order, dk, n, dout, dstat, A.st), "derivative kernel");
+        check_launch(launch_derivatives(c, order, dk, n, dout, dstat, A.st), "derivative kernel", A.st);
         copy_d2h(A.hbuf, dout, ob, A.st);
         int* hstat = reinterpret_cast<int*>(A.hbuf + al256(ob));
         copy_d2h(hstat, dstat, sizeof(int), A.st);
@@ -2072,9 +2081,9 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
             tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, need_wpart, &dgd.wpart, &dgd.tcount, &dgd.work);
         }
         if (pl->kind == 0)
-            check_cuda(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel");
+            check_launch(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel", st);
         else
-            check_cuda(lz::launch_atm(pl->P, dgd, partials, grid_blocks, st), "atm kernel");
+            check_launch(lz::launch_atm(pl->P, dgd, partials, grid_blocks, st), "atm kernel", st);
     });
 }
 
@@ -2083,8 +2092,7 @@ int lz_plan_product_at(const lz_plan* pl, const double* k, int64_t n, double* ou
         if (pl->kind != 0) throw Error{LZ_EINVAL, "lz_plan_product_at needs a product plan"};
         DeviceGuard dg(pl->device);
         const int4 m = make_int4(pl->mult[0], pl->mult[1], pl->mult[2], pl->mult[3]);
-        check_cuda(lz::launch_product_at(pl->P, m, k, n, out, auto_lanes(n), status, (cudaStream_t)stream),
-                   "product kernel");
+        check_launch(lz::launch_product_at(pl->P, m, k, n, out, auto_lanes(n), status, (cudaStream_t)stream), "product kernel", (cudaStream_t)stream);
     });
 }
 
@@ -2129,7 +2137,7 @@ static int device_of(const void* p) {
 int lz_reduce_partials(const double* partials, int64_t n_tiles, int ncomp, double* out, void* stream) {
     return guarded([&] {
         DeviceGuard dg(device_of(partials));
-        check_cuda(lz::launch_reduce(partials, n_tiles, ncomp, out, (cudaStream_t)stream), "reduce kernel");
+        check_launch(lz::launch_reduce(partials, n_tiles, ncomp, out, (cudaStream_t)stream), "reduce kernel", (cudaStream_t)stream);
     });
 }
 
@@ -2141,9 +2149,8 @@ int lz_reduce_chunks(const double* partials, int64_t n_tiles, int ncomp, int64_t
             throw Error{LZ_EINVAL, "chunk range outside the tile vector"};
         if (chunk_hi == chunk_lo) return;
         DeviceGuard dg(device_of(partials));
-        check_cuda(lz::launch_chunks(partials, n_tiles, ncomp, chunk_tiles, chunk_lo, chunk_hi, chunk_out,
-                                     (cudaStream_t)stream),
-                   "chunk kernel");
+        check_launch(lz::launch_chunks(partials, n_tiles, ncomp, chunk_tiles, chunk_lo, chunk_hi, chunk_out,
+                                     (cudaStream_t)stream), "chunk kernel", (cudaStream_t)stream);
     });
 }
 
@@ -2241,8 +2248,8 @@ int lz_plan_integrate_host(const lz_plan* pl, const lz_grid* g, double* out) {
         gg.tile_hi = 0;
         rc = lz_plan_integrate(pl, &gg, dp, 0, A.st);
         if (rc != LZ_OK) throw Error{rc, g_last_error};
-        check_cuda(lz::launch_chunks(dp, n_tiles, ncomp, chunk_tiles, 0, n_chunks, dc, A.st), "chunk reduce");
-        check_cuda(lz::launch_reduce(dc, n_chunks, ncomp, dout, A.st), "reduce");
+        check_launch(lz::launch_chunks(dp, n_tiles, ncomp, chunk_tiles, 0, n_chunks, dc, A.st), "chunk reduce", A.st);
+        check_launch(lz::launch_reduce(dc, n_chunks, ncomp, dout, A.st), "reduce", A.st);
         copy_d2h(A.hbuf, dout, sizeof(double) * ncomp, A.st);
         check_cuda(cudaStreamSynchronize(A.st), "sync");
         std::memcpy(out, A.hbuf, sizeof(double) * ncomp);
@@ -2288,7 +2295,7 @@ int lz_ctx_reg_derivatives_device(const lz_ctx* c, int order, int* alphas, doubl
             int64_t off = 0;
             for (int total = 0; total <= order; total += 2) {
                 const lz::DevDeriv& P = ensure_deriv_g(c, total, 1, order);
-                check_cuda(lz::launch_deriv_g(P, nullptr, 1, dout + off, nullptr, A.st), "taylor kernel");
+                check_launch(lz::launch_deriv_g(P, nullptr, 1, dout + off, nullptr, A.st), "taylor kernel", A.st);
                 off += P.n_alpha;
             }
             copy_d2h(A.hbuf, dout, ob, A.st);
@@ -2333,8 +2340,8 @@ int lz_direct_sum3(int device, int d, const double* a, int64_t L, int kind, cons
         for (int i = 0; i < d * d; ++i) hA[i] = a[i];
         copy_h2d(dA, hA, sizeof(hA), ar.st);
         const double nz[3] = {nus ? nus[0] : 0.0, nus ? nus[1] : 0.0, nus ? nus[2] : 0.0};
-        check_cuda(lz::launch_direct(d, kind, L, npts, dA, nz, dp, nblocks, ar.st), "direct kernel");
-        check_cuda(lz::launch_reduce(dp, nblocks, 1, dout, ar.st), "reduce");
+        check_launch(lz::launch_direct(d, kind, L, npts, dA, nz, dp, nblocks, ar.st), "direct kernel", ar.st);
+        check_launch(lz::launch_reduce(dp, nblocks, 1, dout, ar.st), "reduce", ar.st);
         copy_d2h(ar.hbuf, dout, sizeof(double), ar.st);
         check_cuda(cudaStreamSynchronize(ar.st), "sync");
         double v;
@@ -2393,9 +2400,9 @@ int lz_fp64_peak(int device, double* tflops, double* ms_out) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
-        check_cuda(lz::launch_probe(scratch, iters / 8, blocks, threads, 0), "probe");  // warm-up
+        check_launch(lz::launch_probe(scratch, iters / 8, blocks, threads, 0), "probe", 0);  // warm-up
         cudaEventRecord(a, 0);
-        check_cuda(lz::launch_probe(scratch, iters, blocks, threads, 0), "probe");
+        check_launch(lz::launch_probe(scratch, iters, blocks, threads, 0), "probe", 0);
         cudaEventRecord(b, 0);
         check_cuda(cudaEventSynchronize(b), "sync");
         float ms = 0.f;

@@ -123,7 +123,7 @@ template <class T> LZ_HDI T expint_series_frac(T p, T x) {
 //   p near integer  : continued fraction (the series cancels catastrophically;
 //                     mirrors the reference's Lentz branch, L/incgamma.py:32-55,110-111)
 //   otherwise       : non-integer series
-template <class T> LZ_HDI T expint(T p, T x) {
+template <class T> LZ_HDI T expint_base(T p, T x) {
     using std::exp;
     using std::floor;
     T pr = floor(p + T(0.5));
@@ -137,22 +137,30 @@ template <class T> LZ_HDI T expint(T p, T x) {
         }
         return e;
     }
-    if (p < T(0)) {
-        // non-integer p < 0: E_{p0}, p0 = p + N in (0, 1), then the same stable recurrence
+    if (x > T(1)) return expint_cf(p, x, 100000);
+    if (dist < T(1e-12)) return expint_series_int(int(pr), x);
+    if (dist < T(1e-3)) return expint_cf(p, x, 100000);
+    return expint_series_frac(p, x);
+}
+
+template <class T> LZ_HDI T expint(T p, T x) {
+    using std::exp;
+    using std::floor;
+    const T pr = floor(p + T(0.5));
+    if (p < T(0) && labs_(p - pr) >= T(1e-12)) {
+        // non-integer p < 0: E_{p0}, p0 = p + N in (0, 1), then the stable recurrence
         // E_{q-1} = (e^{-x} + (1 - q) E_q) / x (all terms positive for q < 1).  The continued
-        // fraction alone loses up to 1e-5 relative near x = 1 at p = -11.
+        // fraction alone loses up to 1e-5 relative near x = 1 at p = -11.  (No recursion: device
+        // code keeps a static stack size.)
         const int n = int(floor(-p)) + 1;
         const T p0 = p + T(n);
-        T e = expint(p0, x);
+        T e = expint_base(p0, x);
         const T emx = exp(-x);
         T q = p0;
         for (int i = 0; i < n; ++i, q -= T(1)) e = (emx + (T(1) - q) * e) / x;
         return e;
     }
-    if (x > T(1)) return expint_cf(p, x, 100000);
-    if (dist < T(1e-12)) return expint_series_int(int(pr), x);
-    if (dist < T(1e-3)) return expint_cf(p, x, 100000);
-    return expint_series_frac(p, x);
+    return expint_base(p, x);
 }
 
 // Upper incomplete gamma Gamma(s, x) = x^s E_{1-s}(x), x > 0 (L/incgamma.py:97-114).
