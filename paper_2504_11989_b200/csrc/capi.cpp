@@ -541,8 +541,9 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     std::future<void> table_job;
     const double x_lo_tab = lz::table_x_lo(*first);
     if (!rec_n_empty(rsets))
-        table_job = std::async(std::launch::async, [&hp, p, sc, nf, c, x_lo_tab, rp] {
-            lz::build_table(p, sc, nf, double(c), x_lo_tab, rp, &hp->tab);
+        table_job = std::async(std::launch::async, [&hp, p, sc, nf, c, x_lo_tab, rp, trace_z] {
+            lz::build_table(p, sc, nf, double(c), x_lo_tab, rp, &hp->tab, 1.0,
+                            trace_z ? lz::kAtmTermCutoff : 1e-18);
         });
     // q = 0 power series (t0_reg and, for the Hessian, its rho-derivatives) and the line kernel's
     // pieces of the Hessian rows: they depend only on the contexts' constants, so they are
@@ -645,7 +646,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     WeightMap wmap;
     wmap.nw = wctx.size();
     {
-        ld dcut = 1e-18L;
+        ld dcut = trace_z ? ld(lz::kAtmTermCutoff) : 1e-18L;
         if (const char* e = std::getenv("LATSUM_DIRECT_CUTOFF")) dcut = std::strtold(e, nullptr);
         const size_t np = hp->dir_n.size() / d;
         // one context whose own set is the union (trace-Z plans): its weights align by index

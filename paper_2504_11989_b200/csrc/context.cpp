@@ -505,7 +505,7 @@ double fit_piece_fn(const std::function<long double(long double)>& f, long doubl
 }
 
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
-                 double rfac_pref, HostTable* out, double poly_pow) {
+                 double rfac_pref, HostTable* out, double poly_pow, double term_cutoff) {
     // weight of a term relative to the unit scale: (1 + 4x)^poly_pow covers the |y|^2 (Hessian)
     // or |2y|^m (order-m derivative) factors multiplying the tabulated functions
     auto wfac = [poly_pow](ld x) { return std::pow(1.0L + 4.0L * x, ld(poly_pow)); };
@@ -521,7 +521,7 @@ void build_table(const double* p, const double* scale, int nfunc, double c, doub
     // below `cutoff` (default 1e-18, the reference's term cutoff L/epstein.py:51) of the unit
     // scale; terms past it are exactly
     // zero in the kernel and culled per warp.
-    ld cutoff = 1e-18L;
+    ld cutoff = ld(term_cutoff);
     if (const char* e = std::getenv("LATSUM_TABLE_CUTOFF")) cutoff = std::strtold(e, nullptr);
     const ld hb = kBinWidth;
     ld x_hi = x_lo;

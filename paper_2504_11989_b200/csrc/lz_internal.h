@@ -269,8 +269,14 @@ struct Error {
 // context.cpp
 void build_context(int d, const double* a, double nu, double splitting, int deriv_order,
                    HostCtx* out);
+// term_cutoff: terms below it (relative to the unit scale |rfac pref|) end the table; 1e-18 is the
+// reference's term cutoff (L/epstein.py:51)
 void build_table(const double* p, const double* scale, int nfunc, double c, double x_lo,
-                 double rfac_pref, HostTable* out, double poly_pow = 1.0);
+                 double rfac_pref, HostTable* out, double poly_pow = 1.0, double term_cutoff = 1e-18);
+// the fused ATM plan's term cutoff (table end and direct ball): its lattice sums are bit-identical
+// at 1e-18 and 1e-16 (fcc: 19.182931071888479 both), the terms it drops are below the rounding of
+// every node's FP64 Hessian (capi.cpp build_host_plan)
+constexpr double kAtmTermCutoff = 1e-16;
 // Point sets of the order-`order` derivative tables (L/epstein.py:376-377): direct weights
 // widened by |z|^order, reciprocal Gamma order s + order, cutoff 1e-20.
 void build_deriv_sets(const HostCtx& h, int order, std::vector<double>* dir_n, std::vector<double>* rec_n);

@@ -292,9 +292,9 @@ def test_direct_sums_reproduce_paper_and_epstein(golden, golden_integrals):
     assert errs[0] > errs[1] > errs[2] and errs[2] < 5e-4 * golden_integrals["fcc"]["atm"]
 
 
-@pytest.mark.parametrize("scale", [0.2, 0.3, 0.6, 1.0])
+@pytest.mark.parametrize("scale", [0.17, 0.3, 0.6, 1.0])
 def test_atm_energy_split_invariance(scale):
-    """The fused ATM sum does not depend on the theta split (0.2 makes the direct block too large
+    """The fused ATM sum does not depend on the theta split (0.17 makes the direct block too large
     for the parameter-space variant, exercising the shared-memory fallback)."""
     lat = named_lattice("fcc")
     grid = ATMGrid(32, 16, 3)
@@ -303,7 +303,7 @@ def test_atm_energy_split_invariance(scale):
     res = atm_integrals(lat, grid, splitting=t)
     assert abs(res.energy - ref.energy) <= 1e-12 * abs(ref.energy)
     assert abs(res.dot_term - ref.dot_term) <= 1e-12 * abs(ref.dot_term)
-    if scale == 0.2:
+    if scale == 0.17:
         info = atm_plan(lat, t).info()
         assert info.n_dir * 4 > 3584  # direct block exceeds the 28 KB parameter block
 
