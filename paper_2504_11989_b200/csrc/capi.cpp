@@ -99,7 +99,12 @@ std::atomic<int64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st, bool async = true) {
     g_h2d_bytes += int64_t(bytes);
     if (async) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
-    else check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "h2d");
+    else {
+        // a pageable cudaMemcpy returns once the source is staged, not when the DMA lands; the
+        // kernels run on non-blocking streams that do not order after the legacy stream, so wait
+        check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "h2d");
+        check_cuda(cudaStreamSynchronize(cudaStreamLegacy), "h2d sync");
+    }
 }
 
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {

@@ -1705,7 +1705,8 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                         sts_f64(lsave + 24u + 8u * a, ax == 0 ? P.B[a * D] : ax == 1 ? P.B[a * D + 1] : P.B[a * D + 2]);
                     }
                     sts_f64(lsave + 48u, u);
-                    sts_f64(lsave + 56u, g.wu[iu]);
+                    // line pairs past the grid (a partial last tile) carry weight 0
+                    sts_f64(lsave + 56u, cp < g.n_cell / 2 ? g.wu[iu] : 0.0);
                     sts_f64(lsave + 64u, g.wv[iv2]);
                 }
                 line_planes(P, V.s_line, scr, ax, kap0);  // (its first __syncwarp orders the stores)
