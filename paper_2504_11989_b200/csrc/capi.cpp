@@ -149,6 +149,11 @@ struct HostPlan {
     std::vector<unsigned char> line;
     int line_K[3] = {0, 0, 0}, line_P[3] = {0, 0, 0}, line_slot_off[3] = {0, 0, 0}, line_meta_off[3] = {0, 0, 0};
     double line_sign = 1.0;
+    // row-factorised direct block (trace-Z ATM plans, d = 3; see build_row_block)
+    std::vector<double> row_pts;
+    std::vector<int> row_idx;
+    int row_on = 0, row_nJ = 0, row_PS = 0, row_NI = 0;
+    int row_jmin[3] = {0, 0, 0};
     lz::HostTable tab;
     lz::CtxConst ctx[lz::kMaxCtx];
     lz::CtxConst hctx;
@@ -472,6 +477,105 @@ static bool build_line_block(HostPlan* hp, const WeightMap& wmap,
         std::fprintf(stderr, "line block: %zu points, K = %d/%d/%d, planes = %d/%d/%d, %zu bytes\n", np,
                      hp->line_K[0], hp->line_K[1], hp->line_K[2], hp->line_P[0], hp->line_P[1], hp->line_P[2],
                      hp->line.size());
+    return true;
+}
+
+// Row-factorised direct block for the ATM kernel (d = 3; kernels.cu row_table_kernel / row_planes).
+// With the line's kappa_0 = (0, kappa_b, kappa_c) (kappa_c = u, the radial node; kappa_b = 2 s1 u v2)
+// the plane sums of build_line_block factor once more over the rows n_b = j of each plane:
+//   C_m = sum_j e^{2 pi i kappa_b j} D_{m,j}(u),   D_{m,j}(u) = sum_{n_c} W_n e^{2 pi i u n_c},
+// and D depends only on (axis, radial node): a small table kernel forms it once per launch for the
+// grid's n_u radial nodes, and a line costs one complex multiply-add per (row, plane, channel)
+// instead of one term per lattice point.  Nothing of this block is staged in shared memory, so the
+// direct set may grow (smaller split, fewer reciprocal terms per node).
+// Per axis the half lattice is {n : (n_a, n_b, n_c) >lex 0}; rows are stored sorted by (j, m, n_c).
+// Returns false when the set does not fit the kernel's fixed limits.
+static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A, long double hscale, int hidx) {
+    const int d = 3;
+    const size_t np = hp->dir_n.size() / d;
+    hp->row_on = 0;
+    hp->row_pts.clear();
+    hp->row_idx.clear();
+    if (np == 0) return false;
+    std::vector<std::array<double, 3>> v(np);
+    int sign = 0;
+    for (size_t i = 0; i < np; ++i) {
+        const double* n = &hp->dir_n[i * d];
+        long double z[3];
+        for (int a = 0; a < 3; ++a) {
+            z[a] = 0.0L;
+            for (int b = 0; b < 3; ++b) z[a] += (long double)A[a * 3 + b] * n[b];
+        }
+        const long double w = wmap.at(pack_key(d, n))[hidx] * hscale;
+        const int sg = w < 0 ? -1 : 1;
+        if (sign != 0 && sg != sign) return false;  // mixed weight signs
+        sign = sg;
+        const long double r = std::sqrt(std::fabs(w));
+        for (int a = 0; a < 3; ++a) v[i][a] = double(r * z[a]);
+    }
+    struct Pt {
+        long j, m, l;
+        size_t i;
+        bool operator<(const Pt& o) const { return std::tie(j, m, l) < std::tie(o.j, o.m, o.l); }
+    };
+    std::vector<Pt> pts[3];
+    long jlo[3], jhi[3];
+    int planes[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        const int b = (ax + 1) % 3, c = (ax + 2) % 3;
+        pts[ax].reserve(np);
+        jlo[ax] = 0, jhi[ax] = 0;
+        long mmax = 0;
+        for (size_t i = 0; i < np; ++i) {
+            long n[3];
+            for (int a = 0; a < 3; ++a) n[a] = std::lround(hp->dir_n[i * d + a]);
+            const bool pos = n[ax] > 0 || (n[ax] == 0 && (n[b] > 0 || (n[b] == 0 && n[c] > 0)));
+            if (!pos)
+                for (int a = 0; a < 3; ++a) n[a] = -n[a];
+            pts[ax].push_back({n[b], n[ax], n[c], i});
+            jlo[ax] = std::min(jlo[ax], n[b]);
+            jhi[ax] = std::max(jhi[ax], n[b]);
+            mmax = std::max(mmax, n[ax]);
+        }
+        if (mmax + 1 > lz::kLinePlanes) return false;
+        planes[ax] = int(mmax + 1);
+        std::sort(pts[ax].begin(), pts[ax].end());
+    }
+    const int pmax = std::max(planes[0], std::max(planes[1], planes[2]));
+    const int rounds = (6 * pmax + 31) / 32;
+    if (rounds > lz::kRowRounds) return false;
+    const int NI = 32 * rounds, PS = (NI + 5) / 6;
+    long nJ = 0;
+    for (int ax = 0; ax < 3; ++ax) nJ = std::max(nJ, jhi[ax] - jlo[ax] + 1);
+    if (nJ > 128) return false;
+    hp->row_idx.assign(size_t(3) * size_t(nJ) * size_t(PS) * 2, 0);
+    hp->row_pts.reserve(np * 12);
+    for (int ax = 0; ax < 3; ++ax) {
+        const auto& pp = pts[ax];
+        for (size_t q = 0; q < pp.size();) {
+            size_t e = q;
+            while (e < pp.size() && pp[e].j == pp[q].j && pp[e].m == pp[q].m) ++e;
+            const size_t slot = (size_t(ax) * size_t(nJ) + size_t(pp[q].j - jlo[ax])) * size_t(PS) + size_t(pp[q].m);
+            hp->row_idx[2 * slot] = int(hp->row_pts.size() / 4);
+            hp->row_idx[2 * slot + 1] = int(e - q);
+            for (size_t t = q; t < e; ++t) {
+                hp->row_pts.push_back(double(pp[t].l));
+                for (int a = 0; a < 3; ++a) hp->row_pts.push_back(v[pp[t].i][a]);
+            }
+            q = e;
+        }
+        hp->row_jmin[ax] = int(jlo[ax]);
+        hp->line_P[ax] = planes[ax];
+        hp->line_K[ax] = 0;
+    }
+    hp->line_sign = double(sign);
+    hp->row_nJ = int(nJ);
+    hp->row_PS = PS;
+    hp->row_NI = NI;
+    hp->row_on = 1;
+    if (std::getenv("LATSUM_DEBUG_LINE"))
+        std::fprintf(stderr, "row block: %zu points, planes %d/%d/%d, rows j %ld, items %d (%d rounds)\n", np,
+                     planes[0], planes[1], planes[2], nJ, NI, rounds);
     return true;
 }
 
@@ -862,7 +966,13 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     };
     lap("sort");
     hp->line.clear();
-    if (trace_z && d == 3 && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
+    hp->row_on = 0;
+    // ATM kernel form (LATSUM_LINE): 2 (default) row-factorised direct block, 1 line block staged
+    // in shared memory, 0 slab walk
+    int line_env = 2;
+    if (const char* e = std::getenv("LATSUM_LINE")) line_env = std::atoi(e);
+    if (trace_z && d == 3 && line_env >= 2) build_row_block(hp, wmap, first->A, hscale, hw);
+    if (trace_z && d == 3 && !hp->row_on && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
     lap("line block");
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
@@ -909,16 +1019,17 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // The line kernel (kernels.cu tile_kernel_l) does not read the slab block: skip it when the
     // line block exists, the kernel is not disabled (LATSUM_LINE=0) and its shared-memory image
     // (everything but the slab block, the count table and 24 warp scratches) fits comfortably.
-    bool need_slab = hp->line.empty();
+    bool need_slab = hp->line.empty() && !hp->row_on;
     if (!need_slab) {
-        const char* e = std::getenv("LATSUM_LINE");
         const size_t qs = size_t((d + 1) & ~1);
         auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
         const size_t img = a16(8 * hp->rec_norm.size() * qs) + a16(8 * hp->rec_norm.size()) +
                            a16(8 * hp->tab.coef.size()) + a16(4 * hp->tab.dir.size()) +
                            a16(8 * size_t(hp->nctx + 2) * lz::kT0) + a16(hp->line.size());
-        need_slab = (e && std::atoi(e) == 0) || img + 1024 + 24 * 3200 + 8192 > 227 * 1024 ||
-                    hp->rec_norm.size() > 720;  // kernels.cu kLineQ
+        need_slab = line_env == 0 || img + 1024 + 24 * 4000 + 8192 > 227 * 1024 ||
+                    hp->rec_norm.size() > 512 ||  // kernels.cu kLineQ
+                    hp->q0_nb < 1 || hp->q0_nb > 48;  // kernels.cu kQ0Max
+        if (need_slab) hp->row_on = 0;
     }
     if (need_slab) build_slab();
     lap("slab block");
@@ -991,6 +1102,15 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     }
     P.line_bytes = unsigned(hp.line.size());
     P.line_sign = hp.line_sign;
+    P.row_on = hp.row_on;
+    P.row_nJ = hp.row_nJ;
+    P.row_PS = hp.row_PS;
+    P.row_NI = hp.row_NI;
+    for (int a = 0; a < 3; ++a) P.row_jmin[a] = hp.row_jmin[a];
+    if (hp.row_on) {
+        P.row_pts = upload(hp.row_pts, allocs);
+        P.row_idx = upload(hp.row_idx, allocs);
+    }
     for (int a = 0; a < 3; ++a) {
         P.line_K[a] = hp.line_K[a];
         P.line_P[a] = hp.line_P[a];
@@ -1223,7 +1343,9 @@ const GridArrays& grid_arrays(const lz_plan* plan, const lz_grid* g) {
 struct Scratch {
     double* wpart = nullptr;        // [cap_w * 8][2] warp partials (only launches that need them)
     unsigned int* tcount = nullptr; // [cap + 2]: tile counters, then the work-queue counters
+    double* dtab = nullptr;         // row-factorised ATM kernel: D table (grow-only)
     int64_t cap = 0, cap_w = 0;
+    size_t cap_d = 0;               // bytes
 };
 std::mutex g_scratch_mu;
 std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
@@ -1243,7 +1365,7 @@ void keep_pool(int device) {
 }
 
 void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, bool need_wpart, double** wpart,
-                  unsigned int** tcount, unsigned int** work) {
+                  unsigned int** tcount, unsigned int** work, size_t dtab_bytes = 0, double** dtab = nullptr) {
     keep_pool(device);
     auto& pool = g_scratch;
     std::lock_guard<std::mutex> lock(g_scratch_mu);
@@ -1264,6 +1386,14 @@ void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, bool need_wpart,
         s.wpart = static_cast<double*>(p);
         s.cap_w = n_tiles;
     }
+    if (dtab_bytes > s.cap_d) {
+        if (s.dtab) check_cuda(cudaFreeAsync(s.dtab, st), "cudaFreeAsync");
+        void* p = nullptr;
+        check_cuda(cudaMallocAsync(&p, dtab_bytes, st), "cudaMallocAsync");
+        s.dtab = static_cast<double*>(p);
+        s.cap_d = dtab_bytes;
+    }
+    if (dtab) *dtab = dtab_bytes ? s.dtab : nullptr;
     *wpart = need_wpart ? s.wpart : nullptr;
     *tcount = s.tcount;
     *work = s.tcount + s.cap;
@@ -2084,7 +2214,13 @@ int lz_plan_integrate(const lz_plan* pl, const lz_grid* g, double* partials, int
             lz::DevGrid tmp;
             fill_grid(pl->d, &full, &tmp);
             const bool need_wpart = pl->kind != 1 || lz::atm_needs_wpart(pl->P, dgd);
-            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, need_wpart, &dgd.wpart, &dgd.tcount, &dgd.work);
+            // row-factorised ATM plans: the D table of this grid's radial nodes (kernels.cu row_table_kernel)
+            const size_t dbytes = pl->kind == 1 && pl->P.row_on
+                                      ? size_t(3) * size_t(dgd.n_u) * size_t(pl->P.row_nJ) * size_t(pl->P.row_NI) * 16
+                                      : 0;
+            dgd.dtab = nullptr;
+            tile_scratch(pl->device, st, (tmp.n_patch + 7) / 8, need_wpart, &dgd.wpart, &dgd.tcount, &dgd.work,
+                         dbytes, &dgd.dtab);
         }
         if (pl->kind == 0)
             check_launch(lz::launch_product(pl->P, dgd, pl->mult, partials, grid_blocks, st), "product kernel", st);
@@ -2203,6 +2339,7 @@ int lz_release_caches(int device) {
                     cudaSetDevice(it->first.first);
                     cudaDeviceSynchronize();
                     if (it->second.wpart) cudaFree(it->second.wpart);
+                    if (it->second.dtab) cudaFree(it->second.dtab);
                     if (it->second.tcount) cudaFree(it->second.tcount);
                     it = g_scratch.erase(it);
                 } else {

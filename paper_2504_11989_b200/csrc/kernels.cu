@@ -1249,9 +1249,11 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // point index) with the phase carried by complex rotation from slot to slot (step factors from a
 // per-warp table); phase 2: fixed-order segmented shuffle reduction of each plane over its lane
 // group; phase 3: per lane, one complex rotation per plane.
-// per-warp scratch: the step table [32] (phase 1) / C_m [planes][12] from 0, the mirror node's
-// direct-space channels [6][32] doubles from 1536, the line pair's constants (9 doubles) from 3072
-constexpr uint32_t kLineScrBytes = 3072u + 80u;
+// per-warp scratch: the step table [32] / rotation table (phase 1) and then C_m [planes][12] from 0
+// (kCmBytes), the mirror node's direct-space channels [6][32] doubles after it, then the line
+// pair's constants (9 doubles)
+constexpr uint32_t kCmBytes = 96u * uint32_t(kLinePlanes);
+constexpr uint32_t kLineScrBytes = kCmBytes + 1536u + 80u;
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
 // scratch as [m][12] doubles, valid until the next call.
@@ -1346,6 +1348,118 @@ __device__ __forceinline__ void line_planes(const DevPlan& P, uint32_t lb, uint3
     __syncwarp();
 }
 
+// Row-factorised plane sums (capi.cpp build_row_block): C_m = sum_j e^{2 pi i kappa_b j} D_{m,j}(u)
+// with D of the line's (axis, radial node) from the table row_table_kernel wrote.  Lane l owns
+// the items (6 m + channel) = 32 r + l of R rounds; the rotation factors come from a per-warp
+// table (one sincos per row index), D is read coalesced (512 bytes per warp load, L1/L2
+// resident: consecutive tickets share the radial node).  Leaves C_m (line_sign folded into D) in
+// the warp's scratch as [m][12] doubles like line_planes.
+template <int R>
+__device__ __forceinline__ void row_planes_r(const DevPlan& P, const double2* __restrict__ D, uint32_t scr,
+                                             int np, int nJ) {
+    const int lane = threadIdx.x & 31;
+    const int NI = P.row_NI;
+    double2 acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
+    const double2* Dp = D + lane;
+#pragma unroll 2
+    for (int jj = 0; jj < nJ; ++jj) {
+        const double2 rot = lds_f64x2(scr + 16u * jj);
+        double2 dv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) dv[r] = __ldg(Dp + 32 * r);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            acc[r].x = fma(rot.x, dv[r].x, fma(-rot.y, dv[r].y, acc[r].x));
+            acc[r].y = fma(rot.x, dv[r].y, fma(rot.y, dv[r].x, acc[r].y));
+        }
+        Dp += NI;
+    }
+    __syncwarp();  // the rotation table is read by every lane before C overwrites it
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int item = 32 * r + lane;
+        if (item < 6 * np) sts_f64x2(scr + 16u * item, acc[r].x, acc[r].y);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void row_planes(const DevPlan& P, const DevGrid& g, uint32_t scr, int ax, int iu,
+                                           double kb) {
+    const int lane = threadIdx.x & 31;
+    const int nJ = P.row_nJ;
+    const int jmin = ax == 0 ? P.row_jmin[0] : ax == 1 ? P.row_jmin[1] : P.row_jmin[2];
+    const int np = ax == 0 ? P.line_P[0] : ax == 1 ? P.line_P[1] : P.line_P[2];
+    __syncwarp();  // the previous line's C read by every lane before the table overwrites it
+    for (int jj = lane; jj < nJ; jj += 32) {
+        double sn, cs;
+        sincos2pi(kb * double(jmin + jj), sn, cs);
+        sts_f64x2(scr + 16u * jj, cs, sn);
+    }
+    __syncwarp();
+    const double2* D = reinterpret_cast<const double2*>(g.dtab) +
+                       (size_t(ax) * size_t(g.n_u) + size_t(iu)) * size_t(nJ) * size_t(P.row_NI);
+    switch (P.row_NI >> 5) {
+        case 1: row_planes_r<1>(P, D, scr, np, nJ); break;
+        case 2: row_planes_r<2>(P, D, scr, np, nJ); break;
+        case 3: row_planes_r<3>(P, D, scr, np, nJ); break;
+        case 4: row_planes_r<4>(P, D, scr, np, nJ); break;
+        default: row_planes_r<5>(P, D, scr, np, nJ); break;
+    }
+}
+
+// D table of the row-factorised direct block: one thread per (axis, radial node, row index jj,
+// plane slot m) sums its row's points, W_n e^{2 pi i u n_c} with W_n = line_sign v v^T (six
+// channels), and writes the six items 6 m + channel (zero for slots without a row and for the
+// padding items up to row_NI).
+__global__ void __launch_bounds__(128) row_table_kernel(DevPlan P, DevGrid g) {
+    const int PS = P.row_PS, nJ = P.row_nJ, NI = P.row_NI;
+    const int64_t total = int64_t(3) * g.n_u * nJ * PS;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int slot = int(t % PS);
+    int64_t r = t / PS;
+    const int jj = int(r % nJ);
+    r /= nJ;
+    const int iu = int(r % g.n_u);
+    const int ax = int(r / g.n_u);
+    const int2 row = reinterpret_cast<const int2*>(P.row_idx)[(size_t(ax) * nJ + jj) * PS + slot];
+    const double u = g.u[iu];
+    double acc[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) acc[c] = 0.0;
+    const double2* pts = reinterpret_cast<const double2*>(P.row_pts) + 2 * size_t(row.x);
+    for (int q = 0; q < row.y; ++q) {
+        const double2 p0 = __ldg(pts + 2 * q), p1 = __ldg(pts + 2 * q + 1);  // (n_c, v)
+        double ps, pc;
+        sincos2pi(u * p0.x, ps, pc);
+        const double v[3] = {p0.y, p1.x, p1.y};
+        double pr[3], pi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            pr[a] = v[a] * pc;
+            pi[a] = v[a] * ps;
+        }
+        int c = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = a; b < 3; ++b) {
+                acc[2 * c] = fma(pr[a], v[b], acc[2 * c]);
+                acc[2 * c + 1] = fma(pi[a], v[b], acc[2 * c + 1]);
+                ++c;
+            }
+    }
+    const double sgn = P.line_sign;
+    double2* out = reinterpret_cast<double2*>(g.dtab) + ((size_t(ax) * size_t(g.n_u) + size_t(iu)) * size_t(nJ) + size_t(jj)) * size_t(NI);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const int item = slot * 6 + c;
+        if (item < NI) out[item] = make_double2(sgn * acc[2 * c], sgn * acc[2 * c + 1]);
+    }
+}
+
 // Phase 3 for the mirror pair of nodes +-x (x = kappa_ax) of the current line:
 //   hh(+-x) = A -+ B,  A = sum_m Re C_m cos 2 pi x m,  B = sum_m Im C_m sin 2 pi x m.
 __device__ __forceinline__ void line_node_pair(const DevPlan& P, uint32_t scr, int ax, double x, double (&hp)[6],
@@ -1389,8 +1503,8 @@ __device__ __forceinline__ void line_node_pair(const DevPlan& P, uint32_t scr, i
 constexpr int kDirParam = 3584;
 // line kernel parameter block: the Hessian's two q = 0 series rows and up to kLineQ reciprocal
 // vectors at the padded stride 4 (d = 3)
-constexpr int kLineQ = 720;
-constexpr int kQ0Max = 16;  // line kernel: Hessian q = 0 pieces (bins of kBinWidth in x = c rho)
+constexpr int kLineQ = 512;
+constexpr int kQ0Max = 48;  // line kernel: Hessian q = 0 pieces (bins of kBinWidth in x = c rho)
 constexpr uint32_t kQ0Bytes = uint32_t(kQ0Max) * piece_stride(2) * 8u;
 struct __align__(16) LineParam {
     double q0[kQ0Max * piece_stride(2)];
@@ -1403,7 +1517,8 @@ struct __align__(16) DirBlock {
 // LINE (ATM, d = 3): direct space from the plan's line block (no slab block staged).  The warp
 // walks lines (cell, v2, u) instead of patches: the per-plane sums C_m depend only on the line,
 // so they are formed once (line_planes) and serve the line's npv patches of 32 v1 nodes each.
-template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR, bool LINE = false>
+template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR, bool LINE = false,
+          bool ROW = false>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1686,7 +1801,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
             // line-pair constants kept in the warp's scratch (broadcast reloads per pv instead of
             // registers live across the node evaluations)
-            const uint32_t lsave = scr + 3072u;
+            const uint32_t lsave = scr + kCmBytes + 1536u;
             {
                 const double u = g.u[iu];
                 const double s1 = ((cp / D) & 1) ? -1.0 : 1.0;
@@ -1709,9 +1824,11 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                     sts_f64(lsave + 56u, cp < g.n_cell / 2 ? g.wu[iu] : 0.0);
                     sts_f64(lsave + 64u, g.wv[iv2]);
                 }
-                line_planes(P, V.s_line, scr, ax, kap0);  // (its first __syncwarp orders the stores)
+                // (the first __syncwarp of either form orders the stores)
+                if constexpr (ROW) row_planes(P, g, scr, ax, iu, kb);
+                else line_planes(P, V.s_line, scr, ax, kap0);
             }
-            const uint32_t hsave = scr + 1536u + 8u * lane;  // [6][32] doubles
+            const uint32_t hsave = scr + kCmBytes + 8u * lane;  // [6][32] doubles
             // the line pair is exactly one tile and lies in the range: this warp owns the tile and
             // sums it directly (per lane in fixed patch order, then one fixed xor tree)
             const bool own = per_lp == kTileWarps && pfirst >= p_lo && pfirst + per_lp <= p_hi;
@@ -1796,10 +1913,12 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 // ATM with the line-factorised direct block (plans with P.line_bytes > 0): WPC warps, each with
 // a kLineScrBytes shared scratch after the staged image.  The warp-uniform reads of the
 // reciprocal loop and the q = 0 series come from the parameter block (constant cache, no LSU).
-template <int WPC, int UNR>
+// ROW: plane sums from the D table of the row-factorised direct block (row_planes) instead of the
+// staged line block.
+template <int WPC, int UNR, bool ROW = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
     tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials, const __grid_constant__ LineParam LP) {
-    tile_body<3, 1, true, 1, true, WPC, UNR, false, true>(P, g, make_int4(0, 0, 0, 0), partials, LP.q0);
+    tile_body<3, 1, true, 1, true, WPC, UNR, false, true, ROW>(P, g, make_int4(0, 0, 0, 0), partials, LP.q0);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -2200,10 +2319,11 @@ static int line_unroll() {
     return v;
 }
 
-template <int WPC, int UNR>
+template <int WPC, int UNR, bool ROW = false>
 static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
-    auto kern = tile_kernel_l<WPC, UNR>;
+    auto kern = tile_kernel_l<WPC, UNR, ROW>;
+    if (ROW && (!g.dtab || !P.row_pts || !P.row_idx)) return cudaErrorInvalidValue;
     const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes + size_t(WPC) * kLineScrBytes;
     if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
     cudaError_t e = set_smem(kern, sm);
@@ -2225,13 +2345,20 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     int64_t cap = grid_blocks > 0 ? grid_blocks : blocks_for(kern, sm, threads);
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
+    if constexpr (ROW) {
+        // the D table of every (axis, radial node) of the grid (a shard recomputes all of it: ~10 us)
+        const int64_t total = int64_t(3) * g.n_u * P.row_nJ * P.row_PS;
+        row_table_kernel<<<unsigned((total + 127) / 128), 128, 0, st>>>(P, g);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     kern<<<blocks, threads, sm, st>>>(P, g, partials, lp);
     return cudaGetLastError();
 }
 
 // The ATM launch takes the line kernel for this plan and grid (launch_tile_t, d = 3)
 static bool line_eligible(const DevPlan& P, const DevGrid& g) {
-    if (P.d != 3 || !P.line_bytes || !line_mode() || g.pu != 1 || g.pv != 32) return false;
+    if (P.d != 3 || (!P.line_bytes && !P.row_on) || !line_mode() || g.pu != 1 || g.pv != 32) return false;
     const size_t bytes = plan_smem_bytes(P);
     const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
                         size_t(line_mode()) * kLineScrBytes + 1024;
@@ -2245,6 +2372,13 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
+        if (line_eligible(P, g) && P.row_on) {
+            switch (line_mode() * 10 + line_unroll()) {
+                case 161: return launch_tile_l<16, 1, true>(P, g, partials, grid_blocks, st, bytes);
+                case 241: return launch_tile_l<24, 1, true>(P, g, partials, grid_blocks, st, bytes);
+                default: return launch_tile_l<20, 1, true>(P, g, partials, grid_blocks, st, bytes);
+            }
+        }
         if (line_eligible(P, g)) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1>(P, g, partials, grid_blocks, st, bytes);
@@ -2257,7 +2391,7 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
         }
     }
     // plans whose slab block was skipped (capi.cpp build_host_plan) run only on the line kernel
-    if (MODE == 1 && P.line_bytes && P.n_direct == 0) return cudaErrorInvalidValue;
+    if (MODE == 1 && (P.line_bytes || P.row_on) && P.n_direct == 0) return cudaErrorInvalidValue;
     if constexpr (MODE == 1) {
         if (smem && cdir_enabled() && P.n_direct <= kDirParam && P.direct_host) {
             if constexpr (D == 3) {

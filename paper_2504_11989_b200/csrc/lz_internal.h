@@ -15,7 +15,8 @@ enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
 
 constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
-constexpr int kLinePlanes = 16;  // planes per axis of the line-factorised ATM direct block
+constexpr int kLinePlanes = 24;  // planes per axis of the line- / row-factorised ATM direct block
+constexpr int kRowRounds = 5;    // row-factorised block: most 32-item rounds of the plane sums (6 kLinePlanes <= 32 kRowRounds)
 // Degree of the piecewise polynomials (kDeg + 1 coefficients): 7 or 8.  Degree 7 on bins of
 // 0.125 in x saves two DFMA, one DMUL and one 16-byte load per function pair and term but needs
 // ~1.8x the pieces for the same 6e-16 bound; measured slower (fcc ATM 14.4 -> 20.8 ms, C1 2^20
@@ -138,6 +139,18 @@ struct DevPlan {
     unsigned line_bytes;   // 0: no line block
     int line_K[3], line_P[3], line_slot_off[3], line_meta_off[3];
     double line_sign;
+    // Row-factorised direct block (capi.cpp build_row_block; global memory, read only by
+    // row_table_kernel): per axis a the half lattice {(n_a, n_b, n_c) >lex 0} grouped into rows
+    // (m = n_a, j = n_b).  row_pts: 4 doubles per point (n_c, v), rows contiguous; row_idx:
+    // (first point, length) of row (a, jj = j - row_jmin[a], m) at [(a row_nJ + jj) row_PS + m].
+    // The table kernel writes D[a][iu][jj][item = 6 m + channel] (complex, row_NI items per row
+    // index, zero where no row exists) for every radial node; line_P[a] = planes of axis a.
+    const double* row_pts;
+    const int* row_idx;
+    int row_on;            // 1: the ATM kernel takes its plane sums from the D table
+    int row_nJ, row_PS, row_NI;
+    int row_jmin[3];
+    int pad6_;
 };
 
 // Derivative plan (deriv.cu): one context, derivatives of total order `order` (0..12) at
@@ -180,6 +193,7 @@ struct DevGrid {
     double* wpart;             // [n_tiles * 8][ncomp] warp partials (scratch)
     unsigned int* tcount;      // [n_tiles] arrival counters, zero between launches
     unsigned int* work;        // [2] line kernel work queue: next ticket, warps done (zero between launches)
+    double* dtab;              // row-factorised ATM kernel: D table [3][n_u][row_nJ][row_NI] complex (scratch)
 };
 
 
