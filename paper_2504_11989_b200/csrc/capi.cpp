@@ -1026,7 +1026,9 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         const size_t img = a16(8 * hp->rec_norm.size() * qs) + a16(8 * hp->rec_norm.size()) +
                            a16(8 * hp->tab.coef.size()) + a16(4 * hp->tab.dir.size()) +
                            a16(8 * size_t(hp->nctx + 2) * lz::kT0) + a16(hp->line.size());
-        need_slab = line_env == 0 || img + 1024 + 24 * 4000 + 8192 > 227 * 1024 ||
+        // (row kernel: 20 warps x kRowScrBytes, the q = 0 pieces, the count table, angular nodes)
+        const size_t extra = hp->row_on ? 20 * 7000 + 12 * 1024 : 1024 + 24 * 4000 + 8192;
+        need_slab = line_env == 0 || img + extra > 227 * 1024 ||
                     hp->rec_norm.size() > 512 ||  // kernels.cu kLineQ
                     hp->q0_nb < 1 || hp->q0_nb > 48;  // kernels.cu kQ0Max
         if (need_slab) hp->row_on = 0;

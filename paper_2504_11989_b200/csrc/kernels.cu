@@ -66,6 +66,9 @@ struct View {
     uint32_t s_end;        // first byte after the staged image (per-warp scratch follows)
     uint32_t s_cnt;        // line kernel: count table cnt[i] = #{q : |q| <= i h} (kCntEntries int32)
     uint32_t s_q0;         // line kernel: the Hessian's q = 0 pieces (kQ0Max x piece_stride(2) doubles)
+    uint32_t s_v;          // row kernel: the grid's angular nodes [n_v] and weights [n_v] (0: not staged)
+    uint32_t s_cand;       // row kernel: the line pair's reciprocal candidates (uint16 indices, per warp)
+    int n_cand;
     double cnt_inv_h;      // 1 / h
     // line kernel: warp-uniform reads of the reciprocal vectors (padded stride) from the kernel's
     // parameter space (LineParam)
@@ -375,6 +378,19 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 #define LZ_P1_UNROLL 1
 #endif
 constexpr int kP1Unroll = LZ_P1_UNROLL;  // phase-1 slots per loop iteration
+// row-factorised ATM kernel: tickets per CTA block (A/B: -DLZ_ROW_BLOCK=1 per-warp tickets) and
+// row indices per iteration of the plane-sum loop
+#ifndef LZ_ROW_BLOCK
+#define LZ_ROW_BLOCK 32
+#endif
+#ifndef LZ_ROW_UNROLL
+#define LZ_ROW_UNROLL 2
+#endif
+#ifndef LZ_ROW_PREFETCH
+#define LZ_ROW_PREFETCH 0
+#endif
+constexpr int kRowBlock = LZ_ROW_BLOCK;
+constexpr int kRowUnroll = LZ_ROW_UNROLL;
 // Ticket order of the line kernel's work queue (A/B: -DLZ_LINE_ORDER=0 plain, 1 radial index
 // descending, 2 ascending)
 #ifndef LZ_LINE_ORDER
@@ -606,12 +622,13 @@ template <int D, int NCTX, bool HESS, bool ALIAS = false> struct NodeAcc {
 // XDIR (line kernel, with TRZ): the direct-space Hessian channels arrive precomputed in hx
 // (line_direct) and the slab walk is skipped.
 template <int D, int NCTX, bool HESS, bool ALIAS = false, int UNR = 2, bool SMEM = true, bool CDIR = false,
-          bool TRZ = false, bool XDIR = false>
+          bool TRZ = false, bool XDIR = false, bool XLIST = false>
 __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const double (&kap)[D],
                                           const double (&k)[D], int gl, int G, uint32_t flags,
                                           NodeAcc<D, NCTX, HESS, ALIAS>& out, const double* hx = nullptr) {
     static_assert(!TRZ || (HESS && ALIAS), "trace-Z needs the aliased Hessian plan");
     static_assert(!XDIR || TRZ, "external direct block only for trace-Z plans");
+    static_assert(!XLIST || XDIR, "candidate list only with the external direct block");
     using Acc = NodeAcc<D, NCTX, HESS, ALIAS>;
     constexpr int NF = Acc::NF;
     constexpr int NS = Acc::NS;
@@ -828,7 +845,9 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
 #pragma unroll
     for (int a = 0; a < D; ++a) kmag = fma(k[a], k[a], kmag);
     int n_eff, n_in_line = 0;
-    if constexpr (XDIR) {
+    if constexpr (XLIST) {
+        n_eff = 0;  // (the line pair's candidate list replaces the per-patch culling, below)
+    } else if constexpr (XDIR) {
         // line warp: |k|^2 is convex along the line, so its maximum is at an end lane (padding
         // lanes repeat the last node); n_eff / n_in from the count table, rounded outwards /
         // inwards (r_cut and r_in carry 1e-9 relative margins against rounding)
@@ -915,7 +934,14 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         }
     };
     // lookup variant: checked (marker bins, or k not reduced into the cell), in-cell, branch-free
-    if (P.tab.has_marker || (flags & 1u)) {
+    if constexpr (XLIST) {
+        // row kernel: the q whose distance to the line pair's whole segment is within r_cut were
+        // listed once per line pair (tile_body); every other q is zero for all of its nodes
+        (void)n_eff;
+        (void)n_in_line;
+        for (int c = 0; c < V.n_cand; ++c)
+            term(int(lds_u16(V.s_cand + 2u * uint32_t(c))), std::integral_constant<int, 1>{});
+    } else if (P.tab.has_marker || (flags & 1u)) {
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 0>{});
     } else if (!P.tab.branchfree) {
@@ -1038,14 +1064,16 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         if (q0_table) {
             fp = ALIAS ? P.alias_ratio * f0[0] : f0[NCTX];
             fpp = f0[Acc::FPP];
-        } else if (q0_series && rho > 0.0) {
+        } else if (XLIST || (q0_series && rho > 0.0)) {
+            // (XLIST: the caller checked the log case nu = d + 2 with q = 0 pieces; grid nodes have
+            // rho > 0, and a plan without reciprocal points keeps its series over the whole box)
             const double kk = XDIR ? P.h_kk : C.sing_coef * C.inv_vol / (C.pref * C.rfac);
             double s1, s2;
-            if (XDIR && C.branch == kLogCase && C.log_m == 1) {
+            if (XLIST || (XDIR && C.branch == kLogCase && C.log_m == 1)) {
                 // nu = d + 2 (the ATM Z_5): s1 = kk (log(pi rho) + 1), s2 = kk / rho
                 s1 = kk * (fast_log(kPi * rho) + 1.0);
                 s2 = kk * fast_rcp(rho);
-            } else if (C.branch == kLogCase) {
+            } else if (!XLIST && C.branch == kLogCase) {
                 const int m = C.log_m;
                 double rm1 = 1.0;  // rho^{m-1}
                 if (m == 0) rm1 = 1.0 / rho;
@@ -1053,10 +1081,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
                 const double L = log(kPi * rho);
                 s1 = kk * rm1 * (double(m) * L + 1.0);
                 s2 = kk * (rm1 / rho) * (double(m * (m - 1)) * L + double(2 * m - 1));
-            } else {
+            } else if constexpr (!XLIST) {
                 const double p1 = C.sing_q4 != kNoQuarter ? pow_quarter(rho, C.sing_q4 - 4) : pow(rho, -C.s - 1.0);
                 s1 = -kk * C.s * p1;
                 s2 = kk * C.s * (C.s + 1.0) * p1 / rho;
+            } else {
+                s1 = s2 = 0.0;
             }
             double r1, r2;
             if constexpr (XDIR) {
@@ -1081,10 +1111,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
             }
             fp = r1 + s1;
             fpp = r2 + s2;
-        } else {
+        } else if constexpr (!XLIST) {
             const double x0 = C.c * rho;
             fp = -pow(C.c, C.s + 1.0) * expint_dev(-C.s, x0);
             fpp = pow(C.c, C.s + 2.0) * expint_dev(-C.s - 1.0, x0);
+        } else {
+            fp = fpp = 0.0;
         }
         const double G1 = (ALIAS ? P.alias_ratio * racc[0] : g1) + fp;
         if constexpr (XDIR) {
@@ -1254,6 +1286,10 @@ __device__ __forceinline__ bool node_of(const DevGrid& g, int64_t patch, int lan
 // pair's constants (9 doubles)
 constexpr uint32_t kCmBytes = 96u * uint32_t(kLinePlanes);
 constexpr uint32_t kLineScrBytes = kCmBytes + 1536u + 80u;
+// row kernel: three saved channel sets (the quad's nodes -x0, +x1, -x1) instead of one
+constexpr int kRowCand = 64;  // most reciprocal candidates of a line pair on the fast path
+constexpr uint32_t kRowScrBytes = kCmBytes + 3u * 1536u + 80u + 2u * uint32_t(kRowCand);
+constexpr int kRowMaxV = 1024;  // angular nodes and weights staged in shared memory up to this n_v
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
 // scratch as [m][12] doubles, valid until the next call.
@@ -1363,7 +1399,7 @@ __device__ __forceinline__ void row_planes_r(const DevPlan& P, const double2* __
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
     const double2* Dp = D + lane;
-#pragma unroll 2
+#pragma unroll kRowUnroll
     for (int jj = 0; jj < nJ; ++jj) {
         const double2 rot = lds_f64x2(scr + 16u * jj);
         double2 dv[R];
@@ -1494,6 +1530,60 @@ __device__ __forceinline__ void line_node_pair(const DevPlan& P, uint32_t scr, i
     }
 }
 
+// Phase 3 of the row kernel for two mirror pairs +-x0, +-x1 of the current line in one pass over
+// the planes (each C_m load feeds four nodes); cos / sin 2 pi x m by the Chebyshev recurrence
+// f_{m+1} = 2 cos(2 pi x) f_m - f_{m-1}, two planes per iteration with the pair of values advanced
+// in place.  hh(+x0) is returned in registers, hh(-x0), hh(+x1), hh(-x1) go to the warp's three
+// saved channel sets at hs (+ 1536 bytes per set, [6][32] doubles each; hs includes 8 lane).
+__device__ __forceinline__ void line_node_quad(uint32_t scr, int np, double x0, double x1, double (&hp0)[6],
+                                               uint32_t hs) {
+    double s0, c0, s1, c1;
+    sincos2pi(x0, s0, c0);
+    sincos2pi(x1, s1, c1);
+    double A0[6], B0[6], A1[6], B1[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        A0[c] = A1[c] = lds_f64(scr + 16u * c);  // Re C_0 (half plane)
+        B0[c] = B1[c] = 0.0;
+    }
+    const double t0 = c0 + c0, t1 = c1 + c1;
+    double ca0 = 1.0, cb0 = c0, sa0 = 0.0, sb0 = s0;  // (m - 1, m) at m = 1
+    double ca1 = 1.0, cb1 = c1, sa1 = 0.0, sb1 = s1;
+    auto plane = [&](uint32_t cp, double cc0, double ss0, double cc1, double ss1) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const double2 w = lds_f64x2(cp + 16u * c);
+            A0[c] = fma(w.x, cc0, A0[c]);
+            B0[c] = fma(w.y, ss0, B0[c]);
+            A1[c] = fma(w.x, cc1, A1[c]);
+            B1[c] = fma(w.y, ss1, B1[c]);
+        }
+    };
+    int m = 1;
+    uint32_t cp = scr + 96u;
+#pragma unroll 1
+    for (; m + 1 < np; m += 2, cp += 192u) {
+        plane(cp, cb0, sb0, cb1, sb1);
+        ca0 = fma(t0, cb0, -ca0);
+        sa0 = fma(t0, sb0, -sa0);
+        ca1 = fma(t1, cb1, -ca1);
+        sa1 = fma(t1, sb1, -sa1);
+        plane(cp + 96u, ca0, sa0, ca1, sa1);
+        cb0 = fma(t0, ca0, -cb0);
+        sb0 = fma(t0, sa0, -sb0);
+        cb1 = fma(t1, ca1, -cb1);
+        sb1 = fma(t1, sa1, -sb1);
+    }
+    if (m < np) plane(cp, cb0, sb0, cb1, sb1);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        hp0[c] = A0[c] - B0[c];
+        sts_f64(hs + 256u * c, A0[c] + B0[c]);
+        sts_f64(hs + 1536u + 256u * c, A1[c] - B1[c]);
+        sts_f64(hs + 3072u + 256u * c, A1[c] + B1[c]);
+    }
+}
+
 // MODE 0: product  prod_j Z_j^{m_j}           (1 component)
 // MODE 1: ATM      [Z_3^3, tr(M_5^3)]          (2 components; NCTX = 1, HESS)
 // One CTA = TPC tiles of 8 warps sharing ONE staged copy of the plan
@@ -1528,12 +1618,22 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
     if constexpr (CDIR) V.dir = cdir;
     const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // LINE: [count table][q = 0 pieces][per-warp scratch] after the image
-    const uint32_t scr = V.s_end + 4u * kCntEntries + (LINE ? kQ0Bytes : 0u) + kLineScrBytes * uint32_t(warp_all);
+    // ROW: [angular nodes and weights] too, and the larger per-warp scratch
+    const uint32_t vbytes = ROW && g.n_v <= kRowMaxV ? uint32_t(align16(16u * uint32_t(g.n_v))) : 0u;
+    const uint32_t scr = V.s_end + 4u * kCntEntries + (LINE ? kQ0Bytes : 0u) + vbytes +
+                         (ROW ? kRowScrBytes : kLineScrBytes) * uint32_t(warp_all);
     if constexpr (LINE) {
         V.p_rq = cdir + kQ0Max * piece_stride(2);  // LineParam::rq
         V.s_cnt = V.s_end;
         V.s_q0 = V.s_end + 4u * kCntEntries;
         for (int i = threadIdx.x; i < P.q0_nb * piece_stride(2); i += blockDim.x) sts_f64(V.s_q0 + 8u * i, cdir[i]);
+        V.s_v = vbytes ? V.s_q0 + kQ0Bytes : 0u;
+        if (vbytes) {
+            for (int i = threadIdx.x; i < g.n_v; i += blockDim.x) {
+                sts_f64(V.s_v + 8u * i, g.v[i]);
+                sts_f64(V.s_v + 8u * (g.n_v + i), g.wv[i]);
+            }
+        }
         const double qmax = P.n_rec > 0 ? V.rec_norm[P.n_rec - 1] : 1.0;
         const double h = (qmax > 0.0 ? qmax : 1.0) / double(kCntEntries - 2);
         V.cnt_inv_h = 1.0 / h;
@@ -1779,10 +1879,46 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         const int64_t n_lp = lp_hi - lp_lo;
         const bool by_radius = LZ_LINE_ORDER != 0 && lp_lo % g.n_u == 0 && n_lp % g.n_u == 0;
         const int64_t n_outer = by_radius ? n_lp / g.n_u : 1;
+        // ROW: the CTA takes blocks of kRowBlock consecutive tickets (same axis and radial node, so
+        // its warps read the same D rows and share them through L1) and hands them to its warps
+        // from a shared (block << 32 | next) word; the warp that finds the block used up refills it
+        // from the global counter, the others retry until the new block is published.
+        __shared__ unsigned long long s_queue;
+        constexpr unsigned kDoneBlk = 0xffffffffu;
+        if constexpr (ROW) {
+            if (threadIdx.x == 0) s_queue = (0xfffffffeull << 32) | unsigned(kRowBlock);
+            __syncthreads();
+        }
         auto grab = [&]() -> int64_t {
-            unsigned t = 0;
-            if (lane == 0) t = atomicAdd(g.work, 1u);
-            return int64_t(__shfl_sync(0xffffffffu, t, 0));
+            if constexpr (ROW) {
+                long long t = 0;
+                if (lane == 0) {
+                    for (;;) {
+                        const unsigned long long cur = atomicAdd(&s_queue, 1ull);
+                        const unsigned blk = unsigned(cur >> 32), idx = unsigned(cur);
+                        if (blk == kDoneBlk) {
+                            t = n_lp;
+                            break;
+                        }
+                        if (idx < unsigned(kRowBlock)) {
+                            t = int64_t(blk) * kRowBlock + idx;
+                            if (t < n_lp) break;
+                            continue;  // past the end of a partial last block
+                        }
+                        if (idx == unsigned(kRowBlock)) {
+                            const unsigned nb = atomicAdd(g.work, 1u);
+                            const unsigned long long nv =
+                                int64_t(nb) * kRowBlock >= n_lp ? (uint64_t(kDoneBlk) << 32) : (uint64_t(nb) << 32);
+                            atomicExch(&s_queue, nv);
+                        }
+                    }
+                }
+                return int64_t(__shfl_sync(0xffffffffu, t, 0));
+            } else {
+                unsigned t = 0;
+                if (lane == 0) t = atomicAdd(g.work, 1u);
+                return int64_t(__shfl_sync(0xffffffffu, t, 0));
+            }
         };
         for (int64_t tk = grab(); tk < n_lp; tk = grab()) {
             int64_t lp = lp_lo + tk;
@@ -1796,12 +1932,25 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             const int iv2 = int(r % g.nv2), cp = int(r / g.nv2);
             const int ax = cp % D;  // the cells' pyramid: lanes vary kappa_ax
             const int64_t pfirst = lp * per_lp;
+#if LZ_ROW_PREFETCH
+            if constexpr (ROW) {
+                // first ticket of a CTA block: pull the block's D rows (one axis and radial node)
+                // into L1 for the warps that follow
+                if (tk % kRowBlock == 0) {
+                    const size_t bytes = size_t(P.row_nJ) * size_t(P.row_NI) * 16;
+                    const char* base = reinterpret_cast<const char*>(g.dtab) +
+                                       (size_t(ax) * size_t(g.n_u) + size_t(iu)) * bytes;
+                    for (size_t o = size_t(lane) * 128; o < bytes; o += 32 * 128)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + o));
+                }
+            }
+#endif
             // the line pair's nodes: kappa = kappa0 +- x e_ax (x = 2 u v1, + for the s0 = +1 cell,
             // - for its mirror), k = B kappa = k0 +- x B e_ax; kappa0 = u roll_ax(0, 2 s1 v2, 1)
             // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
             // line-pair constants kept in the warp's scratch (broadcast reloads per pv instead of
             // registers live across the node evaluations)
-            const uint32_t lsave = scr + kCmBytes + 1536u;
+            const uint32_t lsave = scr + kCmBytes + (ROW ? 3u * 1536u : 1536u);
             {
                 const double u = g.u[iu];
                 const double s1 = ((cp / D) & 1) ? -1.0 : 1.0;
@@ -1835,6 +1984,123 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             double tacc[NCOMP];
 #pragma unroll
             for (int c = 0; c < NCOMP; ++c) tacc[c] = 0.0;
+            if constexpr (ROW) {
+                // Fast path: the whole line pair is owned by this warp, the angular nodes are staged
+                // and fill whole patch pairs.  Two patches (and their mirrors) per pass over the
+                // planes; the reciprocal candidates are listed once for the whole line pair.
+                if (own && V.s_v && (npv & 1) == 0 && npv * 32 == g.n_v && !P.tab.has_marker && !P.tab.branchfree &&
+                    P.hctx.branch == kLogCase && P.hctx.log_m == 1 && P.n_rec > 0) {
+                    const int np = ax == 0 ? P.line_P[0] : ax == 1 ? P.line_P[1] : P.line_P[2];
+                    const uint32_t sv = V.s_v + 8u * lane, sw = sv + 8u * uint32_t(g.n_v);
+                    // candidates: q with dist(-q, segment [k0 - xm dk, k0 + xm dk]) <= r_cut (xm the
+                    // line's largest |x|); each lane tests one q per round, survivors in index order
+                    int ncand = 0;
+                    {
+                        const double vm = fmax(lds_f64(V.s_v), lds_f64(V.s_v + 8u * uint32_t(g.n_v - 1)));
+                        const double xm = 2.0 * lds_f64(lsave + 48u) * vm * (1.0 + 1e-12);
+                        double e0[D], dv[D], dd = 0.0;
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            const double dk = lds_f64(lsave + 24u + 8u * a);
+                            e0[a] = fma(-xm, dk, lds_f64(lsave + 8u * a));
+                            dv[a] = 2.0 * xm * dk;
+                            dd = fma(dv[a], dv[a], dd);
+                        }
+                        const double idd = dd > 0.0 ? 1.0 / dd : 0.0;
+                        const double rc2 = P.r_cut * P.r_cut * (1.0 + 1e-12);
+                        const uint32_t cl = lsave + 80u;
+                        // |q| <= r_cut + max |k| over the segment (an end point): from the count
+                        // table, rounded outwards
+                        int n_try;
+                        {
+                            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                a0 = fma(e0[a], e0[a], a0);
+                                const double e1 = e0[a] + dv[a];
+                                a1 = fma(e1, e1, a1);
+                            }
+                            const double km = sqrt(fmax(a0, a1)) * (1.0 + 1e-9);
+                            const double xe = fma(P.r_cut + km, V.cnt_inv_h, 0.5) + kMagic;  // floor + 1
+                            n_try = int(lds_u32(V.s_cnt + 4u * uint32_t(min(__double2loint(xe), kCntEntries - 1))));
+                        }
+                        for (int i0 = 0; i0 < n_try; i0 += 32) {
+                            bool hit = false;
+                            if (i0 + lane < n_try) {
+                                const double2 qa = lds_f64x2(V.s_rec_q + 32u * uint32_t(i0 + lane));
+                                const double qc = lds_f64(V.s_rec_q + 32u * uint32_t(i0 + lane) + 16u);
+                                const double w[D] = {qa.x + e0[0], qa.y + e0[1], qc + e0[2]};
+                                double wd = 0.0;
+#pragma unroll
+                                for (int a = 0; a < D; ++a) wd = fma(w[a], dv[a], wd);
+                                const double t = fmin(fmax(-wd * idd, 0.0), 1.0);
+                                double e2 = 0.0;
+#pragma unroll
+                                for (int a = 0; a < D; ++a) {
+                                    const double e = fma(t, dv[a], w[a]);
+                                    e2 = fma(e, e, e2);
+                                }
+                                hit = e2 <= rc2;
+                            }
+                            const unsigned m = __ballot_sync(0xffffffffu, hit);
+                            const int pos = ncand + __popc(m & ((1u << lane) - 1u));
+                            if (hit && pos < kRowCand)
+                                asm volatile("st.shared.u16 [%0], %1;" ::"r"(cl + 2u * uint32_t(pos)), "h"(uint16_t(i0 + lane)) : "memory");
+                            ncand += __popc(m);
+                        }
+                        __syncwarp();
+                    }
+                    if (ncand <= kRowCand) {
+                        V.s_cand = lsave + 80u;
+                        V.n_cand = ncand;
+                        for (int pv = 0; pv < npv; pv += 2) {
+                            double hp[6];
+                            {
+                                const double u2 = 2.0 * lds_f64(lsave + 48u);
+                                line_node_quad(scr, np, u2 * lds_f64(sv + 256u * uint32_t(pv)),
+                                               u2 * lds_f64(sv + 256u * uint32_t(pv + 1)), hp, hsave);
+                            }
+                            // the four nodes +-x0, +-x1: k = k0 +- x dk, weight wu wv2 wv1 (x and the
+                            // weight re-derived per node instead of held across the evaluations)
+#pragma unroll 1
+                            for (int nd = 0; nd < 4; ++nd) {
+                                const uint32_t po = 256u * uint32_t(pv + (nd >> 1));
+                                const double xs = (nd & 1 ? -2.0 : 2.0) * lds_f64(lsave + 48u) * lds_f64(sv + po);
+                                double k[D];
+#pragma unroll
+                                for (int a = 0; a < D; ++a)
+                                    k[a] = fma(xs, lds_f64(lsave + 24u + 8u * a), lds_f64(lsave + 8u * a));
+                                if (nd > 0) {
+#pragma unroll
+                                    for (int c = 0; c < 6; ++c)
+                                        hp[c] = lds_f64(hsave + 1536u * uint32_t(nd - 1) + 256u * c);
+                                }
+                                NodeAcc<D, NCTX, HESS, true> acc;
+                                eval_node<D, NCTX, HESS, true, UNR, true, false, true, true, true>(P, V, k, k, 0, 1, 0u, acc, hp);
+                                const double h00 = acc.h[0], h01 = acc.h[1], h02 = acc.h[2], h11 = acc.h[3],
+                                             h12 = acc.h[4], h22 = acc.h[5];
+                                const double tr = (h00 + h11) + h22;
+                                const double d01 = h01 * h01, d02 = h02 * h02, d12 = h12 * h12;
+                                const double cub = fma(h00 * h00, h00, fma(h11 * h11, h11, h22 * h22 * h22));
+                                const double mix = fma(d01, h00 + h11, fma(d02, h00 + h22, d12 * (h11 + h22)));
+                                const double tr3 = fma(3.0, mix, fma(6.0 * h01, h02 * h12, cub));
+                                const double cm = P.h_cm, zt = cm * tr;
+                                const double wn = (lds_f64(lsave + 56u) * lds_f64(sw + po)) * lds_f64(lsave + 64u);
+                                tacc[0] += wn * (zt * zt * zt);
+                                tacc[1] += wn * ((cm * cm * cm) * tr3);
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < NCOMP; ++c) {
+                            double v = tacc[c];
+#pragma unroll
+                            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                            if (lane == 0) partials[(pfirst / kTileWarps) * NCOMP + c] = v;
+                        }
+                        continue;
+                    }
+                }
+            }
             for (int pv = 0; pv < npv; ++pv) {
                 const int64_t patch = pfirst + pv;  // mirror 0; mirror 1 is patch + npv
                 const bool in0 = patch >= p_lo && patch < p_hi, in1 = patch + npv >= p_lo && patch + npv < p_hi;
@@ -2324,7 +2590,9 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
                                  cudaStream_t st, size_t bytes) {
     auto kern = tile_kernel_l<WPC, UNR, ROW>;
     if (ROW && (!g.dtab || !P.row_pts || !P.row_idx)) return cudaErrorInvalidValue;
-    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes + size_t(WPC) * kLineScrBytes;
+    const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
+                      (ROW ? (g.n_v <= kRowMaxV ? align16(16u * size_t(g.n_v)) : 0) + size_t(WPC) * kRowScrBytes
+                           : size_t(WPC) * kLineScrBytes);
     if (sm > size_t(smem_optin())) return cudaErrorInvalidValue;
     cudaError_t e = set_smem(kern, sm);
     if (e != cudaSuccess) return e;
@@ -2361,7 +2629,9 @@ static bool line_eligible(const DevPlan& P, const DevGrid& g) {
     if (P.d != 3 || (!P.line_bytes && !P.row_on) || !line_mode() || g.pu != 1 || g.pv != 32) return false;
     const size_t bytes = plan_smem_bytes(P);
     const size_t need = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
-                        size_t(line_mode()) * kLineScrBytes + 1024;
+                        (P.row_on ? (g.n_v <= kRowMaxV ? align16(16u * size_t(g.n_v)) : 0) +
+                                        size_t(line_mode()) * kRowScrBytes
+                                  : size_t(line_mode()) * kLineScrBytes) + 1024;
     return need <= size_t(smem_optin()) && P.n_rec <= kLineQ && P.q0_nb >= 1 && P.q0_nb <= kQ0Max;
 }
 

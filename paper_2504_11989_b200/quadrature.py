@@ -266,7 +266,12 @@ def product_plan(lattice: Lattice, nus_key: tuple, splitting: float | None = Non
 # (L/epstein.py:107).  The lattice sum is split-invariant; a smaller split moves work from the
 # reciprocal sum (table lookups, ~64 instructions per term) to the direct sum (phase rotations,
 # ~18 per point).  Measured on B200: see DESIGN.md section 3.2.
-ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "0.13"))
+# Round 2: the row-factorised direct space (d = 3) costs one complex multiply-add per (row, plane,
+# channel) and line, so the split drops to 0.05 (fcc: 6,107 direct points, ~3 reciprocal terms per
+# node); d <= 2 plans (slab walk) keep 0.13.
+ATM_SPLIT_SCALE = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE", "0.05"))
+ATM_X_LO_MAX = 8.0
+ATM_SPLIT_SCALE_LOW_D = float(os.environ.get("LATSUM_ATM_SPLIT_SCALE_2D", "0.13"))
 
 
 _HELPER = None
@@ -283,8 +288,17 @@ def _helper():
 @lru_cache(maxsize=64)
 def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
     """Plan for the ATM integrand [Z_3^3, tr(M_5^3)], M_5 = polynomial-weighted zeta at nu = 5."""
-    if splitting is None and ATM_SPLIT_SCALE != 1.0:
-        splitting = ATM_SPLIT_SCALE * lattice.volume ** (-2.0 / lattice.d)
+    auto_split = splitting is None
+    if splitting is None:
+        scale = ATM_SPLIT_SCALE if lattice.d == 3 else ATM_SPLIT_SCALE_LOW_D
+        if scale != 1.0:
+            splitting = scale * lattice.volume ** (-2.0 / lattice.d)
+            if lattice.d == 3:
+                # the line kernel's q = 0 pieces cover x = c |k|^2 <= x_lo = c sigma_min(B)^2 / 4
+                # (csrc/context.cpp table_x_lo) in bins of 0.25: keep x_lo <= 8 (32 bins, and the
+                # rho series they are fitted from converges well inside its 64 terms)
+                sig2 = 1.0 / float(np.linalg.eigvalsh(lattice.a.T @ lattice.a).max())
+                splitting = max(splitting, math.pi * sig2 / (4.0 * ATM_X_LO_MAX))
     # the two contexts' host enumerations are independent native calls (GIL released): overlap them
     # (one helper thread, kept for the process)
     # Both contexts are private to this (cached) plan and enumerate only what it reads: Z_3 lends
@@ -295,7 +309,13 @@ def atm_plan(lattice: Lattice, splitting: float | None = None) -> Plan:
     z5 = f5.result()
     h = C.c_void_p()
     N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)), "atm plan")
-    return Plan(h, lattice.d, 2, (z3, z5))
+    plan = Plan(h, lattice.d, 2, (z3, z5))
+    if auto_split and lattice.d == 3 and ATM_SPLIT_SCALE < ATM_SPLIT_SCALE_LOW_D and \
+            plan.info().smem_bytes > 120_000:
+        # the direct set did not fit the row-factorised block (very anisotropic cells): the slab
+        # walk pays per direct point, so it gets the larger split
+        return atm_plan(lattice, ATM_SPLIT_SCALE_LOW_D * lattice.volume ** (-2.0 / lattice.d))
+    return plan
 
 
 def _distinct(contexts):
