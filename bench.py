@@ -309,8 +309,9 @@ def config_block(world):
             "nodes_per_step": N_NODES, "zeta_evals_per_node": 1, "terms_per_node": TERMS_PER_NODE,
             "parallelism": f"node-shard x{world} (96 fixed chunks) + 1 NCCL all-reduce of chunk sums"
                            if world > 1 else "1 GPU",
-            "l2": "node data generated on device; tables (<120 KB) live in shared memory; L2 flushed "
-                  "(256 MB write) between timed steps"}
+            "l2": "node data generated on device; tables (~50 KB) live in shared memory, the direct-space "
+                  "row table (~18 MB, rebuilt every step by row_table_kernel) in L2; L2 flushed (256 MB write) "
+                  "between timed steps"}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -474,7 +475,7 @@ def run_ours(args):
                      "ncu": {k: cnt.get(k) for k in ("fp64_pipe_active", "issue_active", "lsu_wavefronts",
                                                      "warps_active", "registers")}},
         "exchange_bytes_per_step": S.exchange_bytes if world > 1 else 0,
-        "gpu_launches": 3 * args.steps,   # tile kernel + chunk reduce + total per step
+        "gpu_launches": 4 * args.steps,   # row table + tile kernel + chunk reduce + total per step
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

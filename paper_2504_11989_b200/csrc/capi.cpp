@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <array>
+#include <cfloat>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -513,17 +514,15 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
         const long double r = std::sqrt(std::fabs(w));
         for (int a = 0; a < 3; ++a) v[i][a] = double(r * z[a]);
     }
-    struct Pt {
-        long j, m, l;
-        size_t i;
-        bool operator<(const Pt& o) const { return std::tie(j, m, l) < std::tie(o.j, o.m, o.l); }
-    };
-    std::vector<Pt> pts[3];
+    // canonical (m = n_a, j = n_b, l = n_c) of every point per axis, then a counting sort by row
+    // (j, m): the order inside a row is the points' own (only the rounding of the row sums
+    // depends on it)
+    std::vector<int32_t> can[3];
     long jlo[3], jhi[3];
     int planes[3];
     for (int ax = 0; ax < 3; ++ax) {
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
-        pts[ax].reserve(np);
+        can[ax].resize(np * 3);
         jlo[ax] = 0, jhi[ax] = 0;
         long mmax = 0;
         for (size_t i = 0; i < np; ++i) {
@@ -532,14 +531,15 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
             const bool pos = n[ax] > 0 || (n[ax] == 0 && (n[b] > 0 || (n[b] == 0 && n[c] > 0)));
             if (!pos)
                 for (int a = 0; a < 3; ++a) n[a] = -n[a];
-            pts[ax].push_back({n[b], n[ax], n[c], i});
+            can[ax][3 * i] = int32_t(n[ax]);
+            can[ax][3 * i + 1] = int32_t(n[b]);
+            can[ax][3 * i + 2] = int32_t(n[c]);
             jlo[ax] = std::min(jlo[ax], n[b]);
             jhi[ax] = std::max(jhi[ax], n[b]);
             mmax = std::max(mmax, n[ax]);
         }
         if (mmax + 1 > lz::kLinePlanes) return false;
         planes[ax] = int(mmax + 1);
-        std::sort(pts[ax].begin(), pts[ax].end());
     }
     const int pmax = std::max(planes[0], std::max(planes[1], planes[2]));
     const int rounds = (6 * pmax + 31) / 32;
@@ -549,20 +549,24 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
     for (int ax = 0; ax < 3; ++ax) nJ = std::max(nJ, jhi[ax] - jlo[ax] + 1);
     if (nJ > 128) return false;
     hp->row_idx.assign(size_t(3) * size_t(nJ) * size_t(PS) * 2, 0);
-    hp->row_pts.reserve(np * 12);
+    hp->row_pts.assign(np * 12, 0.0);
+    std::vector<int> fill(size_t(nJ) * size_t(PS));
     for (int ax = 0; ax < 3; ++ax) {
-        const auto& pp = pts[ax];
-        for (size_t q = 0; q < pp.size();) {
-            size_t e = q;
-            while (e < pp.size() && pp[e].j == pp[q].j && pp[e].m == pp[q].m) ++e;
-            const size_t slot = (size_t(ax) * size_t(nJ) + size_t(pp[q].j - jlo[ax])) * size_t(PS) + size_t(pp[q].m);
-            hp->row_idx[2 * slot] = int(hp->row_pts.size() / 4);
-            hp->row_idx[2 * slot + 1] = int(e - q);
-            for (size_t t = q; t < e; ++t) {
-                hp->row_pts.push_back(double(pp[t].l));
-                for (int a = 0; a < 3; ++a) hp->row_pts.push_back(v[pp[t].i][a]);
-            }
-            q = e;
+        int* idx = &hp->row_idx[size_t(ax) * size_t(nJ) * size_t(PS) * 2];
+        auto slot_of = [&](size_t i) {
+            return size_t(can[ax][3 * i + 1] - jlo[ax]) * size_t(PS) + size_t(can[ax][3 * i]);
+        };
+        for (size_t i = 0; i < np; ++i) ++idx[2 * slot_of(i) + 1];
+        int start = int(size_t(ax) * np);
+        for (size_t sl = 0; sl < fill.size(); ++sl) {
+            idx[2 * sl] = start;
+            fill[sl] = start;
+            start += idx[2 * sl + 1];
+        }
+        for (size_t i = 0; i < np; ++i) {
+            double* o = &hp->row_pts[size_t(fill[slot_of(i)]++) * 4];
+            o[0] = double(can[ax][3 * i + 2]);
+            for (int a = 0; a < 3; ++a) o[1 + a] = v[i][a];
         }
         hp->row_jmin[ax] = int(jlo[ax]);
         hp->line_P[ax] = planes[ax];
@@ -813,10 +817,35 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         const size_t nk = kept.size() / d, nwc = wctx.size();
         wmap.idx.reserve(2 * nk);
         wmap.rows.assign(nk * nwc, 0.0L);
-        lz::parallel_for(int64_t(nk), 32, [&](int64_t i) {
+        // w_z depends on |z|^2 only: points on one shell of the lattice's symmetry (fcc at the ATM
+        // split: 6,107 points, ~140 distinct radii) share one evaluation.  Points are grouped by
+        // |z|^2 (sorted; equal within 64 long-double roundings of the three-term sum of squares --
+        // far below the weight's sensitivity) and the group's first point is evaluated.
+        std::vector<ld> r2v(nk);
+        for (size_t i = 0; i < nk; ++i) {
+            ld r2 = 0.0L;
+            for (int a = 0; a < d; ++a) {
+                ld za = 0.0L;
+                for (int b = 0; b < d; ++b) za += ld(first->A[a * d + b]) * kept[i * d + b];
+                r2 += za * za;
+            }
+            r2v[i] = r2;
+        }
+        std::vector<uint32_t> ord(nk), rep;  // rep: first (sorted) index of every group
+        for (size_t i = 0; i < nk; ++i) ord[i] = uint32_t(i);
+        std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return r2v[a] < r2v[b] || (r2v[a] == r2v[b] && a < b); });
+        std::vector<uint32_t> group(nk);
+        for (size_t s = 0; s < nk; ++s) {
+            if (s == 0 || r2v[ord[s]] - r2v[ord[rep.back()]] > 64.0L * LDBL_EPSILON * r2v[ord[s]]) rep.push_back(uint32_t(s));
+            group[ord[s]] = uint32_t(rep.size() - 1);
+        }
+        std::vector<ld> gw(rep.size() * nwc);
+        lz::parallel_for(int64_t(rep.size()), 8, [&](int64_t gi) {
             ld z[lz::kMaxDim];
-            for (size_t j = 0; j < nwc; ++j) wmap.rows[size_t(i) * nwc + j] = direct_weight(*wctx[j], &kept[i * d], z);
+            for (size_t j = 0; j < nwc; ++j) gw[size_t(gi) * nwc + j] = direct_weight(*wctx[j], &kept[size_t(ord[rep[gi]]) * d], z);
         });
+        for (size_t i = 0; i < nk; ++i)
+            for (size_t j = 0; j < nwc; ++j) wmap.rows[i * nwc + j] = gw[size_t(group[i]) * nwc + j];
         for (size_t i = 0; i < nk; ++i) wmap.idx.emplace(pack_key(d, &kept[i * d]), uint32_t(i));
         hp->dir_n.swap(kept);
     }
@@ -972,7 +1001,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     int line_env = 2;
     if (const char* e = std::getenv("LATSUM_LINE")) line_env = std::atoi(e);
     if (trace_z && d == 3 && line_env >= 2) build_row_block(hp, wmap, first->A, hscale, hw);
-    if (trace_z && d == 3 && !hp->row_on && !build_line_block(hp, wmap, first->A, hscale, hw)) hp->line.clear();
+    if (trace_z && d == 3 && !hp->row_on && line_env >= 1 && !build_line_block(hp, wmap, first->A, hscale, hw))
+        hp->line.clear();
     lap("line block");
     // reciprocal points, sorted by |q| (stable) for the per-warp culling bound
     const size_t nrec = rec_n.size() / d;
@@ -1348,6 +1378,7 @@ struct Scratch {
     double* dtab = nullptr;         // row-factorised ATM kernel: D table (grow-only)
     int64_t cap = 0, cap_w = 0;
     size_t cap_d = 0;               // bytes
+
 };
 std::mutex g_scratch_mu;
 std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
@@ -1396,6 +1427,7 @@ void tile_scratch(int device, cudaStream_t st, int64_t n_tiles, bool need_wpart,
         s.cap_d = dtab_bytes;
     }
     if (dtab) *dtab = dtab_bytes ? s.dtab : nullptr;
+
     *wpart = need_wpart ? s.wpart : nullptr;
     *tcount = s.tcount;
     *work = s.tcount + s.cap;

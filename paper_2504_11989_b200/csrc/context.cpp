@@ -20,6 +20,9 @@
 #include <future>
 #include <mutex>
 #include <thread>
+#include <unordered_map>
+#include <cfloat>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -167,32 +170,53 @@ static void enumerate_direct(const HostCtx& h, int poly_order, double tol, std::
         std::vector<double> sn(size_t(m) * d), sz(size_t(m) * d), sw(m);
         std::vector<ld> smag(m);
         std::vector<char> out(m, 0);
-        // per point in parallel (large shells), reduced below in the fixed point order
-        parallel_for(m, 128, [&](int64_t j) {
+        // per point in parallel (large shells), reduced below in the fixed point order.  The
+        // weight depends on |z|^2 only, so the shell's points are grouped by it first (sorted;
+        // equal within 64 long-double roundings) and one point per group evaluates the Gamma
+        // function -- a symmetric lattice has a handful of distinct radii per max-norm shell.
+        std::vector<ld> r2s(m);
+        parallel_for(m, 512, [&](int64_t j) {
             const int* n = &shell[idx[j] * d];
-            ld z[kMaxDim], r2 = 0.0L;
+            ld r2 = 0.0L;
             for (int a = 0; a < d; ++a) {
-                z[a] = 0.0L;
-                for (int b = 0; b < d; ++b) z[a] += ld(h.A[a * d + b]) * n[b];
-                r2 += z[a] * z[a];
+                ld za = 0.0L;
+                for (int b = 0; b < d; ++b) za += ld(h.A[a * d + b]) * n[b];
+                sn[size_t(j) * d + a] = double(n[a]);
+                sz[size_t(j) * d + a] = double(za);
+                r2 += za * za;
             }
+            r2s[j] = r2;
+        });
+        std::vector<int> ord(m), rep, group(m);
+        for (int j = 0; j < m; ++j) ord[j] = j;
+        std::sort(ord.begin(), ord.end(), [&](int a, int b) { return r2s[a] < r2s[b] || (r2s[a] == r2s[b] && a < b); });
+        for (int s = 0; s < m; ++s) {
+            if (s == 0 || r2s[ord[s]] - r2s[ord[rep.back()]] > 64.0L * LDBL_EPSILON * r2s[ord[s]]) rep.push_back(s);
+            group[ord[s]] = int(rep.size()) - 1;
+        }
+        std::vector<double> gw(rep.size());
+        std::vector<ld> gmag(rep.size());
+        std::vector<char> gout(rep.size(), 0);
+        parallel_for(int64_t(rep.size()), 16, [&](int64_t gi) {
+            const ld r2 = r2s[ord[rep[gi]]];
             if (r2_ball > 0.0 && double(r2) > r2_ball) {
-                out[j] = 1;
-                smag[j] = 0.0L;
-                sw[j] = 0.0;
+                gout[gi] = 1;
+                gmag[gi] = 0.0L;
+                gw[gi] = 0.0;
                 return;
             }
             // truncation decisions and the reported weights need double precision only (the
             // reference computes them in double)
             const double xd = double(kPiL * t * r2), r2d = double(r2), nud = double(nu);
             const double w = upper_gamma<double>(nud / 2.0, xd) * std::pow(r2d, -nud / 2.0);
-            smag[j] = std::fabs(ld(w)) * ld(std::pow(r2d, double(poly_order) / 2.0));
-            for (int a = 0; a < d; ++a) {
-                sn[size_t(j) * d + a] = double(n[a]);
-                sz[size_t(j) * d + a] = double(z[a]);
-            }
-            sw[j] = w;
+            gmag[gi] = std::fabs(ld(w)) * ld(std::pow(r2d, double(poly_order) / 2.0));
+            gw[gi] = w;
         });
+        for (int j = 0; j < m; ++j) {
+            out[j] = gout[group[j]];
+            smag[j] = gmag[group[j]];
+            sw[j] = gw[group[j]];
+        }
         ld mag = 0.0L, wsum = 0.0L;
         for (int j = 0; j < m; ++j) {
             mag = std::max(mag, smag[j]);
@@ -347,6 +371,96 @@ void build_context(int d, const double* a, double nu, double splitting, int deri
     if (hess.valid()) hess.get();
 }
 
+// Plan-private Hessian direct set (ball_sets): every lex-positive lattice point with |z|^2 <=
+// r2_ball, enumerated directly -- outer coordinates over their bounding ranges (|n_a| <= R |b_a|,
+// b_a the a-th reciprocal basis vector), the last one from the quadratic |A n|^2 <= R^2 -- instead
+// of max-norm shells whose cube corners lie far outside the ball.  Weights as in enumerate_direct
+// (double precision, one Gamma function per distinct |z|^2).  The order of the points is the
+// enumeration's; the plan sorts them itself.
+static void enumerate_ball(const HostCtx& h, double r2_ball, std::vector<double>* pn, std::vector<double>* pz,
+                           std::vector<double>* pw) {
+    const int d = h.d;
+    const ld R2 = ld(r2_ball), R = std::sqrt(R2);
+    pn->clear();
+    pz->clear();
+    pw->clear();
+    long lim[kMaxDim];
+    for (int a = 0; a < d; ++a) {
+        ld nb = 0.0L;  // |b_a|^2, b_a = a-th row of A^{-1} = a-th column of B
+        for (int r = 0; r < d; ++r) nb += ld(h.B[r * d + a]) * h.B[r * d + a];
+        lim[a] = long(std::floor(R * std::sqrt(nb) * (1.0L + 1e-12L))) + 1;
+    }
+    ld al[kMaxDim], aa = 0.0L;  // last basis vector (column d - 1 of A)
+    for (int r = 0; r < d; ++r) {
+        al[r] = h.A[r * d + (d - 1)];
+        aa += al[r] * al[r];
+    }
+    std::vector<ld> r2s;
+    long n[kMaxDim] = {0, 0, 0, 0};
+    // odometer over the outer coordinates n_0 .. n_{d-2}
+    for (int a = 0; a + 1 < d; ++a) n[a] = -lim[a];
+    if (d >= 2) n[0] = 0;  // lex-positive points have n_0 >= 0
+    for (;;) {
+        ld zo[kMaxDim], cc = 0.0L, bb = 0.0L;
+        for (int r = 0; r < d; ++r) {
+            zo[r] = 0.0L;
+            for (int a = 0; a + 1 < d; ++a) zo[r] += ld(h.A[r * d + a]) * n[a];
+            cc += zo[r] * zo[r];
+            bb += zo[r] * al[r];
+        }
+        const ld disc = bb * bb - aa * (cc - R2);
+        if (disc >= 0.0L) {
+            const ld sq = std::sqrt(disc);
+            const long lo = long(std::ceil((-bb - sq) / aa - 1e-9L)), hi = long(std::floor((-bb + sq) / aa + 1e-9L));
+            for (long l = lo; l <= hi; ++l) {
+                n[d - 1] = l;
+                int nn[kMaxDim];
+                for (int a = 0; a < d; ++a) nn[a] = int(n[a]);
+                if (!lex_positive(nn, d)) continue;
+                ld r2 = 0.0L, z[kMaxDim];
+                for (int r = 0; r < d; ++r) {
+                    z[r] = zo[r] + al[r] * l;
+                    r2 += z[r] * z[r];
+                }
+                if (r2 > R2) continue;
+                for (int a = 0; a < d; ++a) {
+                    pn->push_back(double(n[a]));
+                    pz->push_back(double(z[a]));
+                }
+                r2s.push_back(r2);
+            }
+        }
+        int a = d - 2;
+        for (; a >= 0; --a) {
+            if (++n[a] <= lim[a]) break;
+            n[a] = a == 0 ? 0 : -lim[a];
+        }
+        if (a < 0) break;
+    }
+    // groups of equal |z|^2 as rounded to double (these weights are double-precision and serve
+    // the plan's truncation decisions only; the plan recomputes the kept ones in long double)
+    const size_t m = r2s.size();
+    pw->assign(m, 0.0);
+    std::unordered_map<uint64_t, uint32_t> seen;
+    seen.reserve(m / 4 + 16);
+    std::vector<uint32_t> group(m);
+    std::vector<double> gr2;
+    for (size_t j = 0; j < m; ++j) {
+        const double r2d = double(r2s[j]);
+        uint64_t bits;
+        std::memcpy(&bits, &r2d, sizeof(bits));
+        const auto it = seen.emplace(bits, uint32_t(gr2.size()));
+        if (it.second) gr2.push_back(r2d);
+        group[j] = it.first->second;
+    }
+    std::vector<double> gw(gr2.size());
+    const double nud = h.k.nu, td = h.k.split;
+    parallel_for(int64_t(gr2.size()), 16, [&](int64_t gi) {
+        gw[gi] = upper_gamma<double>(nud / 2.0, double(kPiL) * td * gr2[gi]) * std::pow(gr2[gi], -nud / 2.0);
+    });
+    for (size_t j = 0; j < m; ++j) (*pw)[j] = gw[group[j]];
+}
+
 void build_hess_sets(HostCtx& h) {
     if (h.has_hess || !h.want_hess || h.k.branch == kTrivial) return;
     // Hessian sets: the derivative-table enumerators of L/epstein.py:376-377
@@ -369,8 +483,17 @@ void build_hess_sets(HostCtx& h) {
             r2_ball = hi * (1.0 + 1e-9);
         }
     }
-    enumerate_direct(h, 2, kTermCutoff, &h.hdir_n, &h.hdir_z, &h.hdir_w, r2_ball);
+    const bool tm = std::getenv("LATSUM_TIMING") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    if (r2_ball > 0.0) enumerate_ball(h, r2_ball, &h.hdir_n, &h.hdir_z, &h.hdir_w);
+    else enumerate_direct(h, 2, kTermCutoff, &h.hdir_n, &h.hdir_z, &h.hdir_w, 0.0);
+    auto t1 = std::chrono::steady_clock::now();
     enumerate_reciprocal(h, h.k.s + 2.0, kTermCutoff, &h.hrec_n, &h.hrec_q);
+    if (tm)
+        std::fprintf(stderr, "  hess sets: direct %.3f ms (%zu points), reciprocal %.3f ms (%zu)\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(), h.hdir_w.size(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(),
+                     h.hrec_n.size() / h.d);
     h.has_hess = 1;
 }
 

@@ -386,9 +386,6 @@ constexpr int kP1Unroll = LZ_P1_UNROLL;  // phase-1 slots per loop iteration
 #ifndef LZ_ROW_UNROLL
 #define LZ_ROW_UNROLL 2
 #endif
-#ifndef LZ_ROW_PREFETCH
-#define LZ_ROW_PREFETCH 0
-#endif
 constexpr int kRowBlock = LZ_ROW_BLOCK;
 constexpr int kRowUnroll = LZ_ROW_UNROLL;
 // Ticket order of the line kernel's work queue (A/B: -DLZ_LINE_ORDER=0 plain, 1 radial index
@@ -1932,19 +1929,6 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
             const int iv2 = int(r % g.nv2), cp = int(r / g.nv2);
             const int ax = cp % D;  // the cells' pyramid: lanes vary kappa_ax
             const int64_t pfirst = lp * per_lp;
-#if LZ_ROW_PREFETCH
-            if constexpr (ROW) {
-                // first ticket of a CTA block: pull the block's D rows (one axis and radial node)
-                // into L1 for the warps that follow
-                if (tk % kRowBlock == 0) {
-                    const size_t bytes = size_t(P.row_nJ) * size_t(P.row_NI) * 16;
-                    const char* base = reinterpret_cast<const char*>(g.dtab) +
-                                       (size_t(ax) * size_t(g.n_u) + size_t(iu)) * bytes;
-                    for (size_t o = size_t(lane) * 128; o < bytes; o += 32 * 128)
-                        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + o));
-                }
-            }
-#endif
             // the line pair's nodes: kappa = kappa0 +- x e_ax (x = 2 u v1, + for the s0 = +1 cell,
             // - for its mirror), k = B kappa = k0 +- x B e_ax; kappa0 = u roll_ax(0, 2 s1 v2, 1)
             // (L/quadrature.py:143-152); both mirrors share the weight wu wv1 wv2
@@ -2563,14 +2547,16 @@ static int atm_shape() {
     return shape;
 }
 
-// Line-factorised ATM kernel (plans with a line block): default on, LATSUM_LINE=0 falls back to
-// the slab walk; LATSUM_LINE_WPC in {16, 20, 24} warps per CTA.
+// Warps per CTA of the line / row kernels (plans with a line or row block; the plan builder picks
+// the form, capi.cpp build_host_plan / LATSUM_LINE): LATSUM_LINE_WPC in {16, 20, 24}.
 static int line_mode() {
     static int v = -1;
     if (v < 0) {
         v = 20;
-        if (const char* e = std::getenv("LATSUM_LINE")) v = std::atoi(e) == 0 ? 0 : v;
-        if (const char* e = std::getenv("LATSUM_LINE_WPC")) v = v ? std::atoi(e) : 0;
+        if (const char* e = std::getenv("LATSUM_LINE_WPC")) {
+            const int w = std::atoi(e);
+            if (w == 16 || w == 20 || w == 24) v = w;
+        }
     }
     return v;
 }
@@ -2614,7 +2600,8 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     int blocks = int(need < cap ? need : cap);
     if (blocks < 1) return cudaSuccess;
     if constexpr (ROW) {
-        // the D table of every (axis, radial node) of the grid (a shard recomputes all of it: ~10 us)
+        // the D table of every (axis, radial node) of the grid, rebuilt by every launch (~15 us; a
+        // shard computes all of it)
         const int64_t total = int64_t(3) * g.n_u * P.row_nJ * P.row_PS;
         row_table_kernel<<<unsigned((total + 127) / 128), 128, 0, st>>>(P, g);
         e = cudaGetLastError();

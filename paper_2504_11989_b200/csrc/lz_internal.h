@@ -15,7 +15,10 @@ enum Branch : int { kGeneric = 0, kLogCase = 1, kTrivial = 2 };
 
 constexpr int kMaxDim = 4;     // L/lattice.py:20
 constexpr int kMaxCtx = 4;     // distinct exponents fused into one product kernel
-constexpr int kLinePlanes = 24;  // planes per axis of the line- / row-factorised ATM direct block
+#ifndef LZ_LINE_PLANES
+#define LZ_LINE_PLANES 24
+#endif
+constexpr int kLinePlanes = LZ_LINE_PLANES;  // planes per axis of the line- / row-factorised ATM direct block
 constexpr int kRowRounds = 5;    // row-factorised block: most 32-item rounds of the plane sums (6 kLinePlanes <= 32 kRowRounds)
 // Degree of the piecewise polynomials (kDeg + 1 coefficients): 7 or 8.  Degree 7 on bins of
 // 0.125 in x saves two DFMA, one DMUL and one 16-byte load per function pair and term but needs

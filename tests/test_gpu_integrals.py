@@ -456,3 +456,48 @@ def test_atm_generic_lattices(name):
     for key, nus in (("z333", (3, 3, 3)), ("zm155", (-1, 5, 5)), ("z135", (1, 3, 5))):
         v, _ = integrate_product(lat, nus, cfg)
         assert abs(v - g[key]) <= max(1e-12 * abs(g[key]), 2 * g[key + "_err"]), (key, v, g[key])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["fcc", "bcc", "triclinic"])
+@pytest.mark.parametrize("grid", [(4, 128, 3), (3, 64, 3), (2, 96, 3), (2, 40, 3)])
+def test_atm_kernel_forms_agree(name, grid, monkeypatch):
+    """The three ATM kernel forms -- row-factorised direct space (D table per axis and radial node,
+    the default), the shared-memory line block (LATSUM_LINE=1) and the slab walk (LATSUM_LINE=0)
+    -- give the same sums on the same split.  Grids: whole patch pairs (the row kernel's
+    four-node fast path), two patches per line, an odd patch count and a partial last patch
+    (its per-patch path)."""
+    from paper_2504_11989_b200 import Lattice
+    lat = named_lattice(name) if name != "triclinic" else \
+        Lattice(np.array([[1.0, 0.15, 0.25], [0.0, 1.1, 0.3], [0.05, 0.0, 0.95]]))
+    t = 0.13 * lat.volume ** (-2.0 / 3.0)
+    out = {}
+    for form in ("2", "1", "0"):
+        monkeypatch.setenv("LATSUM_LINE", form)
+        atm_plan.cache_clear()
+        out[form] = atm_integrals(lat, ATMGrid(*grid), splitting=t)
+    monkeypatch.delenv("LATSUM_LINE")
+    atm_plan.cache_clear()
+    for form in ("1", "0"):
+        assert abs(out[form].zeta333 - out["2"].zeta333) <= 2e-13 * abs(out["2"].zeta333), form
+        assert abs(out[form].dot_term - out["2"].dot_term) <= 2e-13 * abs(out["2"].dot_term), form
+
+
+@pytest.mark.gpu
+def test_atm_default_plan_uses_row_block():
+    """The default fcc / bcc ATM plans take the row-factorised block (no slab or line block staged:
+    the shared-memory image is the tables only) at the low split, and a very flat cell that does
+    not fit it falls back to the slab walk at the larger split."""
+    from paper_2504_11989_b200 import Lattice
+    for name in ("fcc", "bcc"):
+        lat = named_lattice(name)
+        info = atm_plan(lat).info()
+        assert info.smem_bytes < 70_000 and info.n_dir > 4000
+        assert abs(info.split - 0.05 * lat.volume ** (-2.0 / 3.0)) < 1e-15
+    flat = Lattice(np.diag([1.0, 1.0, 0.3]))
+    info = atm_plan(flat).info()
+    assert abs(info.split - 0.13 * flat.volume ** (-2.0 / 3.0)) < 1e-15
+    res = atm_integrals(flat, ATMGrid(2, 8, 3))
+    s = O.atm_grid(flat.a, 2, 8, 3)
+    assert abs(res.zeta333 - 8 * s[0]) <= 1e-12 * abs(8 * s[0])
+    assert abs(res.dot_term - 8 * s[1]) <= 1e-12 * max(1.0, abs(8 * s[1]))
