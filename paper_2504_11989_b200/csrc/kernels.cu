@@ -23,11 +23,16 @@
 //                    L/quadrature.py:393-397) or the ATM integrand
 //                    [Z_3^3, tr M_5^3] (C3), reduced deterministically to one
 //                    partial per 256-node tile (slot-disjoint for multi-GPU)
-//   tile_kernel_l  : the ATM kernel (d = 3, default): line-factorised direct space --
-//                    a warp's 32 nodes lie on one line of the grid, so the direct sum
-//                    becomes warp-uniform plane sums C_m (formed once per line pair of
-//                    mirror cells, 8 patches) plus one rotation per plane and node
-//   tile_kernel_c  : the previous ATM variant (fallback, LATSUM_LINE=0) with the direct
+//   tile_kernel_l  : the ATM kernel (d = 3): a warp's 32 nodes lie on one line of the grid,
+//                    so the direct sum becomes warp-uniform plane sums C_m (formed once per
+//                    line pair of mirror cells, 8 patches) plus one rotation per plane and
+//                    node.  ROW (default): C_m = sum_j e^{2 pi i kappa_b j} D_{m,j}(u) from the
+//                    D table of row_table_kernel -- one complex multiply-add per row index,
+//                    plane and channel; four nodes per lane and pass over the planes;
+//                    reciprocal candidates listed once per line pair.  !ROW (LATSUM_LINE=1):
+//                    C_m summed point by point from a shared-memory line block
+//   row_table_kernel: D_{m,j}(u) = sum_{n_c} W_n e^{2 pi i u n_c} per (axis, radial node)
+//   tile_kernel_c  : the slab-walk ATM variant (fallback, LATSUM_LINE=0) with the direct
 //                    block in parameter space and a free warps-per-CTA count
 //   reduce_kernel  : fixed-order compensated sum of the tile partials
 //   fp64_probe     : DFMA-chain peak probe for the roofline denominator
