@@ -1451,7 +1451,9 @@ __device__ __forceinline__ void row_planes(const DevPlan& P, const DevGrid& g, u
 // plane slot m) sums its row's points, W_n e^{2 pi i u n_c} with W_n = line_sign v v^T (six
 // channels), and writes the six items 6 m + channel (zero for slots without a row and for the
 // padding items up to row_NI).
-__global__ void __launch_bounds__(128) row_table_kernel(DevPlan P, DevGrid g) {
+// axes: bit a set = some line of the launch's tile range has pyramid axis a (a shard of a multi-GPU
+// sum usually meets one or two of the three).
+__global__ void __launch_bounds__(128) row_table_kernel(DevPlan P, DevGrid g, unsigned axes) {
     const int PS = P.row_PS, nJ = P.row_nJ, NI = P.row_NI;
     const int64_t total = int64_t(3) * g.n_u * nJ * PS;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1462,6 +1464,7 @@ __global__ void __launch_bounds__(128) row_table_kernel(DevPlan P, DevGrid g) {
     r /= nJ;
     const int iu = int(r % g.n_u);
     const int ax = int(r / g.n_u);
+    if (!((axes >> ax) & 1u)) return;
     const int2 row = reinterpret_cast<const int2*>(P.row_idx)[(size_t(ax) * nJ + jj) * PS + slot];
     const double u = g.u[iu];
     double acc[12];
@@ -1596,7 +1599,10 @@ constexpr int kDirParam = 3584;
 // line kernel parameter block: the Hessian's two q = 0 series rows and up to kLineQ reciprocal
 // vectors at the padded stride 4 (d = 3)
 constexpr int kLineQ = 512;
-constexpr int kQ0Max = 48;  // line kernel: Hessian q = 0 pieces (bins of kBinWidth in x = c rho)
+#ifndef LZ_Q0_MAX
+#define LZ_Q0_MAX 48
+#endif
+constexpr int kQ0Max = LZ_Q0_MAX;  // line kernel: Hessian q = 0 pieces (bins of kBinWidth in x = c rho)
 constexpr uint32_t kQ0Bytes = uint32_t(kQ0Max) * piece_stride(2) * 8u;
 struct __align__(16) LineParam {
     double q0[kQ0Max * piece_stride(2)];
@@ -2607,8 +2613,13 @@ static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* par
     if constexpr (ROW) {
         // the D table of every (axis, radial node) of the grid, rebuilt by every launch (~15 us; a
         // shard computes all of it)
+        // line pair lp = (cp nv2 + iv2) n_u + iu has axis cp mod 3 (tile_body LINE walk)
+        const int64_t per_cp = int64_t(g.nv2) * g.n_u;
+        const int64_t cp_lo = (p_lo / per_lp) / per_cp, cp_hi = ((p_hi - 1) / per_lp) / per_cp;
+        unsigned axes = 0;
+        for (int64_t cp = cp_lo; cp <= cp_hi && cp < cp_lo + 3; ++cp) axes |= 1u << unsigned(cp % 3);
         const int64_t total = int64_t(3) * g.n_u * P.row_nJ * P.row_PS;
-        row_table_kernel<<<unsigned((total + 127) / 128), 128, 0, st>>>(P, g);
+        row_table_kernel<<<unsigned((total + 127) / 128), 128, 0, st>>>(P, g, axes);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
