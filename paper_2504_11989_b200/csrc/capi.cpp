@@ -212,11 +212,22 @@ void union_points(int d, const std::vector<const std::vector<double>*>& sets, st
 }
 
 // Weights of the kept direct points, one row of `nw` channels per point, found by packed key.
+// `keys[i]` is the packed key of row i; the key -> row map is built on first use (the row-
+// factorised ATM block reads its rows through `row_of`, the sorted order's row indices, and
+// never needs it).
 struct WeightMap {
-    std::unordered_map<uint64_t, uint32_t> idx;
+    mutable std::unordered_map<uint64_t, uint32_t> idx;
+    std::vector<uint64_t> keys;
     std::vector<long double> rows;
+    std::vector<uint32_t> row_of;   // row of hp->dir_n[i] after the lexicographic sort
     size_t nw = 0;
-    const long double* at(uint64_t key) const { return &rows[size_t(idx.at(key)) * nw]; }
+    const long double* at(uint64_t key) const {
+        if (idx.empty() && !keys.empty()) {
+            idx.reserve(2 * keys.size());
+            for (size_t i = 0; i < keys.size(); ++i) idx.emplace(keys[i], uint32_t(i));
+        }
+        return &rows[size_t(idx.at(key)) * nw];
+    }
 };
 
 // Direct-space weight w_z = Gamma(nu/2, pi t |z|^2) |z|^-nu (L/epstein.py:139), long double.
@@ -507,7 +518,7 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
             z[a] = 0.0L;
             for (int b = 0; b < 3; ++b) z[a] += (long double)A[a * 3 + b] * n[b];
         }
-        const long double w = wmap.at(pack_key(d, n))[hidx] * hscale;
+        const long double w = wmap.rows[size_t(wmap.row_of[i]) * wmap.nw + size_t(hidx)] * hscale;
         const int sg = w < 0 ? -1 : 1;
         if (sign != 0 && sg != sign) return false;  // mixed weight signs
         sign = sg;
@@ -815,7 +826,6 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         // which the cancellation between the regular and singular parts near the log-case
         // exponents (nu -> d + 2m) can amplify past the 1e-12 parity bar
         const size_t nk = kept.size() / d, nwc = wctx.size();
-        wmap.idx.reserve(2 * nk);
         wmap.rows.assign(nk * nwc, 0.0L);
         // w_z depends on |z|^2 only: points on one shell of the lattice's symmetry (fcc at the ATM
         // split: 6,107 points, ~140 distinct radii) share one evaluation.  Points are grouped by
@@ -846,7 +856,8 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         });
         for (size_t i = 0; i < nk; ++i)
             for (size_t j = 0; j < nwc; ++j) wmap.rows[i * nwc + j] = gw[size_t(group[i]) * nwc + j];
-        for (size_t i = 0; i < nk; ++i) wmap.idx.emplace(pack_key(d, &kept[i * d]), uint32_t(i));
+        wmap.keys.resize(nk);
+        for (size_t i = 0; i < nk; ++i) wmap.keys[i] = pack_key(d, &kept[i * d]);
         hp->dir_n.swap(kept);
     }
     lap("union+ball");
@@ -865,11 +876,14 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         // lexicographic order = order of the packed keys (most significant field first; the
         // points are distinct, so no ties)
         std::vector<std::pair<uint64_t, uint32_t>> ord(np);
-        for (size_t i = 0; i < np; ++i) ord[i] = {pack_key(d, &hp->dir_n[i * d]), uint32_t(i)};
+        for (size_t i = 0; i < np; ++i) ord[i] = {wmap.keys[i], uint32_t(i)};
         std::sort(ord.begin(), ord.end());
         std::vector<double> pts(np * d);
-        for (size_t i = 0; i < np; ++i)
+        wmap.row_of.resize(np);
+        for (size_t i = 0; i < np; ++i) {
             for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[size_t(ord[i].second) * d + a];
+            wmap.row_of[i] = ord[i].second;
+        }
         hp->dir_n.swap(pts);
         auto key = [&](size_t i, int a) { return std::lround(hp->dir_n[i * d + a]); };
         // maximal runs (for plan info only)
