@@ -1071,7 +1071,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
                            a16(8 * hp->tab.coef.size()) + a16(4 * hp->tab.dir.size()) +
                            a16(8 * size_t(hp->nctx + 2) * lz::kT0) + a16(hp->line.size());
         // (row kernel: 20 warps x kRowScrBytes, the q = 0 pieces, the count table, angular nodes)
-        const size_t extra = hp->row_on ? 20 * 7000 + 12 * 1024 : 1024 + 24 * 4000 + 8192;
+        const size_t extra = hp->row_on ? 20 * 7120 + 13 * 1024 : 1024 + 24 * 4000 + 8192;
         need_slab = line_env == 0 || img + extra > 227 * 1024 ||
                     hp->rec_norm.size() > 512 ||  // kernels.cu kLineQ
                     hp->q0_nb < 1 || hp->q0_nb > 48;  // kernels.cu kQ0Max

@@ -1291,7 +1291,7 @@ constexpr uint32_t kLineScrBytes = kCmBytes + 1536u + 80u;
 // row kernel: three saved channel sets (the quad's nodes -x0, +x1, -x1) instead of one
 constexpr int kRowCand = 64;  // most reciprocal candidates of a line pair on the fast path
 constexpr uint32_t kRowScrBytes = kCmBytes + 3u * 1536u + 80u + 2u * uint32_t(kRowCand);
-constexpr int kRowMaxV = 1024;  // angular nodes and weights staged in shared memory up to this n_v
+constexpr int kRowMaxV = 256;   // angular nodes and weights staged in shared memory up to this n_v (4 KB)
 
 // Phases 1-2 for one line (kappa_0 of lane 0's node): leaves C_m (times line_sign) in the warp's
 // scratch as [m][12] doubles, valid until the next call.

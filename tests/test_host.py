@@ -259,6 +259,37 @@ def test_host_only_plans():
     assert N.lib().lz_plan_create_atm(c3.handle, c3.handle, C.byref(h3)) != 0
 
 
+def test_atm_plan_row_block_host_only():
+    """The default d = 3 ATM plan at the low split is the row-factorised one: no slab or line block
+    in the shared-memory image (tables only) although the direct set is large; LATSUM_LINE=0
+    brings the slab block back; a cell too flat for the row block's plane limit keeps a slab."""
+    import ctypes as C
+    import os
+    from paper_2504_11989_b200 import Lattice
+    from paper_2504_11989_b200.quadrature import Plan
+
+    def host_plan(lat, scale):
+        t = scale * lat.volume ** (-2.0 / 3.0)
+        z3 = EpsteinContext(lat, 3.0, splitting=t, deriv_order=-1, device=-1)
+        z5 = EpsteinContext(lat, 5.0, splitting=t, deriv_order=-2, device=-1)
+        h = C.c_void_p()
+        N.check(N.lib().lz_plan_create_atm(z3.handle, z5.handle, C.byref(h)))
+        return Plan(h, 3, 2, (z3, z5)).info()
+
+    for name in ("fcc", "bcc"):
+        info = host_plan(named_lattice(name), 0.05)
+        assert 5000 < info.n_dir < 7000 and info.smem_bytes < 70_000, (name, info.n_dir, info.smem_bytes)
+    os.environ["LATSUM_LINE"] = "0"
+    try:
+        slab = host_plan(named_lattice("fcc"), 0.13)
+    finally:
+        del os.environ["LATSUM_LINE"]
+    row = host_plan(named_lattice("fcc"), 0.13)
+    assert slab.n_dir == row.n_dir and slab.smem_bytes > row.smem_bytes + 30_000
+    flat = host_plan(Lattice(np.diag([1.0, 1.0, 0.3])), 0.05)
+    assert flat.smem_bytes > 120_000   # slab walk: quadrature.atm_plan then re-plans at the larger split
+
+
 def test_allreduce_partials_argument_errors():
     """The C-ABI all-reduce validates its arguments before touching CUDA or NCCL."""
     assert N.lib().lz_allreduce_partials(None, 0, None, None) == N.LZ_EINVAL
