@@ -469,6 +469,11 @@ def run_ours(args):
                      "frac": achieved / pk.value, "traffic": cnt.get("dram_bytes_per_launch"),
                      "kernel": cnt.get("kernel"), "kernel_ms": kern_ms,
                      "flops_per_node": cnt["flops_per_unit"], "flops_source": cnt.get("source"),
+                     "flops_per_reference_term": cnt["flops_per_unit"] / TERMS_PER_NODE,
+                     "terms_evaluated_per_node": {
+                         "reciprocal": 0.70, "q0": 1, "direct": "16 plane rotations per node (plane sums "
+                         "shared by the 256 nodes of a line pair, from the per-(axis, radial node) row table)",
+                         "source": "profiles/r02k_atm_segments.txt (execution counts of the term code)"},
                      "flops_stale": cnt["stale"],
                      "peak_source": "measured live: DFMA-chain probe lz_fp64_peak (MEASURED_PEAKS.json has "
                                     "no FP64 entry)",
