@@ -336,17 +336,41 @@ class RegZetaTaylor:
         w = np.asarray(w, dtype=float)
         single = w.ndim == 1
         w = np.atleast_2d(w)
-        total = 2 * k
-        acc = np.zeros(len(w))
-        for alpha, val in self.derivs.items():
-            if sum(alpha) != total or val == 0.0:
-                continue
-            mult = math.factorial(total)
-            for a in alpha:
-                mult //= math.factorial(a)
-            acc += mult * np.prod(w ** np.array(alpha), axis=1) * val
-        acc /= math.factorial(total)
+        alphas, coef = self._order_terms(2 * k)
+        if len(coef) == 0:
+            acc = np.zeros(len(w))
+        else:
+            # all multi-indices of the order at once: power ladders w_a^0..w_a^total by repeated
+            # multiplication, gathered per multi-index
+            total = 2 * k
+            acc = None
+            for a in range(w.shape[1]):
+                ladder = np.empty((len(w), total + 1))
+                ladder[:, 0] = 1.0
+                for e in range(1, total + 1):
+                    ladder[:, e] = ladder[:, e - 1] * w[:, a]
+                term = ladder[:, alphas[:, a]]
+                acc = term if acc is None else acc * term
+            acc = acc @ coef
         return acc[0] if single else acc
+
+    def _order_terms(self, total: int):
+        """Multi-indices of one total order with nonzero entries and their coefficients
+        multinomial(alpha) D^alpha Z_reg(0) / total! (cached per table)."""
+        cache = self.__dict__.setdefault("_terms", {})
+        if total not in cache:
+            al, cf = [], []
+            for alpha, val in self.derivs.items():
+                if sum(alpha) != total or val == 0.0:
+                    continue
+                mult = math.factorial(total)
+                for a in alpha:
+                    mult //= math.factorial(a)
+                al.append(alpha)
+                cf.append(mult * val / math.factorial(total))
+            d = self.lattice.d
+            cache[total] = (np.array(al, dtype=np.intp).reshape(len(al), d), np.array(cf, dtype=float))
+        return cache[total]
 
 
 @lru_cache(maxsize=4096)
