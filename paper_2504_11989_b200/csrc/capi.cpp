@@ -1153,6 +1153,8 @@ lz::DevPlan upload_plan(const HostPlan& hp, std::vector<void*>* allocs) {
     P.row_PS = hp.row_PS;
     P.row_NI = hp.row_NI;
     for (int a = 0; a < 3; ++a) P.row_jmin[a] = hp.row_jmin[a];
+    P.row_cand_max = 64;  // kernels.cu kRowCand
+    if (const char* e = std::getenv("LATSUM_ROW_CAND_MAX")) P.row_cand_max = std::max(0, std::min(64, std::atoi(e)));
     if (hp.row_on) {
         P.row_pts = upload(hp.row_pts, allocs);
         P.row_idx = upload(hp.row_idx, allocs);

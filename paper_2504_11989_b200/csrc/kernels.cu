@@ -941,8 +941,12 @@ __device__ __forceinline__ void eval_node(const DevPlan& P, const View& V, const
         // listed once per line pair (tile_body); every other q is zero for all of its nodes
         (void)n_eff;
         (void)n_in_line;
-        for (int c = 0; c < V.n_cand; ++c)
-            term(int(lds_u16(V.s_cand + 2u * uint32_t(c))), std::integral_constant<int, 1>{});
+        if (V.n_cand >= 0) {
+            for (int c = 0; c < V.n_cand; ++c)
+                term(int(lds_u16(V.s_cand + 2u * uint32_t(c))), std::integral_constant<int, 1>{});
+        } else {  // the list overflowed: all -n_cand points within r_cut + max |k| of the line pair
+            for (int i = 0; i < -V.n_cand; ++i) term(i, std::integral_constant<int, 1>{});
+        }
     } else if (P.tab.has_marker || (flags & 1u)) {
 #pragma unroll UNR
         for (int i = gl; i < n_eff; i += G) term(i, std::integral_constant<int, 0>{});
@@ -1616,7 +1620,7 @@ struct __align__(16) DirBlock {
 // walks lines (cell, v2, u) instead of patches: the per-plane sums C_m depend only on the line,
 // so they are formed once (line_planes) and serve the line's npv patches of 32 v1 nodes each.
 template <int D, int NCTX, bool HESS, int MODE, bool SMEM, int WPC, int UNR, bool CDIR, bool LINE = false,
-          bool ROW = false>
+          bool ROW = false, bool FAST = false>
 __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, int4 mult,
                                           double* __restrict__ partials, const double* cdir) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1983,13 +1987,15 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                 // Fast path: the whole line pair is owned by this warp, the angular nodes are staged
                 // and fill whole patch pairs.  Two patches (and their mirrors) per pass over the
                 // planes; the reciprocal candidates are listed once for the whole line pair.
-                if (own && V.s_v && (npv & 1) == 0 && npv * 32 == g.n_v && !P.tab.has_marker && !P.tab.branchfree &&
-                    P.hctx.branch == kLogCase && P.hctx.log_m == 1 && P.n_rec > 0) {
+                // (FAST: the launch checked these conditions for every line pair -- row_fast_eligible
+                // -- and the kernel carries no per-patch code)
+                if (FAST || (own && V.s_v && (npv & 1) == 0 && npv * 32 == g.n_v && !P.tab.has_marker &&
+                             !P.tab.branchfree && P.hctx.branch == kLogCase && P.hctx.log_m == 1 && P.n_rec > 0)) {
                     const int np = ax == 0 ? P.line_P[0] : ax == 1 ? P.line_P[1] : P.line_P[2];
                     const uint32_t sv = V.s_v + 8u * lane, sw = sv + 8u * uint32_t(g.n_v);
                     // candidates: q with dist(-q, segment [k0 - xm dk, k0 + xm dk]) <= r_cut (xm the
                     // line's largest |x|); each lane tests one q per round, survivors in index order
-                    int ncand = 0;
+                    int ncand = 0, n_try_all = 0;
                     {
                         const double vm = fmax(lds_f64(V.s_v), lds_f64(V.s_v + 8u * uint32_t(g.n_v - 1)));
                         const double xm = 2.0 * lds_f64(lsave + 48u) * vm * (1.0 + 1e-12);
@@ -2018,6 +2024,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                             const double km = sqrt(fmax(a0, a1)) * (1.0 + 1e-9);
                             const double xe = fma(P.r_cut + km, V.cnt_inv_h, 0.5) + kMagic;  // floor + 1
                             n_try = int(lds_u32(V.s_cnt + 4u * uint32_t(min(__double2loint(xe), kCntEntries - 1))));
+                            n_try_all = n_try;
                         }
                         for (int i0 = 0; i0 < n_try; i0 += 32) {
                             bool hit = false;
@@ -2039,15 +2046,17 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                             }
                             const unsigned m = __ballot_sync(0xffffffffu, hit);
                             const int pos = ncand + __popc(m & ((1u << lane) - 1u));
-                            if (hit && pos < kRowCand)
+                            if (hit && pos < kRowCand)  // (capacity of the scratch list; cand_max <= kRowCand)
                                 asm volatile("st.shared.u16 [%0], %1;" ::"r"(cl + 2u * uint32_t(pos)), "h"(uint16_t(i0 + lane)) : "memory");
                             ncand += __popc(m);
                         }
                         __syncwarp();
                     }
-                    if (ncand <= kRowCand) {
+                    const int cand_max = min(kRowCand, P.row_cand_max);
+                    if (FAST || ncand <= cand_max) {
                         V.s_cand = lsave + 80u;
-                        V.n_cand = ncand;
+                        // a list that overflowed (FAST only): every node tests all n_try points itself
+                        V.n_cand = ncand <= cand_max ? ncand : -n_try_all;
                         for (int pv = 0; pv < npv; pv += 2) {
                             double hp[6];
                             {
@@ -2096,6 +2105,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                     }
                 }
             }
+            if constexpr (!FAST)
             for (int pv = 0; pv < npv; ++pv) {
                 const int64_t patch = pfirst + pv;  // mirror 0; mirror 1 is patch + npv
                 const bool in0 = patch >= p_lo && patch < p_hi, in1 = patch + npv >= p_lo && patch + npv < p_hi;
@@ -2133,7 +2143,7 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                     run_node(patch + npv, km, wm, hm, own ? tacc : nullptr);
                 }
             }
-            if (own) {
+            if (!FAST && own) {
 #pragma unroll
                 for (int c = 0; c < NCOMP; ++c) {
                     double v = tacc[c];
@@ -2176,10 +2186,12 @@ __global__ void __launch_bounds__(32 * WPC, 1)
 // reciprocal loop and the q = 0 series come from the parameter block (constant cache, no LSU).
 // ROW: plane sums from the D table of the row-factorised direct block (row_planes) instead of the
 // staged line block.
-template <int WPC, int UNR, bool ROW = false>
+// FAST (with ROW): every line pair of the launch takes the four-node fast path (the host checked
+// row_fast_eligible), so the kernel carries no per-patch code.
+template <int WPC, int UNR, bool ROW = false, bool FAST = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
     tile_kernel_l(DevPlan P, DevGrid g, double* __restrict__ partials, const __grid_constant__ LineParam LP) {
-    tile_body<3, 1, true, 1, true, WPC, UNR, false, true, ROW>(P, g, make_int4(0, 0, 0, 0), partials, LP.q0);
+    tile_body<3, 1, true, 1, true, WPC, UNR, false, true, ROW, FAST>(P, g, make_int4(0, 0, 0, 0), partials, LP.q0);
 }
 
 // Fixed-order compensated (Neumaier) sum of tile partials, one block.
@@ -2582,10 +2594,10 @@ static int line_unroll() {
     return v;
 }
 
-template <int WPC, int UNR, bool ROW = false>
+template <int WPC, int UNR, bool ROW = false, bool FAST = false>
 static cudaError_t launch_tile_l(const DevPlan& P, const DevGrid& g, double* partials, int grid_blocks,
                                  cudaStream_t st, size_t bytes) {
-    auto kern = tile_kernel_l<WPC, UNR, ROW>;
+    auto kern = tile_kernel_l<WPC, UNR, ROW, FAST>;
     if (ROW && (!g.dtab || !P.row_pts || !P.row_idx)) return cudaErrorInvalidValue;
     const size_t sm = bytes - align16(sizeof(double) * P.n_direct) + 4u * kCntEntries + kQ0Bytes +
                       (ROW ? (g.n_v <= kRowMaxV ? align16(16u * size_t(g.n_v)) : 0) + size_t(WPC) * kRowScrBytes
@@ -2638,6 +2650,19 @@ static bool line_eligible(const DevPlan& P, const DevGrid& g) {
     return need <= size_t(smem_optin()) && P.n_rec <= kLineQ && P.q0_nb >= 1 && P.q0_nb <= kQ0Max;
 }
 
+// Every line pair of the launch meets the row kernel's fast-path conditions (tile_body): whole
+// patch pairs with staged angular nodes, a line pair = one tile (so any tile range owns whole line
+// pairs), in-cell tables, the log-case Hessian context.  LATSUM_ROW_FAST=0 keeps the general kernel.
+static bool row_fast_eligible(const DevPlan& P, const DevGrid& g) {
+    static const bool on = [] {
+        const char* e = std::getenv("LATSUM_ROW_FAST");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on && g.n_v <= kRowMaxV && (g.npv & 1) == 0 && g.npv * 32 == g.n_v && 2 * g.npv == kTileWarps &&
+           g.n_cell == 12 && !P.tab.has_marker && !P.tab.branchfree && P.hctx.branch == kLogCase &&
+           P.hctx.log_m == 1 && P.n_rec > 0;
+}
+
 template <int D, int NCTX, bool HESS, int MODE>
 static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, double* partials, int grid_blocks,
                                  cudaStream_t st) {
@@ -2645,6 +2670,8 @@ static cudaError_t launch_tile_t(const DevPlan& P, const DevGrid& g, int4 mult, 
     if (P.blob_bytes != bytes) return cudaErrorInvalidValue;  // plan image must match the layout
     const bool smem = bytes + 2048 <= size_t(smem_optin());
     if constexpr (MODE == 1 && D == 3) {
+        if (line_eligible(P, g) && P.row_on && line_mode() == 20 && row_fast_eligible(P, g))
+            return launch_tile_l<20, 1, true, true>(P, g, partials, grid_blocks, st, bytes);
         if (line_eligible(P, g) && P.row_on) {
             switch (line_mode() * 10 + line_unroll()) {
                 case 161: return launch_tile_l<16, 1, true>(P, g, partials, grid_blocks, st, bytes);

@@ -153,7 +153,7 @@ struct DevPlan {
     int row_on;            // 1: the ATM kernel takes its plane sums from the D table
     int row_nJ, row_PS, row_NI;
     int row_jmin[3];
-    int pad6_;
+    int row_cand_max;      // candidate-list capacity used by the kernel (<= kRowCand; LATSUM_ROW_CAND_MAX, tests)
 };
 
 // Derivative plan (deriv.cu): one context, derivatives of total order `order` (0..12) at

@@ -501,3 +501,20 @@ def test_atm_default_plan_uses_row_block():
     s = O.atm_grid(flat.a, 2, 8, 3)
     assert abs(res.zeta333 - 8 * s[0]) <= 1e-12 * abs(8 * s[0])
     assert abs(res.dot_term - 8 * s[1]) <= 1e-12 * max(1.0, abs(8 * s[1]))
+
+
+@pytest.mark.gpu
+def test_atm_row_kernel_candidate_overflow(monkeypatch):
+    """A line pair whose reciprocal candidates overflow the per-warp list makes every node test all
+    points within reach itself (fast-path kernel) or takes the per-patch culling (general kernel):
+    forced with a zero-capacity list, both give the default result bit for bit (the same terms in
+    the same order; the rest contribute exact zeros)."""
+    lat = named_lattice("fcc")
+    grid = ATMGrid(6, 128, 3)
+    ref = atm_integrals(lat, grid)
+    monkeypatch.setenv("LATSUM_ROW_CAND_MAX", "0")
+    atm_plan.cache_clear()
+    res = atm_integrals(lat, grid)
+    monkeypatch.delenv("LATSUM_ROW_CAND_MAX")
+    atm_plan.cache_clear()
+    assert res.zeta333 == ref.zeta333 and res.dot_term == ref.dot_term
