@@ -385,11 +385,17 @@ __device__ __noinline__ double expint_dev(double p, double x) { return expint<do
 constexpr int kP1Unroll = LZ_P1_UNROLL;  // phase-1 slots per loop iteration
 // row-factorised ATM kernel: tickets per CTA block (A/B: -DLZ_ROW_BLOCK=1 per-warp tickets) and
 // row indices per iteration of the plane-sum loop
+#ifndef LZ_NODE_PEEL
+#define LZ_NODE_PEEL 1
+#endif
+#ifndef LZ_QUAD_PEEL
+#define LZ_QUAD_PEEL 0
+#endif
 #ifndef LZ_ROW_BLOCK
 #define LZ_ROW_BLOCK 32
 #endif
 #ifndef LZ_ROW_UNROLL
-#define LZ_ROW_UNROLL 2
+#define LZ_ROW_UNROLL 3
 #endif
 constexpr int kRowBlock = LZ_ROW_BLOCK;
 constexpr int kRowUnroll = LZ_ROW_UNROLL;
@@ -1550,11 +1556,24 @@ __device__ __forceinline__ void line_node_quad(uint32_t scr, int np, double x0, 
     sincos2pi(x0, s0, c0);
     sincos2pi(x1, s1, c1);
     double A0[6], B0[6], A1[6], B1[6];
+#if LZ_QUAD_PEEL
+    // A/B (not kept by default): planes 0 and 1 seed the accumulators
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const double a0 = lds_f64(scr + 16u * c);
+        const double2 w = lds_f64x2(scr + 96u + 16u * c);
+        A0[c] = fma(w.x, c0, a0);
+        A1[c] = fma(w.x, c1, a0);
+        B0[c] = w.y * s0;
+        B1[c] = w.y * s1;
+    }
+#else
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
         A0[c] = A1[c] = lds_f64(scr + 16u * c);  // Re C_0 (half plane)
         B0[c] = B1[c] = 0.0;
     }
+#endif
     const double t0 = c0 + c0, t1 = c1 + c1;
     double ca0 = 1.0, cb0 = c0, sa0 = 0.0, sb0 = s0;  // (m - 1, m) at m = 1
     double ca1 = 1.0, cb1 = c1, sa1 = 0.0, sb1 = s1;
@@ -1568,8 +1587,16 @@ __device__ __forceinline__ void line_node_quad(uint32_t scr, int np, double x0, 
             B1[c] = fma(w.y, ss1, B1[c]);
         }
     };
+#if LZ_QUAD_PEEL
+    int m = 2;
+    uint32_t cp = scr + 192u;
+    ca0 = cb0, sa0 = sb0, ca1 = cb1, sa1 = sb1;           // m - 1 = 1
+    cb0 = fma(t0, c0, -1.0), sb0 = t0 * s0;                // m = 2: cos 2a = 2 cos^2 a - 1, sin 2a = 2 cos a sin a
+    cb1 = fma(t1, c1, -1.0), sb1 = t1 * s1;
+#else
     int m = 1;
     uint32_t cp = scr + 96u;
+#endif
 #pragma unroll 1
     for (; m + 1 < np; m += 2, cp += 192u) {
         plane(cp, cb0, sb0, cb1, sb1);
@@ -2066,19 +2093,13 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                             }
                             // the four nodes +-x0, +-x1: k = k0 +- x dk, weight wu wv2 wv1 (x and the
                             // weight re-derived per node instead of held across the evaluations)
-#pragma unroll 1
-                            for (int nd = 0; nd < 4; ++nd) {
+                            auto one_node = [&](int nd) {
                                 const uint32_t po = 256u * uint32_t(pv + (nd >> 1));
                                 const double xs = (nd & 1 ? -2.0 : 2.0) * lds_f64(lsave + 48u) * lds_f64(sv + po);
                                 double k[D];
 #pragma unroll
                                 for (int a = 0; a < D; ++a)
                                     k[a] = fma(xs, lds_f64(lsave + 24u + 8u * a), lds_f64(lsave + 8u * a));
-                                if (nd > 0) {
-#pragma unroll
-                                    for (int c = 0; c < 6; ++c)
-                                        hp[c] = lds_f64(hsave + 1536u * uint32_t(nd - 1) + 256u * c);
-                                }
                                 NodeAcc<D, NCTX, HESS, true> acc;
                                 eval_node<D, NCTX, HESS, true, UNR, true, false, true, true, true>(P, V, k, k, 0, 1, 0u, acc, hp);
                                 const double h00 = acc.h[0], h01 = acc.h[1], h02 = acc.h[2], h11 = acc.h[3],
@@ -2092,7 +2113,38 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                                 const double wn = (lds_f64(lsave + 56u) * lds_f64(sw + po)) * lds_f64(lsave + 64u);
                                 tacc[0] += wn * (zt * zt * zt);
                                 tacc[1] += wn * ((cm * cm * cm) * tr3);
+                            };
+#if LZ_NODE_PEEL == 2
+                            one_node(0);
+#pragma unroll
+                            for (int nd = 1; nd < 4; ++nd) {
+#pragma unroll
+                                for (int c = 0; c < 6; ++c)
+                                    hp[c] = lds_f64(hsave + 1536u * uint32_t(nd - 1) + 256u * c);
+                                one_node(nd);
                             }
+#elif LZ_NODE_PEEL
+                            // node +x0 straight from the pass's registers, the other three from
+                            // their saved channel sets
+                            one_node(0);
+#pragma unroll 1
+                            for (int nd = 1; nd < 4; ++nd) {
+#pragma unroll
+                                for (int c = 0; c < 6; ++c)
+                                    hp[c] = lds_f64(hsave + 1536u * uint32_t(nd - 1) + 256u * c);
+                                one_node(nd);
+                            }
+#else
+#pragma unroll 1
+                            for (int nd = 0; nd < 4; ++nd) {
+                                if (nd > 0) {
+#pragma unroll
+                                    for (int c = 0; c < 6; ++c)
+                                        hp[c] = lds_f64(hsave + 1536u * uint32_t(nd - 1) + 256u * c);
+                                }
+                                one_node(nd);
+                            }
+#endif
                         }
 #pragma unroll
                         for (int c = 0; c < NCOMP; ++c) {
