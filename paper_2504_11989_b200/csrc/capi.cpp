@@ -510,28 +510,31 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
     hp->row_idx.clear();
     if (np == 0) return false;
     std::vector<std::array<double, 3>> v(np);
-    int sign = 0;
-    for (size_t i = 0; i < np; ++i) {
-        const double* n = &hp->dir_n[i * d];
+    std::vector<signed char> sg(np);
+    lz::parallel_for(int64_t(np), 1024, [&](int64_t i) {
+        const double* n = &hp->dir_n[size_t(i) * d];
         long double z[3];
         for (int a = 0; a < 3; ++a) {
             z[a] = 0.0L;
             for (int b = 0; b < 3; ++b) z[a] += (long double)A[a * 3 + b] * n[b];
         }
-        const long double w = wmap.rows[size_t(wmap.row_of[i]) * wmap.nw + size_t(hidx)] * hscale;
-        const int sg = w < 0 ? -1 : 1;
-        if (sign != 0 && sg != sign) return false;  // mixed weight signs
-        sign = sg;
+        const long double w = wmap.rows[size_t(wmap.row_of[size_t(i)]) * wmap.nw + size_t(hidx)] * hscale;
+        sg[size_t(i)] = w < 0 ? -1 : 1;
         const long double r = std::sqrt(std::fabs(w));
-        for (int a = 0; a < 3; ++a) v[i][a] = double(r * z[a]);
-    }
+        for (int a = 0; a < 3; ++a) v[size_t(i)][a] = double(r * z[a]);
+    });
+    const int sign = sg[0];
+    for (size_t i = 1; i < np; ++i)
+        if (sg[i] != sign) return false;  // mixed weight signs
     // canonical (m = n_a, j = n_b, l = n_c) of every point per axis, then a counting sort by row
     // (j, m): the order inside a row is the points' own (only the rounding of the row sums
     // depends on it)
     std::vector<int32_t> can[3];
     long jlo[3], jhi[3];
     int planes[3];
-    for (int ax = 0; ax < 3; ++ax) {
+    bool too_many[3] = {false, false, false};
+    lz::parallel_for(3, 1, [&](int64_t axl) {
+        const int ax = int(axl);
         const int b = (ax + 1) % 3, c = (ax + 2) % 3;
         can[ax].resize(np * 3);
         jlo[ax] = 0, jhi[ax] = 0;
@@ -549,9 +552,10 @@ static bool build_row_block(HostPlan* hp, const WeightMap& wmap, const double* A
             jhi[ax] = std::max(jhi[ax], n[b]);
             mmax = std::max(mmax, n[ax]);
         }
-        if (mmax + 1 > lz::kLinePlanes) return false;
+        too_many[ax] = mmax + 1 > lz::kLinePlanes;
         planes[ax] = int(mmax + 1);
-    }
+    });
+    if (too_many[0] || too_many[1] || too_many[2]) return false;
     const int pmax = std::max(planes[0], std::max(planes[1], planes[2]));
     const int rounds = (6 * pmax + 31) / 32;
     if (rounds > lz::kRowRounds) return false;
@@ -828,9 +832,9 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         const size_t nk = kept.size() / d, nwc = wctx.size();
         wmap.rows.assign(nk * nwc, 0.0L);
         // w_z depends on |z|^2 only: points on one shell of the lattice's symmetry (fcc at the ATM
-        // split: 6,107 points, ~140 distinct radii) share one evaluation.  Points are grouped by
-        // |z|^2 (sorted; equal within 64 long-double roundings of the three-term sum of squares --
-        // far below the weight's sensitivity) and the group's first point is evaluated.
+        // split: 6,107 points, ~140 distinct radii) share one evaluation: the group's first point
+        // is evaluated (members equal it within 64 long-double roundings of the three-term sum of
+        // squares -- far below the weight's sensitivity).
         std::vector<ld> r2v(nk);
         for (size_t i = 0; i < nk; ++i) {
             ld r2 = 0.0L;
@@ -841,18 +845,29 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
             }
             r2v[i] = r2;
         }
-        std::vector<uint32_t> ord(nk), rep;  // rep: first (sorted) index of every group
-        for (size_t i = 0; i < nk; ++i) ord[i] = uint32_t(i);
-        std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return r2v[a] < r2v[b] || (r2v[a] == r2v[b] && a < b); });
-        std::vector<uint32_t> group(nk);
-        for (size_t s = 0; s < nk; ++s) {
-            if (s == 0 || r2v[ord[s]] - r2v[ord[rep.back()]] > 64.0L * LDBL_EPSILON * r2v[ord[s]]) rep.push_back(uint32_t(s));
-            group[ord[s]] = uint32_t(rep.size() - 1);
+        // groups by the double rounding of |z|^2 (hash), members checked against the group's
+        // long-double value (a point that does not match opens its own group)
+        std::vector<uint32_t> rep, group(nk);  // rep: first point of every group
+        {
+            std::unordered_map<uint64_t, uint32_t> seen;
+            seen.reserve(nk / 4 + 16);
+            for (size_t i = 0; i < nk; ++i) {
+                const double r2d = double(r2v[i]);
+                uint64_t bits;
+                std::memcpy(&bits, &r2d, sizeof(bits));
+                const auto it = seen.emplace(bits, uint32_t(rep.size()));
+                if (!it.second && std::fabs(r2v[i] - r2v[rep[it.first->second]]) <= 64.0L * LDBL_EPSILON * r2v[i]) {
+                    group[i] = it.first->second;
+                } else {
+                    group[i] = uint32_t(rep.size());
+                    rep.push_back(uint32_t(i));
+                }
+            }
         }
         std::vector<ld> gw(rep.size() * nwc);
         lz::parallel_for(int64_t(rep.size()), 8, [&](int64_t gi) {
             ld z[lz::kMaxDim];
-            for (size_t j = 0; j < nwc; ++j) gw[size_t(gi) * nwc + j] = direct_weight(*wctx[j], &kept[size_t(ord[rep[gi]]) * d], z);
+            for (size_t j = 0; j < nwc; ++j) gw[size_t(gi) * nwc + j] = direct_weight(*wctx[j], &kept[size_t(rep[gi]) * d], z);
         });
         for (size_t i = 0; i < nk; ++i)
             for (size_t j = 0; j < nwc; ++j) wmap.rows[i * nwc + j] = gw[size_t(group[i]) * nwc + j];
@@ -871,34 +886,56 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     // slab: z = zc + j' e2 + l' e3 (zc = slab center, e2 = A e_{d-1}, e3 = A e_d), so three
     // channels w l'^m (m = 0, 1, 2) replace the d(d+1)/2 channels w z_a z_b and the row and
     // slab folds carry the j' and zc parts.
+    // ATM kernel form (LATSUM_LINE): 2 (default) row-factorised direct block, 1 line block staged
+    // in shared memory, 0 slab walk
+    int line_env = 2;
+    if (const char* e = std::getenv("LATSUM_LINE")) line_env = std::atoi(e);
+    const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
+    const int hw = int(wctx.size()) - 1;  // the Hessian context's slot in the wmap rows
+    hp->line.clear();
+    hp->row_on = 0;
     {
         const size_t np = hp->dir_n.size() / d;
         // lexicographic order = order of the packed keys (most significant field first; the
-        // points are distinct, so no ties)
-        std::vector<std::pair<uint64_t, uint32_t>> ord(np);
-        for (size_t i = 0; i < np; ++i) ord[i] = {wmap.keys[i], uint32_t(i)};
-        std::sort(ord.begin(), ord.end());
+        // points are distinct, so no ties).  The sort works on copies, so the row-factorised block
+        // (which groups the points itself and takes them in any order) is built beside it.
         std::vector<double> pts(np * d);
-        wmap.row_of.resize(np);
-        for (size_t i = 0; i < np; ++i) {
-            for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[size_t(ord[i].second) * d + a];
-            wmap.row_of[i] = ord[i].second;
+        std::vector<uint32_t> sorted_row(np);
+        std::vector<int> runs;
+        auto sort_job = [&]() {
+            std::vector<std::pair<uint64_t, uint32_t>> ord(np);
+            for (size_t i = 0; i < np; ++i) ord[i] = {wmap.keys[i], uint32_t(i)};
+            std::sort(ord.begin(), ord.end());
+            for (size_t i = 0; i < np; ++i) {
+                for (int a = 0; a < d; ++a) pts[i * d + a] = hp->dir_n[size_t(ord[i].second) * d + a];
+                sorted_row[i] = ord[i].second;
+            }
+            auto key = [&](size_t i, int a) { return std::lround(pts[i * d + a]); };
+            // maximal runs (for plan info only)
+            for (size_t i = 0; i < np; ++i) {
+                bool cont = i > 0;
+                for (int a = 0; cont && a < d - 1; ++a) cont = key(i, a) == key(i - 1, a);
+                cont = cont && key(i, d - 1) == key(i - 1, d - 1) + 1;
+                if (cont) {
+                    runs.back() += 1;
+                } else {
+                    runs.push_back(int(i));
+                    runs.push_back(1);
+                }
+            }
+        };
+        if (trace_z && d == 3 && line_env >= 2 && hess) {
+            std::future<void> sj = std::async(std::launch::async, sort_job);
+            wmap.row_of.resize(np);
+            for (size_t i = 0; i < np; ++i) wmap.row_of[i] = uint32_t(i);  // rows follow the unsorted order
+            build_row_block(hp, wmap, first->A, hscale, hw);
+            sj.get();
+        } else {
+            sort_job();
         }
         hp->dir_n.swap(pts);
-        auto key = [&](size_t i, int a) { return std::lround(hp->dir_n[i * d + a]); };
-        // maximal runs (for plan info only)
-        hp->run_info.clear();
-        for (size_t i = 0; i < np; ++i) {
-            bool cont = i > 0;
-            for (int a = 0; cont && a < d - 1; ++a) cont = key(i, a) == key(i - 1, a);
-            cont = cont && key(i, d - 1) == key(i - 1, d - 1) + 1;
-            if (cont) {
-                hp->run_info.back() += 1;
-            } else {
-                hp->run_info.push_back(int(i));
-                hp->run_info.push_back(1);
-            }
-        }
+        wmap.row_of.swap(sorted_row);
+        hp->run_info.swap(runs);
     }
     const int nh = hess ? 3 : 0;
     if (trace_z && !hess) throw Error{LZ_EINVAL, "trace-Z plans need the Hessian context"};
@@ -909,8 +946,6 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
         hp->e3[a] = first->A[a * d + d - 1];
         if (d >= 2) hp->e2[a] = first->A[a * d + d - 2];
     }
-    const ld hscale = hess ? -2.0L * ld(lz::kPi) * ld(lz::kPi) / ld(hess->k.rfac) : 0.0L;
-    const int hw = int(wctx.size()) - 1;  // the Hessian context's slot in the wmap rows
     // the slab block (built last, below, unless the line block replaces it)
     auto build_slab = [&]() {
     {
@@ -1008,13 +1043,7 @@ void build_host_plan(const std::vector<const lz::HostCtx*>& plain, const lz::Hos
     }
     };
     lap("sort");
-    hp->line.clear();
-    hp->row_on = 0;
-    // ATM kernel form (LATSUM_LINE): 2 (default) row-factorised direct block, 1 line block staged
-    // in shared memory, 0 slab walk
-    int line_env = 2;
-    if (const char* e = std::getenv("LATSUM_LINE")) line_env = std::atoi(e);
-    if (trace_z && d == 3 && line_env >= 2) build_row_block(hp, wmap, first->A, hscale, hw);
+    // (the row-factorised block was built beside the sort, above)
     if (trace_z && d == 3 && !hp->row_on && line_env >= 1 && !build_line_block(hp, wmap, first->A, hscale, hw))
         hp->line.clear();
     lap("line block");
