@@ -624,6 +624,13 @@ def secondary(np, torch):
                             "lambda_c": crit, "k_atm_fcc": fc.k_atm, "k_atm_bcc": bc.k_atm,
                             "points": len(pts)}
     out["shard_balance"] = shard_balance(torch)
+    # the bcc ATM sum of C5 on the same grid (17 planes per axis: four 32-item rounds of the plane
+    # sums instead of fcc's three)
+    from paper_2504_11989_b200.quadrature import atm_plan
+    bplan = atm_plan(named_lattice("bcc"))
+    _, bnt = bplan.tiles(*GRID)
+    bpart = torch.zeros(bnt * 2, dtype=torch.float64, device="cuda")
+    out["c3_bcc_atm_sum_ms"] = _time_cuda(lambda: bplan.integrate_device(bpart, *GRID), 10, torch)
     # the reference's own route to the fcc ATM energy (Prop. 2.4: three continued integrals with
     # its adaptive GK15/G7 refinement, method="adaptive", every round's zeta products on the GPU)
     fcc = named_lattice("fcc")
