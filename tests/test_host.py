@@ -259,6 +259,39 @@ def test_host_only_plans():
     assert N.lib().lz_plan_create_atm(c3.handle, c3.handle, C.byref(h3)) != 0
 
 
+def test_directional_coeff_matches_term_loop():
+    """RegZetaTaylor.directional_coeff (one gather over power ladders per order) against the plain
+    loop over multi-indices, multinomial(alpha) w^alpha D^alpha / (2k)! (L/epstein.py:449-466), on a
+    synthetic table in d = 3 up to order 12, for a batch of directions and a single one."""
+    import itertools
+    import math
+    from paper_2504_11989_b200.epstein import RegZetaTaylor
+    rng = np.random.default_rng(5)
+    d, order = 3, 12
+    derivs = {a: float(rng.normal()) for a in itertools.product(range(order + 1), repeat=d)
+              if sum(a) <= order and sum(a) % 2 == 0}
+    derivs[(2, 0, 0)] = 0.0   # zero entries are skipped
+    tab = RegZetaTaylor(named_lattice("fcc"), 3.0, order, derivs)
+    w = rng.normal(size=(9, d))
+    w[0, 1] = 0.0             # 0^0 = 1
+    for k in range(order // 2 + 1):
+        ref = np.zeros(len(w))
+        for alpha, val in derivs.items():
+            if sum(alpha) != 2 * k:
+                continue
+            mult = math.factorial(2 * k)
+            for a in alpha:
+                mult //= math.factorial(a)
+            ref += mult * np.prod(w ** np.array(alpha), axis=1) * val
+        ref /= math.factorial(2 * k)
+        got = tab.directional_coeff(w, k)
+        scale = np.max(np.abs(ref)) + 1e-300
+        assert np.max(np.abs(got - ref)) <= 1e-12 * scale, k
+        assert abs(tab.directional_coeff(w[3], k) - got[3]) <= 1e-15 * scale
+    with pytest.raises(ValueError):
+        tab.directional_coeff(w, order // 2 + 1)
+
+
 def test_atm_plan_row_block_host_only():
     """The default d = 3 ATM plan at the low split is the row-factorised one: no slab or line block
     in the shared-memory image (tables only) although the direct set is large; LATSUM_LINE=0
