@@ -1924,8 +1924,13 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
         // from the global counter, the others retry until the new block is published.
         __shared__ unsigned long long s_queue;
         constexpr unsigned kDoneBlk = 0xffffffffu;
+        // block size: kRowBlock for a whole grid, halved (down to 4) while a launch has fewer than
+        // 16 blocks per CTA -- the shards of a multi-GPU sum (an eighth of the C3 grid is 2.6 blocks
+        // of 32 per CTA: a third of the CTAs would run one block longer than the rest)
+        int rb = kRowBlock;
+        while (rb > 4 && n_lp < int64_t(gridDim.x) * 16 * rb) rb >>= 1;
         if constexpr (ROW) {
-            if (threadIdx.x == 0) s_queue = (0xfffffffeull << 32) | unsigned(kRowBlock);
+            if (threadIdx.x == 0) s_queue = (0xfffffffeull << 32) | unsigned(rb);
             __syncthreads();
         }
         auto grab = [&]() -> int64_t {
@@ -1939,15 +1944,15 @@ __device__ __forceinline__ void tile_body(const DevPlan& P, const DevGrid& g, in
                             t = n_lp;
                             break;
                         }
-                        if (idx < unsigned(kRowBlock)) {
-                            t = int64_t(blk) * kRowBlock + idx;
+                        if (idx < unsigned(rb)) {
+                            t = int64_t(blk) * rb + idx;
                             if (t < n_lp) break;
                             continue;  // past the end of a partial last block
                         }
-                        if (idx == unsigned(kRowBlock)) {
+                        if (idx == unsigned(rb)) {
                             const unsigned nb = atomicAdd(g.work, 1u);
                             const unsigned long long nv =
-                                int64_t(nb) * kRowBlock >= n_lp ? (uint64_t(kDoneBlk) << 32) : (uint64_t(nb) << 32);
+                                int64_t(nb) * rb >= n_lp ? (uint64_t(kDoneBlk) << 32) : (uint64_t(nb) << 32);
                             atomicExch(&s_queue, nv);
                         }
                     }
