@@ -460,13 +460,13 @@ def test_atm_generic_lattices(name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["fcc", "bcc", "triclinic"])
-@pytest.mark.parametrize("grid", [(4, 128, 3), (3, 64, 3), (2, 96, 3), (2, 40, 3)])
+@pytest.mark.parametrize("grid", [(4, 128, 3), (3, 64, 3), (2, 96, 3), (2, 40, 3), (1, 288, 3)])
 def test_atm_kernel_forms_agree(name, grid, monkeypatch):
     """The three ATM kernel forms -- row-factorised direct space (D table per axis and radial node,
     the default), the shared-memory line block (LATSUM_LINE=1) and the slab walk (LATSUM_LINE=0)
     -- give the same sums on the same split.  Grids: whole patch pairs (the row kernel's
     four-node fast path), two patches per line, an odd patch count and a partial last patch
-    (its per-patch path)."""
+    (its per-patch path), and more angular nodes than the row kernel stages in shared memory."""
     from paper_2504_11989_b200 import Lattice
     lat = named_lattice(name) if name != "triclinic" else \
         Lattice(np.array([[1.0, 0.15, 0.25], [0.0, 1.1, 0.3], [0.05, 0.0, 0.95]]))
